@@ -1,0 +1,260 @@
+/*
+ * splatlm_b200.h -- C ABI of the B200 (sm_100a) 3DGS-LM inner-solver library
+ * libsplatlm_b200.so.
+ *
+ * Every entry point takes plain device pointers, sizes and a cudaStream_t,
+ * never allocates, launches asynchronously and returns an int status
+ * (SLM_OK = 0).  Scratch sizes for CUB-backed calls are queried with the
+ * *_workspace functions.  The Python package paper_2409_12892_b200 binds this
+ * header with ctypes and re-exposes the reference's
+ * Python API (`splatlm.*`); the "replaces" notes cite the reference function
+ * each call implements.  Reference paths are relative to
+ * /root/reference/pkg/src/splatlm/.
+ */
+#ifndef SPLATLM_B200_H
+#define SPLATLM_B200_H
+
+#include <stdint.h>
+
+#ifdef __CUDACC__
+#include <cuda_runtime.h>
+typedef uint2 slm_u2;
+typedef float4 slm_f4;
+#else
+typedef struct CUstream_st* cudaStream_t;
+typedef struct { uint32_t x, y; } slm_u2;
+typedef struct { float x, y, z, w; } slm_f4;
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (mapped to the reference's exception classes in Python) */
+#define SLM_OK 0
+#define SLM_ERR_ARG 1     /* bad argument: ValueError */
+#define SLM_ERR_CUDA 2    /* CUDA launch/runtime error: RuntimeError */
+#define SLM_ERR_LAYOUT 3  /* LayoutError (scene.py:48-49) -- raised by the host layer */
+#define SLM_ERR_ORDER 4   /* CacheOrderError (jacobian.py:42-43) -- host layer */
+#define SLM_ERR_SIZE 5    /* size beyond the 32-bit CUB limits / ImageSizeError */
+
+/* ---- value types --------------------------------------------------------- */
+
+/* one pinhole view (scene.py:272-304); C = -R^T t precomputed on the host */
+typedef struct {
+  double R[9];
+  double t[3];
+  double fx, fy, cx, cy;
+  double C[3];
+  int W, H;
+  long long pix_base; /* first subset-global pixel index of this view */
+} SlmCamera;
+
+/* RenderConfig (rasterizer.py:22-48) plus the background colour */
+typedef struct {
+  double alpha_min, t_stop, alpha_clamp, cov_eps, z_near;
+  double cull_sigma; /* <= 0 disables the footprint cull */
+  double reach_fac;  /* sqrt(max(0, 2 ln(1/alpha_min))); <= 0: unbounded bbox */
+  double bg[3];
+} SlmRastCfg;
+
+/* fp64 projected splat (ProjectedSplats row, rasterizer.py:63-75), 96 B */
+typedef struct {
+  double mx, my, ca, cb, cc, o, c0, c1, c2;
+  int x0, x1, y0, y1;
+  unsigned flags; /* bit0 valid, bits1..3 colour clamp per channel */
+  int pad;
+} SlmSplat;
+
+/* per (gaussian, view) pair geometry used by the entry chain, 32 B */
+typedef struct {
+  double mx, my;
+  float ka, kb, kc, inv_o;
+} SlmPairGeo;
+
+typedef struct {
+  long long pix_base;
+  int W, H;
+} SlmView;
+
+/* rasteriser launch arguments (both passes) */
+typedef struct {
+  const slm_u2* tile_range;
+  const uint32_t* inst_gid;
+  const SlmSplat* splats;
+  int W, H, tiles_x;
+  long long pix_base;
+  SlmRastCfg cfg;
+  uint32_t* px_count;
+  double* rgb;
+  double* t_final;
+  int* pair_cnt;
+  const long long* pix_off;
+  const int* pidx;
+  const int* seg_idx;
+  uint32_t* rec_idx;
+  float *rec_ae, *rec_at, *rec_d0, *rec_d1, *rec_d2;
+  uint32_t* ent_gid;
+  uint32_t* ent_xy;
+  long long view_entry_base;
+  int* chunk_seg;
+  long long* trav_gid;
+  double* trav_alpha;
+  double* trav_T;
+} SlmRasterArgs;
+
+/* residual weights (residuals.py:249-296) */
+typedef struct {
+  const double* img;
+  const void* gt;
+  int gt_f32;
+  int W, H;
+  double lambda1, lambda2, eps_den;
+  double ssim_c1, ssim_c2;
+  int mode; /* 0 l1ssim, 1 l2 */
+  int win;
+  const double* taps;
+  const double* cw_y;
+  const double* cw_x;
+  double* tmp;
+  slm_f4* gradr;
+  slm_f4* cgrad;
+  double* energy_part;
+  double *o_gradr, *o_cgrad, *o_rabs, *o_rssim, *o_drabs, *o_drssim;
+} SlmResidArgs;
+
+/* gaussian-order scatter of one view (sort_cache_by_gaussians, jacobian.py:93-105) */
+typedef struct {
+  const uint32_t* sorted_gid;
+  const uint32_t* sorted_src;
+  const uint32_t* ent_xy;
+  long long Ev, view_base, G;
+  int v;
+  const int* pidx;
+  const long long* pair_off;
+  const long long* vscan;
+  const float *ae, *at, *d0, *d1, *d2;
+  uint32_t* g_idx;
+  float *g_ae, *g_at, *g_d0, *g_d1, *g_d2;
+  int* chunk_seg;
+  int* g_src;
+} SlmGaussOrderArgs;
+
+/* one cache record stream (pixel or gaussian order) for the product kernels */
+typedef struct {
+  const uint32_t* idx;
+  const float *ae, *at, *d0, *d1, *d2;
+  long long E;
+  const int* chunk_seg;
+  void* head; /* carry scratch, n_chunks * slm_carry_bytes(D) */
+  void* tail;
+} SlmWsrStream;
+
+/* ---- sizes (ctypes layout checks) --------------------------------------- */
+int slm_camera_size(void);
+int slm_rastcfg_size(void);
+int slm_splat_size(void);
+int slm_pair_geo_size(void);
+int slm_view_size(void);
+int slm_raster_args_size(void);
+int slm_resid_args_size(void);
+int slm_gauss_order_args_size(void);
+int slm_wsr_stream_size(void);
+long long slm_carry_bytes(int D);
+
+/* ---- projection / rasterisation ------------------------------------------
+ * replaces project_scene (rasterizer.py:116-165): fp64 splats of one view,
+ * depth keys (fp64 bits, ~0 for culled) and gid values for the depth sort.
+ * err |= 1 on non-finite parameters (rasterizer.py:124-125), 2 on a zero
+ * quaternion (rasterizer.py:81-82). */
+int slm_preprocess(const double* x_am, long long G, int sh_degree, const SlmCamera* cam, const SlmRastCfg* cfg,
+                   SlmSplat* out, unsigned long long* depth_key, uint32_t* order_val, int* err, cudaStream_t s);
+/* stable radix sort of (u64 key, u32 value) pairs -- the (depth, gid) order of
+ * render (rasterizer.py:328-330) and the tile-instance sort */
+long long slm_sort_pairs_u64_workspace(long long n);
+int slm_sort_pairs_u64(void* ws, long long ws_bytes, const unsigned long long* keys_in, unsigned long long* keys_out,
+                       const uint32_t* vals_in, uint32_t* vals_out, long long n, int begin_bit, int end_bit,
+                       cudaStream_t s);
+/* tile binning of the depth-sorted splats (replaces the per-splat bbox walk,
+ * rasterizer.py:253-261, 283-287) */
+int slm_tile_count(const uint32_t* sorted_gid, const unsigned long long* sorted_key, long long G,
+                   const SlmSplat* splats, int tiles_x, int tiles_y, unsigned long long* n_inst, cudaStream_t s);
+int slm_tile_emit(const uint32_t* sorted_gid, const unsigned long long* inst_off, long long G, const SlmSplat* splats,
+                  int tiles_x, int tiles_y, int rank_bits, unsigned long long* keys, uint32_t* vals, cudaStream_t s);
+int slm_tile_ranges(const unsigned long long* keys, long long n, int rank_bits, slm_u2* ranges, int n_tiles,
+                    cudaStream_t s);
+/* render (rasterizer.py:319-358): COUNT pass = image, T_final, per-pixel and
+ * per-(view, gaussian) entry counts; FILL pass = pixel-order cache records
+ * (build_cache, jacobian.py:383-409) and optionally the Traversals arrays */
+int slm_raster_count(const SlmRasterArgs* a, cudaStream_t s);
+int slm_raster_fill(const SlmRasterArgs* a, cudaStream_t s);
+
+/* ---- residuals: compute_residuals (residuals.py:249-296) ----------------- */
+int slm_residuals(const SlmResidArgs* a, int blocks, cudaStream_t s);
+
+/* ---- cache assembly ------------------------------------------------------ */
+long long slm_scan_i64_workspace(long long n);
+int slm_scan_i64(void* ws, long long wsb, const long long* in, long long* out, long long n, cudaStream_t s);
+long long slm_scan_i32_workspace(long long n);
+int slm_scan_i32(void* ws, long long wsb, const int* in, int* out, long long n, cudaStream_t s);
+long long slm_sort_pairs_u32_workspace(long long n);
+int slm_sort_pairs_u32(void* ws, long long wsb, const uint32_t* kin, uint32_t* kout, const uint32_t* vin,
+                       uint32_t* vout, long long n, int begin_bit, int end_bit, cudaStream_t s);
+int slm_iota_u32(uint32_t* out, long long n, cudaStream_t s);
+int slm_px_prepare(const uint32_t* cnt, long long n, long long* cnt64, int* nonempty, cudaStream_t s);
+int slm_px_segments(const uint32_t* cnt, const int* seg_idx, long long n, const SlmCamera* cams_dev, int n_views,
+                    slm_u2* seg_info, cudaStream_t s);
+int slm_pairs_prepare(const int* cnt, int V, long long G, long long* cntT, int* flagT, long long* cntV,
+                      cudaStream_t s);
+int slm_pairs_emit(const int* cnt, int V, long long G, const int* pair_of, const long long* off_of,
+                   const SlmSplat* splats, long long* pair_off, int* pair_gid, uint32_t* pair_vm, SlmPairGeo* geo,
+                   int* pidx, int* gpo, int n_pairs, long long n_entries, cudaStream_t s);
+/* replaces sort_cache_by_gaussians (jacobian.py:93-105) for one view */
+int slm_gauss_scatter(const SlmGaussOrderArgs* a, cudaStream_t s);
+
+/* ---- products --------------------------------------------------------------
+ * apply_j (jacobian.py:419-455) fused with weight_residuals (458-464) when
+ * gradr != NULL; pm holds the per-pair forward chain from slm_pair_forward */
+int slm_apply_j(const SlmWsrStream* pix, const slm_u2* seg_info, const SlmPairGeo* geo, const void* pm,
+                const slm_f4* gradr, slm_f4* u, cudaStream_t s);
+/* apply_jt (jacobian.py:467-483), first half: 9 partials per pair */
+int slm_apply_jt_pairs(const SlmWsrStream* gs, const SlmPairGeo* geo, const uint32_t* pair_vm, const SlmView* views,
+                       const slm_f4* u, float* acc, cudaStream_t s);
+/* diag_jtj (jacobian.py:486-512), first half: 42 moments per pair */
+int slm_diag_pairs(const SlmWsrStream* gs, const SlmPairGeo* geo, const uint32_t* pair_vm, const SlmView* views,
+                   const slm_f4* gradr, float* mom, cudaStream_t s);
+/* forward chain m = dy/dx p per pair; p[a*sa + g*sg] (either layout) */
+int slm_pair_forward(const float* xs, long long G, int sh_degree, const int* pair_gid, const uint32_t* pair_vm,
+                     const SlmCamera* cams, int n_pairs, const float* p, long long sa, long long sg, void* pm,
+                     cudaStream_t s);
+/* backward chain per gaussian, attribute-major out (jacobian.py:314-353):
+ * mode 0 from J^T partials, mode 1 from diag moments; out = scale * chain
+ * (+ lam * max(M, 1e-12) * p and p.out block partials when p != NULL) */
+int slm_backward_blocks(long long G);
+int slm_pair_backward(const float* xs, long long G, int sh_degree, const int* gpo, const uint32_t* pair_vm,
+                      const SlmCamera* cams, const float* acc, int mode, float scale, const float* p,
+                      const float* Mdiag, float lam, float* out, double* dot_part, cudaStream_t s);
+
+/* ---- PCG (Alg. 1; SPEC pcg_solve 391-399) ------------------ */
+int slm_vec_blocks(void);
+int slm_pcg_pupdate(float* p, const float* r, const float* M, const double* st, long long n, cudaStream_t s);
+int slm_pcg_update(int mode, float* x, float* r, const float* p, const float* g, const float* b, const float* M,
+                   double* st, const double* dot_part, int n_dot, double* part, long long n, cudaStream_t s);
+int slm_pcg_finalize(int mode, double* st, const double* part, cudaStream_t s);
+
+/* ---- Eq. 7 combine (SPEC solve_normal_equations_batched 400-408) --------- */
+int slm_combine_acc(float* num, float* den, const float* delta, const float* M, long long n, cudaStream_t s);
+int slm_combine_fin(float* out, const float* num, const float* den, long long n, cudaStream_t s);
+
+/* ---- layouts and helpers ---------------------------------------------------
+ * sort_x / sort_x_inverse (scene.py:79-92) are transposes of the P x G matrix */
+int slm_transpose_f32(const float* in, float* out, long long rows, long long cols, cudaStream_t s);
+int slm_transpose_f64(const double* in, double* out, long long rows, long long cols, cudaStream_t s);
+int slm_f64_to_f32(const double* in, float* out, long long n, cudaStream_t s);
+int slm_axpy_scene(const double* x, const float* d, double gamma, double* out, long long n, cudaStream_t s);
+int slm_sum_parts(const double* part, int n, double* out, cudaStream_t s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPLATLM_B200_H */

@@ -1,0 +1,224 @@
+// PCG vector kernels (Alg. 1), the Eq. 7
+// weighted-mean combine and the sortX layout
+// permutation (ref: scene.py:79-92).
+//
+// Scalars (r^T z, p^T g, alpha, beta, ...) live in a device fp64 state block;
+// every reduction is a fixed-shape fp64 tree, so the solver is bitwise
+// deterministic and needs one 8-byte host read per iteration (exit test).
+#include "slm_common.cuh"
+
+// state layout (double[16])
+#define ST_RZ 0
+#define ST_PG 2
+#define ST_BB 3
+#define ST_RR 4
+#define ST_ALPHA 5
+#define ST_BETA 6
+#define ST_FLAGS 7   // bit0 non-SPD (p^T g <= 0), bit1 converged
+#define ST_ITERS 8
+
+#define VEC_BLOCKS 1184  // 148 SMs x 8, fixed -> deterministic partial shapes
+#define VEC_THREADS 256
+
+__device__ __forceinline__ float mfloor(float m) { return fmaxf(m, 1e-12f); }
+
+// p = r / Mf + beta * p
+__global__ void k_pcg_pupdate(float* __restrict__ p, const float* __restrict__ r, const float* __restrict__ M,
+                              const double* __restrict__ st, long long n) {
+  const float beta = (float)st[ST_BETA];
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = r[i] / mfloor(M[i]) + beta * p[i];
+}
+
+// sum of a block-partials array in a fixed order (every block gets the same bits)
+__device__ double sum_parts(const double* __restrict__ part, int n, double* sm) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
+  double t = block_sum_d(s, sm);
+  __shared__ double bc;
+  if (threadIdx.x == 0) bc = t;
+  __syncthreads();
+  return bc;
+}
+
+// INIT (mode 0): x = p (= x0), r = b - g;   partials: r.r/Mf, r.r, b.b
+// STEP (mode 1): alpha = rz / pg; x += alpha p; r -= alpha g; partials r.r/Mf, r.r
+__global__ void k_pcg_update(int mode, float* __restrict__ x, float* __restrict__ r, const float* __restrict__ p,
+                             const float* __restrict__ g, const float* __restrict__ b, const float* __restrict__ M,
+                             double* __restrict__ st, const double* __restrict__ dot_part, int n_dot,
+                             double* __restrict__ part /*[3][VEC_BLOCKS]*/, long long n) {
+  __shared__ double sm[32];
+  float alpha = 0.f;
+  if (mode == 1) {
+    double pg = sum_parts(dot_part, n_dot, sm);
+    double a = st[ST_RZ] / pg;
+    alpha = (float)a;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st[ST_PG] = pg;
+      st[ST_ALPHA] = a;
+    }
+  }
+  double s_rz = 0.0, s_rr = 0.0, s_bb = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    float ri;
+    if (mode == 0) {
+      x[i] = p[i];
+      ri = b[i] - g[i];
+      s_bb += (double)b[i] * b[i];
+    } else {
+      x[i] += alpha * p[i];
+      ri = r[i] - alpha * g[i];
+    }
+    r[i] = ri;
+    s_rz += (double)ri * ri / (double)mfloor(M[i]);
+    s_rr += (double)ri * ri;
+  }
+  double t;
+  t = block_sum_d(s_rz, sm);
+  if (threadIdx.x == 0) part[blockIdx.x] = t;
+  t = block_sum_d(s_rr, sm);
+  if (threadIdx.x == 0) part[VEC_BLOCKS + blockIdx.x] = t;
+  if (mode == 0) {
+    t = block_sum_d(s_bb, sm);
+    if (threadIdx.x == 0) part[2 * VEC_BLOCKS + blockIdx.x] = t;
+  }
+}
+
+// single block: beta = rz_new / rz, exit flags
+__global__ void k_pcg_finalize(int mode, double* __restrict__ st, const double* __restrict__ part, int nb) {
+  __shared__ double sm[32];
+  double rz = sum_parts(part, nb, sm);
+  double rr = sum_parts(part + VEC_BLOCKS, nb, sm);
+  double bb = mode == 0 ? sum_parts(part + 2 * VEC_BLOCKS, nb, sm) : 0.0;
+  if (threadIdx.x == 0) {
+    double flags = 0.0;
+    if (mode == 0) {
+      st[ST_BB] = bb;
+      st[ST_BETA] = 0.0;
+      st[ST_ITERS] = 0.0;
+    } else {
+      double pg = st[ST_PG];
+      if (!(pg > 0.0)) flags = 1.0;
+      st[ST_BETA] = rz / st[ST_RZ];
+      st[ST_ITERS] += 1.0;
+      if (flags == 0.0 && rr < 0.01 * st[ST_BB]) flags = 2.0;
+    }
+    st[ST_RZ] = rz;
+    st[ST_RR] = rr;
+    st[ST_FLAGS] = flags;
+  }
+}
+
+// Eq. 7: num += M * delta, den += M;  finalize delta = num / max(den, 1e-12)
+__global__ void k_combine_acc(float* __restrict__ num, float* __restrict__ den, const float* __restrict__ delta,
+                              const float* __restrict__ M, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const float m = M[i];
+    num[i] += m * delta[i];
+    den[i] += m;
+  }
+}
+
+__global__ void k_combine_fin(float* __restrict__ out, const float* __restrict__ num, const float* __restrict__ den,
+                              long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = num[i] / fmaxf(den[i], 1e-12f);
+}
+
+// (rows x cols) -> (cols x rows) tiled transpose; sortX is the transpose of
+// the P x G attribute-major matrix (ref: scene.py:79-92)
+template <typename T>
+__global__ void k_transpose(const T* __restrict__ in, T* __restrict__ out, long long rows, long long cols) {
+  __shared__ T tile[32][33];
+  long long c0 = (long long)blockIdx.x * 32, r0 = (long long)blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    long long r = r0 + k, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[k][threadIdx.x] = in[r * cols + c];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    long long c = c0 + k, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][k];
+  }
+}
+
+__global__ void k_f64_to_f32(const double* __restrict__ in, float* __restrict__ out, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = (float)in[i];
+}
+
+// x_out = x + gamma * delta (fp64 scene, fp32 direction) -- line search / step
+__global__ void k_axpy_scene(const double* __restrict__ x, const float* __restrict__ d, double gamma,
+                             double* __restrict__ out, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = x[i] + gamma * (double)d[i];
+}
+
+__global__ void k_sum_parts(const double* __restrict__ part, int n, double* __restrict__ out) {
+  __shared__ double sm[32];
+  double t = sum_parts(part, n, sm);
+  if (threadIdx.x == 0) *out = t;
+}
+
+extern "C" {
+
+int slm_vec_blocks() { return VEC_BLOCKS; }
+
+int slm_pcg_pupdate(float* p, const float* r, const float* M, const double* st, long long n, cudaStream_t s) {
+  k_pcg_pupdate<<<VEC_BLOCKS, VEC_THREADS, 0, s>>>(p, r, M, st, n);
+  return slm_cuda_status();
+}
+
+int slm_pcg_update(int mode, float* x, float* r, const float* p, const float* g, const float* b, const float* M,
+                   double* st, const double* dot_part, int n_dot, double* part, long long n, cudaStream_t s) {
+  k_pcg_update<<<VEC_BLOCKS, VEC_THREADS, 0, s>>>(mode, x, r, p, g, b, M, st, dot_part, n_dot, part, n);
+  return slm_cuda_status();
+}
+
+int slm_pcg_finalize(int mode, double* st, const double* part, cudaStream_t s) {
+  k_pcg_finalize<<<1, 1024, 0, s>>>(mode, st, part, VEC_BLOCKS);
+  return slm_cuda_status();
+}
+
+int slm_combine_acc(float* num, float* den, const float* delta, const float* M, long long n, cudaStream_t s) {
+  k_combine_acc<<<VEC_BLOCKS, VEC_THREADS, 0, s>>>(num, den, delta, M, n);
+  return slm_cuda_status();
+}
+
+int slm_combine_fin(float* out, const float* num, const float* den, long long n, cudaStream_t s) {
+  k_combine_fin<<<VEC_BLOCKS, VEC_THREADS, 0, s>>>(out, num, den, n);
+  return slm_cuda_status();
+}
+
+int slm_transpose_f32(const float* in, float* out, long long rows, long long cols, cudaStream_t s) {
+  if (rows <= 0 || cols <= 0) return SLM_OK;
+  dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+  if (grid.y > 65535) return SLM_ERR_SIZE;
+  k_transpose<float><<<grid, dim3(32, 8), 0, s>>>(in, out, rows, cols);
+  return slm_cuda_status();
+}
+
+int slm_transpose_f64(const double* in, double* out, long long rows, long long cols, cudaStream_t s) {
+  if (rows <= 0 || cols <= 0) return SLM_OK;
+  dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+  if (grid.y > 65535) return SLM_ERR_SIZE;
+  k_transpose<double><<<grid, dim3(32, 8), 0, s>>>(in, out, rows, cols);
+  return slm_cuda_status();
+}
+
+int slm_f64_to_f32(const double* in, float* out, long long n, cudaStream_t s) {
+  k_f64_to_f32<<<VEC_BLOCKS, VEC_THREADS, 0, s>>>(in, out, n);
+  return slm_cuda_status();
+}
+
+int slm_axpy_scene(const double* x, const float* d, double gamma, double* out, long long n, cudaStream_t s) {
+  k_axpy_scene<<<VEC_BLOCKS, VEC_THREADS, 0, s>>>(x, d, gamma, out, n);
+  return slm_cuda_status();
+}
+
+int slm_sum_parts(const double* part, int n, double* out, cudaStream_t s) {
+  k_sum_parts<<<1, 1024, 0, s>>>(part, n, out);
+  return slm_cuda_status();
+}
+
+}  // extern "C"

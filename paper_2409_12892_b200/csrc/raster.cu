@@ -1,0 +1,396 @@
+// fp64 projection, depth order, tile binning and the two-pass tile rasteriser
+// that emits the gradient cache (the forward half of buildCache_p1).
+//
+// Parity contract: every discrete decision (valid mask, bbox, (depth, gid)
+// order, alpha >= alpha_min, T >= t_stop, alpha clamp) is taken in fp64 with
+// the reference's operation order (ref: rasterizer.py:116-165, 253-316), so
+// cache indexing matches the CPU reference bit for bit.
+#include "slm_common.cuh"
+
+#include <cub/cub.cuh>
+
+// ---------------------------------------------------------------------------
+// projection (ref: rasterizer.py:78-165)
+// ---------------------------------------------------------------------------
+template <int K>
+__global__ void k_preprocess(const double* __restrict__ x, long long G, SlmCamera cam, SlmRastCfg cfg,
+                             SlmSplat* __restrict__ out, unsigned long long* __restrict__ depth_key,
+                             uint32_t* __restrict__ order_val, int* __restrict__ err) {
+  long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; g < G; g += (long long)gridDim.x * blockDim.x) {
+    double p0 = x[g], p1 = x[G + g], p2 = x[2 * G + g];
+    double qw = x[3 * G + g], qx = x[4 * G + g], qy = x[5 * G + g], qz = x[6 * G + g];
+    double l0 = x[7 * G + g], l1 = x[8 * G + g], l2 = x[9 * G + g];
+    double logit = x[10 * G + g];
+    bool finite = isfinite(p0) && isfinite(p1) && isfinite(p2) && isfinite(qw) && isfinite(qx) &&
+                  isfinite(qy) && isfinite(qz) && isfinite(l0) && isfinite(l1) && isfinite(l2) &&
+                  isfinite(logit);
+    for (int a = 11; a < 11 + 3 * K; ++a) finite = finite && isfinite(x[(long long)a * G + g]);
+    if (!finite) atomicOr(err, 1);
+
+    const double* R = cam.R;
+    // cam_points = positions @ R^T + t
+    double X0 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(p0, R[0]), __dmul_rn(p1, R[1])), __dmul_rn(p2, R[2])), cam.t[0]);
+    double X1 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(p0, R[3]), __dmul_rn(p1, R[4])), __dmul_rn(p2, R[5])), cam.t[1]);
+    double X2 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(p0, R[6]), __dmul_rn(p1, R[7])), __dmul_rn(p2, R[8])), cam.t[2]);
+    bool valid = X2 > cfg.z_near;
+    double zz = valid ? X2 : 1.0;
+    double mx = __dadd_rn(__ddiv_rn(__dmul_rn(cam.fx, X0), zz), cam.cx);
+    double my = __dadd_rn(__ddiv_rn(__dmul_rn(cam.fy, X1), zz), cam.cy);
+
+    double qn = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+    if (qn < 1e-12) atomicOr(err, 2);
+    double w = qw / qn, a = qx / qn, b = qy / qn, c = qz / qn;
+    double Rg[9] = {1 - 2 * (b * b + c * c), 2 * (a * b - w * c), 2 * (a * c + w * b),
+                    2 * (a * b + w * c), 1 - 2 * (a * a + c * c), 2 * (b * c - w * a),
+                    2 * (a * c - w * b), 2 * (b * c + w * a), 1 - 2 * (a * a + b * b)};
+    double s2[3] = {exp(2.0 * l0), exp(2.0 * l1), exp(2.0 * l2)};
+    // world covariance R diag(s^2) R^T
+    double Sw[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        Sw[i * 3 + k] = Rg[i * 3 + 0] * s2[0] * Rg[k * 3 + 0] + Rg[i * 3 + 1] * s2[1] * Rg[k * 3 + 1] +
+                        Rg[i * 3 + 2] * s2[2] * Rg[k * 3 + 2];
+    // camera covariance R Sw R^T
+    double T1[9], Sc[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        T1[i * 3 + k] = R[i * 3 + 0] * Sw[0 * 3 + k] + R[i * 3 + 1] * Sw[1 * 3 + k] + R[i * 3 + 2] * Sw[2 * 3 + k];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        Sc[i * 3 + k] = T1[i * 3 + 0] * R[k * 3 + 0] + T1[i * 3 + 1] * R[k * 3 + 1] + T1[i * 3 + 2] * R[k * 3 + 2];
+    double Xs0 = valid ? X0 : 0.0, Xs1 = valid ? X1 : 0.0, Xs2 = valid ? X2 : 1.0;
+    double iz = 1.0 / Xs2;
+    double A00 = cam.fx * iz, A02 = -cam.fx * Xs0 * iz * iz;
+    double A11 = cam.fy * iz, A12 = -cam.fy * Xs1 * iz * iz;
+    // cov2 = A Sc A^T (A has zeros at (0,1), (1,0))
+    double r00 = A00 * Sc[0] + A02 * Sc[6], r01 = A00 * Sc[1] + A02 * Sc[7], r02 = A00 * Sc[2] + A02 * Sc[8];
+    double r11 = A11 * Sc[4] + A12 * Sc[7], r12 = A11 * Sc[5] + A12 * Sc[8], r10 = A11 * Sc[3] + A12 * Sc[6];
+    double c00 = r00 * A00 + r02 * A02;
+    double c01 = r01 * A11 + r02 * A12;
+    double c11 = r11 * A11 + r12 * A12;
+    (void)r10;
+    double va = c00 + cfg.cov_eps, vb = c01, vc = c11 + cfg.cov_eps;
+    double det = va * vc - vb * vb;
+    valid = valid && (det > 0.0);
+    double detu = det > 0.0 ? det : 1.0;
+    double ca = vc / detu, cb = -vb / detu, cc = va / detu;
+
+    // view-dependent colour
+    double v0 = p0 - cam.C[0], v1 = p1 - cam.C[1], v2 = p2 - cam.C[2];
+    double vn = sqrt(v0 * v0 + v1 * v1 + v2 * v2);
+    double d0 = v0 / vn, d1 = v1 / vn, d2 = v2 / vn;
+    double Y[16];
+    sh_basis<double, K>(d0, d1, d2, Y);
+    double col[3];
+    unsigned clampbits = 0;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      double raw = 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) raw += x[(long long)(11 + ch * K + k) * G + g] * Y[k];
+      raw += 0.5;
+      col[ch] = raw > 0.0 ? raw : 0.0;
+      if (raw <= 0.0) clampbits |= (1u << (1 + ch));
+    }
+    double lam = 0.5 * (va + vc) + sqrt(0.25 * (va - vc) * (va - vc) + vb * vb);
+    if (cfg.cull_sigma > 0.0) {
+      double rad = cfg.cull_sigma * sqrt(lam);
+      valid = valid && (mx + rad > 0.0) && (mx - rad < (double)cam.W) && (my + rad > 0.0) &&
+              (my - rad < (double)cam.H);
+    }
+    double o = 1.0 / (1.0 + exp(-logit));
+    int x0 = 0, x1 = cam.W - 1, y0 = 0, y1 = cam.H - 1;
+    if (cfg.reach_fac > 0.0) {
+      double reach = cfg.reach_fac * sqrt(lam);
+      double fx0 = ceil(mx - reach - 0.5), fx1 = floor(mx + reach - 0.5);
+      double fy0 = ceil(my - reach - 0.5), fy1 = floor(my + reach - 0.5);
+      x0 = fx0 > 0.0 ? (fx0 < 1e9 ? (int)fx0 : 1000000000) : 0;
+      y0 = fy0 > 0.0 ? (fy0 < 1e9 ? (int)fy0 : 1000000000) : 0;
+      x1 = fx1 < (double)(cam.W - 1) ? (fx1 > -1e9 ? (int)fx1 : -1000000000) : cam.W - 1;
+      y1 = fy1 < (double)(cam.H - 1) ? (fy1 > -1e9 ? (int)fy1 : -1000000000) : cam.H - 1;
+    }
+    if (!finite) valid = false;
+    SlmSplat s;
+    s.mx = mx; s.my = my; s.ca = ca; s.cb = cb; s.cc = cc; s.o = o;
+    s.c0 = col[0]; s.c1 = col[1]; s.c2 = col[2];
+    s.x0 = x0; s.x1 = x1; s.y0 = y0; s.y1 = y1;
+    s.flags = (valid ? SLM_FLAG_VALID : 0u) | clampbits;
+    s.pad = 0;
+    out[g] = s;
+    depth_key[g] = valid ? (unsigned long long)__double_as_longlong(X2) : ~0ull;
+    order_val[g] = (uint32_t)g;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// tile binning: instances (tile, depth rank) -> gid, sorted by tile then rank
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool splat_tiles(const SlmSplat& s, int tiles_x, int tiles_y, int& tx0, int& tx1,
+                                            int& ty0, int& ty1) {
+  if (!(s.flags & SLM_FLAG_VALID) || s.x0 > s.x1 || s.y0 > s.y1) return false;
+  tx0 = s.x0 / SLM_TILE; tx1 = s.x1 / SLM_TILE;
+  ty0 = s.y0 / SLM_TILE; ty1 = s.y1 / SLM_TILE;
+  if (tx1 >= tiles_x) tx1 = tiles_x - 1;
+  if (ty1 >= tiles_y) ty1 = tiles_y - 1;
+  return tx0 <= tx1 && ty0 <= ty1;
+}
+
+__global__ void k_tile_count(const uint32_t* __restrict__ sorted_gid, const unsigned long long* __restrict__ sorted_key,
+                             long long G, const SlmSplat* __restrict__ splats, int tiles_x, int tiles_y,
+                             unsigned long long* __restrict__ n_inst) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; i < G; i += (long long)gridDim.x * blockDim.x) {
+    unsigned long long n = 0;
+    if (sorted_key[i] != ~0ull) {
+      int tx0, tx1, ty0, ty1;
+      if (splat_tiles(splats[sorted_gid[i]], tiles_x, tiles_y, tx0, tx1, ty0, ty1))
+        n = (unsigned long long)(tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+    }
+    n_inst[i] = n;
+  }
+}
+
+__global__ void k_tile_emit(const uint32_t* __restrict__ sorted_gid, const unsigned long long* __restrict__ inst_off,
+                            long long G, const SlmSplat* __restrict__ splats, int tiles_x, int tiles_y,
+                            int rank_bits, unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; i < G; i += (long long)gridDim.x * blockDim.x) {
+    unsigned long long beg = inst_off[i], end = inst_off[i + 1];
+    if (beg == end) continue;
+    uint32_t g = sorted_gid[i];
+    int tx0, tx1, ty0, ty1;
+    splat_tiles(splats[g], tiles_x, tiles_y, tx0, tx1, ty0, ty1);
+    unsigned long long k = beg;
+    for (int ty = ty0; ty <= ty1; ++ty)
+      for (int tx = tx0; tx <= tx1; ++tx) {
+        keys[k] = ((unsigned long long)(ty * tiles_x + tx) << rank_bits) | (unsigned long long)i;
+        vals[k] = g;
+        ++k;
+      }
+  }
+}
+
+__global__ void k_tile_ranges(const unsigned long long* __restrict__ keys, long long n, int rank_bits,
+                              uint2* __restrict__ ranges) {
+  long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; j < n; j += (long long)gridDim.x * blockDim.x) {
+    unsigned t = (unsigned)(keys[j] >> rank_bits);
+    if (j == 0 || (unsigned)(keys[j - 1] >> rank_bits) != t) ranges[t].x = (unsigned)j;
+    if (j == n - 1 || (unsigned)(keys[j + 1] >> rank_bits) != t) ranges[t].y = (unsigned)(j + 1);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// tile rasteriser (ref: rasterizer.py:264-316), one 16x16 tile per CTA,
+// one pixel per thread, splats staged in shared memory in batches.
+//   COUNT pass: per-pixel entry count, rendered colour, T_final, and the
+//               per-(view, gaussian) entry counts (warp-aggregated atomics).
+//   FILL pass : writes the pixel-order cache records; dc/dalpha uses the
+//               per-pixel colour total from the COUNT pass (ref: jacobian.py:391-399).
+// ---------------------------------------------------------------------------
+typedef SlmRasterArgs RasterArgs;
+
+#define RB 256
+template <bool FILL>
+__global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
+  __shared__ double s_mx[RB], s_my[RB], s_ca[RB], s_cb[RB], s_cc[RB], s_o[RB];
+  __shared__ double s_c0[RB], s_c1[RB], s_c2[RB];
+  __shared__ int4 s_box[RB];
+  __shared__ uint32_t s_gid[RB];
+
+  const int tiles_x = A.tiles_x;
+  const int tile = blockIdx.x;
+  const int tx = tile % tiles_x, ty = tile / tiles_x;
+  const int lx = threadIdx.x % SLM_TILE, ly = threadIdx.x / SLM_TILE;
+  const int px = tx * SLM_TILE + lx, py = ty * SLM_TILE + ly;
+  const bool inside = px < A.W && py < A.H;
+  const int pix = py * A.W + px;
+  const uint2 rng = A.tile_range[tile];
+  const double dxp = (double)px + 0.5, dyp = (double)py + 0.5;
+  const double amin = A.cfg.alpha_min, tstop = A.cfg.t_stop, aclamp = A.cfg.alpha_clamp;
+  const int lane = threadIdx.x & 31;
+
+  double T = 1.0, C0 = 0.0, C1 = 0.0, C2 = 0.0;
+  uint32_t cnt = 0;
+  bool done = !inside;
+  long long e = 0;
+  double tot0 = 0, tot1 = 0, tot2 = 0;
+  int seg = 0;
+  if (FILL && inside) {
+    e = A.pix_off[A.pix_base + pix];
+    tot0 = A.rgb[(size_t)pix * 3 + 0];
+    tot1 = A.rgb[(size_t)pix * 3 + 1];
+    tot2 = A.rgb[(size_t)pix * 3 + 2];
+    done = A.pix_off[A.pix_base + pix + 1] == e;
+    if (!done && A.seg_idx) seg = A.seg_idx[A.pix_base + pix];
+  }
+
+  for (unsigned base = rng.x; base < rng.y; base += RB) {
+    if (__syncthreads_and(done)) break;
+    unsigned j = base + threadIdx.x;
+    if (j < rng.y) {
+      uint32_t g = A.inst_gid[j];
+      const SlmSplat s = A.splats[g];
+      s_mx[threadIdx.x] = s.mx; s_my[threadIdx.x] = s.my;
+      s_ca[threadIdx.x] = s.ca; s_cb[threadIdx.x] = s.cb; s_cc[threadIdx.x] = s.cc;
+      s_o[threadIdx.x] = s.o;
+      s_c0[threadIdx.x] = s.c0; s_c1[threadIdx.x] = s.c1; s_c2[threadIdx.x] = s.c2;
+      s_box[threadIdx.x] = make_int4(s.x0, s.x1, s.y0, s.y1);
+      s_gid[threadIdx.x] = g;
+    }
+    __syncthreads();
+    const int nb = min((unsigned)RB, rng.y - base);
+    for (int k = 0; k < nb; ++k) {
+      bool keep = false;
+      double a = 0.0;
+      const int4 bx = s_box[k];
+      if (!done && px >= bx.x && px <= bx.y && py >= bx.z && py <= bx.w) {
+        // -(1/2) d^T conic d in the reference's evaluation order
+        double dx = __dsub_rn(dxp, s_mx[k]);
+        double dy = __dsub_rn(dyp, s_my[k]);
+        double q = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(s_ca[k], dx), dx), __dmul_rn(s_cc[k], __dmul_rn(dy, dy))),
+                             __dmul_rn(__dmul_rn(__dmul_rn(2.0, s_cb[k]), dy), dx));
+        a = __dmul_rn(s_o[k], exp(__dmul_rn(-0.5, q)));
+        a = a < aclamp ? a : aclamp;
+        keep = (a >= amin) && (a > 0.0) && (T >= tstop);
+      }
+      if (keep) {
+        const double wgt = __dmul_rn(a, T);
+        C0 = __dadd_rn(C0, __dmul_rn(wgt, s_c0[k]));
+        C1 = __dadd_rn(C1, __dmul_rn(wgt, s_c1[k]));
+        C2 = __dadd_rn(C2, __dmul_rn(wgt, s_c2[k]));
+        if (FILL && A.rec_idx) {
+          const uint32_t g = s_gid[k];
+          const double om = 1.0 - a;
+          const float d0 = (float)(s_c0[k] * T - (tot0 - C0) / om);
+          const float d1 = (float)(s_c1[k] * T - (tot1 - C1) / om);
+          const float d2 = (float)(s_c2[k] * T - (tot2 - C2) / om);
+          const uint32_t q = (uint32_t)A.pidx[g];
+          A.rec_idx[e] = q | (cnt == 0 ? SLM_HEAD : 0u);
+          A.rec_ae[e] = a < aclamp ? (float)a : 0.0f;
+          A.rec_at[e] = (float)wgt;
+          A.rec_d0[e] = d0;
+          A.rec_d1[e] = d1;
+          A.rec_d2[e] = d2;
+          const long long le = e - A.view_entry_base;
+          if (A.ent_gid) A.ent_gid[le] = g;
+          if (A.ent_xy) A.ent_xy[le] = ((uint32_t)py << 16) | (uint32_t)px;
+          if (A.chunk_seg && (e & (SLM_CHUNK - 1)) == 0) A.chunk_seg[e / SLM_CHUNK] = seg;
+        }
+        if (FILL) {
+          if (A.trav_gid) {
+            const long long le = e - A.view_entry_base;
+            A.trav_gid[le] = s_gid[k];
+            A.trav_alpha[le] = a;
+            A.trav_T[le] = T;
+          }
+          ++e;
+        }
+        T = __dmul_rn(T, 1.0 - a);
+        ++cnt;
+        if (T < tstop) done = true;  // no later splat can pass T >= t_stop
+      }
+      if (!FILL) {
+        unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (m && lane == __ffs(m) - 1) atomicAdd(&A.pair_cnt[s_gid[k]], __popc(m));
+      }
+    }
+    __syncthreads();
+  }
+  if (!FILL && inside) {
+    A.px_count[pix] = cnt;
+    A.rgb[(size_t)pix * 3 + 0] = __dadd_rn(C0, __dmul_rn(A.cfg.bg[0], T));
+    A.rgb[(size_t)pix * 3 + 1] = __dadd_rn(C1, __dmul_rn(A.cfg.bg[1], T));
+    A.rgb[(size_t)pix * 3 + 2] = __dadd_rn(C2, __dmul_rn(A.cfg.bg[2], T));
+    A.t_final[pix] = T;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// C-ABI entry points
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int slm_preprocess(const double* x, long long G, int sh_degree, const SlmCamera* cam, const SlmRastCfg* cfg,
+                   SlmSplat* out, unsigned long long* depth_key, uint32_t* order_val, int* err,
+                   cudaStream_t stream) {
+  if (G <= 0 || !x || !cam || !cfg || !out) return SLM_ERR_ARG;
+  unsigned blocks = slm_blocks(G, 256);
+  switch (sh_degree) {
+    case 0: k_preprocess<1><<<blocks, 256, 0, stream>>>(x, G, *cam, *cfg, out, depth_key, order_val, err); break;
+    case 1: k_preprocess<4><<<blocks, 256, 0, stream>>>(x, G, *cam, *cfg, out, depth_key, order_val, err); break;
+    case 2: k_preprocess<9><<<blocks, 256, 0, stream>>>(x, G, *cam, *cfg, out, depth_key, order_val, err); break;
+    case 3: k_preprocess<16><<<blocks, 256, 0, stream>>>(x, G, *cam, *cfg, out, depth_key, order_val, err); break;
+    default: return SLM_ERR_ARG;
+  }
+  return slm_cuda_status();
+}
+
+// stable (depth, gid) order of the valid splats: CUB radix sort over the
+// fp64 depth bit patterns (positive doubles order like their bits)
+long long slm_sort_pairs_u64_workspace(long long n) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const unsigned long long*)nullptr,
+                                  (unsigned long long*)nullptr, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (int)n);
+  return (long long)bytes;
+}
+
+int slm_sort_pairs_u64(void* ws, long long ws_bytes, const unsigned long long* keys_in, unsigned long long* keys_out,
+                       const uint32_t* vals_in, uint32_t* vals_out, long long n, int begin_bit, int end_bit,
+                       cudaStream_t stream) {
+  if (n <= 0) return SLM_OK;
+  if (n > 0x7fffffffLL) return SLM_ERR_SIZE;
+  size_t bytes = (size_t)ws_bytes;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(ws, bytes, keys_in, keys_out, vals_in, vals_out, (int)n,
+                                                  begin_bit, end_bit, stream);
+  return e == cudaSuccess ? SLM_OK : SLM_ERR_CUDA;
+}
+
+int slm_tile_count(const uint32_t* sorted_gid, const unsigned long long* sorted_key, long long G,
+                   const SlmSplat* splats, int tiles_x, int tiles_y, unsigned long long* n_inst,
+                   cudaStream_t stream) {
+  k_tile_count<<<slm_blocks(G, 256), 256, 0, stream>>>(sorted_gid, sorted_key, G, splats, tiles_x, tiles_y, n_inst);
+  return slm_cuda_status();
+}
+
+int slm_tile_emit(const uint32_t* sorted_gid, const unsigned long long* inst_off, long long G, const SlmSplat* splats,
+                  int tiles_x, int tiles_y, int rank_bits, unsigned long long* keys, uint32_t* vals,
+                  cudaStream_t stream) {
+  k_tile_emit<<<slm_blocks(G, 256), 256, 0, stream>>>(sorted_gid, inst_off, G, splats, tiles_x, tiles_y, rank_bits,
+                                                       keys, vals);
+  return slm_cuda_status();
+}
+
+int slm_tile_ranges(const unsigned long long* keys, long long n, int rank_bits, uint2* ranges, int n_tiles,
+                    cudaStream_t stream) {
+  cudaMemsetAsync(ranges, 0, sizeof(uint2) * (size_t)n_tiles, stream);
+  if (n > 0) k_tile_ranges<<<slm_blocks(n, 256), 256, 0, stream>>>(keys, n, rank_bits, ranges);
+  return slm_cuda_status();
+}
+
+int slm_raster_count(const RasterArgs* a, cudaStream_t stream) {
+  int tiles_y = (a->H + SLM_TILE - 1) / SLM_TILE;
+  k_raster<false><<<a->tiles_x * tiles_y, RB, 0, stream>>>(*a);
+  return slm_cuda_status();
+}
+
+int slm_raster_fill(const RasterArgs* a, cudaStream_t stream) {
+  int tiles_y = (a->H + SLM_TILE - 1) / SLM_TILE;
+  k_raster<true><<<a->tiles_x * tiles_y, RB, 0, stream>>>(*a);
+  return slm_cuda_status();
+}
+
+int slm_raster_args_size() { return (int)sizeof(RasterArgs); }
+int slm_camera_size() { return (int)sizeof(SlmCamera); }
+int slm_rastcfg_size() { return (int)sizeof(SlmRastCfg); }
+int slm_splat_size() { return (int)sizeof(SlmSplat); }
+
+}  // extern "C"

@@ -1,0 +1,211 @@
+"""PCG inner solver, Eq. 7 combine and the LM direction (SPEC-only in the
+reference: pcg_solve SPEC:391-399, solve_normal_equations_batched SPEC:400-408;
+Alg. 1; Eq. 7).
+
+All vectors are attribute-major float32 device tensors; scalars stay on the
+device (one 8-byte read per iteration for the exit test).  Multi-GPU: image
+subsets are sharded round-robin over ranks; each rank accumulates
+num = sum M_i * Delta_i and den = sum M_i, then ONE all_reduce(SUM) of the
+packed [num; den] over NCCL combines them.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib
+from ._lib import call, ptr, stream_ptr
+from .engine import CacheSet, LossConfig
+from .errors import NonSPDError
+from .scene import Layout, ParamVector
+
+ST_RZ, ST_PG, ST_BB, ST_RR, ST_ALPHA, ST_BETA, ST_FLAGS, ST_ITERS = 0, 2, 3, 4, 5, 6, 7, 8
+
+
+@dataclass(frozen=True)
+class BatchSchedule:
+    """ref SPEC:379-380 (BatchSchedule); strided selection SPEC:477."""
+    n_batches: int = 1
+    selection: str = "strided"
+
+    def batches(self, n_views: int) -> list[list[int]]:
+        if self.n_batches < 1:
+            raise ValueError("n_b must be >= 1")
+        return [list(range(j, n_views, self.n_batches)) for j in range(self.n_batches)]
+
+
+@dataclass
+class PCGWorkspace:
+    """x, r, p, g vectors + device scalar block (SPEC PCGWorkspace)."""
+    n: int
+    device: torch.device
+    x: torch.Tensor = field(init=False)
+    r: torch.Tensor = field(init=False)
+    p: torch.Tensor = field(init=False)
+    g: torch.Tensor = field(init=False)
+    st: torch.Tensor = field(init=False)
+    part: torch.Tensor = field(init=False)
+
+    def __post_init__(self):
+        f = torch.float32
+        self.x = torch.empty(self.n, dtype=f, device=self.device)
+        self.r = torch.empty(self.n, dtype=f, device=self.device)
+        self.p = torch.empty(self.n, dtype=f, device=self.device)
+        self.g = torch.empty(self.n, dtype=f, device=self.device)
+        self.st = torch.zeros(16, dtype=torch.float64, device=self.device)
+        self.part = torch.zeros(3 * _lib.load().slm_vec_blocks(), dtype=torch.float64, device=self.device)
+
+
+def pcg_run(cache: CacheSet, b: torch.Tensor, M: torch.Tensor, lam: float, max_iters: int,
+            ws: PCGWorkspace | None = None, stats: dict | None = None, timer=None) -> torch.Tensor:
+    """Alg. 1 on the device; returns x (attribute-major fp32, owned by ws).
+
+    Raises NonSPDError when p^T g <= 0."""
+    n = b.numel()
+    ws = ws or PCGWorkspace(n, b.device)
+    nb = _lib.load().slm_backward_blocks(cache.G)
+    dot_part = torch.zeros(nb, dtype=torch.float64, device=b.device)
+    s = stream_ptr()
+    ws.st.zero_()
+    ws.p.zero_()
+    # p := b / Mf  (= x0, Alg. 1 line 4); g0 = A x0
+    call("slm_pcg_pupdate", ptr(ws.p), ptr(b), ptr(M), ptr(ws.st), n, s)
+    _product(cache, ws.p, ws.g, lam, M, dot_part, timer)
+    call("slm_pcg_update", 0, ptr(ws.x), ptr(ws.r), ptr(ws.p), ptr(ws.g), ptr(b), ptr(M), ptr(ws.st),
+         ptr(dot_part), nb, ptr(ws.part), n, s)
+    call("slm_pcg_finalize", 0, ptr(ws.st), ptr(ws.part), s)
+    products = 1
+    bb = float(ws.st[ST_BB].item())
+    iters = 0
+    if bb > 0.0:
+        for _ in range(max_iters):
+            call("slm_pcg_pupdate", ptr(ws.p), ptr(ws.r), ptr(M), ptr(ws.st), n, s)
+            _product(cache, ws.p, ws.g, lam, M, dot_part, timer)
+            products += 1
+            call("slm_pcg_update", 1, ptr(ws.x), ptr(ws.r), ptr(ws.p), ptr(ws.g), ptr(b), ptr(M), ptr(ws.st),
+                 ptr(dot_part), nb, ptr(ws.part), n, s)
+            call("slm_pcg_finalize", 1, ptr(ws.st), ptr(ws.part), s)
+            iters += 1
+            flags = int(ws.st[ST_FLAGS].item())
+            if flags & 1:
+                raise NonSPDError(f"p^T g = {float(ws.st[ST_PG].item())} <= 0 at PCG iteration {iters}")
+            if flags & 2:
+                break
+    if stats is not None:
+        stats["products"] = products
+        stats["iterations"] = iters
+        stats["rr"] = float(ws.st[ST_RR].item())
+        stats["bb"] = bb
+    return ws.x
+
+
+def _product(cache, p, g, lam, M, dot_part, timer):
+    if timer is None:
+        cache.jtwj(p, g, lam, M, dot_part)
+    else:
+        with timer:
+            cache.jtwj(p, g, lam, M, dot_part)
+
+
+def pcg_solve(scene, cache, b: ParamVector, M_diag: ParamVector, lambda_reg: float, max_iters: int,
+              stats: dict | None = None) -> ParamVector:
+    """SPEC:391-399 signature. cache: CacheSet or jacobian.GradientCache."""
+    cs = getattr(cache, "cacheset", cache)
+    b.require_layout(Layout.ATTRIBUTE_MAJOR)
+    M_diag.require_layout(Layout.ATTRIBUTE_MAJOR)
+    bv = b.values.float().contiguous()
+    Mv = M_diag.values.float().contiguous()
+    x = pcg_run(cs, bv, Mv, float(lambda_reg), int(max_iters), stats=stats)
+    return ParamVector(x.clone(), Layout.ATTRIBUTE_MAJOR, scene.num_gaussians, scene.params_per_gaussian)
+
+
+class Combiner:
+    """Eq. 7 accumulator: num += M * Delta, den += M; finalize num / max(den, 1e-12)."""
+
+    def __init__(self, n: int, device):
+        self.buf = torch.zeros(2 * n, dtype=torch.float32, device=device)
+        self.n = n
+        self.accepted = 0
+
+    @property
+    def num(self):
+        return self.buf[: self.n]
+
+    @property
+    def den(self):
+        return self.buf[self.n:]
+
+    def add(self, delta: torch.Tensor, M: torch.Tensor):
+        call("slm_combine_acc", ptr(self.num), ptr(self.den), ptr(delta), ptr(M), self.n, stream_ptr())
+        self.accepted += 1
+
+    def allreduce(self, group=None):
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+            dist.all_reduce(self.buf, op=dist.ReduceOp.SUM, group=group)
+            acc = torch.tensor([self.accepted], dtype=torch.int64, device=self.buf.device)
+            dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
+            self.accepted = int(acc.item())
+
+    def finalize(self) -> torch.Tensor:
+        out = torch.empty(self.n, dtype=torch.float32, device=self.buf.device)
+        call("slm_combine_fin", ptr(out), ptr(self.num), ptr(self.den), self.n, stream_ptr())
+        return out
+
+
+@dataclass
+class StepReport:
+    delta: torch.Tensor
+    energy: float
+    batches_accepted: int
+    entries: list
+    pcg: list
+    product_ms: list
+
+
+def lm_direction(scene, cameras, gts, schedule: BatchSchedule = BatchSchedule(), lambda_reg: float = 1e-4,
+                 n_iters: int = 8, config=None, loss: LossConfig = LossConfig(), rank: int = 0,
+                 world_size: int = 1, product_timer=None, keep_caches: bool = False) -> StepReport:
+    """One LM update direction: per subset cache build, b, M, PCG, Eq. 7
+    combine; subsets are sharded round-robin over ranks."""
+    n = scene.param_count
+    comb = Combiner(n, scene.device)
+    ws = PCGWorkspace(n, scene.device)
+    energy = 0.0
+    entries, pcg_stats = [], []
+    caches = []
+    for j, views in enumerate(schedule.batches(len(cameras))):
+        if j % world_size != rank or not views:
+            continue
+        cs = CacheSet(scene, [cameras[i] for i in views], [gts[i] for i in views], config, loss)
+        energy += sum(cs.energies)
+        entries.append(cs.E)
+        b = cs.rhs()
+        M = cs.diag()
+        st = {}
+        try:
+            d = pcg_run(cs, b, M, lambda_reg, n_iters, ws, stats=st, timer=product_timer)
+        except NonSPDError:
+            pcg_stats.append({"rejected": True})
+            continue
+        pcg_stats.append(st)
+        comb.add(d, M)
+        if keep_caches:
+            caches.append(cs)
+        del cs
+    comb.allreduce()
+    if comb.accepted == 0:
+        raise NonSPDError("all batches rejected by PCG failure")
+    rep = StepReport(comb.finalize(), energy, comb.accepted, entries, pcg_stats, [])
+    rep.caches = caches
+    return rep
+
+
+def solve_normal_equations_batched(scene, dataset, schedule: BatchSchedule, lambda_reg: float, n_iters: int = 8,
+                                   config=None, loss: LossConfig = LossConfig()) -> ParamVector:
+    """SPEC:400-408; dataset = (cameras, gt images)."""
+    cameras, gts = dataset
+    rep = lm_direction(scene, cameras, gts, schedule, lambda_reg, n_iters, config, loss)
+    return ParamVector(rep.delta, Layout.ATTRIBUTE_MAJOR, scene.num_gaussians, scene.params_per_gaussian)
