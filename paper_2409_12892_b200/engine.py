@@ -103,6 +103,31 @@ def ssim_host_tables(H, W, window, sigma):
     return k, cw(H), cw(W)
 
 
+class PhaseTimer:
+    """CUDA-event phase accounting on the current stream: tick(name) charges the
+    time since the previous tick to `name`."""
+
+    def __init__(self):
+        self.events = []
+
+    def tick(self, name):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(torch.cuda.current_stream())
+        self.events.append((name, e))
+
+    def summary(self) -> dict:
+        torch.cuda.synchronize()
+        out = {}
+        for (_, a), (name, b) in zip(self.events, self.events[1:]):
+            out[name] = out.get(name, 0.0) + a.elapsed_time(b)
+        return out
+
+
+class _NoTimer:
+    def tick(self, name):
+        pass
+
+
 class ViewFrame:
     """Per-view products of the COUNT phase (splats, tile lists, image)."""
 
@@ -235,7 +260,7 @@ class CacheSet:
     """
 
     def __init__(self, scene: GaussianScene, cameras: list[Camera], gts=None, config=None, loss=LossConfig(),
-                 keep_source_index: bool = False, residual_exports: bool = False, weights=None):
+                 keep_source_index: bool = False, residual_exports: bool = False, weights=None, timer=None):
         from .rasterizer import DEFAULT_CONFIG
         self.scene = scene
         self.config = config if config is not None else DEFAULT_CONFIG
@@ -260,6 +285,8 @@ class CacheSet:
         cfg_s = rast_cfg_struct(self.config, scene.background)
         self.cfg_s = cfg_s
         err = torch.zeros(1, dtype=torch.int32, device=dev)
+        T = timer if timer is not None else _NoTimer()
+        T.tick("start")
 
         # ---- COUNT phase (per view) --------------------------------------
         self.px_count = torch.zeros(self.N + 1, dtype=torch.int32, device=dev)
@@ -279,6 +306,7 @@ class CacheSet:
         for v, cam in enumerate(self.cameras):
             fr = ViewFrame(cam, self.pix_bases[v])
             project_and_bin(scene, fr, cfg_s, err)
+            T.tick("project_sort_bin")
             hw = cam.num_pixels
             fr.rgb = torch.empty(hw * 3, dtype=torch.float64, device=dev)
             fr.t_final = torch.empty(hw, dtype=torch.float64, device=dev)
@@ -287,11 +315,13 @@ class CacheSet:
             a.rgb, a.t_final = ptr(fr.rgb), ptr(fr.t_final)
             a.pair_cnt = C.c_void_p(self.pair_cnt.data_ptr() + v * G * 4)
             call("slm_raster_count", _lib.byref(a), stream_ptr())
+            T.tick("raster_count")
             if have_res:
                 ex = {} if residual_exports else None
                 energy_parts.append(residual_pass(fr, gts[v], loss, self.gradr, self.cgrad, ex))
                 if residual_exports:
                     self.residual_exports.append(ex)
+                T.tick("residuals")
             self.frames.append(fr)
         e = int(err.item())
         if e & 1:
@@ -347,6 +377,7 @@ class CacheSet:
              Pn, self.E, stream_ptr())
         del cntT, flagT, off_of, pair_of, splats_all
 
+        T.tick("segments_pairs")
         # ---- FILL phase: pixel-order records, then gaussian order ------------
         E = self.E
         n_chunks = (E + CHUNK - 1) // CHUNK
@@ -374,6 +405,7 @@ class CacheSet:
             a.view_entry_base = e0
             a.chunk_seg = ptr(self.chunk_seg_pix)
             call("slm_raster_fill", _lib.byref(a), stream_ptr())
+            T.tick("raster_fill")
             if Ev == 0:
                 continue
             iota = _empty(Ev, torch.int32, dev)
@@ -390,6 +422,7 @@ class CacheSet:
             g.chunk_seg = ptr(self.chunk_seg_gau)
             g.g_src = ptr(self.g_src) if self.g_src is not None else None
             call("slm_gauss_scatter", _lib.byref(g), stream_ptr())
+            T.tick("gauss_order")
             del ent_gid, ent_xy, iota, sk, sv
         del pidx, vscan, seg_idx
         for fr in self.frames:  # keep images for exports; tile lists are not needed any more

@@ -35,6 +35,19 @@ class BatchSchedule:
             raise ValueError("n_b must be >= 1")
         return [list(range(j, n_views, self.n_batches)) for j in range(self.n_batches)]
 
+    def shard(self, n_views: int, rank: int, world: int) -> list[tuple[int, list[int]]]:
+        """Subsets owned by `rank`: subset j -> rank j mod world."""
+        return [(j, v) for j, v in enumerate(self.batches(n_views)) if j % world == rank and v]
+
+
+def allreduce_sum_(buf: torch.Tensor, group=None) -> torch.Tensor:
+    """In-place SUM all_reduce when a process group with >1 rank is up
+    (NCCL on GPU boxes, gloo in the CPU tests); no-op otherwise."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    return buf
+
 
 @dataclass
 class PCGWorkspace:
@@ -142,11 +155,12 @@ class Combiner:
         self.accepted += 1
 
     def allreduce(self, group=None):
+        """ONE packed all_reduce of [num; den] plus the accepted-batch count."""
         import torch.distributed as dist
-        if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
-            dist.all_reduce(self.buf, op=dist.ReduceOp.SUM, group=group)
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+            allreduce_sum_(self.buf, group)
             acc = torch.tensor([self.accepted], dtype=torch.int64, device=self.buf.device)
-            dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
+            allreduce_sum_(acc, group)
             self.accepted = int(acc.item())
 
     def finalize(self) -> torch.Tensor:
@@ -176,9 +190,7 @@ def lm_direction(scene, cameras, gts, schedule: BatchSchedule = BatchSchedule(),
     energy = 0.0
     entries, pcg_stats = [], []
     caches = []
-    for j, views in enumerate(schedule.batches(len(cameras))):
-        if j % world_size != rank or not views:
-            continue
+    for j, views in schedule.shard(len(cameras), rank, world_size):
         cs = CacheSet(scene, [cameras[i] for i in views], [gts[i] for i in views], config, loss)
         energy += sum(cs.energies)
         entries.append(cs.E)

@@ -1,0 +1,89 @@
+"""Per-phase CUDA-event breakdown of one subset of a bench config.
+
+    python tools/profile_subset.py [--config c3] [--views 25] [--reps 3]
+
+Prints JSON: build phases, rhs, diag, and the four kernels of one
+J^T W J p product (pair forward, applyJ, applyJT pairs, pair backward).
+Used to pick ncu targets; not a bench number.
+"""
+
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2409_12892_b200.engine import CacheSet, PhaseTimer  # noqa: E402
+from paper_2409_12892_b200.solver import BatchSchedule, pcg_run  # noqa: E402
+
+
+def ev():
+    e = torch.cuda.Event(enable_timing=True)
+    e.record()
+    return e
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--skip-pcg", action="store_true")
+    args = ap.parse_args()
+    cfg = dict(bench.CONFIGS[args.config])
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    views = BatchSchedule(cfg["subsets"]).batches(cfg["views"])[0]
+    cfg_one = dict(cfg)
+    init, cams, gts = bench.make_workload(cfg_one, dev)
+    scene = init.to_device(dev)
+    cams = [cams[i] for i in views]
+    gts = [gts[i] for i in views]
+    out = {}
+    for rep in range(args.reps):
+        T = PhaseTimer()
+        cs = CacheSet(scene, cams, gts, timer=T)
+        T.tick("done")
+        phases = T.summary()
+        a = ev()
+        b = cs.rhs()
+        c = ev()
+        M = cs.diag()
+        d = ev()
+        torch.cuda.synchronize()
+        phases["rhs"] = a.elapsed_time(c)
+        phases["diag"] = c.elapsed_time(d)
+        p = torch.randn(scene.param_count, device=dev)
+        g = torch.empty_like(p)
+        k = []
+        for _ in range(3):
+            e0 = ev()
+            cs.pair_forward(p)
+            e1 = ev()
+            cs.apply_j_raw(weighted=True)
+            e2 = ev()
+            cs.apply_jt_raw(cs.u, g, 1.0, p, M, 1e-4, None)
+            e3 = ev()
+            k.append((e0, e1, e2, e3))
+        torch.cuda.synchronize()
+        e0, e1, e2, e3 = k[-1]
+        phases["prod_pair_forward"] = e0.elapsed_time(e1)
+        phases["prod_apply_j"] = e1.elapsed_time(e2)
+        phases["prod_apply_jt+backward"] = e2.elapsed_time(e3)
+        if not args.skip_pcg:
+            s0 = ev()
+            pcg_run(cs, b, M, 1e-4, cfg["iters"])
+            s1 = ev()
+            torch.cuda.synchronize()
+            phases["pcg_total"] = s0.elapsed_time(s1)
+        phases.update(E=cs.E, N=cs.N, pairs=cs.n_pairs, G=cs.G, mem_gb=torch.cuda.max_memory_allocated() / 1e9)
+        out = phases
+        del cs
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
