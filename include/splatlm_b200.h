@@ -85,19 +85,28 @@ typedef struct {
   int W, H, tiles_x;
   long long pix_base;
   SlmRastCfg cfg;
-  uint32_t* px_count;
-  double* rgb;
-  double* t_final;
-  int* pair_cnt;
-  const long long* pix_off;
-  const int* pidx;
-  const int* seg_idx;
+  /* COUNT outputs */
+  uint32_t* px_count;   /* [HW] entries per pixel */
+  double* rgb;          /* [HW*3] rendered colour incl. background (FILL: input) */
+  double* t_final;      /* [HW] */
+  uint8_t* rowcnt;      /* [n_inst*16] entries per (tile instance, pixel row); may be NULL */
+  /* FILL inputs */
+  const long long* pix_off;   /* subset-global pixel-order offsets, indexed by gp */
+  const int* pidx;            /* [G] pair index of (this view, g) */
+  const int* seg_idx;         /* [subset pixels] ordinal among non-empty pixels */
+  const long long* pair_off;  /* [P+1] gaussian-order pair offsets */
+  const uint32_t* inst_base;  /* [n_inst*16] offset of each (instance, row) run in its pair */
+  /* FILL outputs: pixel-order records */
   uint32_t* rec_idx;
   float *rec_ae, *rec_at, *rec_d0, *rec_d1, *rec_d2;
-  uint32_t* ent_gid;
-  uint32_t* ent_xy;
-  long long view_entry_base;
   int* chunk_seg;
+  /* FILL outputs: gaussian-order records */
+  uint32_t* g_idx;
+  float *g_ae, *g_at, *g_d0, *g_d1, *g_d2;
+  int* g_chunk_seg;
+  int* g_src;                 /* optional source_index (view-local pixel-order position) */
+  long long view_entry_base;
+  /* optional traversal export (rasterizer.py:209-243), view-local entry index */
   long long* trav_gid;
   double* trav_alpha;
   double* trav_T;
@@ -123,23 +132,6 @@ typedef struct {
   double *o_gradr, *o_cgrad, *o_rabs, *o_rssim, *o_drabs, *o_drssim;
 } SlmResidArgs;
 
-/* gaussian-order scatter of one view (sort_cache_by_gaussians, jacobian.py:93-105) */
-typedef struct {
-  const uint32_t* sorted_gid;
-  const uint32_t* sorted_src;
-  const uint32_t* ent_xy;
-  long long Ev, view_base, G;
-  int v;
-  const int* pidx;
-  const long long* pair_off;
-  const long long* vscan;
-  const float *ae, *at, *d0, *d1, *d2;
-  uint32_t* g_idx;
-  float *g_ae, *g_at, *g_d0, *g_d1, *g_d2;
-  int* chunk_seg;
-  int* g_src;
-} SlmGaussOrderArgs;
-
 /* one cache record stream (pixel or gaussian order) for the product kernels */
 typedef struct {
   const uint32_t* idx;
@@ -158,7 +150,6 @@ int slm_pair_geo_size(void);
 int slm_view_size(void);
 int slm_raster_args_size(void);
 int slm_resid_args_size(void);
-int slm_gauss_order_args_size(void);
 int slm_wsr_stream_size(void);
 long long slm_carry_bytes(int D);
 
@@ -180,7 +171,16 @@ int slm_sort_pairs_u64(void* ws, long long ws_bytes, const unsigned long long* k
 int slm_tile_count(const uint32_t* sorted_gid, const unsigned long long* sorted_key, long long G,
                    const SlmSplat* splats, int tiles_x, int tiles_y, unsigned long long* n_inst, cudaStream_t s);
 int slm_tile_emit(const uint32_t* sorted_gid, const unsigned long long* inst_off, long long G, const SlmSplat* splats,
-                  int tiles_x, int tiles_y, int rank_bits, unsigned long long* keys, uint32_t* vals, cudaStream_t s);
+                  int tiles_x, int tiles_y, int rank_bits, unsigned long long* keys, uint32_t* vals,
+                  uint32_t* inst_g_pre, cudaStream_t s);
+int slm_tile_post(const uint32_t* sorted_pre, const uint32_t* inst_g_pre, long long n, uint32_t* inst_gid,
+                  uint32_t* post_of_pre, cudaStream_t s);
+/* per-(view, gaussian) entry counts (pair_cnt) and, with base_out, the
+ * row-major run offsets that place each entry in its gaussian-order pair
+ * block -- the stable (gid, pixel) order of jacobian.py:96 without a sort */
+int slm_inst_base(const uint32_t* sorted_gid, const unsigned long long* inst_off, long long G, const SlmSplat* splats,
+                  int tiles_x, int tiles_y, const uint32_t* post_of_pre, const uint8_t* rowcnt, uint32_t* base_out,
+                  int* pair_cnt, cudaStream_t s);
 int slm_tile_ranges(const unsigned long long* keys, long long n, int rank_bits, slm_u2* ranges, int n_tiles,
                     cudaStream_t s);
 /* render (rasterizer.py:319-358): COUNT pass = image, T_final, per-pixel and
@@ -204,13 +204,14 @@ int slm_iota_u32(uint32_t* out, long long n, cudaStream_t s);
 int slm_px_prepare(const uint32_t* cnt, long long n, long long* cnt64, int* nonempty, cudaStream_t s);
 int slm_px_segments(const uint32_t* cnt, const int* seg_idx, long long n, const SlmCamera* cams_dev, int n_views,
                     slm_u2* seg_info, cudaStream_t s);
-int slm_pairs_prepare(const int* cnt, int V, long long G, long long* cntT, int* flagT, long long* cntV,
-                      cudaStream_t s);
-int slm_pairs_emit(const int* cnt, int V, long long G, const int* pair_of, const long long* off_of,
+/* (view, gaussian) pairs in (view, gid) order: counts -> flags/scans, then
+ * pair offsets / geometry / maps and the gid-major CSR (gpo, gp_list) used by
+ * the per-gaussian backward chain.  Together with slm_inst_base and the FILL
+ * pass this replaces sort_cache_by_gaussians (jacobian.py:93-105). */
+int slm_pairs_prepare(const int* cnt, int V, long long G, long long* cntV, int* flagV, int* flagT, cudaStream_t s);
+int slm_pairs_emit(const int* cnt, int V, long long G, const int* pair_of, const long long* vscan, const int* tscan,
                    const SlmSplat* splats, long long* pair_off, int* pair_gid, uint32_t* pair_vm, SlmPairGeo* geo,
-                   int* pidx, int* gpo, int n_pairs, long long n_entries, cudaStream_t s);
-/* replaces sort_cache_by_gaussians (jacobian.py:93-105) for one view */
-int slm_gauss_scatter(const SlmGaussOrderArgs* a, cudaStream_t s);
+                   int* pidx, int* gpo, int* gp_list, int n_pairs, long long n_entries, cudaStream_t s);
 
 /* ---- products --------------------------------------------------------------
  * apply_j (jacobian.py:419-455) fused with weight_residuals (458-464) when
@@ -231,9 +232,9 @@ int slm_pair_forward(const float* xs, long long G, int sh_degree, const int* pai
  * mode 0 from J^T partials, mode 1 from diag moments; out = scale * chain
  * (+ lam * max(M, 1e-12) * p and p.out block partials when p != NULL) */
 int slm_backward_blocks(long long G);
-int slm_pair_backward(const float* xs, long long G, int sh_degree, const int* gpo, const uint32_t* pair_vm,
-                      const SlmCamera* cams, const float* acc, int mode, float scale, const float* p,
-                      const float* Mdiag, float lam, float* out, double* dot_part, cudaStream_t s);
+int slm_pair_backward(const float* xs, long long G, int sh_degree, const int* gpo, const int* gp_list,
+                      const uint32_t* pair_vm, const SlmCamera* cams, const float* acc, int mode, float scale,
+                      const float* p, const float* Mdiag, float lam, float* out, double* dot_part, cudaStream_t s);
 
 /* ---- PCG (Alg. 1; SPEC pcg_solve 391-399) ------------------ */
 int slm_vec_blocks(void);

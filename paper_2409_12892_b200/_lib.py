@@ -41,11 +41,13 @@ class SlmView(C.Structure):
 class SlmRasterArgs(C.Structure):
     _fields_ = [("tile_range", c_vp), ("inst_gid", c_vp), ("splats", c_vp),
                 ("W", c_i), ("H", c_i), ("tiles_x", c_i), ("pix_base", c_ll), ("cfg", SlmRastCfg),
-                ("px_count", c_vp), ("rgb", c_vp), ("t_final", c_vp), ("pair_cnt", c_vp),
-                ("pix_off", c_vp), ("pidx", c_vp), ("seg_idx", c_vp),
+                ("px_count", c_vp), ("rgb", c_vp), ("t_final", c_vp), ("rowcnt", c_vp),
+                ("pix_off", c_vp), ("pidx", c_vp), ("seg_idx", c_vp), ("pair_off", c_vp), ("inst_base", c_vp),
                 ("rec_idx", c_vp), ("rec_ae", c_vp), ("rec_at", c_vp), ("rec_d0", c_vp), ("rec_d1", c_vp),
-                ("rec_d2", c_vp), ("ent_gid", c_vp), ("ent_xy", c_vp), ("view_entry_base", c_ll),
-                ("chunk_seg", c_vp), ("trav_gid", c_vp), ("trav_alpha", c_vp), ("trav_T", c_vp)]
+                ("rec_d2", c_vp), ("chunk_seg", c_vp),
+                ("g_idx", c_vp), ("g_ae", c_vp), ("g_at", c_vp), ("g_d0", c_vp), ("g_d1", c_vp), ("g_d2", c_vp),
+                ("g_chunk_seg", c_vp), ("g_src", c_vp), ("view_entry_base", c_ll),
+                ("trav_gid", c_vp), ("trav_alpha", c_vp), ("trav_T", c_vp)]
 
 
 class SlmResidArgs(C.Structure):
@@ -55,15 +57,6 @@ class SlmResidArgs(C.Structure):
                 ("gradr", c_vp), ("cgrad", c_vp), ("energy_part", c_vp),
                 ("o_gradr", c_vp), ("o_cgrad", c_vp), ("o_rabs", c_vp), ("o_rssim", c_vp),
                 ("o_drabs", c_vp), ("o_drssim", c_vp)]
-
-
-class SlmGaussOrderArgs(C.Structure):
-    _fields_ = [("sorted_gid", c_vp), ("sorted_src", c_vp), ("ent_xy", c_vp),
-                ("Ev", c_ll), ("view_base", c_ll), ("G", c_ll), ("v", c_i),
-                ("pidx", c_vp), ("pair_off", c_vp), ("vscan", c_vp),
-                ("ae", c_vp), ("at", c_vp), ("d0", c_vp), ("d1", c_vp), ("d2", c_vp),
-                ("g_idx", c_vp), ("g_ae", c_vp), ("g_at", c_vp), ("g_d0", c_vp), ("g_d1", c_vp), ("g_d2", c_vp),
-                ("chunk_seg", c_vp), ("g_src", c_vp)]
 
 
 class SlmWsrStream(C.Structure):
@@ -80,13 +73,15 @@ DIAG_D = 42
 _SIGS = {
     "slm_camera_size": (c_i, []), "slm_rastcfg_size": (c_i, []), "slm_splat_size": (c_i, []),
     "slm_pair_geo_size": (c_i, []), "slm_view_size": (c_i, []), "slm_raster_args_size": (c_i, []),
-    "slm_resid_args_size": (c_i, []), "slm_gauss_order_args_size": (c_i, []),
+    "slm_resid_args_size": (c_i, []),
     "slm_wsr_stream_size": (c_i, []), "slm_carry_bytes": (c_ll, [c_i]),
     "slm_preprocess": (c_i, [c_vp, c_ll, c_i, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "slm_sort_pairs_u64_workspace": (c_ll, [c_ll]),
     "slm_sort_pairs_u64": (c_i, [c_vp, c_ll, c_vp, c_vp, c_vp, c_vp, c_ll, c_i, c_i, c_vp]),
     "slm_tile_count": (c_i, [c_vp, c_vp, c_ll, c_vp, c_i, c_i, c_vp, c_vp]),
-    "slm_tile_emit": (c_i, [c_vp, c_vp, c_ll, c_vp, c_i, c_i, c_i, c_vp, c_vp, c_vp]),
+    "slm_tile_emit": (c_i, [c_vp, c_vp, c_ll, c_vp, c_i, c_i, c_i, c_vp, c_vp, c_vp, c_vp]),
+    "slm_tile_post": (c_i, [c_vp, c_vp, c_ll, c_vp, c_vp, c_vp]),
+    "slm_inst_base": (c_i, [c_vp, c_vp, c_ll, c_vp, c_i, c_i, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "slm_tile_ranges": (c_i, [c_vp, c_ll, c_i, c_vp, c_i, c_vp]),
     "slm_raster_count": (c_i, [c_vp, c_vp]),
     "slm_raster_fill": (c_i, [c_vp, c_vp]),
@@ -101,16 +96,15 @@ _SIGS = {
     "slm_px_prepare": (c_i, [c_vp, c_ll, c_vp, c_vp, c_vp]),
     "slm_px_segments": (c_i, [c_vp, c_vp, c_ll, c_vp, c_i, c_vp, c_vp]),
     "slm_pairs_prepare": (c_i, [c_vp, c_i, c_ll, c_vp, c_vp, c_vp, c_vp]),
-    "slm_pairs_emit": (c_i, [c_vp, c_i, c_ll, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i, c_ll,
-                             c_vp]),
-    "slm_gauss_scatter": (c_i, [c_vp, c_vp]),
+    "slm_pairs_emit": (c_i, [c_vp, c_i, c_ll, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                             c_i, c_ll, c_vp]),
     "slm_apply_j": (c_i, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "slm_apply_jt_pairs": (c_i, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "slm_diag_pairs": (c_i, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "slm_pair_forward": (c_i, [c_vp, c_ll, c_i, c_vp, c_vp, c_vp, c_i, c_vp, c_ll, c_ll, c_vp, c_vp]),
     "slm_backward_blocks": (c_i, [c_ll]),
-    "slm_pair_backward": (c_i, [c_vp, c_ll, c_i, c_vp, c_vp, c_vp, c_vp, c_i, c_f, c_vp, c_vp, c_f, c_vp, c_vp,
-                                c_vp]),
+    "slm_pair_backward": (c_i, [c_vp, c_ll, c_i, c_vp, c_vp, c_vp, c_vp, c_vp, c_i, c_f, c_vp, c_vp, c_f, c_vp,
+                                c_vp, c_vp]),
     "slm_vec_blocks": (c_i, []),
     "slm_pcg_pupdate": (c_i, [c_vp, c_vp, c_vp, c_vp, c_ll, c_vp]),
     "slm_pcg_update": (c_i, [c_i, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i, c_vp, c_ll, c_vp]),
@@ -146,7 +140,7 @@ def load():
         fn.argtypes = args
     checks = {"slm_camera_size": SlmCamera, "slm_rastcfg_size": SlmRastCfg, "slm_view_size": SlmView,
               "slm_raster_args_size": SlmRasterArgs, "slm_resid_args_size": SlmResidArgs,
-              "slm_gauss_order_args_size": SlmGaussOrderArgs, "slm_wsr_stream_size": SlmWsrStream}
+              "slm_wsr_stream_size": SlmWsrStream}
     for fn, st in checks.items():
         if getattr(lib, fn)() != C.sizeof(st):
             raise SplatLMError(f"ABI mismatch: {fn} = {getattr(lib, fn)()} vs ctypes {C.sizeof(st)}")

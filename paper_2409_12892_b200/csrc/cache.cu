@@ -1,10 +1,11 @@
-// Gradient-cache assembly: pixel segments, (gaussian, view) pairs, and the
-// gaussian-order record stream (sortCacheByGaussians).
+// Gradient-cache assembly: pixel segments and (gaussian, view) pairs.
 //
-// Gaussian order = (gid, view, pixel row-major); restricted to one view it is
-// exactly the reference's np.lexsort((pixel_ids, gaussian_ids))
-// (ref: jacobian.py:93-105), produced by a stable radix sort of each view's
-// pixel-order entries by gid followed by a scatter into pair blocks.
+// The gaussian-order record stream itself (sortCacheByGaussians, PAPER:273,
+// 305-306) is written directly by the FILL raster pass (raster.cu): pairs are
+// numbered in (view, gid) order and each pair's block is filled in pixel
+// row-major order, so one view's gaussian-order sequence equals the
+// reference's np.lexsort((pixel_ids, gaussian_ids)) (ref: jacobian.py:93-105)
+// with no sort at all.
 #include "slm_common.cuh"
 
 #include <cub/cub.cuh>
@@ -66,7 +67,7 @@ __global__ void k_px_prepare(const uint32_t* __restrict__ cnt, long long n, long
   }
 }
 
-// seg_info[seg] = {gp, (y << 16) | x}; views are given by a gp -> view table
+// seg_info[seg] = {gp, (y << 16) | x}
 __global__ void k_px_segments(const uint32_t* __restrict__ cnt, const int* __restrict__ seg_idx, long long n,
                               const SlmCamera* __restrict__ cams, int n_views, uint2* __restrict__ seg_info) {
   for (long long gp = blockIdx.x * (long long)blockDim.x + threadIdx.x; gp < n; gp += (long long)gridDim.x * blockDim.x) {
@@ -80,79 +81,56 @@ __global__ void k_px_segments(const uint32_t* __restrict__ cnt, const int* __res
 }
 
 // ---------------------------------------------------------------------------
-// pairs: (gaussian, view) with >= 1 entry, numbered in (gid, view) order
+// pairs: (gaussian, view) with >= 1 entry, numbered in (view, gid) order so
+// that one view's pairs -- and the gaussian-order records, u and grad_r_sq
+// they touch -- are contiguous and L2-resident while that view is streamed.
+// The per-gaussian backward chain reaches its pairs through a gid-major CSR
+// (gpo / gp_list).
 // ---------------------------------------------------------------------------
 __global__ void k_pairs_prepare(const int* __restrict__ cnt /*[V][G]*/, int V, long long G,
-                                long long* __restrict__ cntT /*[G*V]*/, int* __restrict__ flagT,
-                                long long* __restrict__ cntV /*[V*G] view-major int64*/) {
+                                long long* __restrict__ cntV /*[V*G] view-major*/, int* __restrict__ flagV,
+                                int* __restrict__ flagT /*[G*V] gid-major*/) {
   long long n = (long long)V * G;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    long long g = i / V;
-    int v = (int)(i % V);
-    int c = cnt[(long long)v * G + g];
-    cntT[i] = c;
-    flagT[i] = c > 0;
-    cntV[(long long)v * G + g] = c;
+    const int c = cnt[i];
+    cntV[i] = c;
+    flagV[i] = c > 0;
+    const long long v = i / G, g = i % G;
+    flagT[g * V + v] = c > 0;
   }
 }
 
 __global__ void k_pairs_emit(const int* __restrict__ cnt, int V, long long G, const int* __restrict__ pair_of,
-                             const long long* __restrict__ off_of, const SlmSplat* __restrict__ splats /*[V][G]*/,
-                             long long* __restrict__ pair_off, int* __restrict__ pair_gid,
-                             uint32_t* __restrict__ pair_vm, SlmPairGeo* __restrict__ geo, int* __restrict__ pidx,
-                             int* __restrict__ gpo /*[G+1]*/, int n_pairs, long long n_entries) {
+                             const long long* __restrict__ vscan, const int* __restrict__ tscan,
+                             const SlmSplat* __restrict__ splats /*[V][G]*/, long long* __restrict__ pair_off,
+                             int* __restrict__ pair_gid, uint32_t* __restrict__ pair_vm,
+                             SlmPairGeo* __restrict__ geo, int* __restrict__ pidx, int* __restrict__ gpo /*[G+1]*/,
+                             int* __restrict__ gp_list, int n_pairs, long long n_entries) {
   long long n = (long long)V * G;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    long long g = i / V;
-    int v = (int)(i % V);
-    if (v == 0) gpo[g] = pair_of[i];
-    long long vg = (long long)v * G + g;
-    int c = cnt[vg];
+    const long long v = i / G, g = i % G;
+    if (v == 0) gpo[g] = tscan[g * V];
+    const int c = cnt[i];
     if (c <= 0) {
-      pidx[vg] = -1;
+      pidx[i] = -1;
       continue;
     }
-    int q = pair_of[i];
-    pair_off[q] = off_of[i];
+    const int q = pair_of[i];
+    pair_off[q] = vscan[i];
     pair_gid[q] = (int)g;
-    const SlmSplat s = splats[vg];
+    const SlmSplat s = splats[i];
     pair_vm[q] = (uint32_t)v | (((s.flags >> 1) & 7u) << 16);
     SlmPairGeo pg;
     pg.mx = s.mx; pg.my = s.my;
     pg.ka = (float)s.ca; pg.kb = (float)s.cb; pg.kc = (float)s.cc;
     pg.inv_o = (float)(1.0 / s.o);
     geo[q] = pg;
-    pidx[vg] = q;
+    pidx[i] = q;
+    gp_list[tscan[g * V + v]] = q;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     gpo[G] = n_pairs;
     pair_off[n_pairs] = n_entries;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// gaussian-order stream for one view: scatter the gid-sorted entries into
-// their pair blocks
-// ---------------------------------------------------------------------------
-typedef SlmGaussOrderArgs GaussOrderArgs;
-
-__global__ void k_gauss_scatter(GaussOrderArgs A) {
-  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < A.Ev; j += (long long)gridDim.x * blockDim.x) {
-    uint32_t g = A.sorted_gid[j];
-    uint32_t sl = A.sorted_src[j];
-    long long vg = (long long)A.v * A.G + g;
-    int q = A.pidx[vg];
-    long long base = A.pair_off[q];
-    long long dest = base + (A.view_base + j - A.vscan[vg]);
-    long long src = A.view_base + sl;
-    A.g_idx[dest] = A.ent_xy[sl] | (dest == base ? SLM_HEAD : 0u);
-    A.g_ae[dest] = A.ae[src];
-    A.g_at[dest] = A.at[src];
-    A.g_d0[dest] = A.d0[src];
-    A.g_d1[dest] = A.d1[src];
-    A.g_d2[dest] = A.d2[src];
-    if ((dest & (SLM_CHUNK - 1)) == 0) A.chunk_seg[dest / SLM_CHUNK] = q;
-    if (A.g_src) A.g_src[dest] = (int)sl;
   }
 }
 
@@ -174,26 +152,17 @@ int slm_px_segments(const uint32_t* cnt, const int* seg_idx, long long n, const 
   return slm_cuda_status();
 }
 
-int slm_pairs_prepare(const int* cnt, int V, long long G, long long* cntT, int* flagT, long long* cntV,
-                      cudaStream_t s) {
-  k_pairs_prepare<<<slm_blocks((long long)V * G, 256), 256, 0, s>>>(cnt, V, G, cntT, flagT, cntV);
+int slm_pairs_prepare(const int* cnt, int V, long long G, long long* cntV, int* flagV, int* flagT, cudaStream_t s) {
+  k_pairs_prepare<<<slm_blocks((long long)V * G, 256), 256, 0, s>>>(cnt, V, G, cntV, flagV, flagT);
   return slm_cuda_status();
 }
 
-int slm_pairs_emit(const int* cnt, int V, long long G, const int* pair_of, const long long* off_of,
+int slm_pairs_emit(const int* cnt, int V, long long G, const int* pair_of, const long long* vscan, const int* tscan,
                    const SlmSplat* splats, long long* pair_off, int* pair_gid, uint32_t* pair_vm, SlmPairGeo* geo,
-                   int* pidx, int* gpo, int n_pairs, long long n_entries, cudaStream_t s) {
-  k_pairs_emit<<<slm_blocks((long long)V * G, 256), 256, 0, s>>>(cnt, V, G, pair_of, off_of, splats, pair_off,
-                                                                  pair_gid, pair_vm, geo, pidx, gpo, n_pairs,
+                   int* pidx, int* gpo, int* gp_list, int n_pairs, long long n_entries, cudaStream_t s) {
+  k_pairs_emit<<<slm_blocks((long long)V * G, 256), 256, 0, s>>>(cnt, V, G, pair_of, vscan, tscan, splats, pair_off,
+                                                                  pair_gid, pair_vm, geo, pidx, gpo, gp_list, n_pairs,
                                                                   n_entries);
-  return slm_cuda_status();
-}
-
-int slm_gauss_order_args_size() { return (int)sizeof(GaussOrderArgs); }
-
-int slm_gauss_scatter(const GaussOrderArgs* a, cudaStream_t s) {
-  if (a->Ev <= 0) return SLM_OK;
-  k_gauss_scatter<<<slm_blocks(a->Ev, 256), 256, 0, s>>>(*a);
   return slm_cuda_status();
 }
 

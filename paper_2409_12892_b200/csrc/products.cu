@@ -510,6 +510,7 @@ __global__ void __launch_bounds__(128) k_pair_forward(const float* __restrict__ 
 template <int K, int MODE>
 __global__ void __launch_bounds__(128) k_pair_backward(const float* __restrict__ xs, long long G,
                                                        const int* __restrict__ gpo,
+                                                       const int* __restrict__ gp_list,
                                                        const uint32_t* __restrict__ pair_vm,
                                                        const SlmCamera* __restrict__ cams,
                                                        const float* __restrict__ acc, float scale,
@@ -526,8 +527,9 @@ __global__ void __launch_bounds__(128) k_pair_backward(const float* __restrict__
     for (int ch = 0; ch < 3; ++ch)
 #pragma unroll
       for (int k = 0; k < K; ++k) osh[ch][k] = 0.f;
-    const int q0 = gpo[g], q1 = gpo[g + 1];
-    for (int q = q0; q < q1; ++q) {
+    const int k0 = gpo[g], k1 = gpo[g + 1];
+    for (int kk = k0; kk < k1; ++kk) {  // this gaussian's pairs, in view order
+      const int q = gp_list[kk];
       const uint32_t vm = pair_vm[q];
       Tab<K> T;
       pair_tab<K>(xs, G, g, cams[vm & 0xffffu], vm >> 16, T);
@@ -667,15 +669,17 @@ int slm_pair_forward(const float* xs, long long G, int sh_degree, const int* pai
 // number of blocks k_pair_backward uses for G gaussians (size of dot_part)
 int slm_backward_blocks(long long G) { return (int)slm_blocks(G, 128, 148LL * 16); }
 
-int slm_pair_backward(const float* xs, long long G, int sh_degree, const int* gpo, const uint32_t* pair_vm,
-                      const SlmCamera* cams, const float* acc, int mode, float scale, const float* p,
-                      const float* Mdiag, float lam, float* out, double* dot_part, cudaStream_t st) {
+int slm_pair_backward(const float* xs, long long G, int sh_degree, const int* gpo, const int* gp_list,
+                      const uint32_t* pair_vm, const SlmCamera* cams, const float* acc, int mode, float scale,
+                      const float* p, const float* Mdiag, float lam, float* out, double* dot_part, cudaStream_t st) {
   unsigned b = (unsigned)slm_backward_blocks(G);
-#define SLM_BW(KK)                                                                                                  \
-  if (mode == 0)                                                                                                    \
-    k_pair_backward<KK, 0><<<b, 128, 0, st>>>(xs, G, gpo, pair_vm, cams, acc, scale, p, Mdiag, lam, out, dot_part); \
-  else                                                                                                              \
-    k_pair_backward<KK, 1><<<b, 128, 0, st>>>(xs, G, gpo, pair_vm, cams, acc, scale, p, Mdiag, lam, out, dot_part);
+#define SLM_BW(KK)                                                                                              \
+  if (mode == 0)                                                                                                \
+    k_pair_backward<KK, 0><<<b, 128, 0, st>>>(xs, G, gpo, gp_list, pair_vm, cams, acc, scale, p, Mdiag, lam, out, \
+                                              dot_part);                                                        \
+  else                                                                                                          \
+    k_pair_backward<KK, 1><<<b, 128, 0, st>>>(xs, G, gpo, gp_list, pair_vm, cams, acc, scale, p, Mdiag, lam, out, \
+                                              dot_part);
   switch (sh_degree) {
     case 0: SLM_BW(1) break;
     case 1: SLM_BW(4) break;

@@ -157,9 +157,13 @@ __global__ void k_tile_count(const uint32_t* __restrict__ sorted_gid, const unsi
   }
 }
 
+// instances are emitted per splat in (tile row, tile column) order; the sort
+// value is the pre-sort instance index so the per-splat grouping can be
+// recovered after the (tile, depth rank) sort (k_tile_post)
 __global__ void k_tile_emit(const uint32_t* __restrict__ sorted_gid, const unsigned long long* __restrict__ inst_off,
                             long long G, const SlmSplat* __restrict__ splats, int tiles_x, int tiles_y,
-                            int rank_bits, unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals) {
+                            int rank_bits, unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals,
+                            uint32_t* __restrict__ inst_g_pre) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   for (; i < G; i += (long long)gridDim.x * blockDim.x) {
     unsigned long long beg = inst_off[i], end = inst_off[i + 1];
@@ -171,9 +175,50 @@ __global__ void k_tile_emit(const uint32_t* __restrict__ sorted_gid, const unsig
     for (int ty = ty0; ty <= ty1; ++ty)
       for (int tx = tx0; tx <= tx1; ++tx) {
         keys[k] = ((unsigned long long)(ty * tiles_x + tx) << rank_bits) | (unsigned long long)i;
-        vals[k] = g;
+        vals[k] = (uint32_t)k;
+        inst_g_pre[k] = g;
         ++k;
       }
+  }
+}
+
+// post-sort list position j: gid and the inverse permutation pre -> post
+__global__ void k_tile_post(const uint32_t* __restrict__ sorted_pre, const uint32_t* __restrict__ inst_g_pre,
+                            long long n, uint32_t* __restrict__ inst_gid, uint32_t* __restrict__ post_of_pre) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+    uint32_t k = sorted_pre[j];
+    inst_gid[j] = inst_g_pre[k];
+    post_of_pre[k] = (uint32_t)j;
+  }
+}
+
+// Per splat (one thread per depth rank): walk its tile instances in pixel
+// row-major order -- tile row, pixel row inside the tile, tile column -- and
+// turn the COUNT pass's per-(instance, row) entry counts into the offset of
+// each (instance, row) run inside the splat's (view, gaussian) pair block.
+// This is the stable (gid, pixel) order of ref: jacobian.py:96 without a sort.
+__global__ void k_inst_base(const uint32_t* __restrict__ sorted_gid, const unsigned long long* __restrict__ inst_off,
+                            long long G, const SlmSplat* __restrict__ splats, int tiles_x, int tiles_y,
+                            const uint32_t* __restrict__ post_of_pre, const uint8_t* __restrict__ rowcnt,
+                            uint32_t* __restrict__ base_out, int* __restrict__ pair_cnt) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < G; i += (long long)gridDim.x * blockDim.x) {
+    unsigned long long beg = inst_off[i], end = inst_off[i + 1];
+    if (beg == end) continue;
+    const uint32_t g = sorted_gid[i];
+    int tx0, tx1, ty0, ty1;
+    splat_tiles(splats[g], tiles_x, tiles_y, tx0, tx1, ty0, ty1);
+    const int nx = tx1 - tx0 + 1;
+    uint32_t cur = 0;
+    for (int ty = ty0; ty <= ty1; ++ty) {
+      const unsigned long long krow = beg + (unsigned long long)(ty - ty0) * nx;
+      for (int ly = 0; ly < SLM_TILE; ++ly)
+        for (int c = 0; c < nx; ++c) {
+          const size_t j = post_of_pre[krow + c];
+          if (base_out) base_out[j * SLM_TILE + ly] = cur;
+          cur += rowcnt[j * SLM_TILE + ly];
+        }
+    }
+    if (pair_cnt) pair_cnt[g] = (int)cur;
   }
 }
 
@@ -190,10 +235,14 @@ __global__ void k_tile_ranges(const unsigned long long* __restrict__ keys, long 
 // ---------------------------------------------------------------------------
 // tile rasteriser (ref: rasterizer.py:264-316), one 16x16 tile per CTA,
 // one pixel per thread, splats staged in shared memory in batches.
-//   COUNT pass: per-pixel entry count, rendered colour, T_final, and the
-//               per-(view, gaussian) entry counts (warp-aggregated atomics).
-//   FILL pass : writes the pixel-order cache records; dc/dalpha uses the
-//               per-pixel colour total from the COUNT pass (ref: jacobian.py:391-399).
+//   COUNT pass: per-pixel entry count, rendered colour, T_final and, per
+//               (tile instance, pixel row), the number of entries (rowcnt).
+//   FILL pass : writes BOTH cache record streams.  Pixel order at
+//               pix_off[pixel] + k; gaussian order at pair_off[pair] +
+//               inst_base[instance][row] + (rank of the pixel among the keepers
+//               of its 16-pixel tile row, from a half-warp ballot).
+//               dc/dalpha uses the per-pixel colour total of the COUNT pass
+//               (ref: jacobian.py:391-399).
 // ---------------------------------------------------------------------------
 typedef SlmRasterArgs RasterArgs;
 
@@ -204,6 +253,7 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
   __shared__ double s_c0[RB], s_c1[RB], s_c2[RB];
   __shared__ int4 s_box[RB];
   __shared__ uint32_t s_gid[RB];
+  __shared__ uint32_t s_rc[FILL ? 1 : RB * SLM_TILE / 4];  // COUNT: bytes [item][tile row]
 
   const int tiles_x = A.tiles_x;
   const int tile = blockIdx.x;
@@ -216,6 +266,9 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
   const double dxp = (double)px + 0.5, dyp = (double)py + 0.5;
   const double amin = A.cfg.alpha_min, tstop = A.cfg.t_stop, aclamp = A.cfg.alpha_clamp;
   const int lane = threadIdx.x & 31;
+  const int half = lane >> 4;
+  const unsigned below = (1u << lx) - 1u;
+  const uint32_t xy = ((uint32_t)py << 16) | (uint32_t)px;
 
   double T = 1.0, C0 = 0.0, C1 = 0.0, C2 = 0.0;
   uint32_t cnt = 0;
@@ -245,6 +298,8 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
       s_box[threadIdx.x] = make_int4(s.x0, s.x1, s.y0, s.y1);
       s_gid[threadIdx.x] = g;
     }
+    if (!FILL)
+      for (int w = threadIdx.x; w < RB * SLM_TILE / 4; w += RB) s_rc[w] = 0u;
     __syncthreads();
     const int nb = min((unsigned)RB, rng.y - base);
     for (int k = 0; k < nb; ++k) {
@@ -261,6 +316,10 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
         a = a < aclamp ? a : aclamp;
         keep = (a >= amin) && (a > 0.0) && (T >= tstop);
       }
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      const unsigned rowm = (half ? (m >> 16) : m) & 0xffffu;
+      if (!FILL && (lane & 15) == 0 && rowm)
+        reinterpret_cast<uint8_t*>(s_rc)[k * SLM_TILE + ly] = (uint8_t)__popc(rowm);
       if (keep) {
         const double wgt = __dmul_rn(a, T);
         C0 = __dadd_rn(C0, __dmul_rn(wgt, s_c0[k]));
@@ -272,17 +331,31 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
           const float d0 = (float)(s_c0[k] * T - (tot0 - C0) / om);
           const float d1 = (float)(s_c1[k] * T - (tot1 - C1) / om);
           const float d2 = (float)(s_c2[k] * T - (tot2 - C2) / om);
+          const float ae = a < aclamp ? (float)a : 0.0f;
+          const float at = (float)wgt;
           const uint32_t q = (uint32_t)A.pidx[g];
+          // pixel order
           A.rec_idx[e] = q | (cnt == 0 ? SLM_HEAD : 0u);
-          A.rec_ae[e] = a < aclamp ? (float)a : 0.0f;
-          A.rec_at[e] = (float)wgt;
+          A.rec_ae[e] = ae;
+          A.rec_at[e] = at;
           A.rec_d0[e] = d0;
           A.rec_d1[e] = d1;
           A.rec_d2[e] = d2;
-          const long long le = e - A.view_entry_base;
-          if (A.ent_gid) A.ent_gid[le] = g;
-          if (A.ent_xy) A.ent_xy[le] = ((uint32_t)py << 16) | (uint32_t)px;
           if (A.chunk_seg && (e & (SLM_CHUNK - 1)) == 0) A.chunk_seg[e / SLM_CHUNK] = seg;
+          // gaussian order: row-major rank of this pixel inside the pair
+          if (A.g_idx) {
+            const long long pb = A.pair_off[q];
+            const long long dest =
+                pb + A.inst_base[(size_t)(base + k) * SLM_TILE + ly] + __popc(rowm & below);
+            A.g_idx[dest] = xy | (dest == pb ? SLM_HEAD : 0u);
+            A.g_ae[dest] = ae;
+            A.g_at[dest] = at;
+            A.g_d0[dest] = d0;
+            A.g_d1[dest] = d1;
+            A.g_d2[dest] = d2;
+            if ((dest & (SLM_CHUNK - 1)) == 0) A.g_chunk_seg[dest / SLM_CHUNK] = (int)q;
+            if (A.g_src) A.g_src[dest] = (int)(e - A.view_entry_base);
+          }
         }
         if (FILL) {
           if (A.trav_gid) {
@@ -297,12 +370,12 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
         ++cnt;
         if (T < tstop) done = true;  // no later splat can pass T >= t_stop
       }
-      if (!FILL) {
-        unsigned m = __ballot_sync(0xffffffffu, keep);
-        if (m && lane == __ffs(m) - 1) atomicAdd(&A.pair_cnt[s_gid[k]], __popc(m));
-      }
     }
     __syncthreads();
+    if (!FILL && A.rowcnt) {
+      uint32_t* dst = reinterpret_cast<uint32_t*>(A.rowcnt + (size_t)base * SLM_TILE);
+      for (int w = threadIdx.x; w < nb * SLM_TILE / 4; w += RB) dst[w] = s_rc[w];
+    }
   }
   if (!FILL && inside) {
     A.px_count[pix] = cnt;
@@ -363,9 +436,24 @@ int slm_tile_count(const uint32_t* sorted_gid, const unsigned long long* sorted_
 
 int slm_tile_emit(const uint32_t* sorted_gid, const unsigned long long* inst_off, long long G, const SlmSplat* splats,
                   int tiles_x, int tiles_y, int rank_bits, unsigned long long* keys, uint32_t* vals,
-                  cudaStream_t stream) {
+                  uint32_t* inst_g_pre, cudaStream_t stream) {
   k_tile_emit<<<slm_blocks(G, 256), 256, 0, stream>>>(sorted_gid, inst_off, G, splats, tiles_x, tiles_y, rank_bits,
-                                                       keys, vals);
+                                                       keys, vals, inst_g_pre);
+  return slm_cuda_status();
+}
+
+int slm_tile_post(const uint32_t* sorted_pre, const uint32_t* inst_g_pre, long long n, uint32_t* inst_gid,
+                  uint32_t* post_of_pre, cudaStream_t stream) {
+  if (n <= 0) return SLM_OK;
+  k_tile_post<<<slm_blocks(n, 256), 256, 0, stream>>>(sorted_pre, inst_g_pre, n, inst_gid, post_of_pre);
+  return slm_cuda_status();
+}
+
+int slm_inst_base(const uint32_t* sorted_gid, const unsigned long long* inst_off, long long G, const SlmSplat* splats,
+                  int tiles_x, int tiles_y, const uint32_t* post_of_pre, const uint8_t* rowcnt, uint32_t* base_out,
+                  int* pair_cnt, cudaStream_t stream) {
+  k_inst_base<<<slm_blocks(G, 128), 128, 0, stream>>>(sorted_gid, inst_off, G, splats, tiles_x, tiles_y, post_of_pre,
+                                                       rowcnt, base_out, pair_cnt);
   return slm_cuda_status();
 }
 

@@ -3,10 +3,11 @@
 `CacheSet` is the B200 counterpart of the reference's per-view
 `GradientCache` (ref: jacobian.py:46-84) generalised to the multi-view batch
 that PCG sums over.  Building it runs, per view: fp64 projection,
-(depth, gid) sort, tile binning, COUNT raster pass, residual weights; then
-per subset: pixel offsets, (gaussian, view) pairs; then per view: FILL raster
-pass (pixel-order records) and the stable gid sort + scatter that produces the
-gaussian-order records (sortCacheByGaussians).
+(depth, gid) sort, tile binning, COUNT raster pass (+ per (tile instance,
+pixel row) entry counts), residual weights; then per subset: pixel offsets and
+(view, gaussian) pairs; then per view: row-major run offsets and the FILL
+raster pass, which writes BOTH record streams -- pixel order and gaussian
+order (sortCacheByGaussians) -- without any sort.
 
 Everything here is host orchestration of libsplatlm_b200 kernels on the
 current torch stream; torch only allocates memory.
@@ -143,6 +144,10 @@ class ViewFrame:
         self.tiles_y = (cam.height + TILE - 1) // TILE
         self.n_inst = 0
         self.energy_part = None
+        self.sorted_gid = None   # int32 [G] depth order
+        self.inst_off = None     # int64 [G+1] instances per depth rank (pre-sort order)
+        self.post_of_pre = None  # int32 [n_inst]
+        self.rowcnt = None       # uint8 [n_inst*16] entries per (instance, pixel row)
 
 
 def project_and_bin(scene: GaussianScene, frame: ViewFrame, cfg_s: _lib.SlmRastCfg, err: torch.Tensor,
@@ -174,16 +179,31 @@ def project_and_bin(scene: GaussianScene, frame: ViewFrame, cfg_s: _lib.SlmRastC
     tile_bits = _bits(n_tiles)
     ik = _empty(total, torch.int64, dev)
     iv = _empty(total, torch.int32, dev)
+    ig = _empty(total, torch.int32, dev)
     call("slm_tile_emit", ptr(sgid), ptr(inst_off), G, ptr(splats), frame.tiles_x, frame.tiles_y, rank_bits,
-         ptr(ik), ptr(iv), stream_ptr())
+         ptr(ik), ptr(iv), ptr(ig), stream_ptr())
     sk = torch.empty_like(ik)
     sv = torch.empty_like(iv)
     sort_u64(ik, sk, iv, sv, total, 0, rank_bits + tile_bits)
     ranges = torch.empty(2 * n_tiles, dtype=torch.int32, device=dev)
     call("slm_tile_ranges", ptr(sk), total, rank_bits, ptr(ranges), n_tiles, stream_ptr())
-    frame.inst_gid = sv
+    inst_gid = _empty(total, torch.int32, dev)
+    post_of_pre = _empty(total, torch.int32, dev)
+    call("slm_tile_post", ptr(sv), ptr(ig), total, ptr(inst_gid), ptr(post_of_pre), stream_ptr())
+    frame.inst_gid = inst_gid
     frame.ranges = ranges
+    frame.sorted_gid = sgid
+    frame.inst_off = inst_off
+    frame.post_of_pre = post_of_pre
     return skeys, sgid
+
+
+def inst_base(scene: GaussianScene, frame: ViewFrame, pair_cnt=None, base_out=None):
+    """Per-(view, gaussian) entry counts and/or the row-major run offsets of
+    each (tile instance, pixel row) inside its gaussian-order pair block."""
+    call("slm_inst_base", ptr(frame.sorted_gid), ptr(frame.inst_off), scene.num_gaussians, ptr(frame.splats),
+         frame.tiles_x, frame.tiles_y, ptr(frame.post_of_pre), ptr(frame.rowcnt), ptr(base_out), ptr(pair_cnt),
+         stream_ptr())
 
 
 def raster_args(frame: ViewFrame, cfg_s) -> _lib.SlmRasterArgs:
@@ -310,11 +330,12 @@ class CacheSet:
             hw = cam.num_pixels
             fr.rgb = torch.empty(hw * 3, dtype=torch.float64, device=dev)
             fr.t_final = torch.empty(hw, dtype=torch.float64, device=dev)
+            fr.rowcnt = torch.zeros(max(fr.n_inst, 1) * TILE, dtype=torch.uint8, device=dev)
             a = raster_args(fr, cfg_s)
             a.px_count = C.c_void_p(self.px_count.data_ptr() + fr.pix_base * 4)
-            a.rgb, a.t_final = ptr(fr.rgb), ptr(fr.t_final)
-            a.pair_cnt = C.c_void_p(self.pair_cnt.data_ptr() + v * G * 4)
+            a.rgb, a.t_final, a.rowcnt = ptr(fr.rgb), ptr(fr.t_final), ptr(fr.rowcnt)
             call("slm_raster_count", _lib.byref(a), stream_ptr())
+            inst_base(scene, fr, pair_cnt=self.pair_cnt[v * G:(v + 1) * G])
             T.tick("raster_count")
             if have_res:
                 ex = {} if residual_exports else None
@@ -351,18 +372,18 @@ class CacheSet:
 
         # ---- pairs -----------------------------------------------------------
         VG = V * G
-        cntT = torch.zeros(VG + 1, dtype=torch.int64, device=dev)
-        flagT = torch.zeros(VG + 1, dtype=torch.int32, device=dev)
         cntV = torch.zeros(VG + 1, dtype=torch.int64, device=dev)
-        call("slm_pairs_prepare", ptr(self.pair_cnt), V, G, ptr(cntT), ptr(flagT), ptr(cntV), stream_ptr())
-        off_of = torch.empty_like(cntT)
-        scan_i64(cntT, off_of)
-        pair_of = torch.empty_like(flagT)
-        scan_i32(flagT, pair_of)
+        flagV = torch.zeros(VG + 1, dtype=torch.int32, device=dev)
+        flagT = torch.zeros(VG + 1, dtype=torch.int32, device=dev)
+        call("slm_pairs_prepare", ptr(self.pair_cnt), V, G, ptr(cntV), ptr(flagV), ptr(flagT), stream_ptr())
         vscan = torch.empty_like(cntV)
         scan_i64(cntV, vscan)
+        pair_of = torch.empty_like(flagV)
+        scan_i32(flagV, pair_of)
+        tscan = torch.empty_like(flagT)
+        scan_i32(flagT, tscan)
         self.n_pairs = int(pair_of[VG].item())
-        if int(off_of[VG].item()) != self.E:
+        if int(vscan[VG].item()) != self.E:
             raise RuntimeError("cache entry count mismatch between pixel and pair counts")
         Pn = self.n_pairs
         self.pair_off = torch.empty(Pn + 1, dtype=torch.int64, device=dev)
@@ -371,11 +392,15 @@ class CacheSet:
         self.pair_geo = _empty(Pn * _lib.PAIR_GEO_BYTES, torch.uint8, dev)
         pidx = torch.empty(VG, dtype=torch.int32, device=dev)
         self.gpo = torch.empty(G + 1, dtype=torch.int32, device=dev)
+        self.gp_list = _empty(Pn, torch.int32, dev)
         splats_all = torch.cat([f.splats for f in self.frames])
-        call("slm_pairs_emit", ptr(self.pair_cnt), V, G, ptr(pair_of), ptr(off_of), ptr(splats_all),
+        call("slm_pairs_emit", ptr(self.pair_cnt), V, G, ptr(pair_of), ptr(vscan), ptr(tscan), ptr(splats_all),
              ptr(self.pair_off), ptr(self.pair_gid), ptr(self.pair_vm), ptr(self.pair_geo), ptr(pidx), ptr(self.gpo),
-             Pn, self.E, stream_ptr())
-        del cntT, flagT, off_of, pair_of, splats_all
+             ptr(self.gp_list), Pn, self.E, stream_ptr())
+        # first pair of each view (pairs are view-major)
+        self.view_pair_base = [int(x) for x in pair_of[torch.tensor([v * G for v in range(V)] + [VG],
+                                                                     device=dev)].cpu().tolist()]
+        del cntV, flagV, flagT, vscan, pair_of, tscan, splats_all
 
         T.tick("segments_pairs")
         # ---- FILL phase: pixel-order records, then gaussian order ------------
@@ -391,43 +416,27 @@ class CacheSet:
         self.chunk_seg_pix = _empty(n_chunks, torch.int32, dev)
         self.chunk_seg_gau = _empty(n_chunks, torch.int32, dev)
         self.g_src = _empty(E, torch.int32, dev) if keep_source_index else None
-        Gbits = _bits(G)
         for v, fr in enumerate(self.frames):
-            e0, e1 = view_off[v], view_off[v + 1]
-            Ev = e1 - e0
-            ent_gid = _empty(Ev, torch.int32, dev)
-            ent_xy = _empty(Ev, torch.int32, dev)
+            e0 = view_off[v]
+            base = _empty(fr.n_inst * TILE, torch.int32, dev)
+            inst_base(scene, fr, base_out=base)
+            T.tick("gauss_order")
             a = raster_args(fr, cfg_s)
             a.rgb = ptr(fr.rgb)
             a.pix_off, a.pidx, a.seg_idx = ptr(self.pix_off), C.c_void_p(pidx.data_ptr() + v * G * 4), ptr(seg_idx)
+            a.pair_off, a.inst_base = ptr(self.pair_off), ptr(base)
             (a.rec_idx, a.rec_ae, a.rec_at, a.rec_d0, a.rec_d1, a.rec_d2) = [ptr(t) for t in self.pix_rec]
-            a.ent_gid, a.ent_xy = ptr(ent_gid), ptr(ent_xy)
-            a.view_entry_base = e0
             a.chunk_seg = ptr(self.chunk_seg_pix)
+            (a.g_idx, a.g_ae, a.g_at, a.g_d0, a.g_d1, a.g_d2) = [ptr(t) for t in self.gau_rec]
+            a.g_chunk_seg = ptr(self.chunk_seg_gau)
+            a.g_src = ptr(self.g_src) if self.g_src is not None else None
+            a.view_entry_base = e0
             call("slm_raster_fill", _lib.byref(a), stream_ptr())
             T.tick("raster_fill")
-            if Ev == 0:
-                continue
-            iota = _empty(Ev, torch.int32, dev)
-            call("slm_iota_u32", ptr(iota), Ev, stream_ptr())
-            sk = torch.empty_like(ent_gid)
-            sv = torch.empty_like(iota)
-            sort_u32(ent_gid, sk, iota, sv, Ev, 0, Gbits)
-            g = _lib.SlmGaussOrderArgs()
-            g.sorted_gid, g.sorted_src, g.ent_xy = ptr(sk), ptr(sv), ptr(ent_xy)
-            g.Ev, g.view_base, g.G, g.v = Ev, e0, G, v
-            g.pidx, g.pair_off, g.vscan = ptr(pidx), ptr(self.pair_off), ptr(vscan)
-            g.ae, g.at, g.d0, g.d1, g.d2 = [ptr(t) for t in self.pix_rec[1:]]
-            (g.g_idx, g.g_ae, g.g_at, g.g_d0, g.g_d1, g.g_d2) = [ptr(t) for t in self.gau_rec]
-            g.chunk_seg = ptr(self.chunk_seg_gau)
-            g.g_src = ptr(self.g_src) if self.g_src is not None else None
-            call("slm_gauss_scatter", _lib.byref(g), stream_ptr())
-            T.tick("gauss_order")
-            del ent_gid, ent_xy, iota, sk, sv
-        del pidx, vscan, seg_idx
+            del base
+        del pidx, seg_idx
         for fr in self.frames:  # keep images for exports; tile lists are not needed any more
-            fr.inst_gid = None
-            fr.ranges = None
+            fr.inst_gid = fr.ranges = fr.rowcnt = fr.post_of_pre = fr.inst_off = fr.sorted_gid = None
         # product scratch
         self.u = torch.empty(self.N * 4, dtype=f32, device=dev)
         self.pm = _empty(Pn * 12, f32, dev)
@@ -479,7 +488,7 @@ class CacheSet:
         s = self._stream("gaussian", 9)
         call("slm_apply_jt_pairs", _lib.byref(s), ptr(self.pair_geo), ptr(self.pair_vm), ptr(self.views_dev), ptr(u),
              ptr(self.pacc), stream_ptr())
-        call("slm_pair_backward", ptr(self.scene.x32()), self.G, self.scene.sh_degree, ptr(self.gpo),
+        call("slm_pair_backward", ptr(self.scene.x32()), self.G, self.scene.sh_degree, ptr(self.gpo), ptr(self.gp_list),
              ptr(self.pair_vm), ptr(self.cams_dev), ptr(self.pacc), 0, float(scale), ptr(p), ptr(M), float(lam),
              ptr(out), ptr(dot_part), stream_ptr())
         return out
@@ -510,7 +519,7 @@ class CacheSet:
             call("slm_diag_pairs", _lib.byref(s), ptr(self.pair_geo), ptr(self.pair_vm), ptr(self.views_dev),
                  ptr(self.gradr), ptr(mom), stream_ptr())
             M = torch.empty(self.G * self.P, dtype=torch.float32, device=self.device)
-            call("slm_pair_backward", ptr(self.scene.x32()), self.G, self.scene.sh_degree, ptr(self.gpo),
+            call("slm_pair_backward", ptr(self.scene.x32()), self.G, self.scene.sh_degree, ptr(self.gpo), ptr(self.gp_list),
                  ptr(self.pair_vm), ptr(self.cams_dev), ptr(mom), 1, 1.0, None, None, 0.0, ptr(M), None,
                  stream_ptr())
             del self._carry[_lib.DIAG_D]
@@ -547,12 +556,10 @@ class CacheSet:
         out = dict(pixel_ids=pixel, gaussian_ids=gid.astype(np.int64), alphas=alpha, alpha_eff=ae,
                    transmittances=T, dc_dalpha=dcda, dc_dcs=at, offsets=pix_off, head=(idx >> 31).astype(bool))
         # gaussian order of this view: its pairs' blocks in pair (= gid) order
-        pv = np.nonzero((pair_vm & 0xFFFF) == v)[0]
+        pv = np.arange(self.view_pair_base[v], self.view_pair_base[v + 1])   # pairs are view-major
+        assert np.all((pair_vm[pv] & 0xFFFF) == v)
         poff = self.pair_off[: self.n_pairs + 1].cpu().numpy()
-        if pv.size:
-            sel = np.concatenate([np.arange(poff[q], poff[q + 1]) for q in pv])
-        else:
-            sel = np.zeros(0, np.int64)
+        sel = np.arange(poff[pv[0]], poff[pv[-1] + 1]) if pv.size else np.zeros(0, np.int64)
         selt = torch.from_numpy(sel).to(self.device)
         gr = [t[selt].cpu().numpy() for t in self.gau_rec] if sel.size else [np.zeros(0)] * 6
         gidx = gr[0].view(np.uint32) if sel.size else np.zeros(0, np.uint32)

@@ -116,7 +116,7 @@ def render(scene: GaussianScene, camera: Camera, config: RenderConfig = DEFAULT_
     fr.rgb = torch.empty(hw * 3, dtype=torch.float64, device=dev)
     fr.t_final = torch.empty(hw, dtype=torch.float64, device=dev)
     a = raster_args(fr, cfg_s)
-    a.px_count, a.rgb, a.t_final, a.pair_cnt = ptr(cnt), ptr(fr.rgb), ptr(fr.t_final), ptr(pair_cnt)
+    a.px_count, a.rgb, a.t_final = ptr(cnt), ptr(fr.rgb), ptr(fr.t_final)
     call("slm_raster_count", _lib.byref(a), stream_ptr())
     splats = ProjectedSplats.from_bytes(fr.splats, G)
     image = fr.rgb.view(camera.height, camera.width, 3)

@@ -40,7 +40,6 @@ def test_struct_layouts():
     assert lib.slm_raster_args_size() == ctypes.sizeof(_lib.SlmRasterArgs)
     assert lib.slm_resid_args_size() == ctypes.sizeof(_lib.SlmResidArgs)
     assert lib.slm_wsr_stream_size() == ctypes.sizeof(_lib.SlmWsrStream)
-    assert lib.slm_gauss_order_args_size() == ctypes.sizeof(_lib.SlmGaussOrderArgs)
     assert lib.slm_splat_size() == 96 and lib.slm_pair_geo_size() == 32
     assert lib.slm_carry_bytes(9) == 44
 
