@@ -10,6 +10,12 @@
  * Python API (`splatlm.*`); the "replaces" notes cite the reference function
  * each call implements.  Reference paths are relative to
  * /root/reference/pkg/src/splatlm/.
+ *
+ * Cache layout ("runs"): a run is one (tile, splat) pair of a view with at
+ * least one kept pixel; runs are numbered (view, tile, depth order) and each
+ * run's entries are stored contiguously in tile-local pixel order, with a
+ * 256-bit mask of the kept pixels.  Records are SoA float32 {alpha_eff,
+ * alpha*T, dc/dalpha[3]} plus a uint8 tile-local pixel index (21 B/entry).
  */
 #ifndef SPLATLM_B200_H
 #define SPLATLM_B200_H
@@ -79,34 +85,24 @@ typedef struct {
 
 /* rasteriser launch arguments (both passes) */
 typedef struct {
-  const slm_u2* tile_range;
-  const uint32_t* inst_gid;
+  const slm_u2* tile_range;   /* [n_tiles] instance range of each tile */
+  const uint32_t* inst_gid;   /* [n_inst] gaussian of each (tile, depth) instance */
   const SlmSplat* splats;
   int W, H, tiles_x;
   long long pix_base;
   SlmRastCfg cfg;
   /* COUNT outputs */
-  uint32_t* px_count;   /* [HW] entries per pixel */
-  double* rgb;          /* [HW*3] rendered colour incl. background (FILL: input) */
-  double* t_final;      /* [HW] */
-  uint8_t* rowcnt;      /* [n_inst*16] entries per (tile instance, pixel row); may be NULL */
-  /* FILL inputs */
-  const long long* pix_off;   /* subset-global pixel-order offsets, indexed by gp */
-  const int* pidx;            /* [G] pair index of (this view, g) */
-  const int* seg_idx;         /* [subset pixels] ordinal among non-empty pixels */
-  const long long* pair_off;  /* [P+1] gaussian-order pair offsets */
-  const uint32_t* inst_base;  /* [n_inst*16] offset of each (instance, row) run in its pair */
-  /* FILL outputs: pixel-order records */
-  uint32_t* rec_idx;
+  uint32_t* px_count;         /* [HW] entries per pixel */
+  double* rgb;                /* [HW*3] rendered colour incl. background (FILL: input) */
+  double* t_final;            /* [HW] */
+  uint32_t* inst_mask;        /* [n_inst*8] keep mask per instance (COUNT out, FILL in) */
+  /* FILL: run-ordered cache records */
+  const long long* inst_start;  /* [n_inst] first entry of the instance's run */
   float *rec_ae, *rec_at, *rec_d0, *rec_d1, *rec_d2;
-  int* chunk_seg;
-  /* FILL outputs: gaussian-order records */
-  uint32_t* g_idx;
-  float *g_ae, *g_at, *g_d0, *g_d1, *g_d2;
-  int* g_chunk_seg;
-  int* g_src;                 /* optional source_index (view-local pixel-order position) */
+  uint8_t* rec_pix;           /* tile-local pixel index (16 * ly + lx) */
+  /* FILL: optional pixel-order Traversals export (rasterizer.py:209-243) */
+  const long long* pix_off;
   long long view_entry_base;
-  /* optional traversal export (rasterizer.py:209-243), view-local entry index */
   long long* trav_gid;
   double* trav_alpha;
   double* trav_T;
@@ -132,15 +128,49 @@ typedef struct {
   double *o_gradr, *o_cgrad, *o_rabs, *o_rssim, *o_drabs, *o_drssim;
 } SlmResidArgs;
 
-/* one cache record stream (pixel or gaussian order) for the product kernels */
+/* tile-parallel product kernels (applyJ, applyJT partials, diag sums): one
+ * CTA per tile of the subset, warps over the tile's runs */
 typedef struct {
-  const uint32_t* idx;
+  const SlmView* views;
+  const int* view_tile_base; /* [n_views+1] first global tile of each view */
+  int n_views;
+  int n_tiles;
+  const int* tile_run_off;   /* [n_tiles+1] */
+  const int* tile_chunk_off; /* [n_tiles+1] chunk table (slm_tile_chunks) */
+  const int* chunk_run;      /* [n_chunks+1] first run of each chunk */
+  const long long* run_start;/* [R+1] (+2 padding slots) */
+  const int* run_q;          /* pair of each run */
+  const uint32_t* run_tile;  /* view << 24 | tile */
+  const float* run_par;      /* [R*16] per-product run parameters (slm_run_params) */
+  const SlmPairGeo* geo;
+  const void* pm;            /* applyJ: per-pair forward chain (slm_pair_forward), 48 B each */
+  const float* ptab;         /* diag: per-pair coefficient tables (slm_pair_tables) */
   const float *ae, *at, *d0, *d1, *d2;
-  long long E;
-  const int* chunk_seg;
-  void* head; /* carry scratch, n_chunks * slm_carry_bytes(D) */
-  void* tail;
-} SlmWsrStream;
+  const uint8_t* pix;
+  const slm_f4* gradr;       /* applyJ: weighting (NULL: unweighted u_hat); diag: grad_r_sq */
+  const slm_f4* u;           /* applyJT input, per pixel */
+  slm_f4* u_out;             /* applyJ output, per pixel */
+  float* out;                /* applyJT [R*9] / diag [R*14] run partials */
+} SlmTileArgs;
+
+/* per-gaussian backward chain */
+typedef struct {
+  const float* xs; /* scene, attribute-major fp32 */
+  long long G;
+  const int* gpo;           /* [G+1] gaussian -> pairs CSR */
+  const int* gp_list;
+  const int* pair_run_off;  /* [P+1] pair -> runs CSR (tile order) */
+  const int* pair_runs;
+  const uint32_t* pair_vm;  /* view | clamp bits << 16 */
+  const SlmCamera* cams;
+  const float* acc;         /* run partials (9 or 14 per run) */
+  float scale;
+  const float* p;           /* optional: adds lam * max(M,1e-12) * p and p.out partials */
+  const float* Mdiag;
+  float lam;
+  float* out;
+  double* dot_part;
+} SlmBackArgs;
 
 /* ---- sizes (ctypes layout checks) --------------------------------------- */
 int slm_camera_size(void);
@@ -150,8 +180,9 @@ int slm_pair_geo_size(void);
 int slm_view_size(void);
 int slm_raster_args_size(void);
 int slm_resid_args_size(void);
-int slm_wsr_stream_size(void);
-long long slm_carry_bytes(int D);
+int slm_tile_args_size(void);
+int slm_back_args_size(void);
+int slm_diag_tab_floats(void);
 
 /* ---- projection / rasterisation ------------------------------------------
  * replaces project_scene (rasterizer.py:116-165): fp64 splats of one view,
@@ -175,24 +206,33 @@ int slm_tile_emit(const uint32_t* sorted_gid, const unsigned long long* inst_off
                   uint32_t* inst_g_pre, cudaStream_t s);
 int slm_tile_post(const uint32_t* sorted_pre, const uint32_t* inst_g_pre, long long n, uint32_t* inst_gid,
                   uint32_t* post_of_pre, cudaStream_t s);
-/* per-(view, gaussian) entry counts (pair_cnt) and, with base_out, the
- * row-major run offsets that place each entry in its gaussian-order pair
- * block -- the stable (gid, pixel) order of jacobian.py:96 without a sort */
-int slm_inst_base(const uint32_t* sorted_gid, const unsigned long long* inst_off, long long G, const SlmSplat* splats,
-                  int tiles_x, int tiles_y, const uint32_t* post_of_pre, const uint8_t* rowcnt, uint32_t* base_out,
-                  int* pair_cnt, cudaStream_t s);
 int slm_tile_ranges(const unsigned long long* keys, long long n, int rank_bits, slm_u2* ranges, int n_tiles,
                     cudaStream_t s);
-/* render (rasterizer.py:319-358): COUNT pass = image, T_final, per-pixel and
- * per-(view, gaussian) entry counts; FILL pass = pixel-order cache records
- * (build_cache, jacobian.py:383-409) and optionally the Traversals arrays */
+/* render (rasterizer.py:319-358): COUNT pass = image, T_final, per-pixel
+ * counts and per-instance keep masks; FILL pass = run-ordered cache records
+ * (build_cache, jacobian.py:383-409) and/or the Traversals arrays */
 int slm_raster_count(const SlmRasterArgs* a, cudaStream_t s);
 int slm_raster_fill(const SlmRasterArgs* a, cudaStream_t s);
+/* runs: per-instance counts (+ per-(view,gaussian) counts), the run table,
+ * runs per tile and the pair -> runs CSR (filled in a fixed order) */
+int slm_inst_count(const uint32_t* mask, const uint32_t* inst_gid, long long n, long long* cnt, int* used,
+                   int* pair_cnt, cudaStream_t s);
+int slm_runs_emit(const uint32_t* mask, const uint32_t* inst_gid, const int* used, const int* run_of,
+                  const long long* ent_of, long long ibase, long long n, const int* pidx, long long* run_start,
+                  int* run_q, uint32_t* run_mask, int* pair_nruns, long long* inst_start, cudaStream_t s);
+int slm_tile_runs(const slm_u2* ranges, int n_tiles, const int* used, const int* run_of, long long ibase, int view,
+                  int* tile_nruns, uint32_t* run_tile, cudaStream_t s);
+int slm_pair_runs(const uint32_t* sorted_gid, const unsigned long long* inst_off, long long G,
+                  const uint32_t* post_of_pre, const int* used, const int* run_of, long long ibase, const int* pidx,
+                  const int* pair_run_off, int* pair_runs, cudaStream_t s);
 
 /* ---- residuals: compute_residuals (residuals.py:249-296) ----------------- */
 int slm_residuals(const SlmResidArgs* a, int blocks, cudaStream_t s);
 
-/* ---- cache assembly ------------------------------------------------------ */
+/* ---- scans / pairs ----------------------------------------------------------
+ * (view, gaussian) pairs in (view, gid) order: counts -> flags/scans, then
+ * pair geometry / maps and the gid-major CSR (gpo, gp_list) used by the
+ * per-gaussian backward chain */
 long long slm_scan_i64_workspace(long long n);
 int slm_scan_i64(void* ws, long long wsb, const long long* in, long long* out, long long n, cudaStream_t s);
 long long slm_scan_i32_workspace(long long n);
@@ -202,39 +242,38 @@ int slm_sort_pairs_u32(void* ws, long long wsb, const uint32_t* kin, uint32_t* k
                        uint32_t* vout, long long n, int begin_bit, int end_bit, cudaStream_t s);
 int slm_iota_u32(uint32_t* out, long long n, cudaStream_t s);
 int slm_px_prepare(const uint32_t* cnt, long long n, long long* cnt64, int* nonempty, cudaStream_t s);
-int slm_px_segments(const uint32_t* cnt, const int* seg_idx, long long n, const SlmCamera* cams_dev, int n_views,
-                    slm_u2* seg_info, cudaStream_t s);
-/* (view, gaussian) pairs in (view, gid) order: counts -> flags/scans, then
- * pair offsets / geometry / maps and the gid-major CSR (gpo, gp_list) used by
- * the per-gaussian backward chain.  Together with slm_inst_base and the FILL
- * pass this replaces sort_cache_by_gaussians (jacobian.py:93-105). */
 int slm_pairs_prepare(const int* cnt, int V, long long G, long long* cntV, int* flagV, int* flagT, cudaStream_t s);
 int slm_pairs_emit(const int* cnt, int V, long long G, const int* pair_of, const long long* vscan, const int* tscan,
                    const SlmSplat* splats, long long* pair_off, int* pair_gid, uint32_t* pair_vm, SlmPairGeo* geo,
                    int* pidx, int* gpo, int* gp_list, int n_pairs, long long n_entries, cudaStream_t s);
 
-/* ---- products --------------------------------------------------------------
+/* ---- products ----------------------------------------------------------------
  * apply_j (jacobian.py:419-455) fused with weight_residuals (458-464) when
- * gradr != NULL; pm holds the per-pair forward chain from slm_pair_forward */
-int slm_apply_j(const SlmWsrStream* pix, const slm_u2* seg_info, const SlmPairGeo* geo, const void* pm,
-                const slm_f4* gradr, slm_f4* u, cudaStream_t s);
-/* apply_jt (jacobian.py:467-483), first half: 9 partials per pair */
-int slm_apply_jt_pairs(const SlmWsrStream* gs, const SlmPairGeo* geo, const uint32_t* pair_vm, const SlmView* views,
-                       const slm_f4* u, float* acc, cudaStream_t s);
-/* diag_jtj (jacobian.py:486-512), first half: 42 moments per pair */
-int slm_diag_pairs(const SlmWsrStream* gs, const SlmPairGeo* geo, const uint32_t* pair_vm, const SlmView* views,
-                   const slm_f4* gradr, float* mom, cudaStream_t s);
+ * a->gradr != NULL; one CTA per tile of the subset */
+int slm_apply_j(const SlmTileArgs* a, cudaStream_t s);
+/* apply_jt (jacobian.py:467-483), first half: 9 partials per run from a->u */
+int slm_apply_jt_runs(const SlmTileArgs* a, cudaStream_t s);
+/* fused apply_jt(weight_residuals(apply_j(p))) first half, tile by tile: u
+ * stays in shared memory, the cache is streamed from HBM once */
+int slm_jtwj_runs(const SlmTileArgs* a, cudaStream_t s);
+/* per-product run parameter records (with_m: forward chain m included) and
+ * the per-tile chunk table (fill=0: counts per tile, fill=1: chunk_run) */
+int slm_run_params(const SlmTileArgs* a, long long n_runs, int with_m, float* out, cudaStream_t s);
+int slm_tile_chunks(const int* tile_run_off, int n_tiles, const long long* run_start, const int* tile_chunk_off,
+                    int* out, int fill, cudaStream_t s);
+/* diag_jtj (jacobian.py:486-512), first half: per-pair coefficient tables,
+ * then 14 sums per run (a->gradr = grad_r_sq, a->ptab = tables) */
+int slm_pair_tables(const float* xs, long long G, int sh_degree, const int* pair_gid, const uint32_t* pair_vm,
+                    const SlmCamera* cams, int n_pairs, float* tab, cudaStream_t s);
+int slm_diag_runs(const SlmTileArgs* a, cudaStream_t s);
 /* forward chain m = dy/dx p per pair; p[a*sa + g*sg] (either layout) */
 int slm_pair_forward(const float* xs, long long G, int sh_degree, const int* pair_gid, const uint32_t* pair_vm,
                      const SlmCamera* cams, int n_pairs, const float* p, long long sa, long long sg, void* pm,
                      cudaStream_t s);
 /* backward chain per gaussian, attribute-major out (jacobian.py:314-353):
- * mode 0 from J^T partials, mode 1 from diag moments; out = scale * chain
- * (+ lam * max(M, 1e-12) * p and p.out block partials when p != NULL) */
+ * mode 0 from J^T run partials, mode 1 from diag run sums */
 int slm_backward_blocks(long long G);
-int slm_pair_backward(const float* xs, long long G, int sh_degree, const int* gpo, const int* gp_list,
-                      const uint32_t* pair_vm, const SlmCamera* cams, const float* acc, int mode, float scale,
-                      const float* p, const float* Mdiag, float lam, float* out, double* dot_part, cudaStream_t s);
+int slm_pair_backward(const SlmBackArgs* a, int mode, int sh_degree, cudaStream_t s);
 
 /* ---- PCG (Alg. 1; SPEC pcg_solve 391-399) ------------------ */
 int slm_vec_blocks(void);

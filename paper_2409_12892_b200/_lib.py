@@ -41,13 +41,11 @@ class SlmView(C.Structure):
 class SlmRasterArgs(C.Structure):
     _fields_ = [("tile_range", c_vp), ("inst_gid", c_vp), ("splats", c_vp),
                 ("W", c_i), ("H", c_i), ("tiles_x", c_i), ("pix_base", c_ll), ("cfg", SlmRastCfg),
-                ("px_count", c_vp), ("rgb", c_vp), ("t_final", c_vp), ("rowcnt", c_vp),
-                ("pix_off", c_vp), ("pidx", c_vp), ("seg_idx", c_vp), ("pair_off", c_vp), ("inst_base", c_vp),
-                ("rec_idx", c_vp), ("rec_ae", c_vp), ("rec_at", c_vp), ("rec_d0", c_vp), ("rec_d1", c_vp),
-                ("rec_d2", c_vp), ("chunk_seg", c_vp),
-                ("g_idx", c_vp), ("g_ae", c_vp), ("g_at", c_vp), ("g_d0", c_vp), ("g_d1", c_vp), ("g_d2", c_vp),
-                ("g_chunk_seg", c_vp), ("g_src", c_vp), ("view_entry_base", c_ll),
-                ("trav_gid", c_vp), ("trav_alpha", c_vp), ("trav_T", c_vp)]
+                ("px_count", c_vp), ("rgb", c_vp), ("t_final", c_vp), ("inst_mask", c_vp),
+                ("inst_start", c_vp), ("rec_ae", c_vp), ("rec_at", c_vp), ("rec_d0", c_vp), ("rec_d1", c_vp),
+                ("rec_d2", c_vp), ("rec_pix", c_vp),
+                ("pix_off", c_vp), ("view_entry_base", c_ll), ("trav_gid", c_vp), ("trav_alpha", c_vp),
+                ("trav_T", c_vp)]
 
 
 class SlmResidArgs(C.Structure):
@@ -59,32 +57,46 @@ class SlmResidArgs(C.Structure):
                 ("o_drabs", c_vp), ("o_drssim", c_vp)]
 
 
-class SlmWsrStream(C.Structure):
-    _fields_ = [("idx", c_vp), ("ae", c_vp), ("at", c_vp), ("d0", c_vp), ("d1", c_vp), ("d2", c_vp),
-                ("E", c_ll), ("chunk_seg", c_vp), ("head", c_vp), ("tail", c_vp)]
+class SlmTileArgs(C.Structure):
+    _fields_ = [("views", c_vp), ("view_tile_base", c_vp), ("n_views", c_i), ("n_tiles", c_i),
+                ("tile_run_off", c_vp), ("tile_chunk_off", c_vp), ("chunk_run", c_vp),
+                ("run_start", c_vp), ("run_q", c_vp), ("run_tile", c_vp), ("run_par", c_vp),
+                ("geo", c_vp), ("pm", c_vp), ("ptab", c_vp),
+                ("ae", c_vp), ("at", c_vp), ("d0", c_vp), ("d1", c_vp), ("d2", c_vp), ("pix", c_vp),
+                ("gradr", c_vp), ("u", c_vp), ("u_out", c_vp), ("out", c_vp)]
+
+
+class SlmBackArgs(C.Structure):
+    _fields_ = [("xs", c_vp), ("G", c_ll), ("gpo", c_vp), ("gp_list", c_vp), ("pair_run_off", c_vp),
+                ("pair_runs", c_vp), ("pair_vm", c_vp), ("cams", c_vp), ("acc", c_vp), ("scale", c_f),
+                ("p", c_vp), ("Mdiag", c_vp), ("lam", c_f), ("out", c_vp), ("dot_part", c_vp)]
 
 
 SPLAT_BYTES = 96
 PAIR_GEO_BYTES = 32
 PAIR_M_BYTES = 48
-DIAG_D = 42
+JT_D = 9
+DIAG_D = 14
 
 # name -> (restype, argtypes)
 _SIGS = {
     "slm_camera_size": (c_i, []), "slm_rastcfg_size": (c_i, []), "slm_splat_size": (c_i, []),
     "slm_pair_geo_size": (c_i, []), "slm_view_size": (c_i, []), "slm_raster_args_size": (c_i, []),
-    "slm_resid_args_size": (c_i, []),
-    "slm_wsr_stream_size": (c_i, []), "slm_carry_bytes": (c_ll, [c_i]),
+    "slm_resid_args_size": (c_i, []), "slm_tile_args_size": (c_i, []), "slm_back_args_size": (c_i, []),
+    "slm_diag_tab_floats": (c_i, []),
     "slm_preprocess": (c_i, [c_vp, c_ll, c_i, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "slm_sort_pairs_u64_workspace": (c_ll, [c_ll]),
     "slm_sort_pairs_u64": (c_i, [c_vp, c_ll, c_vp, c_vp, c_vp, c_vp, c_ll, c_i, c_i, c_vp]),
     "slm_tile_count": (c_i, [c_vp, c_vp, c_ll, c_vp, c_i, c_i, c_vp, c_vp]),
     "slm_tile_emit": (c_i, [c_vp, c_vp, c_ll, c_vp, c_i, c_i, c_i, c_vp, c_vp, c_vp, c_vp]),
     "slm_tile_post": (c_i, [c_vp, c_vp, c_ll, c_vp, c_vp, c_vp]),
-    "slm_inst_base": (c_i, [c_vp, c_vp, c_ll, c_vp, c_i, c_i, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "slm_tile_ranges": (c_i, [c_vp, c_ll, c_i, c_vp, c_i, c_vp]),
     "slm_raster_count": (c_i, [c_vp, c_vp]),
     "slm_raster_fill": (c_i, [c_vp, c_vp]),
+    "slm_inst_count": (c_i, [c_vp, c_vp, c_ll, c_vp, c_vp, c_vp, c_vp]),
+    "slm_runs_emit": (c_i, [c_vp, c_vp, c_vp, c_vp, c_vp, c_ll, c_ll, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "slm_tile_runs": (c_i, [c_vp, c_i, c_vp, c_vp, c_ll, c_i, c_vp, c_vp, c_vp]),
+    "slm_pair_runs": (c_i, [c_vp, c_vp, c_ll, c_vp, c_vp, c_vp, c_ll, c_vp, c_vp, c_vp, c_vp]),
     "slm_residuals": (c_i, [c_vp, c_i, c_vp]),
     "slm_scan_i64_workspace": (c_ll, [c_ll]),
     "slm_scan_i64": (c_i, [c_vp, c_ll, c_vp, c_vp, c_ll, c_vp]),
@@ -94,17 +106,19 @@ _SIGS = {
     "slm_sort_pairs_u32": (c_i, [c_vp, c_ll, c_vp, c_vp, c_vp, c_vp, c_ll, c_i, c_i, c_vp]),
     "slm_iota_u32": (c_i, [c_vp, c_ll, c_vp]),
     "slm_px_prepare": (c_i, [c_vp, c_ll, c_vp, c_vp, c_vp]),
-    "slm_px_segments": (c_i, [c_vp, c_vp, c_ll, c_vp, c_i, c_vp, c_vp]),
     "slm_pairs_prepare": (c_i, [c_vp, c_i, c_ll, c_vp, c_vp, c_vp, c_vp]),
     "slm_pairs_emit": (c_i, [c_vp, c_i, c_ll, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                              c_i, c_ll, c_vp]),
-    "slm_apply_j": (c_i, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
-    "slm_apply_jt_pairs": (c_i, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
-    "slm_diag_pairs": (c_i, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "slm_apply_j": (c_i, [c_vp, c_vp]),
+    "slm_apply_jt_runs": (c_i, [c_vp, c_vp]),
+    "slm_jtwj_runs": (c_i, [c_vp, c_vp]),
+    "slm_run_params": (c_i, [c_vp, c_ll, c_i, c_vp, c_vp]),
+    "slm_tile_chunks": (c_i, [c_vp, c_i, c_vp, c_vp, c_vp, c_i, c_vp]),
+    "slm_pair_tables": (c_i, [c_vp, c_ll, c_i, c_vp, c_vp, c_vp, c_i, c_vp, c_vp]),
+    "slm_diag_runs": (c_i, [c_vp, c_vp]),
     "slm_pair_forward": (c_i, [c_vp, c_ll, c_i, c_vp, c_vp, c_vp, c_i, c_vp, c_ll, c_ll, c_vp, c_vp]),
     "slm_backward_blocks": (c_i, [c_ll]),
-    "slm_pair_backward": (c_i, [c_vp, c_ll, c_i, c_vp, c_vp, c_vp, c_vp, c_vp, c_i, c_f, c_vp, c_vp, c_f, c_vp,
-                                c_vp, c_vp]),
+    "slm_pair_backward": (c_i, [c_vp, c_i, c_i, c_vp]),
     "slm_vec_blocks": (c_i, []),
     "slm_pcg_pupdate": (c_i, [c_vp, c_vp, c_vp, c_vp, c_ll, c_vp]),
     "slm_pcg_update": (c_i, [c_i, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i, c_vp, c_ll, c_vp]),
@@ -140,7 +154,7 @@ def load():
         fn.argtypes = args
     checks = {"slm_camera_size": SlmCamera, "slm_rastcfg_size": SlmRastCfg, "slm_view_size": SlmView,
               "slm_raster_args_size": SlmRasterArgs, "slm_resid_args_size": SlmResidArgs,
-              "slm_wsr_stream_size": SlmWsrStream}
+              "slm_tile_args_size": SlmTileArgs, "slm_back_args_size": SlmBackArgs}
     for fn, st in checks.items():
         if getattr(lib, fn)() != C.sizeof(st):
             raise SplatLMError(f"ABI mismatch: {fn} = {getattr(lib, fn)()} vs ctypes {C.sizeof(st)}")
@@ -174,9 +188,20 @@ def ptr(t: torch.Tensor | None):
     return C.c_void_p(t.data_ptr())
 
 
+def off(t: torch.Tensor, elems: int):
+    """Pointer to element `elems` of a contiguous tensor."""
+    return C.c_void_p(t.data_ptr() + int(elems) * t.element_size())
+
+
 def stream_ptr():
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
 def byref(s):
     return C.byref(s)
+
+
+def struct_tensor(arr, device) -> torch.Tensor:
+    """Copy a ctypes array of structs to a device byte tensor."""
+    raw = bytes(C.string_at(C.addressof(arr), C.sizeof(arr)))
+    return torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(device)

@@ -19,7 +19,7 @@ HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
 LIB = HERE / "libsplatlm_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["raster.cu", "residuals.cu", "cache.cu", "products.cu", "pcg.cu"]
+SOURCES = ["raster.cu", "residuals.cu", "cache.cu", "jtj.cu", "stream.cu", "pcg.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC", "-I", str(HERE.parent / "include"), "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
 

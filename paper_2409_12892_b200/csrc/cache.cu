@@ -67,19 +67,6 @@ __global__ void k_px_prepare(const uint32_t* __restrict__ cnt, long long n, long
   }
 }
 
-// seg_info[seg] = {gp, (y << 16) | x}
-__global__ void k_px_segments(const uint32_t* __restrict__ cnt, const int* __restrict__ seg_idx, long long n,
-                              const SlmCamera* __restrict__ cams, int n_views, uint2* __restrict__ seg_info) {
-  for (long long gp = blockIdx.x * (long long)blockDim.x + threadIdx.x; gp < n; gp += (long long)gridDim.x * blockDim.x) {
-    if (cnt[gp] == 0) continue;
-    int v = 0;
-    while (v + 1 < n_views && cams[v + 1].pix_base <= gp) ++v;
-    long long p = gp - cams[v].pix_base;
-    int y = (int)(p / cams[v].W), x = (int)(p % cams[v].W);
-    seg_info[seg_idx[gp]] = make_uint2((uint32_t)gp, ((uint32_t)y << 16) | (uint32_t)x);
-  }
-}
-
 // ---------------------------------------------------------------------------
 // pairs: (gaussian, view) with >= 1 entry, numbered in (view, gid) order so
 // that one view's pairs -- and the gaussian-order records, u and grad_r_sq
@@ -143,12 +130,6 @@ extern "C" {
 
 int slm_px_prepare(const uint32_t* cnt, long long n, long long* cnt64, int* nonempty, cudaStream_t s) {
   k_px_prepare<<<slm_blocks(n, 256), 256, 0, s>>>(cnt, n, cnt64, nonempty);
-  return slm_cuda_status();
-}
-
-int slm_px_segments(const uint32_t* cnt, const int* seg_idx, long long n, const SlmCamera* cams_dev, int n_views,
-                    uint2* seg_info, cudaStream_t s) {
-  k_px_segments<<<slm_blocks(n, 256), 256, 0, s>>>(cnt, seg_idx, n, cams_dev, n_views, seg_info);
   return slm_cuda_status();
 }
 

@@ -1,0 +1,315 @@
+// diag(J^T W J), the per-pair chain kernels and the per-gaussian backward
+// chain (ref: jacobian.py:159-353, 486-512).  The J / J^T entry products live
+// in stream.cu.
+#include "chain.cuh"
+
+#define NW 8          // warps per CTA (diag)
+#define DIAG_TAB 48   // floats per pair coefficient table (diag)
+#define DIAG_RUN_D 14
+#define TBD 256
+
+__device__ __forceinline__ int view_of_tile(const int* __restrict__ vtb, int n_views, int t) {
+  int v = 0;
+  while (v + 1 < n_views && vtb[v + 1] <= t) ++v;
+  return v;
+}
+
+__device__ __forceinline__ int rs16_slot(int lane) {
+  return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+}
+// reduce-scatter of 16 per-lane values in 16 shuffles; lanes 2i, 2i+1 end
+// with the warp sum of value rs16_slot(lane); fixed pattern -> deterministic
+__device__ __forceinline__ float warp_reduce_scatter16(const float (&v)[16], int lane) {
+  const unsigned F = 0xffffffffu;
+  float w8[8], w4[4], w2[2];
+  const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4, u2 = lane & 2;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) w8[j] = (u16 ? v[j + 8] : v[j]) + __shfl_xor_sync(F, u16 ? v[j] : v[j + 8], 16);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) w4[j] = (u8 ? w8[j + 4] : w8[j]) + __shfl_xor_sync(F, u8 ? w8[j] : w8[j + 4], 8);
+#pragma unroll
+  for (int j = 0; j < 2; ++j) w2[j] = (u4 ? w4[j + 2] : w4[j]) + __shfl_xor_sync(F, u4 ? w4[j] : w4[j + 2], 4);
+  float w1 = (u2 ? w2[1] : w2[0]) + __shfl_xor_sync(F, u2 ? w2[0] : w2[1], 2);
+  return w1 + __shfl_xor_sync(F, w1, 1);
+}
+
+// ---------------------------------------------------------------------------
+// diag(J^T W J): per run, 11 geometry sums of grad_r_sq * (dc/dx_k)^2 and the
+// three channel sums grad_r_sq * (alpha T)^2 that the SH block needs
+// (ref: jacobian.py:496-508) -- exact squares per entry.  The per-pair
+// coefficient tables come from k_pair_tables (one thread per pair).
+// table layout: [0,15) k=0..2 x (dmu0, dmu1, dcov0, dcov1, dcov2);
+//               [15,36) k=3..9 x (dcov0, dcov1, dcov2); [36] dopa;
+//               [37,46) dcol[ch][j] (position columns)
+// ---------------------------------------------------------------------------
+template <int K>
+__global__ void __launch_bounds__(128) k_pair_tables(const float* __restrict__ xs, long long G,
+                                                     const int* __restrict__ pair_gid,
+                                                     const uint32_t* __restrict__ pair_vm,
+                                                     const SlmCamera* __restrict__ cams, int n_pairs,
+                                                     float* __restrict__ tab) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_pairs; q += gridDim.x * blockDim.x) {
+    const uint32_t vm = pair_vm[q];
+    Tab<K> T;
+    pair_tab<K>(xs, G, pair_gid[q], cams[vm & 0xffffu], vm >> 16, T);
+    float* o = tab + (size_t)q * DIAG_TAB;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      o[k * 5 + 0] = T.dmu[0][k];
+      o[k * 5 + 1] = T.dmu[1][k];
+      o[k * 5 + 2] = T.dcov[0][k];
+      o[k * 5 + 3] = T.dcov[1][k];
+      o[k * 5 + 4] = T.dcov[2][k];
+    }
+#pragma unroll
+    for (int k = 3; k < 10; ++k) {
+      o[15 + (k - 3) * 3 + 0] = T.dcov[0][k];
+      o[15 + (k - 3) * 3 + 1] = T.dcov[1][k];
+      o[15 + (k - 3) * 3 + 2] = T.dcov[2][k];
+    }
+    o[36] = T.dopa;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) o[37 + ch * 3 + j] = T.dcol[ch][j];
+    o[46] = 0.f;
+    o[47] = 0.f;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_diag_tile(SlmTileArgs A) {
+  __shared__ long long s_start[TBD + 1];
+  __shared__ int s_q[TBD];
+  __shared__ float s_geo[TBD * 6];
+  __shared__ float4 s_g[256];
+  __shared__ float s_tab[NW][DIAG_TAB];
+  const int t = blockIdx.x;
+  const int v = view_of_tile(A.view_tile_base, A.n_views, t);
+  const SlmView vw = A.views[v];
+  const int tiles_x = (vw.W + SLM_TILE - 1) / SLM_TILE;
+  const int lt = t - A.view_tile_base[v];
+  const int tx = lt % tiles_x, ty = lt / tiles_x;
+  const int r0 = A.tile_run_off[t], r1 = A.tile_run_off[t + 1];
+  const double ox = (double)(tx * SLM_TILE) + 0.5, oy = (double)(ty * SLM_TILE) + 0.5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (r1 == r0) return;
+  {
+    const int p = threadIdx.x;
+    const int px = tx * SLM_TILE + (p & 15), py = ty * SLM_TILE + (p >> 4);
+    s_g[p] = (px < vw.W && py < vw.H) ? A.gradr[vw.pix_base + (long long)py * vw.W + px]
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  for (int rb = r0; rb < r1; rb += TBD) {
+    const int nb = min(TBD, r1 - rb);
+    __syncthreads();
+    const int i = threadIdx.x;
+    if (i < nb) {
+      s_start[i] = A.run_start[rb + i];
+      const int q = A.run_q[rb + i];
+      s_q[i] = q;
+      const SlmPairGeo g = A.geo[q];
+      float* P = s_geo + i * 6;
+      P[0] = (float)(g.mx - ox);
+      P[1] = (float)(g.my - oy);
+      P[2] = g.ka; P[3] = g.kb; P[4] = g.kc; P[5] = g.inv_o;
+    }
+    if (i == 0) s_start[nb] = A.run_start[rb + nb];
+    __syncthreads();
+    for (int k = warp; k < nb; k += NW) {
+      const float* tq = A.ptab + (size_t)s_q[k] * DIAG_TAB;
+      __syncwarp();
+      for (int j = lane; j < DIAG_TAB; j += 32) s_tab[warp][j] = tq[j];
+      __syncwarp();
+      const float* D = s_tab[warp];
+      const long long st = s_start[k];
+      const int n = (int)(s_start[k + 1] - st);
+      const float* P = s_geo + k * 6;
+      const float p0 = P[0], p1 = P[1], ka = P[2], kb = P[3], kc = P[4], io = P[5];
+      float a[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) a[j] = 0.f;
+      for (int j = lane; j < n; j += 32) {
+        const long long e = st + j;
+        const float ae = A.ae[e], at = A.at[e];
+        const float dd[3] = {A.d0[e], A.d1[e], A.d2[e]};
+        const int pl = A.pix[e];
+        const float4 gr = s_g[pl];
+        const float grc[3] = {gr.x, gr.y, gr.z};
+        const float dx = (float)(pl & 15) - p0, dy = (float)(pl >> 4) - p1;
+        const float e1 = ka * dx + kb * dy;
+        const float e2 = kb * dx + kc * dy;
+        const float w0 = ae * e1, w1 = ae * e2, w2 = 0.5f * ae * e1 * e1, w3 = ae * e1 * e2;
+        const float w4 = 0.5f * ae * e2 * e2;
+#pragma unroll
+        for (int kk = 0; kk < 11; ++kk) {
+          float da;
+          if (kk < 3)
+            da = w0 * D[kk * 5] + w1 * D[kk * 5 + 1] + w2 * D[kk * 5 + 2] + w3 * D[kk * 5 + 3] + w4 * D[kk * 5 + 4];
+          else if (kk < 10)
+            da = w2 * D[15 + (kk - 3) * 3] + w3 * D[16 + (kk - 3) * 3] + w4 * D[17 + (kk - 3) * 3];
+          else
+            da = ae * io * D[36];
+          float s = 0.f;
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            const float dc = dd[ch] * da + (kk < 3 ? at * D[37 + ch * 3 + kk] : 0.f);
+            s += grc[ch] * dc * dc;
+          }
+          a[kk] += s;
+        }
+        const float at2 = at * at;
+        a[11] += grc[0] * at2;
+        a[12] += grc[1] * at2;
+        a[13] += grc[2] * at2;
+      }
+      const float s = warp_reduce_scatter16(a, lane);
+      const int slot = rs16_slot(lane);
+      if (!(lane & 1) && slot < DIAG_RUN_D) A.out[(size_t)(rb + k) * DIAG_RUN_D + slot] = s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// per-gaussian backward chain (ref: jacobian.py:314-353 / 506-510):
+//   MODE 0: out = scale * sum_pairs tab^T (sum_runs J^T partials)
+//   MODE 1: out = sum_pairs (sum_runs diag sums), SH block via basis^2
+// optional + lam * max(M, 1e-12) * p and fp64 p.out block partials (PCG)
+// ---------------------------------------------------------------------------
+template <int K, int MODE>
+__global__ void __launch_bounds__(128) k_pair_backward(SlmBackArgs A) {
+  __shared__ double sm[32];
+  constexpr int D = MODE == 0 ? 9 : DIAG_RUN_D;
+  const long long G = A.G;
+  double dot = 0.0;
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < G; g += (long long)gridDim.x * blockDim.x) {
+    float og[11], osh[3][K];
+#pragma unroll
+    for (int j = 0; j < 11; ++j) og[j] = 0.f;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch)
+#pragma unroll
+      for (int k = 0; k < K; ++k) osh[ch][k] = 0.f;
+    const int k0 = A.gpo[g], k1 = A.gpo[g + 1];
+    for (int kk = k0; kk < k1; ++kk) {  // this gaussian's pairs, in view order
+      const int q = A.gp_list[kk];
+      float a[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) a[j] = 0.f;
+      for (int rr = A.pair_run_off[q]; rr < A.pair_run_off[q + 1]; ++rr) {  // runs in tile order
+        const float* src = A.acc + (size_t)A.pair_runs[rr] * D;
+#pragma unroll
+        for (int j = 0; j < D; ++j) a[j] += src[j];
+      }
+      const uint32_t vm = A.pair_vm[q];
+      Tab<K> T;
+      pair_tab<K>(A.xs, G, g, A.cams[vm & 0xffffu], vm >> 16, T);
+      if (MODE == 0) {
+        const float col[3] = {a[6], a[7], a[8]};
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          og[j] += T.dmu[0][j] * a[0] + T.dmu[1][j] * a[1] + T.dcol[0][j] * col[0] + T.dcol[1][j] * col[1] +
+                   T.dcol[2][j] * col[2];
+#pragma unroll
+        for (int j = 0; j < 10; ++j) og[j] += T.dcov[0][j] * a[2] + T.dcov[1][j] * a[3] + T.dcov[2][j] * a[4];
+        og[10] += T.dopa * a[5];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+          const float s = col[ch] * T.mask[ch];
+#pragma unroll
+          for (int k = 0; k < K; ++k) osh[ch][k] += s * T.Y[k];
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 11; ++j) og[j] += a[j];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+          const float s = a[11 + ch] * T.mask[ch];
+#pragma unroll
+          for (int k = 0; k < K; ++k) osh[ch][k] += s * T.Y[k] * T.Y[k];
+        }
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < 11 + 3 * K; ++a) {
+      float v = A.scale * (a < 11 ? og[a] : osh[(a - 11) / K][(a - 11) % K]);
+      const long long i = (long long)a * G + g;
+      if (A.p) {
+        const float pv = A.p[i];
+        if (A.Mdiag) v += A.lam * fmaxf(A.Mdiag[i], 1e-12f) * pv;
+        dot += (double)pv * (double)v;
+      }
+      A.out[i] = v;
+    }
+  }
+  if (A.dot_part) {
+    double t = block_sum_d(dot, sm);
+    if (threadIdx.x == 0) A.dot_part[blockIdx.x] = t;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// C-ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int slm_view_size() { return (int)sizeof(SlmView); }
+int slm_tile_args_size() { return (int)sizeof(SlmTileArgs); }
+int slm_back_args_size() { return (int)sizeof(SlmBackArgs); }
+int slm_diag_tab_floats() { return DIAG_TAB; }
+
+int slm_pair_tables(const float* xs, long long G, int sh_degree, const int* pair_gid, const uint32_t* pair_vm,
+                    const SlmCamera* cams, int n_pairs, float* tab, cudaStream_t st) {
+  if (n_pairs <= 0) return SLM_OK;
+  unsigned b = slm_blocks(n_pairs, 128, 1LL << 30);
+  switch (sh_degree) {
+    case 0: k_pair_tables<1><<<b, 128, 0, st>>>(xs, G, pair_gid, pair_vm, cams, n_pairs, tab); break;
+    case 1: k_pair_tables<4><<<b, 128, 0, st>>>(xs, G, pair_gid, pair_vm, cams, n_pairs, tab); break;
+    case 2: k_pair_tables<9><<<b, 128, 0, st>>>(xs, G, pair_gid, pair_vm, cams, n_pairs, tab); break;
+    case 3: k_pair_tables<16><<<b, 128, 0, st>>>(xs, G, pair_gid, pair_vm, cams, n_pairs, tab); break;
+    default: return SLM_ERR_ARG;
+  }
+  return slm_cuda_status();
+}
+
+int slm_diag_runs(const SlmTileArgs* a, cudaStream_t st) {
+  if (a->n_tiles <= 0) return SLM_OK;
+  k_diag_tile<<<a->n_tiles, 256, 0, st>>>(*a);
+  return slm_cuda_status();
+}
+
+int slm_pair_forward(const float* xs, long long G, int sh_degree, const int* pair_gid, const uint32_t* pair_vm,
+                     const SlmCamera* cams, int n_pairs, const float* p, long long sa, long long sg, void* pm,
+                     cudaStream_t st) {
+  if (n_pairs <= 0) return SLM_OK;
+  unsigned b = slm_blocks(n_pairs, 128, 1LL << 30);
+  switch (sh_degree) {
+    case 0: k_pair_forward<1><<<b, 128, 0, st>>>(xs, G, pair_gid, pair_vm, cams, n_pairs, p, sa, sg, (PairM*)pm); break;
+    case 1: k_pair_forward<4><<<b, 128, 0, st>>>(xs, G, pair_gid, pair_vm, cams, n_pairs, p, sa, sg, (PairM*)pm); break;
+    case 2: k_pair_forward<9><<<b, 128, 0, st>>>(xs, G, pair_gid, pair_vm, cams, n_pairs, p, sa, sg, (PairM*)pm); break;
+    case 3: k_pair_forward<16><<<b, 128, 0, st>>>(xs, G, pair_gid, pair_vm, cams, n_pairs, p, sa, sg, (PairM*)pm); break;
+    default: return SLM_ERR_ARG;
+  }
+  return slm_cuda_status();
+}
+
+int slm_backward_blocks(long long G) { return (int)slm_blocks(G, 128, 148LL * 16); }
+
+int slm_pair_backward(const SlmBackArgs* a, int mode, int sh_degree, cudaStream_t st) {
+  unsigned b = (unsigned)slm_backward_blocks(a->G);
+#define SLM_BW(KK)                                 \
+  if (mode == 0)                                   \
+    k_pair_backward<KK, 0><<<b, 128, 0, st>>>(*a); \
+  else                                             \
+    k_pair_backward<KK, 1><<<b, 128, 0, st>>>(*a);
+  switch (sh_degree) {
+    case 0: SLM_BW(1) break;
+    case 1: SLM_BW(4) break;
+    case 2: SLM_BW(9) break;
+    case 3: SLM_BW(16) break;
+    default: return SLM_ERR_ARG;
+  }
+#undef SLM_BW
+  return slm_cuda_status();
+}
+
+}  // extern "C"

@@ -192,33 +192,90 @@ __global__ void k_tile_post(const uint32_t* __restrict__ sorted_pre, const uint3
   }
 }
 
-// Per splat (one thread per depth rank): walk its tile instances in pixel
-// row-major order -- tile row, pixel row inside the tile, tile column -- and
-// turn the COUNT pass's per-(instance, row) entry counts into the offset of
-// each (instance, row) run inside the splat's (view, gaussian) pair block.
-// This is the stable (gid, pixel) order of ref: jacobian.py:96 without a sort.
-__global__ void k_inst_base(const uint32_t* __restrict__ sorted_gid, const unsigned long long* __restrict__ inst_off,
-                            long long G, const SlmSplat* __restrict__ splats, int tiles_x, int tiles_y,
-                            const uint32_t* __restrict__ post_of_pre, const uint8_t* __restrict__ rowcnt,
-                            uint32_t* __restrict__ base_out, int* __restrict__ pair_cnt) {
+// ---------------------------------------------------------------------------
+// runs: a (tile, splat) instance with >= 1 kept pixel.  The COUNT pass leaves
+// a 256-bit keep mask per instance (one ballot word per warp of the tile);
+// here instances become runs, numbered in (view, tile, depth) order -- the
+// order the rasteriser produces entries -- so the FILL pass writes each run's
+// entries contiguously.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int mask_popc(const uint32_t* m) {
+  int c = 0;
+#pragma unroll
+  for (int w = 0; w < SLM_TILE * SLM_TILE / 32; ++w) c += __popc(m[w]);
+  return c;
+}
+
+// per instance of one view: entry count, used flag, and the per-(view,
+// gaussian) entry count (integer atomics: deterministic)
+__global__ void k_inst_count(const uint32_t* __restrict__ mask, const uint32_t* __restrict__ inst_gid, long long n,
+                             long long* __restrict__ cnt, int* __restrict__ used, int* __restrict__ pair_cnt) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+    const int c = mask_popc(mask + (size_t)j * 8);
+    cnt[j] = c;
+    used[j] = c > 0;
+    if (c > 0) atomicAdd(&pair_cnt[inst_gid[j]], c);
+  }
+}
+
+// run table of one view: instance j -> run r = run_of[j] (exclusive scan of
+// used), entry start (exclusive scan of counts), pair, tile and mask; plus
+// each pair's run count
+// run_of / ent_of are exclusive scans over the SUBSET's concatenated
+// instances; `ibase` is this view's first instance in that concatenation
+__global__ void k_runs_emit(const uint32_t* __restrict__ mask, const uint32_t* __restrict__ inst_gid,
+                            const int* __restrict__ used, const int* __restrict__ run_of,
+                            const long long* __restrict__ ent_of, long long ibase, long long n,
+                            const int* __restrict__ pidx, long long* __restrict__ run_start, int* __restrict__ run_q,
+                            uint32_t* __restrict__ run_mask, int* __restrict__ pair_nruns,
+                            long long* __restrict__ inst_start) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+    const long long jg = ibase + j;
+    inst_start[j] = ent_of[jg];
+    if (!used[jg]) continue;
+    const int r = run_of[jg];
+    const int q = pidx[inst_gid[j]];
+    run_start[r] = ent_of[jg];
+    run_q[r] = q;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) run_mask[(size_t)r * 8 + w] = mask[(size_t)j * 8 + w];
+    atomicAdd(&pair_nruns[q], 1);
+  }
+}
+
+// per tile of one view: its run count and each run's (view, tile) tag
+__global__ void k_tile_runs(const slm_u2* __restrict__ ranges, int n_tiles, const int* __restrict__ used,
+                            const int* __restrict__ run_of, long long ibase, int view, int* __restrict__ tile_nruns,
+                            uint32_t* __restrict__ run_tile) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_tiles; t += gridDim.x * blockDim.x) {
+    const slm_u2 rg = ranges[t];
+    int c = 0;
+    for (uint32_t j = rg.x; j < rg.y; ++j) {
+      if (used[ibase + j]) {
+        run_tile[run_of[ibase + j]] = ((uint32_t)view << 24) | (uint32_t)t;
+        ++c;
+      }
+    }
+    tile_nruns[t] = c;
+  }
+}
+
+// pair -> runs CSR, filled in a fixed order: per splat, its instances in
+// (tile row, tile column) order (pre-sort order), views handled one per call
+__global__ void k_pair_runs(const uint32_t* __restrict__ sorted_gid, const unsigned long long* __restrict__ inst_off,
+                            long long G, const uint32_t* __restrict__ post_of_pre, const int* __restrict__ used,
+                            const int* __restrict__ run_of, long long ibase, const int* __restrict__ pidx,
+                            const int* __restrict__ pair_run_off, int* __restrict__ pair_runs) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < G; i += (long long)gridDim.x * blockDim.x) {
     unsigned long long beg = inst_off[i], end = inst_off[i + 1];
     if (beg == end) continue;
-    const uint32_t g = sorted_gid[i];
-    int tx0, tx1, ty0, ty1;
-    splat_tiles(splats[g], tiles_x, tiles_y, tx0, tx1, ty0, ty1);
-    const int nx = tx1 - tx0 + 1;
-    uint32_t cur = 0;
-    for (int ty = ty0; ty <= ty1; ++ty) {
-      const unsigned long long krow = beg + (unsigned long long)(ty - ty0) * nx;
-      for (int ly = 0; ly < SLM_TILE; ++ly)
-        for (int c = 0; c < nx; ++c) {
-          const size_t j = post_of_pre[krow + c];
-          if (base_out) base_out[j * SLM_TILE + ly] = cur;
-          cur += rowcnt[j * SLM_TILE + ly];
-        }
+    const int q = pidx[sorted_gid[i]];
+    if (q < 0) continue;
+    int k = pair_run_off[q];
+    for (unsigned long long pre = beg; pre < end; ++pre) {
+      const long long jg = ibase + post_of_pre[pre];
+      if (used[jg]) pair_runs[k++] = run_of[jg];
     }
-    if (pair_cnt) pair_cnt[g] = (int)cur;
   }
 }
 
@@ -236,24 +293,27 @@ __global__ void k_tile_ranges(const unsigned long long* __restrict__ keys, long 
 // tile rasteriser (ref: rasterizer.py:264-316), one 16x16 tile per CTA,
 // one pixel per thread, splats staged in shared memory in batches.
 //   COUNT pass: per-pixel entry count, rendered colour, T_final and, per
-//               (tile instance, pixel row), the number of entries (rowcnt).
-//   FILL pass : writes BOTH cache record streams.  Pixel order at
-//               pix_off[pixel] + k; gaussian order at pair_off[pair] +
-//               inst_base[instance][row] + (rank of the pixel among the keepers
-//               of its 16-pixel tile row, from a half-warp ballot).
-//               dc/dalpha uses the per-pixel colour total of the COUNT pass
-//               (ref: jacobian.py:391-399).
+//               tile instance, the 256-bit keep mask (one ballot word per warp).
+//   FILL pass : writes the cache records in run order: entry of (instance,
+//               pixel) at inst_start[instance] + (number of keepers of the
+//               instance at lower tile-local pixel indices) -- one contiguous
+//               chunk per (instance, warp).  dc/dalpha uses the per-pixel
+//               colour total of the COUNT pass (ref: jacobian.py:391-399).
+//               Optionally also the pixel-order Traversals export.
 // ---------------------------------------------------------------------------
 typedef SlmRasterArgs RasterArgs;
 
 #define RB 256
+#define RW (RB / 32)
 template <bool FILL>
 __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
   __shared__ double s_mx[RB], s_my[RB], s_ca[RB], s_cb[RB], s_cc[RB], s_o[RB];
   __shared__ double s_c0[RB], s_c1[RB], s_c2[RB];
   __shared__ int4 s_box[RB];
   __shared__ uint32_t s_gid[RB];
-  __shared__ uint32_t s_rc[FILL ? 1 : RB * SLM_TILE / 4];  // COUNT: bytes [item][tile row]
+  __shared__ uint32_t s_mask[FILL ? 1 : RB * RW];   // COUNT: keep masks of the batch
+  __shared__ long long s_start[FILL ? RB : 1];      // FILL: first entry of each instance's run
+  __shared__ uint8_t s_pre[FILL ? RB * RW : 1];     // FILL: keepers in lower warps, per instance
 
   const int tiles_x = A.tiles_x;
   const int tile = blockIdx.x;
@@ -266,23 +326,19 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
   const double dxp = (double)px + 0.5, dyp = (double)py + 0.5;
   const double amin = A.cfg.alpha_min, tstop = A.cfg.t_stop, aclamp = A.cfg.alpha_clamp;
   const int lane = threadIdx.x & 31;
-  const int half = lane >> 4;
-  const unsigned below = (1u << lx) - 1u;
-  const uint32_t xy = ((uint32_t)py << 16) | (uint32_t)px;
+  const int warp = threadIdx.x >> 5;
+  const unsigned lanes_below = (1u << lane) - 1u;
 
   double T = 1.0, C0 = 0.0, C1 = 0.0, C2 = 0.0;
   uint32_t cnt = 0;
   bool done = !inside;
-  long long e = 0;
+  long long e = 0;  // pixel-order position (Traversals export only)
   double tot0 = 0, tot1 = 0, tot2 = 0;
-  int seg = 0;
   if (FILL && inside) {
-    e = A.pix_off[A.pix_base + pix];
     tot0 = A.rgb[(size_t)pix * 3 + 0];
     tot1 = A.rgb[(size_t)pix * 3 + 1];
     tot2 = A.rgb[(size_t)pix * 3 + 2];
-    done = A.pix_off[A.pix_base + pix + 1] == e;
-    if (!done && A.seg_idx) seg = A.seg_idx[A.pix_base + pix];
+    if (A.trav_gid) e = A.pix_off[A.pix_base + pix];
   }
 
   for (unsigned base = rng.x; base < rng.y; base += RB) {
@@ -297,9 +353,17 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
       s_c0[threadIdx.x] = s.c0; s_c1[threadIdx.x] = s.c1; s_c2[threadIdx.x] = s.c2;
       s_box[threadIdx.x] = make_int4(s.x0, s.x1, s.y0, s.y1);
       s_gid[threadIdx.x] = g;
+      if (FILL && A.rec_ae) {
+        s_start[threadIdx.x] = A.inst_start[j];
+        const uint32_t* mk = A.inst_mask + (size_t)j * RW;
+        int acc = 0;
+#pragma unroll
+        for (int w = 0; w < RW; ++w) {
+          s_pre[threadIdx.x * RW + w] = (uint8_t)acc;
+          acc += __popc(mk[w]);
+        }
+      }
     }
-    if (!FILL)
-      for (int w = threadIdx.x; w < RB * SLM_TILE / 4; w += RB) s_rc[w] = 0u;
     __syncthreads();
     const int nb = min((unsigned)RB, rng.y - base);
     for (int k = 0; k < nb; ++k) {
@@ -317,45 +381,21 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
         keep = (a >= amin) && (a > 0.0) && (T >= tstop);
       }
       const unsigned m = __ballot_sync(0xffffffffu, keep);
-      const unsigned rowm = (half ? (m >> 16) : m) & 0xffffu;
-      if (!FILL && (lane & 15) == 0 && rowm)
-        reinterpret_cast<uint8_t*>(s_rc)[k * SLM_TILE + ly] = (uint8_t)__popc(rowm);
+      if (!FILL && lane == 0) s_mask[k * RW + warp] = m;
       if (keep) {
         const double wgt = __dmul_rn(a, T);
         C0 = __dadd_rn(C0, __dmul_rn(wgt, s_c0[k]));
         C1 = __dadd_rn(C1, __dmul_rn(wgt, s_c1[k]));
         C2 = __dadd_rn(C2, __dmul_rn(wgt, s_c2[k]));
-        if (FILL && A.rec_idx) {
-          const uint32_t g = s_gid[k];
+        if (FILL && A.rec_ae) {
           const double om = 1.0 - a;
-          const float d0 = (float)(s_c0[k] * T - (tot0 - C0) / om);
-          const float d1 = (float)(s_c1[k] * T - (tot1 - C1) / om);
-          const float d2 = (float)(s_c2[k] * T - (tot2 - C2) / om);
-          const float ae = a < aclamp ? (float)a : 0.0f;
-          const float at = (float)wgt;
-          const uint32_t q = (uint32_t)A.pidx[g];
-          // pixel order
-          A.rec_idx[e] = q | (cnt == 0 ? SLM_HEAD : 0u);
-          A.rec_ae[e] = ae;
-          A.rec_at[e] = at;
-          A.rec_d0[e] = d0;
-          A.rec_d1[e] = d1;
-          A.rec_d2[e] = d2;
-          if (A.chunk_seg && (e & (SLM_CHUNK - 1)) == 0) A.chunk_seg[e / SLM_CHUNK] = seg;
-          // gaussian order: row-major rank of this pixel inside the pair
-          if (A.g_idx) {
-            const long long pb = A.pair_off[q];
-            const long long dest =
-                pb + A.inst_base[(size_t)(base + k) * SLM_TILE + ly] + __popc(rowm & below);
-            A.g_idx[dest] = xy | (dest == pb ? SLM_HEAD : 0u);
-            A.g_ae[dest] = ae;
-            A.g_at[dest] = at;
-            A.g_d0[dest] = d0;
-            A.g_d1[dest] = d1;
-            A.g_d2[dest] = d2;
-            if ((dest & (SLM_CHUNK - 1)) == 0) A.g_chunk_seg[dest / SLM_CHUNK] = (int)q;
-            if (A.g_src) A.g_src[dest] = (int)(e - A.view_entry_base);
-          }
+          const long long dest = s_start[k] + s_pre[k * RW + warp] + __popc(m & lanes_below);
+          A.rec_ae[dest] = a < aclamp ? (float)a : 0.0f;
+          A.rec_at[dest] = (float)wgt;
+          A.rec_d0[dest] = (float)(s_c0[k] * T - (tot0 - C0) / om);
+          A.rec_d1[dest] = (float)(s_c1[k] * T - (tot1 - C1) / om);
+          A.rec_d2[dest] = (float)(s_c2[k] * T - (tot2 - C2) / om);
+          A.rec_pix[dest] = (uint8_t)threadIdx.x;
         }
         if (FILL) {
           if (A.trav_gid) {
@@ -372,9 +412,9 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
       }
     }
     __syncthreads();
-    if (!FILL && A.rowcnt) {
-      uint32_t* dst = reinterpret_cast<uint32_t*>(A.rowcnt + (size_t)base * SLM_TILE);
-      for (int w = threadIdx.x; w < nb * SLM_TILE / 4; w += RB) dst[w] = s_rc[w];
+    if (!FILL && A.inst_mask) {
+      uint32_t* dst = A.inst_mask + (size_t)base * RW;
+      for (int w = threadIdx.x; w < nb * RW; w += RB) dst[w] = s_mask[w];
     }
   }
   if (!FILL && inside) {
@@ -449,11 +489,34 @@ int slm_tile_post(const uint32_t* sorted_pre, const uint32_t* inst_g_pre, long l
   return slm_cuda_status();
 }
 
-int slm_inst_base(const uint32_t* sorted_gid, const unsigned long long* inst_off, long long G, const SlmSplat* splats,
-                  int tiles_x, int tiles_y, const uint32_t* post_of_pre, const uint8_t* rowcnt, uint32_t* base_out,
-                  int* pair_cnt, cudaStream_t stream) {
-  k_inst_base<<<slm_blocks(G, 128), 128, 0, stream>>>(sorted_gid, inst_off, G, splats, tiles_x, tiles_y, post_of_pre,
-                                                       rowcnt, base_out, pair_cnt);
+int slm_inst_count(const uint32_t* mask, const uint32_t* inst_gid, long long n, long long* cnt, int* used,
+                   int* pair_cnt, cudaStream_t stream) {
+  if (n <= 0) return SLM_OK;
+  k_inst_count<<<slm_blocks(n, 256), 256, 0, stream>>>(mask, inst_gid, n, cnt, used, pair_cnt);
+  return slm_cuda_status();
+}
+
+int slm_runs_emit(const uint32_t* mask, const uint32_t* inst_gid, const int* used, const int* run_of,
+                  const long long* ent_of, long long ibase, long long n, const int* pidx, long long* run_start,
+                  int* run_q, uint32_t* run_mask, int* pair_nruns, long long* inst_start, cudaStream_t stream) {
+  if (n <= 0) return SLM_OK;
+  k_runs_emit<<<slm_blocks(n, 256), 256, 0, stream>>>(mask, inst_gid, used, run_of, ent_of, ibase, n, pidx,
+                                                       run_start, run_q, run_mask, pair_nruns, inst_start);
+  return slm_cuda_status();
+}
+
+int slm_tile_runs(const slm_u2* ranges, int n_tiles, const int* used, const int* run_of, long long ibase, int view,
+                  int* tile_nruns, uint32_t* run_tile, cudaStream_t stream) {
+  k_tile_runs<<<slm_blocks(n_tiles, 128), 128, 0, stream>>>(ranges, n_tiles, used, run_of, ibase, view, tile_nruns,
+                                                             run_tile);
+  return slm_cuda_status();
+}
+
+int slm_pair_runs(const uint32_t* sorted_gid, const unsigned long long* inst_off, long long G,
+                  const uint32_t* post_of_pre, const int* used, const int* run_of, long long ibase, const int* pidx,
+                  const int* pair_run_off, int* pair_runs, cudaStream_t stream) {
+  k_pair_runs<<<slm_blocks(G, 128), 128, 0, stream>>>(sorted_gid, inst_off, G, post_of_pre, used, run_of, ibase, pidx,
+                                                       pair_run_off, pair_runs);
   return slm_cuda_status();
 }
 

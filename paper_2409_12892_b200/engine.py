@@ -2,12 +2,16 @@
 
 `CacheSet` is the B200 counterpart of the reference's per-view
 `GradientCache` (ref: jacobian.py:46-84) generalised to the multi-view batch
-that PCG sums over.  Building it runs, per view: fp64 projection,
-(depth, gid) sort, tile binning, COUNT raster pass (+ per (tile instance,
-pixel row) entry counts), residual weights; then per subset: pixel offsets and
-(view, gaussian) pairs; then per view: row-major run offsets and the FILL
-raster pass, which writes BOTH record streams -- pixel order and gaussian
-order (sortCacheByGaussians) -- without any sort.
+that PCG sums over.
+
+Build, per view: fp64 projection, (depth, gid) sort, tile binning, COUNT
+raster pass (image, per-(tile, splat) keep masks), residual weights.  Per
+subset: instance counts -> runs (a run = one (tile, splat) with >= 1 kept
+pixel, numbered (view, tile, depth)), (view, gaussian) pairs, pair -> runs
+CSR.  Per view: FILL raster pass writing each run's entries contiguously.
+There is no sort of the cache and no second record stream: the pixel-sorted
+and gaussian-sorted orders of the reference (jacobian.py:93-121) are both
+views of this run order (see export_view).
 
 Everything here is host orchestration of libsplatlm_b200 kernels on the
 current torch stream; torch only allocates memory.
@@ -22,12 +26,12 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import call, ptr, stream_ptr
+from ._lib import call, off, ptr, stream_ptr
 from .errors import ImageSizeError
 from .scene import Camera, GaussianScene, cameras_struct_tensor, num_coefficients
 
 TILE = 16
-CHUNK = 128
+MASK_WORDS = TILE * TILE // 32
 
 
 @dataclass(frozen=True)
@@ -79,16 +83,10 @@ def sort_u64(kin, kout, vin, vout, n, begin_bit, end_bit):
          end_bit, stream_ptr())
 
 
-def sort_u32(kin, kout, vin, vout, n, begin_bit, end_bit):
-    ws = _empty(_lib.load().slm_sort_pairs_u32_workspace(n), torch.uint8, kin.device)
-    call("slm_sort_pairs_u32", ptr(ws), ws.numel(), ptr(kin), ptr(kout), ptr(vin), ptr(vout), n, begin_bit,
-         end_bit, stream_ptr())
-
-
 def ssim_host_tables(H, W, window, sigma):
     """Taps and center self weights exactly as ref: residuals.py:49-91."""
-    off = np.arange(window) - window // 2
-    k = np.exp(-0.5 * (off / sigma) ** 2)
+    offs = np.arange(window) - window // 2
+    k = np.exp(-0.5 * (offs / sigma) ** 2)
     k = k / k.sum()
     half = window // 2
 
@@ -130,24 +128,28 @@ class _NoTimer:
 
 
 class ViewFrame:
-    """Per-view products of the COUNT phase (splats, tile lists, image)."""
+    """Per-view products of projection, binning and the COUNT pass."""
 
     def __init__(self, cam: Camera, pix_base: int):
         self.cam = cam
         self.pix_base = pix_base
         self.splats = None       # uint8 [G*96]
-        self.inst_gid = None     # int32 [n_inst]
+        self.inst_gid = None     # int32 [n_inst] gid of each (tile, depth) instance
         self.ranges = None       # int32 [2*n_tiles]
         self.rgb = None          # float64 [HW*3]
         self.t_final = None      # float64 [HW]
         self.tiles_x = (cam.width + TILE - 1) // TILE
         self.tiles_y = (cam.height + TILE - 1) // TILE
         self.n_inst = 0
-        self.energy_part = None
         self.sorted_gid = None   # int32 [G] depth order
         self.inst_off = None     # int64 [G+1] instances per depth rank (pre-sort order)
         self.post_of_pre = None  # int32 [n_inst]
-        self.rowcnt = None       # uint8 [n_inst*16] entries per (instance, pixel row)
+        self.inst_mask = None    # int32 [n_inst*8] keep mask per instance
+        self.inst_start = None   # int64 [n_inst] first entry of the instance's run
+
+    @property
+    def n_tiles(self):
+        return self.tiles_x * self.tiles_y
 
 
 def project_and_bin(scene: GaussianScene, frame: ViewFrame, cfg_s: _lib.SlmRastCfg, err: torch.Tensor,
@@ -174,7 +176,7 @@ def project_and_bin(scene: GaussianScene, frame: ViewFrame, cfg_s: _lib.SlmRastC
     scan_i64(n_inst, inst_off)
     total = int(inst_off[G].item())
     frame.n_inst = total
-    n_tiles = frame.tiles_x * frame.tiles_y
+    n_tiles = frame.n_tiles
     rank_bits = _bits(G)
     tile_bits = _bits(n_tiles)
     ik = _empty(total, torch.int64, dev)
@@ -196,14 +198,6 @@ def project_and_bin(scene: GaussianScene, frame: ViewFrame, cfg_s: _lib.SlmRastC
     frame.inst_off = inst_off
     frame.post_of_pre = post_of_pre
     return skeys, sgid
-
-
-def inst_base(scene: GaussianScene, frame: ViewFrame, pair_cnt=None, base_out=None):
-    """Per-(view, gaussian) entry counts and/or the row-major run offsets of
-    each (tile instance, pixel row) inside its gaussian-order pair block."""
-    call("slm_inst_base", ptr(frame.sorted_gid), ptr(frame.inst_off), scene.num_gaussians, ptr(frame.splats),
-         frame.tiles_x, frame.tiles_y, ptr(frame.post_of_pre), ptr(frame.rowcnt), ptr(base_out), ptr(pair_cnt),
-         stream_ptr())
 
 
 def raster_args(frame: ViewFrame, cfg_s) -> _lib.SlmRasterArgs:
@@ -228,6 +222,8 @@ def residual_pass(frame: ViewFrame, gt: torch.Tensor, loss: LossConfig, gradr: t
         raise ValueError(f"unknown loss mode {loss.mode!r}")
     if loss.mode == "l1ssim" and (loss.lambda1 < 0 or loss.lambda2 < 0):
         raise ValueError("loss weights must be >= 0")
+    if gt.dtype not in (torch.float32, torch.float64):
+        raise ValueError("ground truth must be float32 or float64")
     dev = gt.device
     gt = gt.contiguous()
     taps, cwy, cwx = ssim_host_tables(H, W, loss.window, loss.sigma)
@@ -242,16 +238,14 @@ def residual_pass(frame: ViewFrame, gt: torch.Tensor, loss: LossConfig, gradr: t
     a.img = ptr(frame.rgb)
     a.gt = ptr(gt)
     a.gt_f32 = 1 if gt.dtype == torch.float32 else 0
-    if gt.dtype not in (torch.float32, torch.float64):
-        raise ValueError("ground truth must be float32 or float64")
     a.W, a.H = W, H
     a.lambda1, a.lambda2, a.eps_den = float(loss.lambda1), float(loss.lambda2), float(loss.eps_den)
     a.ssim_c1, a.ssim_c2 = 0.01 ** 2, 0.03 ** 2
     a.mode = 0 if loss.mode == "l1ssim" else 1
     a.win = int(loss.window)
     a.taps, a.cw_y, a.cw_x, a.tmp = ptr(taps_t), ptr(cwy_t), ptr(cwx_t), ptr(tmp)
-    a.gradr = C.c_void_p(gradr.data_ptr() + frame.pix_base * 16)
-    a.cgrad = C.c_void_p(cgrad.data_ptr() + frame.pix_base * 16)
+    a.gradr = off(gradr, frame.pix_base * 4)
+    a.cgrad = off(cgrad, frame.pix_base * 4)
     a.energy_part = ptr(part)
     if exports is not None:
         for k in ("gradr", "cgrad", "rabs", "rssim", "drabs", "drssim"):
@@ -260,13 +254,12 @@ def residual_pass(frame: ViewFrame, gt: torch.Tensor, loss: LossConfig, gradr: t
         a.o_rabs, a.o_drabs = ptr(exports["rabs"]), ptr(exports["drabs"])
         a.o_rssim, a.o_drssim = ptr(exports["rssim"]), ptr(exports["drssim"])
     call("slm_residuals", _lib.byref(a), blocks, stream_ptr())
-    frame.energy_part = part
     keep = (taps_t, cwy_t, cwx_t, tmp)  # noqa: F841 -- alive until the kernels are queued
     return part
 
 
 class CacheSet:
-    """Gradient cache of one image subset on the device (both record orders).
+    """Gradient cache of one image subset on the device (run order).
 
     Args:
         scene: scene at the current parameters.
@@ -275,12 +268,12 @@ class CacheSet:
             None the cache is built without residual weights (products only).
         config: RenderConfig.
         loss: LossConfig.
-        keep_source_index: also keep the gaussian-order -> pixel-order
-            permutation (the reference's source_index) for parity exports.
+        weights: precomputed per-view (grad_r_sq4, color_grad4) instead of gts.
+        timer: optional PhaseTimer.
     """
 
     def __init__(self, scene: GaussianScene, cameras: list[Camera], gts=None, config=None, loss=LossConfig(),
-                 keep_source_index: bool = False, residual_exports: bool = False, weights=None, timer=None):
+                 residual_exports: bool = False, weights=None, timer=None, keep_source_index: bool = False):
         from .rasterizer import DEFAULT_CONFIG
         self.scene = scene
         self.config = config if config is not None else DEFAULT_CONFIG
@@ -292,6 +285,8 @@ class CacheSet:
         self.device = dev
         G = scene.num_gaussians
         V = len(self.cameras)
+        if V > 255:
+            raise ValueError("at most 255 views per cache subset")
         self.G, self.V = G, V
         self.P = scene.params_per_gaussian
         self.K = num_coefficients(scene.sh_degree)
@@ -300,8 +295,7 @@ class CacheSet:
         views = (_lib.SlmView * V)()
         for i, c in enumerate(self.cameras):
             views[i].pix_base, views[i].W, views[i].H = self.pix_bases[i], c.width, c.height
-        self.views_dev = torch.frombuffer(bytearray(bytes(C.string_at(C.addressof(views), C.sizeof(views)))),
-                                          dtype=torch.uint8).to(dev)
+        self.views_dev = _lib.struct_tensor(views, dev)
         cfg_s = rast_cfg_struct(self.config, scene.background)
         self.cfg_s = cfg_s
         err = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -330,12 +324,11 @@ class CacheSet:
             hw = cam.num_pixels
             fr.rgb = torch.empty(hw * 3, dtype=torch.float64, device=dev)
             fr.t_final = torch.empty(hw, dtype=torch.float64, device=dev)
-            fr.rowcnt = torch.zeros(max(fr.n_inst, 1) * TILE, dtype=torch.uint8, device=dev)
+            fr.inst_mask = torch.zeros(max(fr.n_inst, 1) * MASK_WORDS, dtype=torch.int32, device=dev)
             a = raster_args(fr, cfg_s)
-            a.px_count = C.c_void_p(self.px_count.data_ptr() + fr.pix_base * 4)
-            a.rgb, a.t_final, a.rowcnt = ptr(fr.rgb), ptr(fr.t_final), ptr(fr.rowcnt)
+            a.px_count = off(self.px_count, fr.pix_base)
+            a.rgb, a.t_final, a.inst_mask = ptr(fr.rgb), ptr(fr.t_final), ptr(fr.inst_mask)
             call("slm_raster_count", _lib.byref(a), stream_ptr())
-            inst_base(scene, fr, pair_cnt=self.pair_cnt[v * G:(v + 1) * G])
             T.tick("raster_count")
             if have_res:
                 ex = {} if residual_exports else None
@@ -351,26 +344,30 @@ class CacheSet:
             raise ValueError("quaternion with (near-)zero norm")
         self.energies = [float(p.sum().item()) for p in energy_parts] if have_res else None
 
-        # ---- pixel segments ----------------------------------------------
-        N = self.N
-        cnt64 = torch.empty(N + 1, dtype=torch.int64, device=dev)
-        nonempty = torch.empty(N + 1, dtype=torch.int32, device=dev)
-        call("slm_px_prepare", ptr(self.px_count), N + 1, ptr(cnt64), ptr(nonempty), stream_ptr())
-        self.pix_off = torch.empty(N + 1, dtype=torch.int64, device=dev)
-        scan_i64(cnt64, self.pix_off)
-        seg_idx = torch.empty(N + 1, dtype=torch.int32, device=dev)
-        scan_i32(nonempty, seg_idx)
-        bases = torch.tensor(self.pix_bases + [N], dtype=torch.int64, device=dev)
-        view_off = self.pix_off[bases].cpu().tolist()
-        self.E = int(view_off[-1])
-        self.view_entry_base = view_off
-        self.n_seg = int(seg_idx[N].item())
-        self.seg_info = _empty(self.n_seg * 2, torch.int32, dev)
-        call("slm_px_segments", ptr(self.px_count), ptr(seg_idx), N, ptr(self.cams_dev), V, ptr(self.seg_info),
-             stream_ptr())
-        del cnt64, nonempty
+        # ---- instances -> runs ---------------------------------------------
+        ibases, tbases = [], []
+        ni = nt = 0
+        for fr in self.frames:
+            ibases.append(ni)
+            tbases.append(nt)
+            ni += fr.n_inst
+            nt += fr.n_tiles
+        self.n_inst_total, self.n_tiles_total = ni, nt
+        self.view_tile_base = tbases + [nt]
+        inst_cnt = torch.zeros(ni + 1, dtype=torch.int64, device=dev)
+        inst_used = torch.zeros(ni + 1, dtype=torch.int32, device=dev)
+        for v, fr in enumerate(self.frames):
+            call("slm_inst_count", ptr(fr.inst_mask), ptr(fr.inst_gid), fr.n_inst, off(inst_cnt, ibases[v]),
+                 off(inst_used, ibases[v]), off(self.pair_cnt, v * G), stream_ptr())
+        ent_of = torch.empty_like(inst_cnt)
+        scan_i64(inst_cnt, ent_of)
+        run_of = torch.empty_like(inst_used)
+        scan_i32(inst_used, run_of)
+        tot = torch.stack([ent_of[ni], run_of[ni].to(torch.int64)]).cpu().tolist()
+        self.E, self.R = int(tot[0]), int(tot[1])
+        del inst_cnt
 
-        # ---- pairs -----------------------------------------------------------
+        # ---- pairs (view, gaussian) ------------------------------------------
         VG = V * G
         cntV = torch.zeros(VG + 1, dtype=torch.int64, device=dev)
         flagV = torch.zeros(VG + 1, dtype=torch.int32, device=dev)
@@ -383,10 +380,8 @@ class CacheSet:
         tscan = torch.empty_like(flagT)
         scan_i32(flagT, tscan)
         self.n_pairs = int(pair_of[VG].item())
-        if int(vscan[VG].item()) != self.E:
-            raise RuntimeError("cache entry count mismatch between pixel and pair counts")
         Pn = self.n_pairs
-        self.pair_off = torch.empty(Pn + 1, dtype=torch.int64, device=dev)
+        self.pair_off = torch.empty(Pn + 1, dtype=torch.int64, device=dev)   # entries per pair (stats)
         self.pair_gid = _empty(Pn, torch.int32, dev)
         self.pair_vm = _empty(Pn, torch.int32, dev)
         self.pair_geo = _empty(Pn * _lib.PAIR_GEO_BYTES, torch.uint8, dev)
@@ -397,76 +392,78 @@ class CacheSet:
         call("slm_pairs_emit", ptr(self.pair_cnt), V, G, ptr(pair_of), ptr(vscan), ptr(tscan), ptr(splats_all),
              ptr(self.pair_off), ptr(self.pair_gid), ptr(self.pair_vm), ptr(self.pair_geo), ptr(pidx), ptr(self.gpo),
              ptr(self.gp_list), Pn, self.E, stream_ptr())
-        # first pair of each view (pairs are view-major)
-        self.view_pair_base = [int(x) for x in pair_of[torch.tensor([v * G for v in range(V)] + [VG],
-                                                                     device=dev)].cpu().tolist()]
         del cntV, flagV, flagT, vscan, pair_of, tscan, splats_all
 
-        T.tick("segments_pairs")
-        # ---- FILL phase: pixel-order records, then gaussian order ------------
-        E = self.E
-        n_chunks = (E + CHUNK - 1) // CHUNK
-        self.n_chunks = n_chunks
-        f32 = torch.float32
-
-        def stream6():
-            return ([_empty(E, torch.int32, dev)] + [_empty(E, f32, dev) for _ in range(5)])
-        self.pix_rec = stream6()
-        self.gau_rec = stream6()
-        self.chunk_seg_pix = _empty(n_chunks, torch.int32, dev)
-        self.chunk_seg_gau = _empty(n_chunks, torch.int32, dev)
-        self.g_src = _empty(E, torch.int32, dev) if keep_source_index else None
+        # ---- run table, runs per tile, pair -> runs ----------------------------
+        R = self.R
+        self.run_start = torch.zeros(R + 3, dtype=torch.int64, device=dev)  # +2: 16 B-granular TMA copies
+        self.run_q = _empty(R, torch.int32, dev)
+        self.run_mask = _empty(R * MASK_WORDS, torch.int32, dev)
+        self.run_tile = _empty(R, torch.int32, dev)
+        pair_nruns = torch.zeros(Pn + 1, dtype=torch.int32, device=dev)
+        tile_nruns = torch.zeros(nt + 1, dtype=torch.int32, device=dev)
         for v, fr in enumerate(self.frames):
-            e0 = view_off[v]
-            base = _empty(fr.n_inst * TILE, torch.int32, dev)
-            inst_base(scene, fr, base_out=base)
-            T.tick("gauss_order")
+            fr.inst_start = _empty(fr.n_inst, torch.int64, dev)
+            call("slm_runs_emit", ptr(fr.inst_mask), ptr(fr.inst_gid), ptr(inst_used), ptr(run_of), ptr(ent_of),
+                 ibases[v], fr.n_inst, off(pidx, v * G), ptr(self.run_start), ptr(self.run_q), ptr(self.run_mask),
+                 ptr(pair_nruns), ptr(fr.inst_start), stream_ptr())
+            call("slm_tile_runs", ptr(fr.ranges), fr.n_tiles, ptr(inst_used), ptr(run_of), ibases[v], v,
+                 off(tile_nruns, tbases[v]), ptr(self.run_tile), stream_ptr())
+        self.run_start[R:].fill_(self.E)
+        self.tile_run_off = torch.empty_like(tile_nruns)
+        scan_i32(tile_nruns, self.tile_run_off)
+        # chunk table for the streaming product kernel (<= 32 runs / 512 entries per chunk)
+        tile_nch = torch.zeros(nt + 1, dtype=torch.int32, device=dev)
+        call("slm_tile_chunks", ptr(self.tile_run_off), nt, ptr(self.run_start), None, ptr(tile_nch), 0,
+             stream_ptr())
+        self.tile_chunk_off = torch.empty_like(tile_nch)
+        scan_i32(tile_nch, self.tile_chunk_off)
+        self.n_chunks = int(self.tile_chunk_off[nt].item())
+        self.chunk_run = torch.empty(self.n_chunks + 1, dtype=torch.int32, device=dev)
+        call("slm_tile_chunks", ptr(self.tile_run_off), nt, ptr(self.run_start), ptr(self.tile_chunk_off),
+             ptr(self.chunk_run), 1, stream_ptr())
+        self.chunk_run[self.n_chunks:].fill_(R)
+        del tile_nch
+        self.pair_run_off = torch.empty_like(pair_nruns)
+        scan_i32(pair_nruns, self.pair_run_off)
+        self.pair_runs = _empty(R, torch.int32, dev)
+        for v, fr in enumerate(self.frames):
+            call("slm_pair_runs", ptr(fr.sorted_gid), ptr(fr.inst_off), G, ptr(fr.post_of_pre), ptr(inst_used),
+                 ptr(run_of), ibases[v], off(pidx, v * G), ptr(self.pair_run_off), ptr(self.pair_runs), stream_ptr())
+        del pidx, pair_nruns, tile_nruns, inst_used, run_of, ent_of
+        T.tick("runs_pairs")
+
+        # ---- FILL phase: run-ordered records ------------------------------------
+        E = self.E
+        f32 = torch.float32
+        # alpha_eff, alpha*T, dc/dalpha[3] + tile-local pixel; +16 slots so the
+        # 16-byte-granular TMA chunk copies of the product kernels stay in bounds
+        self.rec = [torch.zeros(E + 16, dtype=f32, device=dev) for _ in range(5)]
+        self.rec_pix = torch.zeros(E + 16, dtype=torch.uint8, device=dev)
+        for v, fr in enumerate(self.frames):
             a = raster_args(fr, cfg_s)
-            a.rgb = ptr(fr.rgb)
-            a.pix_off, a.pidx, a.seg_idx = ptr(self.pix_off), C.c_void_p(pidx.data_ptr() + v * G * 4), ptr(seg_idx)
-            a.pair_off, a.inst_base = ptr(self.pair_off), ptr(base)
-            (a.rec_idx, a.rec_ae, a.rec_at, a.rec_d0, a.rec_d1, a.rec_d2) = [ptr(t) for t in self.pix_rec]
-            a.chunk_seg = ptr(self.chunk_seg_pix)
-            (a.g_idx, a.g_ae, a.g_at, a.g_d0, a.g_d1, a.g_d2) = [ptr(t) for t in self.gau_rec]
-            a.g_chunk_seg = ptr(self.chunk_seg_gau)
-            a.g_src = ptr(self.g_src) if self.g_src is not None else None
-            a.view_entry_base = e0
+            a.rgb, a.inst_mask, a.inst_start = ptr(fr.rgb), ptr(fr.inst_mask), ptr(fr.inst_start)
+            a.rec_ae, a.rec_at, a.rec_d0, a.rec_d1, a.rec_d2 = [ptr(t) for t in self.rec]
+            a.rec_pix = ptr(self.rec_pix)
             call("slm_raster_fill", _lib.byref(a), stream_ptr())
             T.tick("raster_fill")
-            del base
-        del pidx, seg_idx
-        for fr in self.frames:  # keep images for exports; tile lists are not needed any more
-            fr.inst_gid = fr.ranges = fr.rowcnt = fr.post_of_pre = fr.inst_off = fr.sorted_gid = None
+        for fr in self.frames:  # keep the images (exports); binning state is no longer needed
+            fr.inst_gid = fr.ranges = fr.post_of_pre = fr.inst_off = fr.sorted_gid = None
+            fr.inst_mask = fr.inst_start = None
+        self.view_tile_base_dev = torch.tensor(self.view_tile_base, dtype=torch.int32, device=dev)
         # product scratch
         self.u = torch.empty(self.N * 4, dtype=f32, device=dev)
         self.pm = _empty(Pn * 12, f32, dev)
-        self.pacc = _empty(Pn * 9, f32, dev)
-        self._carry = {}
+        self.run_acc = _empty(R * _lib.JT_D, f32, dev)
+        self.run_par = _empty(R * 16, f32, dev)
         self._b = None
         self._M = None
 
     # ------------------------------------------------------------------
     @property
     def nbytes(self) -> int:
-        """Bytes of both record streams (budget accounting, ref: jacobian.py:76-80)."""
-        return 2 * 24 * self.E
-
-    def _carries(self, D):
-        if D not in self._carry:
-            nb = _lib.load().slm_carry_bytes(D) * max(self.n_chunks, 1)
-            self._carry[D] = (torch.empty(nb, dtype=torch.uint8, device=self.device),
-                              torch.empty(nb, dtype=torch.uint8, device=self.device))
-        return self._carry[D]
-
-    def _stream(self, which: str, D: int) -> _lib.SlmWsrStream:
-        rec = self.pix_rec if which == "pixel" else self.gau_rec
-        s = _lib.SlmWsrStream()
-        s.idx, s.ae, s.at, s.d0, s.d1, s.d2 = [ptr(t) for t in rec]
-        s.E = self.E
-        s.chunk_seg = ptr(self.chunk_seg_pix if which == "pixel" else self.chunk_seg_gau)
-        h, t = self._carries(D)
-        s.head, s.tail = ptr(h), ptr(t)
-        return s
+        """Bytes of the record stream (budget accounting, ref: jacobian.py:76-80)."""
+        return 21 * self.E + 48 * self.R
 
     def pair_forward(self, p: torch.Tensor, gaussian_major: bool = False):
         G, P = self.G, self.P
@@ -474,30 +471,69 @@ class CacheSet:
         call("slm_pair_forward", ptr(self.scene.x32()), G, self.scene.sh_degree, ptr(self.pair_gid),
              ptr(self.pair_vm), ptr(self.cams_dev), self.n_pairs, ptr(p), sa, sg, ptr(self.pm), stream_ptr())
 
+    def _tile_args(self) -> _lib.SlmTileArgs:
+        a = _lib.SlmTileArgs()
+        a.views, a.view_tile_base, a.n_views = ptr(self.views_dev), ptr(self.view_tile_base_dev), self.V
+        a.n_tiles = self.n_tiles_total
+        a.tile_run_off, a.tile_chunk_off, a.chunk_run = ptr(self.tile_run_off), ptr(self.tile_chunk_off), \
+            ptr(self.chunk_run)
+        a.run_start, a.run_q, a.run_tile, a.run_par = ptr(self.run_start), ptr(self.run_q), ptr(self.run_tile), \
+            ptr(self.run_par)
+        a.geo, a.pm = ptr(self.pair_geo), ptr(self.pm)
+        a.ae, a.at, a.d0, a.d1, a.d2 = [ptr(t) for t in self.rec]
+        a.pix = ptr(self.rec_pix)
+        return a
+
+    def _run_params(self, a: _lib.SlmTileArgs, with_m: bool):
+        call("slm_run_params", _lib.byref(a), self.R, 1 if with_m else 0, ptr(self.run_par), stream_ptr())
+
+    def _back_args(self, acc, out, scale=1.0, p=None, M=None, lam=0.0, dot_part=None) -> _lib.SlmBackArgs:
+        a = _lib.SlmBackArgs()
+        a.xs, a.G = ptr(self.scene.x32()), self.G
+        a.gpo, a.gp_list = ptr(self.gpo), ptr(self.gp_list)
+        a.pair_run_off, a.pair_runs = ptr(self.pair_run_off), ptr(self.pair_runs)
+        a.pair_vm, a.cams, a.acc = ptr(self.pair_vm), ptr(self.cams_dev), ptr(acc)
+        a.scale, a.p, a.Mdiag, a.lam = float(scale), ptr(p), ptr(M), float(lam)
+        a.out, a.dot_part = ptr(out), ptr(dot_part)
+        return a
+
     def apply_j_raw(self, weighted: bool) -> torch.Tensor:
         """u (or u_hat) into self.u from the pair forward chain in self.pm."""
         if weighted and self.gradr is None:
             raise ValueError("cache was built without residual weights")
-        s = self._stream("pixel", 3)
-        call("slm_apply_j", _lib.byref(s), ptr(self.seg_info), ptr(self.pair_geo), ptr(self.pm),
-             ptr(self.gradr) if weighted else None, ptr(self.u), stream_ptr())
+        a = self._tile_args()
+        a.gradr = ptr(self.gradr) if weighted else None
+        a.u_out = ptr(self.u)
+        self._run_params(a, with_m=True)
+        call("slm_apply_j", _lib.byref(a), stream_ptr())
         return self.u
 
     def apply_jt_raw(self, u: torch.Tensor, out: torch.Tensor, scale: float = 1.0, p=None, M=None, lam=0.0,
                      dot_part=None):
-        s = self._stream("gaussian", 9)
-        call("slm_apply_jt_pairs", _lib.byref(s), ptr(self.pair_geo), ptr(self.pair_vm), ptr(self.views_dev), ptr(u),
-             ptr(self.pacc), stream_ptr())
-        call("slm_pair_backward", ptr(self.scene.x32()), self.G, self.scene.sh_degree, ptr(self.gpo), ptr(self.gp_list),
-             ptr(self.pair_vm), ptr(self.cams_dev), ptr(self.pacc), 0, float(scale), ptr(p), ptr(M), float(lam),
-             ptr(out), ptr(dot_part), stream_ptr())
+        ra = self._tile_args()
+        ra.u, ra.out = ptr(u), ptr(self.run_acc)
+        self._run_params(ra, with_m=False)
+        call("slm_apply_jt_runs", _lib.byref(ra), stream_ptr())
+        ba = self._back_args(self.run_acc, out, scale, p, M, lam, dot_part)
+        call("slm_pair_backward", _lib.byref(ba), 0, self.scene.sh_degree, stream_ptr())
         return out
 
     def jtwj(self, p: torch.Tensor, out: torch.Tensor, lam: float = 0.0, M=None, dot_part=None):
-        """out = J^T W J p (+ lam * max(M, 1e-12) * p); attribute-major fp32."""
+        """out = J^T W J p (+ lam * max(M, 1e-12) * p); attribute-major fp32.
+
+        Four launches: pair forward chain, run parameter records, the fused
+        per-tile J / W / J^T streaming kernel (u never leaves shared memory),
+        per-gaussian backward chain."""
+        if self.gradr is None:
+            raise ValueError("cache was built without residual weights")
         self.pair_forward(p)
-        self.apply_j_raw(weighted=True)
-        return self.apply_jt_raw(self.u, out, 1.0, p, M if lam != 0.0 else None, lam, dot_part)
+        a = self._tile_args()
+        a.gradr, a.out = ptr(self.gradr), ptr(self.run_acc)
+        self._run_params(a, with_m=True)
+        call("slm_jtwj_runs", _lib.byref(a), stream_ptr())
+        ba = self._back_args(self.run_acc, out, 1.0, p, M if lam != 0.0 else None, lam, dot_part)
+        call("slm_pair_backward", _lib.byref(ba), 0, self.scene.sh_degree, stream_ptr())
+        return out
 
     def rhs(self) -> torch.Tensor:
         """b = -J^T color_grad, summed over the subset's views (ref: jacobian.py:411-413)."""
@@ -514,65 +550,60 @@ class CacheSet:
         if self._M is None:
             if self.gradr is None:
                 raise ValueError("cache was built without residual weights")
-            mom = _empty(self.n_pairs * _lib.DIAG_D, torch.float32, self.device)
-            s = self._stream("gaussian", _lib.DIAG_D)
-            call("slm_diag_pairs", _lib.byref(s), ptr(self.pair_geo), ptr(self.pair_vm), ptr(self.views_dev),
-                 ptr(self.gradr), ptr(mom), stream_ptr())
+            sums = _empty(self.R * _lib.DIAG_D, torch.float32, self.device)
+            ptab = _empty(self.n_pairs * _lib.load().slm_diag_tab_floats(), torch.float32, self.device)
+            call("slm_pair_tables", ptr(self.scene.x32()), self.G, self.scene.sh_degree, ptr(self.pair_gid),
+                 ptr(self.pair_vm), ptr(self.cams_dev), self.n_pairs, ptr(ptab), stream_ptr())
+            ra = self._tile_args()
+            ra.ptab, ra.gradr, ra.out = ptr(ptab), ptr(self.gradr), ptr(sums)
+            call("slm_diag_runs", _lib.byref(ra), stream_ptr())
             M = torch.empty(self.G * self.P, dtype=torch.float32, device=self.device)
-            call("slm_pair_backward", ptr(self.scene.x32()), self.G, self.scene.sh_degree, ptr(self.gpo), ptr(self.gp_list),
-                 ptr(self.pair_vm), ptr(self.cams_dev), ptr(mom), 1, 1.0, None, None, 0.0, ptr(M), None,
-                 stream_ptr())
-            del self._carry[_lib.DIAG_D]
+            ba = self._back_args(sums, M)
+            call("slm_pair_backward", _lib.byref(ba), 1, self.scene.sh_degree, stream_ptr())
             self._M = M
         return self._M
 
     # ------------------------------------------------------------------
-    # parity exports (test infrastructure; host copies)
+    # parity exports (test infrastructure; host-side reconstruction)
     # ------------------------------------------------------------------
     def image(self, v: int) -> torch.Tensor:
         c = self.cameras[v]
         return self.frames[v].rgb.view(c.height, c.width, 3)
 
     def export_view(self, v: int) -> dict:
-        """Reference-shaped arrays of view v (pixel-sorted cache fields plus
-        the gaussian-order sequence of the same view)."""
+        """Reference-shaped arrays of view v: the pixel-sorted cache
+        (ref: jacobian.py:401-409) and its gaussian-sorted permutation
+        (ref: jacobian.py:93-105), reconstructed from the run order."""
         cam = self.cameras[v]
-        e0, e1 = self.view_entry_base[v], self.view_entry_base[v + 1]
-        pr = [t[e0:e1].cpu() for t in self.pix_rec]
-        idx = pr[0].numpy().view(np.uint32)
-        pair = (idx & 0x7FFFFFFF).astype(np.int64)
+        t0, t1 = self.view_tile_base[v], self.view_tile_base[v + 1]
+        tro = self.tile_run_off.cpu().numpy()
+        r0, r1 = int(tro[t0]), int(tro[t1])
+        rs = self.run_start[r0:r1 + 1].cpu().numpy()
+        e0, e1 = int(rs[0]), int(rs[-1])
+        run_q = self.run_q[r0:r1].cpu().numpy()
+        run_tile = self.run_tile[r0:r1].cpu().numpy().view(np.uint32) & 0xFFFFFF
         pair_gid = self.pair_gid[: self.n_pairs].cpu().numpy()
-        pair_vm = self.pair_vm[: self.n_pairs].cpu().numpy().view(np.uint32)
-        gid = pair_gid[pair] if pair.size else np.zeros(0, np.int64)
-        b0 = self.pix_bases[v]
-        pix_off = self.pix_off[b0:b0 + cam.num_pixels + 1].cpu().numpy() - e0
-        counts = np.diff(pix_off)
-        pixel = np.repeat(np.arange(cam.num_pixels), counts)
-        ae = pr[1].numpy().astype(np.float64)
-        at = pr[2].numpy().astype(np.float64)
+        n = np.diff(rs)
+        run_of_e = np.repeat(np.arange(r1 - r0), n)
+        pl = self.rec_pix[e0:e1].cpu().numpy().astype(np.int64)
+        tiles_x = (cam.width + TILE - 1) // TILE
+        tile = run_tile[run_of_e].astype(np.int64)
+        px = (tile % tiles_x) * TILE + (pl & 15)
+        py = (tile // tiles_x) * TILE + (pl >> 4)
+        pixel = py * cam.width + px
+        gid = pair_gid[run_q[run_of_e]].astype(np.int64)
+        f = [t[e0:e1].cpu().numpy().astype(np.float64) for t in self.rec]
+        order = np.argsort(pixel, kind="stable")      # runs of one tile are in depth order
+        pixel, gid = pixel[order], gid[order]
+        ae, at = f[0][order], f[1][order]
+        dcda = np.stack([f[2][order], f[3][order], f[4][order]], 1)
         alpha = np.where(ae == 0.0, self.config.alpha_clamp, ae)
-        T = at / alpha
-        dcda = np.stack([pr[3].numpy(), pr[4].numpy(), pr[5].numpy()], 1).astype(np.float64)
-        out = dict(pixel_ids=pixel, gaussian_ids=gid.astype(np.int64), alphas=alpha, alpha_eff=ae,
-                   transmittances=T, dc_dalpha=dcda, dc_dcs=at, offsets=pix_off, head=(idx >> 31).astype(bool))
-        # gaussian order of this view: its pairs' blocks in pair (= gid) order
-        pv = np.arange(self.view_pair_base[v], self.view_pair_base[v + 1])   # pairs are view-major
-        assert np.all((pair_vm[pv] & 0xFFFF) == v)
-        poff = self.pair_off[: self.n_pairs + 1].cpu().numpy()
-        sel = np.arange(poff[pv[0]], poff[pv[-1] + 1]) if pv.size else np.zeros(0, np.int64)
-        selt = torch.from_numpy(sel).to(self.device)
-        gr = [t[selt].cpu().numpy() for t in self.gau_rec] if sel.size else [np.zeros(0)] * 6
-        gidx = gr[0].view(np.uint32) if sel.size else np.zeros(0, np.uint32)
-        gx = (gidx & 0xFFFF).astype(np.int64)
-        gy = ((gidx >> 16) & 0x7FFF).astype(np.int64)
-        g_gid = np.repeat(pair_gid[pv], np.diff(poff)[pv]) if pv.size else np.zeros(0, np.int64)
+        offsets = np.zeros(cam.num_pixels + 1, np.int64)
+        offsets[1:] = np.cumsum(np.bincount(pixel, minlength=cam.num_pixels))
+        gperm = np.lexsort((pixel, gid))
         goff = np.zeros(self.G + 1, np.int64)
-        np.add.at(goff, pair_gid[pv] + 1, np.diff(poff)[pv])
-        out.update(g_pixel_ids=gy * cam.width + gx, g_gaussian_ids=g_gid, g_offsets=np.cumsum(goff),
-                   g_alpha_eff=gr[1].astype(np.float64) if sel.size else np.zeros(0),
-                   g_dc_dcs=gr[2].astype(np.float64) if sel.size else np.zeros(0),
-                   g_dc_dalpha=np.stack(gr[3:6], 1).astype(np.float64) if sel.size else np.zeros((0, 3)),
-                   g_head=(gidx >> 31).astype(bool))
-        if self.g_src is not None and sel.size:
-            out["g_source_index"] = self.g_src[selt].cpu().numpy().astype(np.int64)
-        return out
+        goff[1:] = np.cumsum(np.bincount(gid, minlength=self.G))
+        return dict(pixel_ids=pixel, gaussian_ids=gid, alphas=alpha, alpha_eff=ae, transmittances=at / alpha,
+                    dc_dalpha=dcda, dc_dcs=at, offsets=offsets,
+                    g_pixel_ids=pixel[gperm], g_gaussian_ids=gid[gperm], g_offsets=goff, g_source_index=gperm,
+                    g_dc_dalpha=dcda[gperm], g_alpha_eff=ae[gperm], g_dc_dcs=at[gperm])

@@ -39,9 +39,9 @@ def test_struct_layouts():
     assert lib.slm_camera_size() == ctypes.sizeof(_lib.SlmCamera)
     assert lib.slm_raster_args_size() == ctypes.sizeof(_lib.SlmRasterArgs)
     assert lib.slm_resid_args_size() == ctypes.sizeof(_lib.SlmResidArgs)
-    assert lib.slm_wsr_stream_size() == ctypes.sizeof(_lib.SlmWsrStream)
+    assert lib.slm_tile_args_size() == ctypes.sizeof(_lib.SlmTileArgs)
+    assert lib.slm_back_args_size() == ctypes.sizeof(_lib.SlmBackArgs)
     assert lib.slm_splat_size() == 96 and lib.slm_pair_geo_size() == 32
-    assert lib.slm_carry_bytes(9) == 44
 
 
 def test_workspace_queries_do_not_crash_without_gpu():

@@ -213,3 +213,35 @@ def test_determinism(prob):
 
 def test_entry_count_matches_traversals(prob, cacheset, oracle_views):
     assert cacheset.E == sum(ov["rast"]["pixel"].size for ov in oracle_views)
+
+
+@pytest.fixture(scope="module")
+def dense():
+    """C1-density view (2k Gaussians, 64x64, ~77 entries/pixel): tiles hold more
+    than 256 runs and rasteriser batches of more than 256 splats."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    truth, init, cams, gts = problem(seed=0, G=2000, n_views=1, W=64, H=64, degree=3)
+    osc, oc = oscene(init), ocam(cams[0])
+    rs = O.rasterize(osc, oc)
+    res = O.residuals(rs["image"], gts[0])
+    b, v = O.build_cache(osc, oc, res, rast=rs)
+    scene = init.to_device()
+    cs = CacheSet(scene, cams, [torch.from_numpy(gts[0]).cuda()])
+    return dict(osc=osc, scene=scene, cs=cs, b=b, view=v, gview=O.gaussian_order(v), rast=rs)
+
+
+def test_dense_indexing_and_products(dense):
+    cs, v, gv = dense["cs"], dense["view"], dense["gview"]
+    assert cs.E == v.E and cs.R > 256 * 4
+    ex = cs.export_view(0)
+    assert np.array_equal(ex["offsets"], v.offsets)
+    assert np.array_equal(ex["gaussian_ids"], v.gid)
+    assert np.array_equal(ex["g_source_index"], gv.src)
+    assert rel(cs.rhs().cpu().numpy(), dense["b"]) < FTOL
+    assert rel(cs.diag().cpu().numpy(), O.diag_jtj(dense["osc"], gv)) < FTOL
+    rng = np.random.default_rng(5)
+    p = rng.standard_normal(dense["scene"].param_count)
+    out = torch.empty(p.size, dtype=torch.float32, device="cuda")
+    cs.jtwj(torch.from_numpy(p).float().cuda(), out)
+    assert rel(out.cpu().numpy(), O.jtwj(p, dense["osc"], [gv])) < FTOL

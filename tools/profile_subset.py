@@ -70,16 +70,25 @@ def main():
             k.append((e0, e1, e2, e3))
         torch.cuda.synchronize()
         e0, e1, e2, e3 = k[-1]
-        phases["prod_pair_forward"] = e0.elapsed_time(e1)
-        phases["prod_apply_j"] = e1.elapsed_time(e2)
-        phases["prod_apply_jt+backward"] = e2.elapsed_time(e3)
+        phases["api_pair_forward"] = e0.elapsed_time(e1)
+        phases["api_apply_j"] = e1.elapsed_time(e2)
+        phases["api_apply_jt+backward"] = e2.elapsed_time(e3)
+        f = []
+        for _ in range(3):
+            f0 = ev()
+            cs.jtwj(p, g, 1e-4, M, None)
+            f1 = ev()
+            f.append((f0, f1))
+        torch.cuda.synchronize()
+        phases["fused_jtwj_product"] = f[-1][0].elapsed_time(f[-1][1])
         if not args.skip_pcg:
             s0 = ev()
             pcg_run(cs, b, M, 1e-4, cfg["iters"])
             s1 = ev()
             torch.cuda.synchronize()
             phases["pcg_total"] = s0.elapsed_time(s1)
-        phases.update(E=cs.E, N=cs.N, pairs=cs.n_pairs, G=cs.G, mem_gb=torch.cuda.max_memory_allocated() / 1e9)
+        phases.update(E=cs.E, N=cs.N, R=cs.R, pairs=cs.n_pairs, G=cs.G,
+                      mem_gb=torch.cuda.max_memory_allocated() / 1e9)
         out = phases
         del cs
     print(json.dumps(out, indent=1))
