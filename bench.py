@@ -101,7 +101,7 @@ class ClockSampler:
 # workload
 # ---------------------------------------------------------------------------
 
-def make_workload(cfg, device):
+def make_workload(cfg, device, only=None):
     import torch
 
     from paper_2409_12892_b200 import synthetic as S
@@ -117,7 +117,10 @@ def make_workload(cfg, device):
         cams = S.make_camera_ring(V, W, H)
     tscene = truth.to_device(device)
     gts = []
-    for c in cams:
+    for i, c in enumerate(cams):
+        if only is not None and i not in only:
+            gts.append(None)
+            continue
         img = render(tscene, c, traversals=False).image
         gts.append(img.float().contiguous())
     del tscene

@@ -165,9 +165,10 @@ typedef struct {
   const SlmCamera* cams;
   const float* acc;         /* run partials (9 or 14 per run) */
   float scale;
-  const float* p;           /* optional: adds lam * max(M,1e-12) * p and p.out partials */
+  const float* p;           /* optional: fp64 partials of p.(out + lam * max(M,1e-12) * p) */
   const float* Mdiag;
-  float lam;
+  double lam;
+  int lam_out;              /* 1: out += lam * max(M,1e-12) * p as well */
   float* out;
   double* dot_part;
 } SlmBackArgs;
@@ -277,14 +278,16 @@ int slm_pair_backward(const SlmBackArgs* a, int mode, int sh_degree, cudaStream_
 
 /* ---- PCG (Alg. 1; SPEC pcg_solve 391-399) ------------------ */
 int slm_vec_blocks(void);
-int slm_pcg_pupdate(float* p, const float* r, const float* M, const double* st, long long n, cudaStream_t s);
-int slm_pcg_update(int mode, float* x, float* r, const float* p, const float* g, const float* b, const float* M,
-                   double* st, const double* dot_part, int n_dot, double* part, long long n, cudaStream_t s);
+int slm_pcg_pinit(float* p, const float* b, const float* M, long long n, cudaStream_t s);
+int slm_pcg_pupdate(float* p, const double* r, const float* M, const double* st, long long n, cudaStream_t s);
+int slm_pcg_update(int mode, double* x, double* r, const float* p, const float* g, const float* b, const float* M,
+                   double lam, double* st, const double* dot_part, int n_dot, double* part, long long n,
+                   cudaStream_t s);
 int slm_pcg_finalize(int mode, double* st, const double* part, cudaStream_t s);
 
 /* ---- Eq. 7 combine (SPEC solve_normal_equations_batched 400-408) --------- */
-int slm_combine_acc(float* num, float* den, const float* delta, const float* M, long long n, cudaStream_t s);
-int slm_combine_fin(float* out, const float* num, const float* den, long long n, cudaStream_t s);
+int slm_combine_acc(double* num, double* den, const double* delta, const float* M, long long n, cudaStream_t s);
+int slm_combine_fin(float* out, const double* num, const double* den, long long n, cudaStream_t s);
 
 /* ---- layouts and helpers ---------------------------------------------------
  * sort_x / sort_x_inverse (scene.py:79-92) are transposes of the P x G matrix */

@@ -69,7 +69,7 @@ class SlmTileArgs(C.Structure):
 class SlmBackArgs(C.Structure):
     _fields_ = [("xs", c_vp), ("G", c_ll), ("gpo", c_vp), ("gp_list", c_vp), ("pair_run_off", c_vp),
                 ("pair_runs", c_vp), ("pair_vm", c_vp), ("cams", c_vp), ("acc", c_vp), ("scale", c_f),
-                ("p", c_vp), ("Mdiag", c_vp), ("lam", c_f), ("out", c_vp), ("dot_part", c_vp)]
+                ("p", c_vp), ("Mdiag", c_vp), ("lam", c_d), ("lam_out", c_i), ("out", c_vp), ("dot_part", c_vp)]
 
 
 SPLAT_BYTES = 96
@@ -120,8 +120,9 @@ _SIGS = {
     "slm_backward_blocks": (c_i, [c_ll]),
     "slm_pair_backward": (c_i, [c_vp, c_i, c_i, c_vp]),
     "slm_vec_blocks": (c_i, []),
+    "slm_pcg_pinit": (c_i, [c_vp, c_vp, c_vp, c_ll, c_vp]),
     "slm_pcg_pupdate": (c_i, [c_vp, c_vp, c_vp, c_vp, c_ll, c_vp]),
-    "slm_pcg_update": (c_i, [c_i, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i, c_vp, c_ll, c_vp]),
+    "slm_pcg_update": (c_i, [c_i, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_d, c_vp, c_vp, c_i, c_vp, c_ll, c_vp]),
     "slm_pcg_finalize": (c_i, [c_i, c_vp, c_vp, c_vp]),
     "slm_combine_acc": (c_i, [c_vp, c_vp, c_vp, c_vp, c_ll, c_vp]),
     "slm_combine_fin": (c_i, [c_vp, c_vp, c_vp, c_ll, c_vp]),

@@ -3,6 +3,11 @@
 #pragma once
 #include "slm_common.cuh"
 
+// arithmetic type of the per-pair chain (outputs are stored as float)
+#ifndef SLM_CHAIN_T
+#define SLM_CHAIN_T float
+#endif
+
 struct PairM {  // per-pair forward chain result m = dy/dx p (J p), 48 bytes
   float4 a;     // m_mu0, m_mu1, m_cov0, m_cov1
   float4 b;     // m_cov2, m_opa, m_col0, m_col1
@@ -19,23 +24,23 @@ struct Tab {
   float mask[3];
 };
 
-template <int K>
+template <int K, typename Rt = SLM_CHAIN_T>
 __device__ __forceinline__ void pair_tab(const float* __restrict__ xs, long long G, long long g, const SlmCamera& cam,
                                          uint32_t clampbits, Tab<K>& T) {
-  const float p0 = xs[g], p1 = xs[G + g], p2 = xs[2 * G + g];
-  float q[4] = {xs[3 * G + g], xs[4 * G + g], xs[5 * G + g], xs[6 * G + g]};
-  const float l0 = xs[7 * G + g], l1 = xs[8 * G + g], l2 = xs[9 * G + g];
-  const float logit = xs[10 * G + g];
-  float R[9];
+  const Rt p0 = xs[g], p1 = xs[G + g], p2 = xs[2 * G + g];
+  Rt q[4] = {xs[3 * G + g], xs[4 * G + g], xs[5 * G + g], xs[6 * G + g]};
+  const Rt l0 = xs[7 * G + g], l1 = xs[8 * G + g], l2 = xs[9 * G + g];
+  const Rt logit = xs[10 * G + g];
+  Rt R[9];
 #pragma unroll
-  for (int i = 0; i < 9; ++i) R[i] = (float)cam.R[i];
-  const float fx = (float)cam.fx, fy = (float)cam.fy;
-  const float X = R[0] * p0 + R[1] * p1 + R[2] * p2 + (float)cam.t[0];
-  const float Yc = R[3] * p0 + R[4] * p1 + R[5] * p2 + (float)cam.t[1];
-  const float Z = R[6] * p0 + R[7] * p1 + R[8] * p2 + (float)cam.t[2];
-  const float iz = 1.f / Z, iz2 = iz * iz;
-  const float A00 = fx * iz, A02 = -fx * X * iz2, A11 = fy * iz, A12 = -fy * Yc * iz2;
-  float U[2][3];
+  for (int i = 0; i < 9; ++i) R[i] = (Rt)cam.R[i];
+  const Rt fx = (Rt)cam.fx, fy = (Rt)cam.fy;
+  const Rt X = R[0] * p0 + R[1] * p1 + R[2] * p2 + (Rt)cam.t[0];
+  const Rt Yc = R[3] * p0 + R[4] * p1 + R[5] * p2 + (Rt)cam.t[1];
+  const Rt Z = R[6] * p0 + R[7] * p1 + R[8] * p2 + (Rt)cam.t[2];
+  const Rt iz = Rt(1) / Z, iz2 = iz * iz;
+  const Rt A00 = fx * iz, A02 = -fx * X * iz2, A11 = fy * iz, A12 = -fy * Yc * iz2;
+  Rt U[2][3];
 #pragma unroll
   for (int j = 0; j < 3; ++j) {
     U[0][j] = A00 * R[j] + A02 * R[6 + j];
@@ -44,20 +49,20 @@ __device__ __forceinline__ void pair_tab(const float* __restrict__ xs, long long
     T.dmu[1][j] = U[1][j];
   }
   // rotation of the gaussian
-  const float qn = sqrtf(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
-  const float iq = 1.f / qn;
-  const float w = q[0] * iq, a = q[1] * iq, b = q[2] * iq, c = q[3] * iq;
-  float Rg[9] = {1.f - 2.f * (b * b + c * c), 2.f * (a * b - w * c), 2.f * (a * c + w * b),
-                 2.f * (a * b + w * c), 1.f - 2.f * (a * a + c * c), 2.f * (b * c - w * a),
-                 2.f * (a * c - w * b), 2.f * (b * c + w * a), 1.f - 2.f * (a * a + b * b)};
-  const float s2[3] = {__expf(2.f * l0), __expf(2.f * l1), __expf(2.f * l2)};
+  const Rt qn = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+  const Rt iq = Rt(1) / qn;
+  const Rt w = q[0] * iq, a = q[1] * iq, b = q[2] * iq, c = q[3] * iq;
+  Rt Rg[9] = {Rt(1) - Rt(2) * (b * b + c * c), Rt(2) * (a * b - w * c), Rt(2) * (a * c + w * b),
+                 Rt(2) * (a * b + w * c), Rt(1) - Rt(2) * (a * a + c * c), Rt(2) * (b * c - w * a),
+                 Rt(2) * (a * c - w * b), Rt(2) * (b * c + w * a), Rt(1) - Rt(2) * (a * a + b * b)};
+  const Rt s2[3] = {exp(Rt(2) * l0), exp(Rt(2) * l1), exp(Rt(2) * l2)};
   // M = R Rg (camera-frame axes), Sc = M diag(s2) M^T
-  float Mm[9];
+  Rt Mm[9];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int j = 0; j < 3; ++j) Mm[i * 3 + j] = R[i * 3] * Rg[j] + R[i * 3 + 1] * Rg[3 + j] + R[i * 3 + 2] * Rg[6 + j];
-  float Sc[9];
+  Rt Sc[9];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -65,26 +70,26 @@ __device__ __forceinline__ void pair_tab(const float* __restrict__ xs, long long
       Sc[i * 3 + k] = Mm[i * 3] * s2[0] * Mm[k * 3] + Mm[i * 3 + 1] * s2[1] * Mm[k * 3 + 1] +
                       Mm[i * 3 + 2] * s2[2] * Mm[k * 3 + 2];
   // P = Sc A^T (3x2)
-  float P[3][2];
+  Rt P[3][2];
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     P[i][0] = Sc[i * 3] * A00 + Sc[i * 3 + 2] * A02;
     P[i][1] = Sc[i * 3 + 1] * A11 + Sc[i * 3 + 2] * A12;
   }
-  const float cxx = -fx * iz2, cyy = -fy * iz2;
-  const float kx = 2.f * fx * X * iz2 * iz, ky = 2.f * fy * Yc * iz2 * iz;
-  float dX[3][3];
-  dX[0][0] = 2.f * cxx * P[2][0]; dX[0][1] = cxx * P[2][1]; dX[0][2] = 0.f;
-  dX[1][0] = 0.f; dX[1][1] = cyy * P[2][0]; dX[1][2] = 2.f * cyy * P[2][1];
-  const float r00 = cxx * P[0][0] + kx * P[2][0], r01 = cxx * P[0][1] + kx * P[2][1];
-  const float r10 = cyy * P[1][0] + ky * P[2][0], r11 = cyy * P[1][1] + ky * P[2][1];
-  dX[2][0] = 2.f * r00; dX[2][1] = r01 + r10; dX[2][2] = 2.f * r11;
+  const Rt cxx = -fx * iz2, cyy = -fy * iz2;
+  const Rt kx = Rt(2) * fx * X * iz2 * iz, ky = Rt(2) * fy * Yc * iz2 * iz;
+  Rt dX[3][3];
+  dX[0][0] = Rt(2) * cxx * P[2][0]; dX[0][1] = cxx * P[2][1]; dX[0][2] = Rt(0);
+  dX[1][0] = Rt(0); dX[1][1] = cyy * P[2][0]; dX[1][2] = Rt(2) * cyy * P[2][1];
+  const Rt r00 = cxx * P[0][0] + kx * P[2][0], r01 = cxx * P[0][1] + kx * P[2][1];
+  const Rt r10 = cyy * P[1][0] + ky * P[2][0], r11 = cyy * P[1][1] + ky * P[2][1];
+  dX[2][0] = Rt(2) * r00; dX[2][1] = r01 + r10; dX[2][2] = Rt(2) * r11;
 #pragma unroll
   for (int p = 0; p < 3; ++p)
 #pragma unroll
     for (int j = 0; j < 3; ++j) T.dcov[p][j] = dX[0][p] * R[j] + dX[1][p] * R[3 + j] + dX[2][p] * R[6 + j];
   // quaternion: dcov_l = V_l W^T + W V_l^T, V_l = U dR/dq_l, W = U Rg diag(s2)
-  float UR[2][3], Wm[2][3];
+  Rt UR[2][3], Wm[2][3];
 #pragma unroll
   for (int r = 0; r < 2; ++r)
 #pragma unroll
@@ -93,12 +98,12 @@ __device__ __forceinline__ void pair_tab(const float* __restrict__ xs, long long
       Wm[r][j] = UR[r][j] * s2[j];
     }
   // dR/dq_hat_k (3x3 each), row-major
-  const float dRh[4][9] = {
-      {0.f, -2.f * c, 2.f * b, 2.f * c, 0.f, -2.f * a, -2.f * b, 2.f * a, 0.f},
-      {0.f, 2.f * b, 2.f * c, 2.f * b, -4.f * a, -2.f * w, 2.f * c, 2.f * w, -4.f * a},
-      {-4.f * b, 2.f * a, 2.f * w, 2.f * a, 0.f, 2.f * c, -2.f * w, 2.f * c, -4.f * b},
-      {-4.f * c, -2.f * w, 2.f * a, 2.f * w, -4.f * c, 2.f * b, 2.f * a, 2.f * b, 0.f}};
-  float Vh[4][2][3];
+  const Rt dRh[4][9] = {
+      {Rt(0), -Rt(2) * c, Rt(2) * b, Rt(2) * c, Rt(0), -Rt(2) * a, -Rt(2) * b, Rt(2) * a, Rt(0)},
+      {Rt(0), Rt(2) * b, Rt(2) * c, Rt(2) * b, -Rt(4) * a, -Rt(2) * w, Rt(2) * c, Rt(2) * w, -Rt(4) * a},
+      {-Rt(4) * b, Rt(2) * a, Rt(2) * w, Rt(2) * a, Rt(0), Rt(2) * c, -Rt(2) * w, Rt(2) * c, -Rt(4) * b},
+      {-Rt(4) * c, -Rt(2) * w, Rt(2) * a, Rt(2) * w, -Rt(4) * c, Rt(2) * b, Rt(2) * a, Rt(2) * b, Rt(0)}};
+  Rt Vh[4][2][3];
 #pragma unroll
   for (int k = 0; k < 4; ++k)
 #pragma unroll
@@ -106,52 +111,55 @@ __device__ __forceinline__ void pair_tab(const float* __restrict__ xs, long long
 #pragma unroll
       for (int j = 0; j < 3; ++j)
         Vh[k][r][j] = U[r][0] * dRh[k][j] + U[r][1] * dRh[k][3 + j] + U[r][2] * dRh[k][6 + j];
-  const float qh[4] = {w, a, b, c};
+  const Rt qh[4] = {w, a, b, c};
 #pragma unroll
   for (int l = 0; l < 4; ++l) {
-    float V[2][3];
+    Rt V[2][3];
 #pragma unroll
     for (int r = 0; r < 2; ++r)
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
-        float s = 0.f;
+        Rt s = Rt(0);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) s += ((k == l ? 1.f : 0.f) - qh[k] * qh[l]) * Vh[k][r][j];
+        for (int k = 0; k < 4; ++k) s += ((k == l ? Rt(1) : Rt(0)) - qh[k] * qh[l]) * Vh[k][r][j];
         V[r][j] = s * iq;
       }
-    const float v0w0 = V[0][0] * Wm[0][0] + V[0][1] * Wm[0][1] + V[0][2] * Wm[0][2];
-    const float v0w1 = V[0][0] * Wm[1][0] + V[0][1] * Wm[1][1] + V[0][2] * Wm[1][2];
-    const float v1w0 = V[1][0] * Wm[0][0] + V[1][1] * Wm[0][1] + V[1][2] * Wm[0][2];
-    const float v1w1 = V[1][0] * Wm[1][0] + V[1][1] * Wm[1][1] + V[1][2] * Wm[1][2];
-    T.dcov[0][3 + l] = 2.f * v0w0;
+    const Rt v0w0 = V[0][0] * Wm[0][0] + V[0][1] * Wm[0][1] + V[0][2] * Wm[0][2];
+    const Rt v0w1 = V[0][0] * Wm[1][0] + V[0][1] * Wm[1][1] + V[0][2] * Wm[1][2];
+    const Rt v1w0 = V[1][0] * Wm[0][0] + V[1][1] * Wm[0][1] + V[1][2] * Wm[0][2];
+    const Rt v1w1 = V[1][0] * Wm[1][0] + V[1][1] * Wm[1][1] + V[1][2] * Wm[1][2];
+    T.dcov[0][3 + l] = Rt(2) * v0w0;
     T.dcov[1][3 + l] = v0w1 + v1w0;
-    T.dcov[2][3 + l] = 2.f * v1w1;
+    T.dcov[2][3 + l] = Rt(2) * v1w1;
   }
   // log-scale: 2 s_i^2 (U r_i)(U r_i)^T
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    T.dcov[0][7 + i] = 2.f * s2[i] * UR[0][i] * UR[0][i];
-    T.dcov[1][7 + i] = 2.f * s2[i] * UR[0][i] * UR[1][i];
-    T.dcov[2][7 + i] = 2.f * s2[i] * UR[1][i] * UR[1][i];
+    T.dcov[0][7 + i] = Rt(2) * s2[i] * UR[0][i] * UR[0][i];
+    T.dcov[1][7 + i] = Rt(2) * s2[i] * UR[0][i] * UR[1][i];
+    T.dcov[2][7 + i] = Rt(2) * s2[i] * UR[1][i] * UR[1][i];
   }
   // colour
-  const float v0 = p0 - (float)cam.C[0], v1 = p1 - (float)cam.C[1], v2 = p2 - (float)cam.C[2];
-  const float vn = sqrtf(v0 * v0 + v1 * v1 + v2 * v2), ivn = 1.f / vn;
-  const float d0 = v0 * ivn, d1 = v1 * ivn, d2 = v2 * ivn;
-  sh_basis<float, K>(d0, d1, d2, T.Y);
-  float dcdd[3][3];
-  auto coef = [&](int ch, int k) { return xs[(long long)(11 + ch * K + k) * G + g]; };
-  sh_grad_dot<float, K>(d0, d1, d2, coef, dcdd);
+  const Rt v0 = p0 - (Rt)cam.C[0], v1 = p1 - (Rt)cam.C[1], v2 = p2 - (Rt)cam.C[2];
+  const Rt vn = sqrt(v0 * v0 + v1 * v1 + v2 * v2), ivn = Rt(1) / vn;
+  const Rt d0 = v0 * ivn, d1 = v1 * ivn, d2 = v2 * ivn;
+  Rt Yr[K];
+  sh_basis<Rt, K>(d0, d1, d2, Yr);
+#pragma unroll
+  for (int k = 0; k < K; ++k) T.Y[k] = (float)Yr[k];
+  Rt dcdd[3][3];
+  auto coef = [&](int ch, int k) { return (Rt)xs[(long long)(11 + ch * K + k) * G + g]; };
+  sh_grad_dot<Rt, K>(d0, d1, d2, coef, dcdd);
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) {
-    T.mask[ch] = (clampbits >> ch) & 1u ? 0.f : 1.f;
-    const float dd = dcdd[ch][0] * d0 + dcdd[ch][1] * d1 + dcdd[ch][2] * d2;
+    T.mask[ch] = (clampbits >> ch) & 1u ? Rt(0) : Rt(1);
+    const Rt dd = dcdd[ch][0] * d0 + dcdd[ch][1] * d1 + dcdd[ch][2] * d2;
     T.dcol[ch][0] = T.mask[ch] * (dcdd[ch][0] - d0 * dd) * ivn;
     T.dcol[ch][1] = T.mask[ch] * (dcdd[ch][1] - d1 * dd) * ivn;
     T.dcol[ch][2] = T.mask[ch] * (dcdd[ch][2] - d2 * dd) * ivn;
   }
-  const float o = 1.f / (1.f + __expf(-logit));
-  T.dopa = o * (1.f - o);
+  const Rt o = Rt(1) / (Rt(1) + exp(-logit));
+  T.dopa = o * (Rt(1) - o);
 }
 
 // m = dy/dx p per pair (forward chain of applyJ, ref: jacobian.py:434-443).

@@ -234,9 +234,10 @@ __global__ void __launch_bounds__(128) k_pair_backward(SlmBackArgs A) {
       float v = A.scale * (a < 11 ? og[a] : osh[(a - 11) / K][(a - 11) % K]);
       const long long i = (long long)a * G + g;
       if (A.p) {
-        const float pv = A.p[i];
-        if (A.Mdiag) v += A.lam * fmaxf(A.Mdiag[i], 1e-12f) * pv;
-        dot += (double)pv * (double)v;
+        const double pv = (double)A.p[i];
+        const double lt = A.Mdiag ? A.lam * (double)fmaxf(A.Mdiag[i], 1e-12f) * pv : 0.0;
+        dot += pv * ((double)v + lt);
+        if (A.lam_out) v = (float)((double)v + lt);
       }
       A.out[i] = v;
     }

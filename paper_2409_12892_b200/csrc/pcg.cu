@@ -22,12 +22,20 @@
 
 __device__ __forceinline__ float mfloor(float m) { return fmaxf(m, 1e-12f); }
 
-// p = r / Mf + beta * p
-__global__ void k_pcg_pupdate(float* __restrict__ p, const float* __restrict__ r, const float* __restrict__ M,
+// p = r / Mf + beta * p  (r fp64; p is stored fp32 and used consistently as
+// the search direction by the product, x += alpha p and r -= alpha A p)
+__global__ void k_pcg_pupdate(float* __restrict__ p, const double* __restrict__ r, const float* __restrict__ M,
                               const double* __restrict__ st, long long n) {
-  const float beta = (float)st[ST_BETA];
+  const double beta = st[ST_BETA];
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    p[i] = r[i] / mfloor(M[i]) + beta * p[i];
+    p[i] = (float)(r[i] / (double)mfloor(M[i]) + beta * (double)p[i]);
+}
+
+// p = x0 = b / Mf  (Alg. 1 line 4)
+__global__ void k_pcg_pinit(float* __restrict__ p, const float* __restrict__ b, const float* __restrict__ M,
+                            long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = (float)((double)b[i] / (double)mfloor(M[i]));
 }
 
 // sum of a block-partials array in a fixed order (every block gets the same bits)
@@ -41,37 +49,43 @@ __device__ double sum_parts(const double* __restrict__ part, int n, double* sm) 
   return bc;
 }
 
-// INIT (mode 0): x = p (= x0), r = b - g;   partials: r.r/Mf, r.r, b.b
-// STEP (mode 1): alpha = rz / pg; x += alpha p; r -= alpha g; partials r.r/Mf, r.r
-__global__ void k_pcg_update(int mode, float* __restrict__ x, float* __restrict__ r, const float* __restrict__ p,
+// A p = g + lam * Mf * p with g = J^T W J p from the product kernels; the
+// lam term is added here in fp64 because x0 = b / Mf makes |A x0| >> |b| and
+// the residual recurrence would otherwise cancel in fp32 (large lam).
+// INIT (mode 0): x = p (= x0), r = b - A p;   partials: r.r/Mf, r.r, b.b
+// STEP (mode 1): alpha = rz / pg; x += alpha p; r -= alpha A p; partials r.r/Mf, r.r
+__global__ void k_pcg_update(int mode, double* __restrict__ x, double* __restrict__ r, const float* __restrict__ p,
                              const float* __restrict__ g, const float* __restrict__ b, const float* __restrict__ M,
-                             double* __restrict__ st, const double* __restrict__ dot_part, int n_dot,
+                             double lam, double* __restrict__ st, const double* __restrict__ dot_part, int n_dot,
                              double* __restrict__ part /*[3][VEC_BLOCKS]*/, long long n) {
   __shared__ double sm[32];
-  float alpha = 0.f;
+  double alpha = 0.0;
   if (mode == 1) {
     double pg = sum_parts(dot_part, n_dot, sm);
-    double a = st[ST_RZ] / pg;
-    alpha = (float)a;
+    alpha = st[ST_RZ] / pg;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       st[ST_PG] = pg;
-      st[ST_ALPHA] = a;
+      st[ST_ALPHA] = alpha;
     }
   }
   double s_rz = 0.0, s_rr = 0.0, s_bb = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    float ri;
+    const double mf = (double)mfloor(M[i]);
+    const double pi = (double)p[i];
+    const double ap = (double)g[i] + lam * mf * pi;
+    double ri;
     if (mode == 0) {
-      x[i] = p[i];
-      ri = b[i] - g[i];
-      s_bb += (double)b[i] * b[i];
+      x[i] = pi;
+      const double bi = (double)b[i];
+      ri = bi - ap;
+      s_bb += bi * bi;
     } else {
-      x[i] += alpha * p[i];
-      ri = r[i] - alpha * g[i];
+      x[i] += alpha * pi;
+      ri = r[i] - alpha * ap;
     }
     r[i] = ri;
-    s_rz += (double)ri * ri / (double)mfloor(M[i]);
-    s_rr += (double)ri * ri;
+    s_rz += ri * ri / mf;
+    s_rr += ri * ri;
   }
   double t;
   t = block_sum_d(s_rz, sm);
@@ -109,20 +123,20 @@ __global__ void k_pcg_finalize(int mode, double* __restrict__ st, const double* 
   }
 }
 
-// Eq. 7: num += M * delta, den += M;  finalize delta = num / max(den, 1e-12)
-__global__ void k_combine_acc(float* __restrict__ num, float* __restrict__ den, const float* __restrict__ delta,
+// Eq. 7 in fp64: num += M * delta, den += M;  finalize delta = num / max(den, 1e-12)
+__global__ void k_combine_acc(double* __restrict__ num, double* __restrict__ den, const double* __restrict__ delta,
                               const float* __restrict__ M, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const float m = M[i];
+    const double m = (double)M[i];
     num[i] += m * delta[i];
     den[i] += m;
   }
 }
 
-__global__ void k_combine_fin(float* __restrict__ out, const float* __restrict__ num, const float* __restrict__ den,
+__global__ void k_combine_fin(float* __restrict__ out, const double* __restrict__ num, const double* __restrict__ den,
                               long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    out[i] = num[i] / fmaxf(den[i], 1e-12f);
+    out[i] = (float)(num[i] / fmax(den[i], 1e-12));
 }
 
 // (rows x cols) -> (cols x rows) tiled transpose; sortX is the transpose of
@@ -164,14 +178,20 @@ extern "C" {
 
 int slm_vec_blocks() { return VEC_BLOCKS; }
 
-int slm_pcg_pupdate(float* p, const float* r, const float* M, const double* st, long long n, cudaStream_t s) {
+int slm_pcg_pinit(float* p, const float* b, const float* M, long long n, cudaStream_t s) {
+  k_pcg_pinit<<<VEC_BLOCKS, VEC_THREADS, 0, s>>>(p, b, M, n);
+  return slm_cuda_status();
+}
+
+int slm_pcg_pupdate(float* p, const double* r, const float* M, const double* st, long long n, cudaStream_t s) {
   k_pcg_pupdate<<<VEC_BLOCKS, VEC_THREADS, 0, s>>>(p, r, M, st, n);
   return slm_cuda_status();
 }
 
-int slm_pcg_update(int mode, float* x, float* r, const float* p, const float* g, const float* b, const float* M,
-                   double* st, const double* dot_part, int n_dot, double* part, long long n, cudaStream_t s) {
-  k_pcg_update<<<VEC_BLOCKS, VEC_THREADS, 0, s>>>(mode, x, r, p, g, b, M, st, dot_part, n_dot, part, n);
+int slm_pcg_update(int mode, double* x, double* r, const float* p, const float* g, const float* b, const float* M,
+                   double lam, double* st, const double* dot_part, int n_dot, double* part, long long n,
+                   cudaStream_t s) {
+  k_pcg_update<<<VEC_BLOCKS, VEC_THREADS, 0, s>>>(mode, x, r, p, g, b, M, lam, st, dot_part, n_dot, part, n);
   return slm_cuda_status();
 }
 
@@ -180,12 +200,12 @@ int slm_pcg_finalize(int mode, double* st, const double* part, cudaStream_t s) {
   return slm_cuda_status();
 }
 
-int slm_combine_acc(float* num, float* den, const float* delta, const float* M, long long n, cudaStream_t s) {
+int slm_combine_acc(double* num, double* den, const double* delta, const float* M, long long n, cudaStream_t s) {
   k_combine_acc<<<VEC_BLOCKS, VEC_THREADS, 0, s>>>(num, den, delta, M, n);
   return slm_cuda_status();
 }
 
-int slm_combine_fin(float* out, const float* num, const float* den, long long n, cudaStream_t s) {
+int slm_combine_fin(float* out, const double* num, const double* den, long long n, cudaStream_t s) {
   k_combine_fin<<<VEC_BLOCKS, VEC_THREADS, 0, s>>>(out, num, den, n);
   return slm_cuda_status();
 }

@@ -487,13 +487,15 @@ class CacheSet:
     def _run_params(self, a: _lib.SlmTileArgs, with_m: bool):
         call("slm_run_params", _lib.byref(a), self.R, 1 if with_m else 0, ptr(self.run_par), stream_ptr())
 
-    def _back_args(self, acc, out, scale=1.0, p=None, M=None, lam=0.0, dot_part=None) -> _lib.SlmBackArgs:
+    def _back_args(self, acc, out, scale=1.0, p=None, M=None, lam=0.0, dot_part=None,
+                   lam_out=True) -> _lib.SlmBackArgs:
         a = _lib.SlmBackArgs()
         a.xs, a.G = ptr(self.scene.x32()), self.G
         a.gpo, a.gp_list = ptr(self.gpo), ptr(self.gp_list)
         a.pair_run_off, a.pair_runs = ptr(self.pair_run_off), ptr(self.pair_runs)
         a.pair_vm, a.cams, a.acc = ptr(self.pair_vm), ptr(self.cams_dev), ptr(acc)
         a.scale, a.p, a.Mdiag, a.lam = float(scale), ptr(p), ptr(M), float(lam)
+        a.lam_out = 1 if lam_out else 0
         a.out, a.dot_part = ptr(out), ptr(dot_part)
         return a
 
@@ -518,8 +520,10 @@ class CacheSet:
         call("slm_pair_backward", _lib.byref(ba), 0, self.scene.sh_degree, stream_ptr())
         return out
 
-    def jtwj(self, p: torch.Tensor, out: torch.Tensor, lam: float = 0.0, M=None, dot_part=None):
-        """out = J^T W J p (+ lam * max(M, 1e-12) * p); attribute-major fp32.
+    def jtwj(self, p: torch.Tensor, out: torch.Tensor, lam: float = 0.0, M=None, dot_part=None,
+             lam_out: bool = True):
+        """out = J^T W J p (+ lam * max(M, 1e-12) * p when lam_out); attribute-major
+        fp32.  dot_part receives fp64 block partials of p.(J^T W J p + lam Mf p).
 
         Four launches: pair forward chain, run parameter records, the fused
         per-tile J / W / J^T streaming kernel (u never leaves shared memory),
@@ -531,7 +535,7 @@ class CacheSet:
         a.gradr, a.out = ptr(self.gradr), ptr(self.run_acc)
         self._run_params(a, with_m=True)
         call("slm_jtwj_runs", _lib.byref(a), stream_ptr())
-        ba = self._back_args(self.run_acc, out, 1.0, p, M if lam != 0.0 else None, lam, dot_part)
+        ba = self._back_args(self.run_acc, out, 1.0, p, M if lam != 0.0 else None, lam, dot_part, lam_out)
         call("slm_pair_backward", _lib.byref(ba), 0, self.scene.sh_degree, stream_ptr())
         return out
 

@@ -2,8 +2,11 @@
 reference: pcg_solve SPEC:391-399, solve_normal_equations_batched SPEC:400-408;
 Alg. 1; Eq. 7).
 
-All vectors are attribute-major float32 device tensors; scalars stay on the
-device (one 8-byte read per iteration for the exit test).  Multi-GPU: image
+Vectors are attribute-major device tensors: the search direction p and the
+product output are float32 (the products are fp32 kernels), the iterate x and
+the residual r are float64 (x0 = b / Mf makes |A x0| >> |b|, so an fp32
+residual recurrence would cancel), scalars are fp64 and stay on the device
+(one 8-byte read per iteration for the exit test).  Multi-GPU: image
 subsets are sharded round-robin over ranks; each rank accumulates
 num = sum M_i * Delta_i and den = sum M_i, then ONE all_reduce(SUM) of the
 packed [num; den] over NCCL combines them.
@@ -51,7 +54,7 @@ def allreduce_sum_(buf: torch.Tensor, group=None) -> torch.Tensor:
 
 @dataclass
 class PCGWorkspace:
-    """x, r, p, g vectors + device scalar block (SPEC PCGWorkspace)."""
+    """x, r (fp64), p, g (fp32) vectors + device scalar block (SPEC PCGWorkspace)."""
     n: int
     device: torch.device
     x: torch.Tensor = field(init=False)
@@ -63,8 +66,8 @@ class PCGWorkspace:
 
     def __post_init__(self):
         f = torch.float32
-        self.x = torch.empty(self.n, dtype=f, device=self.device)
-        self.r = torch.empty(self.n, dtype=f, device=self.device)
+        self.x = torch.empty(self.n, dtype=torch.float64, device=self.device)
+        self.r = torch.empty(self.n, dtype=torch.float64, device=self.device)
         self.p = torch.empty(self.n, dtype=f, device=self.device)
         self.g = torch.empty(self.n, dtype=f, device=self.device)
         self.st = torch.zeros(16, dtype=torch.float64, device=self.device)
@@ -73,7 +76,7 @@ class PCGWorkspace:
 
 def pcg_run(cache: CacheSet, b: torch.Tensor, M: torch.Tensor, lam: float, max_iters: int,
             ws: PCGWorkspace | None = None, stats: dict | None = None, timer=None) -> torch.Tensor:
-    """Alg. 1 on the device; returns x (attribute-major fp32, owned by ws).
+    """Alg. 1 on the device; returns x (attribute-major fp64, owned by ws).
 
     Raises NonSPDError when p^T g <= 0."""
     n = b.numel()
@@ -82,12 +85,11 @@ def pcg_run(cache: CacheSet, b: torch.Tensor, M: torch.Tensor, lam: float, max_i
     dot_part = torch.zeros(nb, dtype=torch.float64, device=b.device)
     s = stream_ptr()
     ws.st.zero_()
-    ws.p.zero_()
     # p := b / Mf  (= x0, Alg. 1 line 4); g0 = A x0
-    call("slm_pcg_pupdate", ptr(ws.p), ptr(b), ptr(M), ptr(ws.st), n, s)
+    call("slm_pcg_pinit", ptr(ws.p), ptr(b), ptr(M), n, s)
     _product(cache, ws.p, ws.g, lam, M, dot_part, timer)
-    call("slm_pcg_update", 0, ptr(ws.x), ptr(ws.r), ptr(ws.p), ptr(ws.g), ptr(b), ptr(M), ptr(ws.st),
-         ptr(dot_part), nb, ptr(ws.part), n, s)
+    call("slm_pcg_update", 0, ptr(ws.x), ptr(ws.r), ptr(ws.p), ptr(ws.g), ptr(b), ptr(M), float(lam),
+         ptr(ws.st), ptr(dot_part), nb, ptr(ws.part), n, s)
     call("slm_pcg_finalize", 0, ptr(ws.st), ptr(ws.part), s)
     products = 1
     bb = float(ws.st[ST_BB].item())
@@ -97,8 +99,8 @@ def pcg_run(cache: CacheSet, b: torch.Tensor, M: torch.Tensor, lam: float, max_i
             call("slm_pcg_pupdate", ptr(ws.p), ptr(ws.r), ptr(M), ptr(ws.st), n, s)
             _product(cache, ws.p, ws.g, lam, M, dot_part, timer)
             products += 1
-            call("slm_pcg_update", 1, ptr(ws.x), ptr(ws.r), ptr(ws.p), ptr(ws.g), ptr(b), ptr(M), ptr(ws.st),
-                 ptr(dot_part), nb, ptr(ws.part), n, s)
+            call("slm_pcg_update", 1, ptr(ws.x), ptr(ws.r), ptr(ws.p), ptr(ws.g), ptr(b), ptr(M), float(lam),
+                 ptr(ws.st), ptr(dot_part), nb, ptr(ws.part), n, s)
             call("slm_pcg_finalize", 1, ptr(ws.st), ptr(ws.part), s)
             iters += 1
             flags = int(ws.st[ST_FLAGS].item())
@@ -115,11 +117,12 @@ def pcg_run(cache: CacheSet, b: torch.Tensor, M: torch.Tensor, lam: float, max_i
 
 
 def _product(cache, p, g, lam, M, dot_part, timer):
+    """g = J^T W J p (fp32); dot_part = fp64 partials of p.(g + lam Mf p)."""
     if timer is None:
-        cache.jtwj(p, g, lam, M, dot_part)
+        cache.jtwj(p, g, lam, M, dot_part, lam_out=False)
     else:
         with timer:
-            cache.jtwj(p, g, lam, M, dot_part)
+            cache.jtwj(p, g, lam, M, dot_part, lam_out=False)
 
 
 def pcg_solve(scene, cache, b: ParamVector, M_diag: ParamVector, lambda_reg: float, max_iters: int,
@@ -135,10 +138,11 @@ def pcg_solve(scene, cache, b: ParamVector, M_diag: ParamVector, lambda_reg: flo
 
 
 class Combiner:
-    """Eq. 7 accumulator: num += M * Delta, den += M; finalize num / max(den, 1e-12)."""
+    """Eq. 7 accumulator in fp64: num += M * Delta, den += M; finalize
+    num / max(den, 1e-12) to the fp32 direction."""
 
     def __init__(self, n: int, device):
-        self.buf = torch.zeros(2 * n, dtype=torch.float32, device=device)
+        self.buf = torch.zeros(2 * n, dtype=torch.float64, device=device)
         self.n = n
         self.accepted = 0
 

@@ -177,28 +177,67 @@ def test_reference_api_products(prob, oracle_views):
     assert rel(M.values.cpu().numpy(), O.diag_jtj(prob["osc"], ov["gview"])) < FTOL
 
 
-def test_pcg_parity(prob, cacheset, oracle_views):
-    gv = [ov["gview"] for ov in oracle_views]
-    b = sum(ov["b"] for ov in oracle_views)
-    M = sum(O.diag_jtj(prob["osc"], v) for v in gv)
+@pytest.fixture(scope="module")
+def posed():
+    """A well-posed solve (every Gaussian seen by several 48x48 views).  The
+    3-view 32x28 problem above is so under-determined that 8 PCG iterations
+    amplify 2e-7 product rounding into 1e-3..1e-2 changes of Delta (measured,
+    tools/diag_precision.py); here the same kernels agree to ~5e-6."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    truth, init, cams, gts = problem(seed=2, G=100, n_views=6, W=48, H=48, degree=3)
+    osc = oscene(init)
+    ocs = [ocam(c) for c in cams]
+    views, b = [], 0
+    for c, gt in zip(ocs, gts):
+        rs = O.rasterize(osc, c)
+        bb, v = O.build_cache(osc, c, O.residuals(rs["image"], gt), rast=rs)
+        views.append(O.gaussian_order(v))
+        b = b + bb
+    M = sum(O.diag_jtj(osc, v) for v in views)
+    return dict(init=init, cams=cams, gts=gts, osc=osc, ocams=ocs, views=views, b=b, M=M,
+                scene=init.to_device(), gts_d=[torch.from_numpy(g).cuda() for g in gts])
+
+
+PCG_TOL = 1e-4  # rel-L2 of Delta vs the fp64 oracle after n iterations (measured <= 6e-6)
+
+
+def test_pcg_parity(posed):
+    cs = CacheSet(posed["scene"], posed["cams"], posed["gts_d"])
+    assert rel(cs.rhs().cpu().numpy(), posed["b"]) < FTOL
+    assert rel(cs.diag().cpu().numpy(), posed["M"]) < FTOL
     for lam, iters in ((1.0, 6), (1e-4, 8)):
         st = {}
-        ref = O.pcg(prob["osc"], gv, b, M, lam, iters, stats=st)
-        x = pcg_run(cacheset, cacheset.rhs(), cacheset.diag(), lam, iters).cpu().numpy()
-        Mf = np.maximum(M, 1e-12)
-        well = M >= 1e-6 * np.median(M[M > 0])
-        assert rel(x[well], ref[well]) < 1e-3, (lam, rel(x[well], ref[well]))
-        if lam >= 1.0:
-            assert rel(x, ref) < 1e-3
-        assert np.all(np.isfinite(x)) and Mf.min() > 0
+        ref = O.pcg(posed["osc"], posed["views"], posed["b"], posed["M"], lam, iters, stats=st)
+        gst = {}
+        x = pcg_run(cs, cs.rhs(), cs.diag(), lam, iters, stats=gst).cpu().numpy()
+        assert gst["products"] == st["products"]
+        assert rel(x, ref) < PCG_TOL, (lam, rel(x, ref))
+        assert np.all(np.isfinite(x))
 
 
-def test_lm_direction_batched(prob):
-    osc, oc = prob["osc"], prob["ocams"]
-    ref = O.lm_direction(osc, oc, prob["gts"], n_batches=2, lam=1.0, n_iters=5)
-    rep = lm_direction(prob["scene"], prob["cams"], prob["gts_d"], BatchSchedule(2), 1.0, 5)
+def test_pcg_large_lambda(posed):
+    """lambda = 1e6 gives Delta ~= b / (lambda M) within 1%."""
+    cs = CacheSet(posed["scene"], posed["cams"], posed["gts_d"])
+    lam = 1e6
+    x = pcg_run(cs, cs.rhs(), cs.diag(), lam, 8).cpu().numpy()
+    approx = posed["b"] / (lam * np.maximum(posed["M"], 1e-12))
+    assert rel(x, approx) < 1e-2
+
+
+def test_pcg_zero_rhs(posed):
+    """b = 0 gives Delta = 0 without a product."""
+    cs = CacheSet(posed["scene"], posed["cams"], posed["gts_d"])
+    st = {}
+    x = pcg_run(cs, torch.zeros_like(cs.rhs()), cs.diag(), 1e-4, 8, stats=st)
+    assert torch.count_nonzero(x) == 0
+
+
+def test_lm_direction_batched(posed):
+    ref = O.lm_direction(posed["osc"], posed["ocams"], posed["gts"], n_batches=2, lam=1e-4, n_iters=8)
+    rep = lm_direction(posed["scene"], posed["cams"], posed["gts_d"], BatchSchedule(2), 1e-4, 8)
     assert rep.batches_accepted == 2
-    assert rel(rep.delta.cpu().numpy(), ref) < 1e-3
+    assert rel(rep.delta.cpu().numpy(), ref) < PCG_TOL
 
 
 def test_determinism(prob):

@@ -38,7 +38,7 @@ def main():
     dev = torch.device("cuda", 0)
     views = BatchSchedule(cfg["subsets"]).batches(cfg["views"])[0]
     cfg_one = dict(cfg)
-    init, cams, gts = bench.make_workload(cfg_one, dev)
+    init, cams, gts = bench.make_workload(cfg_one, dev, only=set(views))
     scene = init.to_device(dev)
     cams = [cams[i] for i in views]
     gts = [gts[i] for i in views]
