@@ -16,8 +16,9 @@ ground-truth images copied from pinned host memory and the update direction
 copied back, every step.  `roofline` = the J^T W J p product (pair forward +
 applyJ + applyJT + pair backward) against measured HBM bandwidth, algorithmic
 bytes 48 E + 36 N + 16 M per product.  `--impl reference` times
-the fp64 numpy restatement of the reference (oracle/) on the host cores on a
-bounded sample of the same generator and projects it to the workload.
+the reference's own numpy implementation (pip-installed into baseline/_ref)
+driven through Alg. 1 / Eq. 7 (oracle/ref_driver.py) on the host cores, on a
+bounded sample of the same generator, and projects it to the workload.
 """
 
 from __future__ import annotations
@@ -268,19 +269,20 @@ def run_ours(args, cfg):
 
 
 # ---------------------------------------------------------------------------
-# CPU reference arm: the oracle (fp64 numpy restatement of the reference)
+# CPU reference arm: the reference's own numpy code (baseline/_ref) driven
+# through Alg. 1 + Eq. 7 (oracle/ref_driver.py); the oracle port only when the
+# reference package is absent.
 # ---------------------------------------------------------------------------
 
 def cpu_sample(cfg):
     """Bounded sample of the same generator at the same pixels-per-Gaussian
-    and entries-per-pixel: G_s Gaussians, 2 views, resolution scaled so that
-    W*H / G matches the workload."""
+    (hence the same entries-per-pixel): G_s Gaussians, 2 views, resolution
+    scaled so that W*H / G matches the workload."""
     import numpy as np
 
-    import oracle as O
     from paper_2409_12892_b200 import synthetic as S
     G = cfg["G"]
-    Gs = min(G, 4000)
+    Gs = min(G, 8000)
     scale = np.sqrt(Gs / G)
     W = max(16, int(round(cfg["W"] * scale)))
     H = max(16, int(round(cfg["H"] * scale)))
@@ -291,34 +293,52 @@ def cpu_sample(cfg):
         truth = S.make_footprint_scene(0, Gs, W, H, cfg["degree"], k_target=32.0)
         init = S.perturb(truth, 1, 0.02)
     cams = S.make_camera_ring(2, W, H)
+    return truth, init, cams, (Gs, W, H)
+
+
+def time_cpu_sample(cfg, n_iters):
+    """(seconds, entries, shape, kind, phases) of one LM direction on the sample."""
+    from oracle import ref_driver as RD
+    truth, init, cams, shape = cpu_sample(cfg)
+    R = RD.import_reference()
+    if R is not None:
+        R["parallel"].set_num_threads(1)   # GIL-bound render is slower with more (SURVEY 6)
+        rs, rc = RD.ref_scene(R, truth), [RD.ref_camera(R, c) for c in cams]
+        gts = [R["rasterizer"].render(rs, c).image.rgb for c in rc]
+        si = RD.ref_scene(R, init)
+        ph = {}
+        t0 = time.perf_counter()
+        _, E, _ = RD.lm_direction(R, si, rc, gts, n_batches=1, lam=1e-4, n_iters=n_iters, phases=ph)
+        return time.perf_counter() - t0, E, shape, "reference", ph
+    import oracle as O
 
     def osc(h):
         return O.OScene(h.positions, h.rotations, h.log_scales, h.opacity_logits, h.sh_coeffs, h.sh_degree,
                         h.background)
     ocams = [O.OCamera(c.rotation, c.translation, c.fx, c.fy, c.cx, c.cy, c.width, c.height) for c in cams]
     gts = [O.rasterize(osc(truth), c)["image"] for c in ocams]
-    return osc(init), ocams, gts, (Gs, W, H)
-
-
-def time_cpu_sample(cfg, n_iters):
-    import oracle as O
-    s, cams, gts, shape = cpu_sample(cfg)
+    s = osc(init)
     t0 = time.perf_counter()
-    tr = {}
-    O.lm_direction(s, cams, gts, n_batches=1, lam=1e-4, n_iters=n_iters, trace=tr)
+    O.lm_direction(s, ocams, gts, n_batches=1, lam=1e-4, n_iters=n_iters)
     dt = time.perf_counter() - t0
-    E = sum(O.rasterize(s, c)["pixel"].size for c in cams)
-    return dt, E, shape
+    E = sum(O.rasterize(s, c)["pixel"].size for c in ocams)
+    return dt, E, shape, "port", {}
+
+
+def _sample_text(kind, shape, E, dt, iters, ph):
+    who = "reference splatlm (baseline/_ref) + Alg. 1/Eq. 7 driver" if kind == "reference" else "oracle port"
+    phs = ", ".join(f"{k} {v:.2f}s" for k, v in ph.items())
+    return (f"{who}: LM step on {shape[0]} Gaussians, 2 views @ {shape[1]}x{shape[2]}, {E} entries, "
+            f"{iters} PCG iters = {dt:.2f} s ({1e9 * dt / max(E, 1):.0f} ns/entry; {phs})")
 
 
 def cpu_baseline(cfg, rep, args):
-    dt, E, shape = time_cpu_sample(cfg, cfg["iters"])
+    dt, E, shape, kind, ph = time_cpu_sample(cfg, cfg["iters"])
     E_full = sum(rep.entries) * 1.0
     proj_ms = dt * 1e3 * (E_full / max(E, 1)) if rep.entries else None
-    return {"value": round(proj_ms, 1) if proj_ms else None, "unit": "ms", "cores": 1, "kind": "port",
-            "sample": f"oracle LM step on {shape[0]} Gaussians, 2 views @ {shape[1]}x{shape[2]} "
-                      f"({E} entries, {cfg['iters']} PCG iters) = {dt:.2f} s, projected linearly in cache "
-                      f"entries to the workload's {int(E_full)} entries/step",
+    return {"value": round(proj_ms, 1) if proj_ms else None, "unit": "ms", "cores": 1, "kind": kind,
+            "sample": _sample_text(kind, shape, E, dt, cfg["iters"], ph)
+            + f"; projected linearly in cache entries to the workload's {int(E_full)} entries/step",
             "cpu": _cpu_name(), "os_cpu_count": os.cpu_count()}
 
 
@@ -337,23 +357,24 @@ def run_reference(args, cfg):
     if rank != 0:
         return None
     os.environ.setdefault("OMP_NUM_THREADS", "1")
-    # entries of the full workload: K * pixels (K from the sample, same generator)
     times = []
     for i in range(args.warmup + args.steps):
-        dt, E, shape = time_cpu_sample(cfg, cfg["iters"])
+        dt, E, shape, kind, ph = time_cpu_sample(cfg, cfg["iters"])
         if i >= args.warmup:
             times.append(dt)
     dt = statistics.median(times)
+    # entries of the full workload: K (entries per pixel, from the sample) x pixels
     k = E / (2 * shape[1] * shape[2])
     E_full = k * cfg["views"] * cfg["W"] * cfg["H"]
     ms = dt * 1e3 * E_full / E
     line = {"metric": METRIC, "value": round(ms, 1), "unit": "ms", "n_gpus": 0, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 1), "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"{args.config.upper()} (same generator), projected from a bounded sample"},
-            "cpu_baseline": {"value": round(ms, 1), "unit": "ms", "cores": 1, "kind": "port",
-                             "sample": f"oracle LM step, {shape[0]} Gaussians, 2 views @ {shape[1]}x{shape[2]}, "
-                                       f"{E} entries, median {dt:.2f} s; x{E_full / E:.0f} entries"},
+            "config": {"workload": f"{args.config.upper()} (same generator), projected from a bounded sample",
+                       "entries_per_pixel": round(k, 2)},
+            "cpu_baseline": {"value": round(ms, 1), "unit": "ms", "cores": 1, "kind": kind,
+                             "sample": _sample_text(kind, shape, E, dt, cfg["iters"], ph)
+                             + f"; median of {args.steps}, x{E_full / E:.0f} entries to the workload"},
             "e2e": {"value": round(ms, 1), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return line

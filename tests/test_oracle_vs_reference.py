@@ -61,3 +61,21 @@ def test_ssim_blur_equals_scipy():
         k = O.lm_oracle._taps()
         ref = correlate1d(correlate1d(img, k, axis=0, mode="reflect"), k, axis=1, mode="reflect")
         assert rel(O.ssim_blur(img), ref) < 1e-14
+
+
+def test_lm_direction_oracle_equals_reference_driver():
+    """The oracle's PCG + Eq. 7 restatement against the same loop driven by the
+    reference's own products (oracle/ref_driver.py, the bench reference arm)."""
+    from oracle import ref_driver as RD
+    R = RD.import_reference()
+    if R is None:
+        pytest.skip("reference package not available")
+    truth = S.make_synthetic_scene(2, 40, 2)
+    init = S.perturb(truth, 3, 0.1)
+    cams = S.make_camera_ring(4, 24, 20)
+    gts = [O.rasterize(oscene(truth), ocam(c))["image"] for c in cams]
+    ref, entries, ph = RD.lm_direction(R, RD.ref_scene(R, init), [RD.ref_camera(R, c) for c in cams], gts,
+                                       n_batches=2, lam=1e-2, n_iters=5)
+    got = O.lm_direction(oscene(init), [ocam(c) for c in cams], gts, n_batches=2, lam=1e-2, n_iters=5)
+    assert entries > 0 and "pcg_products" in ph
+    assert rel(got, ref) < 1e-9
