@@ -14,8 +14,9 @@
  * Cache layout ("runs"): a run is one (tile, splat) pair of a view with at
  * least one kept pixel; runs are numbered (view, tile, depth order) and each
  * run's entries are stored contiguously in tile-local pixel order, with a
- * 256-bit mask of the kept pixels.  Records are SoA float32 {alpha_eff,
- * alpha*T, dc/dalpha[3]} plus a uint8 tile-local pixel index (21 B/entry).
+ * 256-bit mask of the kept pixels.  Records are float4 {alpha_eff, alpha*T,
+ * dc/dalpha_r, dc/dalpha_g} + float dc/dalpha_b + uint8 tile-local pixel index
+ * (21 B/entry, three streams so one entry is three shared-memory loads).
  */
 #ifndef SPLATLM_B200_H
 #define SPLATLM_B200_H
@@ -98,7 +99,8 @@ typedef struct {
   uint32_t* inst_mask;        /* [n_inst*8] keep mask per instance (COUNT out, FILL in) */
   /* FILL: run-ordered cache records */
   const long long* inst_start;  /* [n_inst] first entry of the instance's run */
-  float *rec_ae, *rec_at, *rec_d0, *rec_d1, *rec_d2;
+  slm_f4* rec4;               /* {alpha_eff, alpha*T, dc/dalpha_r, dc/dalpha_g} */
+  float* rec_d2;              /* dc/dalpha_b */
   uint8_t* rec_pix;           /* tile-local pixel index (16 * ly + lx) */
   /* FILL: optional pixel-order Traversals export (rasterizer.py:209-243) */
   const long long* pix_off;
@@ -138,14 +140,15 @@ typedef struct {
   const int* tile_run_off;   /* [n_tiles+1] */
   const int* tile_chunk_off; /* [n_tiles+1] chunk table (slm_tile_chunks) */
   const int* chunk_run;      /* [n_chunks+1] first run of each chunk */
+  const uint8_t* chunk_perm; /* [n_chunks*32] J^T schedule: chunk-local runs by decreasing length */
   const long long* run_start;/* [R+1] (+2 padding slots) */
   const int* run_q;          /* pair of each run */
   const uint32_t* run_tile;  /* view << 24 | tile */
-  const float* run_par;      /* [R*16] per-product run parameters (slm_run_params) */
+  const float* run_par;      /* [R*16] run parameter records (slm_pair_forward / slm_run_params) */
   const SlmPairGeo* geo;
-  const void* pm;            /* applyJ: per-pair forward chain (slm_pair_forward), 48 B each */
   const float* ptab;         /* diag: per-pair coefficient tables (slm_pair_tables) */
-  const float *ae, *at, *d0, *d1, *d2;
+  const slm_f4* rec4;
+  const float* d2;
   const uint8_t* pix;
   const slm_f4* gradr;       /* applyJ: weighting (NULL: unweighted u_hat); diag: grad_r_sq */
   const slm_f4* u;           /* applyJT input, per pixel */
@@ -153,17 +156,32 @@ typedef struct {
   float* out;                /* applyJT [R*9] / diag [R*14] run partials */
 } SlmTileArgs;
 
+/* per-pair forward chain + per-run parameter records (applyJ) */
+typedef struct {
+  const float* xs;          /* scene, attribute-major fp32 */
+  long long G;
+  const int* pair_gid;
+  const uint32_t* pair_vm;  /* view | clamp bits << 16 */
+  const SlmCamera* cams;
+  int n_pairs;
+  const float* p;           /* direction, p[a * sa + g * sg] (either layout) */
+  long long sa, sg;
+  const SlmPairGeo* geo;
+  const int* pair_run_off;  /* [P+1] pair -> runs CSR */
+  const int* pair_runs;
+  const uint32_t* run_tile; /* view << 24 | tile */
+  const SlmView* views;
+  float* run_par;           /* [R*16] out */
+} SlmFwdArgs;
+
 /* per-gaussian backward chain */
 typedef struct {
   const float* xs; /* scene, attribute-major fp32 */
   long long G;
-  const int* gpo;           /* [G+1] gaussian -> pairs CSR */
-  const int* gp_list;
-  const int* pair_run_off;  /* [P+1] pair -> runs CSR (tile order) */
-  const int* pair_runs;
+  const int* gpo;           /* [G+1] gaussian -> pairs (pairs are (gid, view)-numbered) */
   const uint32_t* pair_vm;  /* view | clamp bits << 16 */
   const SlmCamera* cams;
-  const float* acc;         /* run partials (9 or 14 per run) */
+  const float* pacc;        /* per-pair sums (9 or 14 per pair, slm_pair_sum) */
   float scale;
   const float* p;           /* optional: fp64 partials of p.(out + lam * max(M,1e-12) * p) */
   const float* Mdiag;
@@ -183,6 +201,7 @@ int slm_raster_args_size(void);
 int slm_resid_args_size(void);
 int slm_tile_args_size(void);
 int slm_back_args_size(void);
+int slm_fwd_args_size(void);
 int slm_diag_tab_floats(void);
 
 /* ---- projection / rasterisation ------------------------------------------
@@ -246,7 +265,7 @@ int slm_px_prepare(const uint32_t* cnt, long long n, long long* cnt64, int* none
 int slm_pairs_prepare(const int* cnt, int V, long long G, long long* cntV, int* flagV, int* flagT, cudaStream_t s);
 int slm_pairs_emit(const int* cnt, int V, long long G, const int* pair_of, const long long* vscan, const int* tscan,
                    const SlmSplat* splats, long long* pair_off, int* pair_gid, uint32_t* pair_vm, SlmPairGeo* geo,
-                   int* pidx, int* gpo, int* gp_list, int n_pairs, long long n_entries, cudaStream_t s);
+                   int* pidx, int* gpo, int n_pairs, long long n_entries, cudaStream_t s);
 
 /* ---- products ----------------------------------------------------------------
  * apply_j (jacobian.py:419-455) fused with weight_residuals (458-464) when
@@ -257,22 +276,27 @@ int slm_apply_jt_runs(const SlmTileArgs* a, cudaStream_t s);
 /* fused apply_jt(weight_residuals(apply_j(p))) first half, tile by tile: u
  * stays in shared memory, the cache is streamed from HBM once */
 int slm_jtwj_runs(const SlmTileArgs* a, cudaStream_t s);
-/* per-product run parameter records (with_m: forward chain m included) and
- * the per-tile chunk table (fill=0: counts per tile, fill=1: chunk_run) */
-int slm_run_params(const SlmTileArgs* a, long long n_runs, int with_m, float* out, cudaStream_t s);
+/* static run parameter records for the J^T-only mode, and the per-tile chunk
+ * table (fill=0: counts per tile, fill=1: chunk_run) + the per-chunk J^T
+ * schedule (runs by decreasing length, slm_chunk_perm) */
+int slm_run_params(const SlmTileArgs* a, long long n_runs, float* out, cudaStream_t s);
 int slm_tile_chunks(const int* tile_run_off, int n_tiles, const long long* run_start, const int* tile_chunk_off,
-                    int* out, int fill, cudaStream_t s);
+                    int* out, uint8_t* chunk_perm, int fill, cudaStream_t s);
+int slm_chunk_perm(const int* chunk_run, long long n_chunks, const long long* run_start, uint8_t* chunk_perm,
+                   cudaStream_t s);
 /* diag_jtj (jacobian.py:486-512), first half: per-pair coefficient tables,
  * then 14 sums per run (a->gradr = grad_r_sq, a->ptab = tables) */
 int slm_pair_tables(const float* xs, long long G, int sh_degree, const int* pair_gid, const uint32_t* pair_vm,
                     const SlmCamera* cams, int n_pairs, float* tab, cudaStream_t s);
 int slm_diag_runs(const SlmTileArgs* a, cudaStream_t s);
-/* forward chain m = dy/dx p per pair; p[a*sa + g*sg] (either layout) */
-int slm_pair_forward(const float* xs, long long G, int sh_degree, const int* pair_gid, const uint32_t* pair_vm,
-                     const SlmCamera* cams, int n_pairs, const float* p, long long sa, long long sg, void* pm,
-                     cudaStream_t s);
+/* forward chain m = dy/dx p per pair (jacobian.py:434-443), written as the
+ * 64-byte parameter record of every run of the pair */
+int slm_pair_forward(const SlmFwdArgs* a, int sh_degree, cudaStream_t s);
+/* per-pair sums of run partials (d = 9 J^T partials or 14 diag sums) */
+int slm_pair_sum(const int* pair_run_off, const int* pair_runs, int n_pairs, const float* run_acc, int d,
+                 float* pacc, cudaStream_t s);
 /* backward chain per gaussian, attribute-major out (jacobian.py:314-353):
- * mode 0 from J^T run partials, mode 1 from diag run sums */
+ * mode 0 from J^T pair sums, mode 1 from diag pair sums */
 int slm_backward_blocks(long long G);
 int slm_pair_backward(const SlmBackArgs* a, int mode, int sh_degree, cudaStream_t s);
 

@@ -42,8 +42,7 @@ class SlmRasterArgs(C.Structure):
     _fields_ = [("tile_range", c_vp), ("inst_gid", c_vp), ("splats", c_vp),
                 ("W", c_i), ("H", c_i), ("tiles_x", c_i), ("pix_base", c_ll), ("cfg", SlmRastCfg),
                 ("px_count", c_vp), ("rgb", c_vp), ("t_final", c_vp), ("inst_mask", c_vp),
-                ("inst_start", c_vp), ("rec_ae", c_vp), ("rec_at", c_vp), ("rec_d0", c_vp), ("rec_d1", c_vp),
-                ("rec_d2", c_vp), ("rec_pix", c_vp),
+                ("inst_start", c_vp), ("rec4", c_vp), ("rec_d2", c_vp), ("rec_pix", c_vp),
                 ("pix_off", c_vp), ("view_entry_base", c_ll), ("trav_gid", c_vp), ("trav_alpha", c_vp),
                 ("trav_T", c_vp)]
 
@@ -59,16 +58,22 @@ class SlmResidArgs(C.Structure):
 
 class SlmTileArgs(C.Structure):
     _fields_ = [("views", c_vp), ("view_tile_base", c_vp), ("n_views", c_i), ("n_tiles", c_i),
-                ("tile_run_off", c_vp), ("tile_chunk_off", c_vp), ("chunk_run", c_vp),
+                ("tile_run_off", c_vp), ("tile_chunk_off", c_vp), ("chunk_run", c_vp), ("chunk_perm", c_vp),
                 ("run_start", c_vp), ("run_q", c_vp), ("run_tile", c_vp), ("run_par", c_vp),
-                ("geo", c_vp), ("pm", c_vp), ("ptab", c_vp),
-                ("ae", c_vp), ("at", c_vp), ("d0", c_vp), ("d1", c_vp), ("d2", c_vp), ("pix", c_vp),
+                ("geo", c_vp), ("ptab", c_vp),
+                ("rec4", c_vp), ("d2", c_vp), ("pix", c_vp),
                 ("gradr", c_vp), ("u", c_vp), ("u_out", c_vp), ("out", c_vp)]
 
 
+class SlmFwdArgs(C.Structure):
+    _fields_ = [("xs", c_vp), ("G", c_ll), ("pair_gid", c_vp), ("pair_vm", c_vp), ("cams", c_vp), ("n_pairs", c_i),
+                ("p", c_vp), ("sa", c_ll), ("sg", c_ll), ("geo", c_vp), ("pair_run_off", c_vp), ("pair_runs", c_vp),
+                ("run_tile", c_vp), ("views", c_vp), ("run_par", c_vp)]
+
+
 class SlmBackArgs(C.Structure):
-    _fields_ = [("xs", c_vp), ("G", c_ll), ("gpo", c_vp), ("gp_list", c_vp), ("pair_run_off", c_vp),
-                ("pair_runs", c_vp), ("pair_vm", c_vp), ("cams", c_vp), ("acc", c_vp), ("scale", c_f),
+    _fields_ = [("xs", c_vp), ("G", c_ll), ("gpo", c_vp), ("pair_vm", c_vp), ("cams", c_vp), ("pacc", c_vp),
+                ("scale", c_f),
                 ("p", c_vp), ("Mdiag", c_vp), ("lam", c_d), ("lam_out", c_i), ("out", c_vp), ("dot_part", c_vp)]
 
 
@@ -83,6 +88,7 @@ _SIGS = {
     "slm_camera_size": (c_i, []), "slm_rastcfg_size": (c_i, []), "slm_splat_size": (c_i, []),
     "slm_pair_geo_size": (c_i, []), "slm_view_size": (c_i, []), "slm_raster_args_size": (c_i, []),
     "slm_resid_args_size": (c_i, []), "slm_tile_args_size": (c_i, []), "slm_back_args_size": (c_i, []),
+    "slm_fwd_args_size": (c_i, []),
     "slm_diag_tab_floats": (c_i, []),
     "slm_preprocess": (c_i, [c_vp, c_ll, c_i, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "slm_sort_pairs_u64_workspace": (c_ll, [c_ll]),
@@ -107,16 +113,18 @@ _SIGS = {
     "slm_iota_u32": (c_i, [c_vp, c_ll, c_vp]),
     "slm_px_prepare": (c_i, [c_vp, c_ll, c_vp, c_vp, c_vp]),
     "slm_pairs_prepare": (c_i, [c_vp, c_i, c_ll, c_vp, c_vp, c_vp, c_vp]),
-    "slm_pairs_emit": (c_i, [c_vp, c_i, c_ll, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+    "slm_pairs_emit": (c_i, [c_vp, c_i, c_ll, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                              c_i, c_ll, c_vp]),
     "slm_apply_j": (c_i, [c_vp, c_vp]),
     "slm_apply_jt_runs": (c_i, [c_vp, c_vp]),
     "slm_jtwj_runs": (c_i, [c_vp, c_vp]),
-    "slm_run_params": (c_i, [c_vp, c_ll, c_i, c_vp, c_vp]),
-    "slm_tile_chunks": (c_i, [c_vp, c_i, c_vp, c_vp, c_vp, c_i, c_vp]),
+    "slm_run_params": (c_i, [c_vp, c_ll, c_vp, c_vp]),
+    "slm_chunk_perm": (c_i, [c_vp, c_ll, c_vp, c_vp, c_vp]),
+    "slm_tile_chunks": (c_i, [c_vp, c_i, c_vp, c_vp, c_vp, c_vp, c_i, c_vp]),
     "slm_pair_tables": (c_i, [c_vp, c_ll, c_i, c_vp, c_vp, c_vp, c_i, c_vp, c_vp]),
     "slm_diag_runs": (c_i, [c_vp, c_vp]),
-    "slm_pair_forward": (c_i, [c_vp, c_ll, c_i, c_vp, c_vp, c_vp, c_i, c_vp, c_ll, c_ll, c_vp, c_vp]),
+    "slm_pair_forward": (c_i, [c_vp, c_i, c_vp]),
+    "slm_pair_sum": (c_i, [c_vp, c_vp, c_i, c_vp, c_i, c_vp, c_vp]),
     "slm_backward_blocks": (c_i, [c_ll]),
     "slm_pair_backward": (c_i, [c_vp, c_i, c_i, c_vp]),
     "slm_vec_blocks": (c_i, []),
@@ -155,7 +163,7 @@ def load():
         fn.argtypes = args
     checks = {"slm_camera_size": SlmCamera, "slm_rastcfg_size": SlmRastCfg, "slm_view_size": SlmView,
               "slm_raster_args_size": SlmRasterArgs, "slm_resid_args_size": SlmResidArgs,
-              "slm_tile_args_size": SlmTileArgs, "slm_back_args_size": SlmBackArgs}
+              "slm_tile_args_size": SlmTileArgs, "slm_back_args_size": SlmBackArgs, "slm_fwd_args_size": SlmFwdArgs}
     for fn, st in checks.items():
         if getattr(lib, fn)() != C.sizeof(st):
             raise SplatLMError(f"ABI mismatch: {fn} = {getattr(lib, fn)()} vs ctypes {C.sizeof(st)}")

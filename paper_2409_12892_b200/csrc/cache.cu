@@ -68,11 +68,10 @@ __global__ void k_px_prepare(const uint32_t* __restrict__ cnt, long long n, long
 }
 
 // ---------------------------------------------------------------------------
-// pairs: (gaussian, view) with >= 1 entry, numbered in (view, gid) order so
-// that one view's pairs -- and the gaussian-order records, u and grad_r_sq
-// they touch -- are contiguous and L2-resident while that view is streamed.
-// The per-gaussian backward chain reaches its pairs through a gid-major CSR
-// (gpo / gp_list).
+// pairs: (gaussian, view) with >= 1 entry, numbered in (gid, view) order:
+// the pairs of one gaussian are contiguous (gpo CSR), so the per-pair chain
+// kernels read each gaussian's parameters once and the per-gaussian backward
+// chain reads its pairs' sums contiguously.
 // ---------------------------------------------------------------------------
 __global__ void k_pairs_prepare(const int* __restrict__ cnt /*[V][G]*/, int V, long long G,
                                 long long* __restrict__ cntV /*[V*G] view-major*/, int* __restrict__ flagV,
@@ -92,7 +91,7 @@ __global__ void k_pairs_emit(const int* __restrict__ cnt, int V, long long G, co
                              const SlmSplat* __restrict__ splats /*[V][G]*/, long long* __restrict__ pair_off,
                              int* __restrict__ pair_gid, uint32_t* __restrict__ pair_vm,
                              SlmPairGeo* __restrict__ geo, int* __restrict__ pidx, int* __restrict__ gpo /*[G+1]*/,
-                             int* __restrict__ gp_list, int n_pairs, long long n_entries) {
+                             int n_pairs, long long n_entries) {
   long long n = (long long)V * G;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const long long v = i / G, g = i % G;
@@ -102,7 +101,7 @@ __global__ void k_pairs_emit(const int* __restrict__ cnt, int V, long long G, co
       pidx[i] = -1;
       continue;
     }
-    const int q = pair_of[i];
+    const int q = tscan[g * V + v];  // (gid, view) numbering
     pair_off[q] = vscan[i];
     pair_gid[q] = (int)g;
     const SlmSplat s = splats[i];
@@ -113,7 +112,6 @@ __global__ void k_pairs_emit(const int* __restrict__ cnt, int V, long long G, co
     pg.inv_o = (float)(1.0 / s.o);
     geo[q] = pg;
     pidx[i] = q;
-    gp_list[tscan[g * V + v]] = q;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     gpo[G] = n_pairs;
@@ -140,10 +138,9 @@ int slm_pairs_prepare(const int* cnt, int V, long long G, long long* cntV, int* 
 
 int slm_pairs_emit(const int* cnt, int V, long long G, const int* pair_of, const long long* vscan, const int* tscan,
                    const SlmSplat* splats, long long* pair_off, int* pair_gid, uint32_t* pair_vm, SlmPairGeo* geo,
-                   int* pidx, int* gpo, int* gp_list, int n_pairs, long long n_entries, cudaStream_t s) {
+                   int* pidx, int* gpo, int n_pairs, long long n_entries, cudaStream_t s) {
   k_pairs_emit<<<slm_blocks((long long)V * G, 256), 256, 0, s>>>(cnt, V, G, pair_of, vscan, tscan, splats, pair_off,
-                                                                  pair_gid, pair_vm, geo, pidx, gpo, gp_list, n_pairs,
-                                                                  n_entries);
+                                                                  pair_gid, pair_vm, geo, pidx, gpo, n_pairs, n_entries);
   return slm_cuda_status();
 }
 

@@ -8,12 +8,6 @@
 #define SLM_CHAIN_T float
 #endif
 
-struct PairM {  // per-pair forward chain result m = dy/dx p (J p), 48 bytes
-  float4 a;     // m_mu0, m_mu1, m_cov0, m_cov1
-  float4 b;     // m_cov2, m_opa, m_col0, m_col1
-  float4 c;     // m_col2, -, -, -
-};
-
 template <int K>
 struct Tab {
   float dmu[2][3];
@@ -162,24 +156,27 @@ __device__ __forceinline__ void pair_tab(const float* __restrict__ xs, long long
   T.dopa = o * (Rt(1) - o);
 }
 
-// m = dy/dx p per pair (forward chain of applyJ, ref: jacobian.py:434-443).
+// Forward chain of applyJ (ref: jacobian.py:434-443) fused with the per-run
+// parameter records of the product kernel: per pair, m = dy/dx p (9 numbers),
+// then one 64-byte record per run of the pair (pairs are numbered (gid, view),
+// so consecutive threads share the gaussian's parameters):
+//   P[0..1] splat centre minus the tile's pixel-centre origin, P[2..4] conic,
+//   P[5] inv_o * m_opa, P[6..10] m_mu0, m_mu1, m_cov0/2, m_cov1, m_cov2/2,
+//   P[11..13] m_col, P[14] inv_o, P[15] 0.
 // p is read with strides so both layouts work: p[a * sa + g * sg].
 template <int K>
-__global__ void __launch_bounds__(128) k_pair_forward(const float* __restrict__ xs, long long G,
-                                                      const int* __restrict__ pair_gid,
-                                                      const uint32_t* __restrict__ pair_vm,
-                                                      const SlmCamera* __restrict__ cams, int n_pairs,
-                                                      const float* __restrict__ p, long long sa, long long sg,
-                                                      PairM* __restrict__ pm) {
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_pairs; q += gridDim.x * blockDim.x) {
-    const long long g = pair_gid[q];
-    const uint32_t vm = pair_vm[q];
+__global__ void __launch_bounds__(128) k_pair_forward(SlmFwdArgs A) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < A.n_pairs; q += gridDim.x * blockDim.x) {
+    const long long g = A.pair_gid[q];
+    const uint32_t vm = A.pair_vm[q];
+    const long long sa = A.sa, sg = A.sg;
+    const float* __restrict__ p = A.p;
     Tab<K> T;
-    pair_tab<K>(xs, G, g, cams[vm & 0xffffu], vm >> 16, T);
+    pair_tab<K>(A.xs, A.G, g, A.cams[vm & 0xffffu], vm >> 16, T);
     float pg[11];
 #pragma unroll
     for (int a = 0; a < 11; ++a) pg[a] = p[a * sa + g * sg];
-    float mmu0 = 0.f, mmu1 = 0.f, mc[3] = {0.f, 0.f, 0.f}, mcol[3] = {0.f, 0.f, 0.f};
+    float mmu0 = 0.f, mmu1 = 0.f, mc[3] = {0.f, 0.f, 0.f}, mcol[3];
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
       mmu0 += T.dmu[0][j] * pg[j];
@@ -196,10 +193,22 @@ __global__ void __launch_bounds__(128) k_pair_forward(const float* __restrict__ 
       for (int k = 0; k < K; ++k) s += T.Y[k] * p[(11 + ch * K + k) * sa + g * sg];
       mcol[ch] = T.dcol[ch][0] * pg[0] + T.dcol[ch][1] * pg[1] + T.dcol[ch][2] * pg[2] + T.mask[ch] * s;
     }
-    PairM m;
-    m.a = make_float4(mmu0, mmu1, mc[0], mc[1]);
-    m.b = make_float4(mc[2], T.dopa * pg[10], mcol[0], mcol[1]);
-    m.c = make_float4(mcol[2], 0.f, 0.f, 0.f);
-    pm[q] = m;
+    const float mopa = T.dopa * pg[10];
+    const SlmPairGeo ge = A.geo[q];
+    const SlmView vw = A.views[vm & 0xffffu];
+    const int tiles_x = (vw.W + SLM_TILE - 1) / SLM_TILE;
+    const float4 r1 = make_float4(ge.kc, ge.inv_o * mopa, mmu0, mmu1);
+    const float4 r2 = make_float4(0.5f * mc[0], mc[1], 0.5f * mc[2], mcol[0]);
+    const float4 r3 = make_float4(mcol[1], mcol[2], ge.inv_o, 0.f);
+    for (int rr = A.pair_run_off[q]; rr < A.pair_run_off[q + 1]; ++rr) {
+      const int r = A.pair_runs[rr];
+      const int lt = (int)(A.run_tile[r] & 0xffffffu);
+      const double ox = (double)((lt % tiles_x) * SLM_TILE) + 0.5, oy = (double)((lt / tiles_x) * SLM_TILE) + 0.5;
+      float4* o = reinterpret_cast<float4*>(A.run_par + (size_t)r * 16);
+      o[0] = make_float4((float)(ge.mx - ox), (float)(ge.my - oy), ge.ka, ge.kb);
+      o[1] = r1;
+      o[2] = r2;
+      o[3] = r3;
+    }
   }
 }

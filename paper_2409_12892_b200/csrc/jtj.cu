@@ -130,8 +130,9 @@ __global__ void __launch_bounds__(256) k_diag_tile(SlmTileArgs A) {
       for (int j = 0; j < 16; ++j) a[j] = 0.f;
       for (int j = lane; j < n; j += 32) {
         const long long e = st + j;
-        const float ae = A.ae[e], at = A.at[e];
-        const float dd[3] = {A.d0[e], A.d1[e], A.d2[e]};
+        const float4 r4 = A.rec4[e];
+        const float ae = r4.x, at = r4.y;
+        const float dd[3] = {r4.z, r4.w, A.d2[e]};
         const int pl = A.pix[e];
         const float4 gr = s_g[pl];
         const float grc[3] = {gr.x, gr.y, gr.z};
@@ -170,13 +171,37 @@ __global__ void __launch_bounds__(256) k_diag_tile(SlmTileArgs A) {
 }
 
 // ---------------------------------------------------------------------------
+// per-pair sums of the run partials (fixed run order -> deterministic):
+// pacc[q] = sum over the pair's runs of acc[run] (D = 9 J^T partials or 14
+// diag sums); pairs are (gid, view)-numbered, so the backward chain below
+// reads them contiguously
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void k_pair_sum(const int* __restrict__ pair_run_off, const int* __restrict__ pair_runs, int n_pairs,
+                           const float* __restrict__ acc, float* __restrict__ pacc) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_pairs; q += gridDim.x * blockDim.x) {
+    float a[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) a[j] = 0.f;
+    for (int rr = pair_run_off[q]; rr < pair_run_off[q + 1]; ++rr) {
+      const float* src = acc + (size_t)pair_runs[rr] * D;
+#pragma unroll
+      for (int j = 0; j < D; ++j) a[j] += src[j];
+    }
+#pragma unroll
+    for (int j = 0; j < D; ++j) pacc[(size_t)q * D + j] = a[j];
+  }
+}
+
+// ---------------------------------------------------------------------------
 // per-gaussian backward chain (ref: jacobian.py:314-353 / 506-510):
-//   MODE 0: out = scale * sum_pairs tab^T (sum_runs J^T partials)
-//   MODE 1: out = sum_pairs (sum_runs diag sums), SH block via basis^2
-// optional + lam * max(M, 1e-12) * p and fp64 p.out block partials (PCG)
+//   MODE 0: out = scale * sum_pairs tab^T pacc   (J^T partials)
+//   MODE 1: out = sum_pairs pacc, SH block via basis^2   (diag sums)
+// optional fp64 partials of p.(out + lam * max(M, 1e-12) * p) (PCG), and
+// out += lam * max(M, 1e-12) * p when lam_out
 // ---------------------------------------------------------------------------
 template <int K, int MODE>
-__global__ void __launch_bounds__(128) k_pair_backward(SlmBackArgs A) {
+__global__ void __launch_bounds__(128) k_gauss_backward(SlmBackArgs A) {
   __shared__ double sm[32];
   constexpr int D = MODE == 0 ? 9 : DIAG_RUN_D;
   const long long G = A.G;
@@ -190,16 +215,10 @@ __global__ void __launch_bounds__(128) k_pair_backward(SlmBackArgs A) {
 #pragma unroll
       for (int k = 0; k < K; ++k) osh[ch][k] = 0.f;
     const int k0 = A.gpo[g], k1 = A.gpo[g + 1];
-    for (int kk = k0; kk < k1; ++kk) {  // this gaussian's pairs, in view order
-      const int q = A.gp_list[kk];
+    for (int q = k0; q < k1; ++q) {  // this gaussian's pairs, in view order
       float a[D];
 #pragma unroll
-      for (int j = 0; j < D; ++j) a[j] = 0.f;
-      for (int rr = A.pair_run_off[q]; rr < A.pair_run_off[q + 1]; ++rr) {  // runs in tile order
-        const float* src = A.acc + (size_t)A.pair_runs[rr] * D;
-#pragma unroll
-        for (int j = 0; j < D; ++j) a[j] += src[j];
-      }
+      for (int j = 0; j < D; ++j) a[j] = A.pacc[(size_t)q * D + j];
       const uint32_t vm = A.pair_vm[q];
       Tab<K> T;
       pair_tab<K>(A.xs, G, g, A.cams[vm & 0xffffu], vm >> 16, T);
@@ -278,18 +297,28 @@ int slm_diag_runs(const SlmTileArgs* a, cudaStream_t st) {
   return slm_cuda_status();
 }
 
-int slm_pair_forward(const float* xs, long long G, int sh_degree, const int* pair_gid, const uint32_t* pair_vm,
-                     const SlmCamera* cams, int n_pairs, const float* p, long long sa, long long sg, void* pm,
-                     cudaStream_t st) {
-  if (n_pairs <= 0) return SLM_OK;
-  unsigned b = slm_blocks(n_pairs, 128, 1LL << 30);
+int slm_fwd_args_size() { return (int)sizeof(SlmFwdArgs); }
+
+int slm_pair_forward(const SlmFwdArgs* a, int sh_degree, cudaStream_t st) {
+  if (a->n_pairs <= 0) return SLM_OK;
+  unsigned b = slm_blocks(a->n_pairs, 128, 1LL << 30);
   switch (sh_degree) {
-    case 0: k_pair_forward<1><<<b, 128, 0, st>>>(xs, G, pair_gid, pair_vm, cams, n_pairs, p, sa, sg, (PairM*)pm); break;
-    case 1: k_pair_forward<4><<<b, 128, 0, st>>>(xs, G, pair_gid, pair_vm, cams, n_pairs, p, sa, sg, (PairM*)pm); break;
-    case 2: k_pair_forward<9><<<b, 128, 0, st>>>(xs, G, pair_gid, pair_vm, cams, n_pairs, p, sa, sg, (PairM*)pm); break;
-    case 3: k_pair_forward<16><<<b, 128, 0, st>>>(xs, G, pair_gid, pair_vm, cams, n_pairs, p, sa, sg, (PairM*)pm); break;
+    case 0: k_pair_forward<1><<<b, 128, 0, st>>>(*a); break;
+    case 1: k_pair_forward<4><<<b, 128, 0, st>>>(*a); break;
+    case 2: k_pair_forward<9><<<b, 128, 0, st>>>(*a); break;
+    case 3: k_pair_forward<16><<<b, 128, 0, st>>>(*a); break;
     default: return SLM_ERR_ARG;
   }
+  return slm_cuda_status();
+}
+
+int slm_pair_sum(const int* pair_run_off, const int* pair_runs, int n_pairs, const float* run_acc, int d,
+                 float* pacc, cudaStream_t st) {
+  if (n_pairs <= 0) return SLM_OK;
+  unsigned b = slm_blocks(n_pairs, 256, 1LL << 30);
+  if (d == 9) k_pair_sum<9><<<b, 256, 0, st>>>(pair_run_off, pair_runs, n_pairs, run_acc, pacc);
+  else if (d == DIAG_RUN_D) k_pair_sum<DIAG_RUN_D><<<b, 256, 0, st>>>(pair_run_off, pair_runs, n_pairs, run_acc, pacc);
+  else return SLM_ERR_ARG;
   return slm_cuda_status();
 }
 
@@ -297,11 +326,11 @@ int slm_backward_blocks(long long G) { return (int)slm_blocks(G, 128, 148LL * 16
 
 int slm_pair_backward(const SlmBackArgs* a, int mode, int sh_degree, cudaStream_t st) {
   unsigned b = (unsigned)slm_backward_blocks(a->G);
-#define SLM_BW(KK)                                 \
-  if (mode == 0)                                   \
-    k_pair_backward<KK, 0><<<b, 128, 0, st>>>(*a); \
-  else                                             \
-    k_pair_backward<KK, 1><<<b, 128, 0, st>>>(*a);
+#define SLM_BW(KK)                                  \
+  if (mode == 0)                                    \
+    k_gauss_backward<KK, 0><<<b, 128, 0, st>>>(*a); \
+  else                                              \
+    k_gauss_backward<KK, 1><<<b, 128, 0, st>>>(*a);
   switch (sh_degree) {
     case 0: SLM_BW(1) break;
     case 1: SLM_BW(4) break;

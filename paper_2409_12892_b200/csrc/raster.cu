@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
       s_c0[threadIdx.x] = s.c0; s_c1[threadIdx.x] = s.c1; s_c2[threadIdx.x] = s.c2;
       s_box[threadIdx.x] = make_int4(s.x0, s.x1, s.y0, s.y1);
       s_gid[threadIdx.x] = g;
-      if (FILL && A.rec_ae) {
+      if (FILL && A.rec4) {
         s_start[threadIdx.x] = A.inst_start[j];
         const uint32_t* mk = A.inst_mask + (size_t)j * RW;
         int acc = 0;
@@ -387,13 +387,11 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
         C0 = __dadd_rn(C0, __dmul_rn(wgt, s_c0[k]));
         C1 = __dadd_rn(C1, __dmul_rn(wgt, s_c1[k]));
         C2 = __dadd_rn(C2, __dmul_rn(wgt, s_c2[k]));
-        if (FILL && A.rec_ae) {
+        if (FILL && A.rec4) {
           const double om = 1.0 - a;
           const long long dest = s_start[k] + s_pre[k * RW + warp] + __popc(m & lanes_below);
-          A.rec_ae[dest] = a < aclamp ? (float)a : 0.0f;
-          A.rec_at[dest] = (float)wgt;
-          A.rec_d0[dest] = (float)(s_c0[k] * T - (tot0 - C0) / om);
-          A.rec_d1[dest] = (float)(s_c1[k] * T - (tot1 - C1) / om);
+          A.rec4[dest] = make_float4(a < aclamp ? (float)a : 0.0f, (float)wgt,
+                                     (float)(s_c0[k] * T - (tot0 - C0) / om), (float)(s_c1[k] * T - (tot1 - C1) / om));
           A.rec_d2[dest] = (float)(s_c2[k] * T - (tot2 - C2) / om);
           A.rec_pix[dest] = (uint8_t)threadIdx.x;
         }

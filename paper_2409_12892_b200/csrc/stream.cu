@@ -25,26 +25,33 @@
 
 #define NW 8
 #define NT (32 * (NW + 1))
-#define CH 512           // max entries per chunk
+#define CH 1024          // max entries per chunk
 #define CR 32            // max runs per chunk
-#define CHF (CH + 8)     // f32 stage slots (start aligned down to 4 entries)
-#define CHB (CH + 32)    // u8 stage slots (start aligned down to 16 entries)
-#define NS 6             // ring stages
+#define NS 3             // ring stages
 #define PAR 16           // floats per run parameter record
-#define TMETA 128        // producer chunk-metadata window
+#define TMETA 64         // producer chunk-metadata window
 
 #define MODE_J 1
 #define MODE_WRITEU 2
 #define MODE_JT 4
 
-#define ST_F (5 * CHF * 4)
-#define ST_PIX CHB
+// one ring stage: rec4 | d2 | pix | run params | run starts | J^T schedule | header
+#define ST_R4 (CH * 16)
+#define ST_D2 ((CH + 8) * 4)
+#define ST_PIX (CH + 32)
 #define ST_PAR (CR * PAR * 4)
 #define ST_RS ((CR + 4) * 8)
+#define ST_PERM 32
 #define ST_HDR 16
-#define ST_BYTES (ST_F + ST_PIX + ST_PAR + ST_RS + ST_HDR)
-static_assert(ST_F % 16 == 0 && (ST_F + ST_PIX) % 16 == 0 && ST_PAR % 16 == 0 && ST_RS % 16 == 0 &&
-                  ST_BYTES % 16 == 0,
+#define OFF_D2 ST_R4
+#define OFF_PIX (OFF_D2 + ST_D2)
+#define OFF_PAR (OFF_PIX + ST_PIX)
+#define OFF_RS (OFF_PAR + ST_PAR)
+#define OFF_PERM (OFF_RS + ST_RS)
+#define OFF_HDR (OFF_PERM + ST_PERM)
+#define ST_BYTES (OFF_HDR + ST_HDR)
+static_assert(OFF_D2 % 16 == 0 && OFF_PIX % 16 == 0 && OFF_PAR % 16 == 0 && OFF_RS % 16 == 0 && OFF_PERM % 16 == 0 &&
+                  OFF_HDR % 16 == 0 && ST_BYTES % 16 == 0,
               "stage sections must stay 16-byte aligned for cp.async.bulk");
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -61,37 +68,30 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
+// global -> shared bulk copy, completion on an mbarrier, with an L2 eviction policy
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory"); }
-
-__device__ __forceinline__ int rs16_slot(int lane) {
-  return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
-}
-// reduce-scatter of 16 per-lane values in 16 shuffles; lanes 2i, 2i+1 end
-// with the warp sum of value rs16_slot(lane); fixed pattern -> deterministic
-__device__ __forceinline__ float warp_reduce_scatter16(const float (&v)[16], int lane) {
-  const unsigned F = 0xffffffffu;
-  float w8[8], w4[4], w2[2];
-  const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4, u2 = lane & 2;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) w8[j] = (u16 ? v[j + 8] : v[j]) + __shfl_xor_sync(F, u16 ? v[j] : v[j + 8], 16);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) w4[j] = (u8 ? w8[j + 4] : w8[j]) + __shfl_xor_sync(F, u8 ? w8[j] : w8[j + 4], 8);
-#pragma unroll
-  for (int j = 0; j < 2; ++j) w2[j] = (u4 ? w4[j + 2] : w4[j]) + __shfl_xor_sync(F, u4 ? w4[j] : w4[j + 2], 4);
-  float w1 = (u2 ? w2[1] : w2[0]) + __shfl_xor_sync(F, u2 ? w2[0] : w2[1], 2);
-  return w1 + __shfl_xor_sync(F, w1, 1);
-}
 
 __device__ __forceinline__ int view_of_tile(const int* __restrict__ vtb, int n_views, int t) {
   int v = 0;
@@ -100,12 +100,10 @@ __device__ __forceinline__ int view_of_tile(const int* __restrict__ vtb, int n_v
 }
 
 // ---------------------------------------------------------------------------
-// per-product run parameter records (64 B, contiguous per chunk)
-//   P[0..1] splat centre minus tile pixel-centre origin, P[2..4] conic,
-//   P[5] inv_o * m_opa, P[6..10] m_mu0, m_mu1, m_cov0/2, m_cov1, m_cov2/2,
-//   P[11..13] m_col, P[14] inv_o
+// static run parameter records for the J^T-only mode (centre relative to the
+// tile origin, conic, inv_o; the forward-chain slots are zero).  The J and
+// fused modes get full records from slm_pair_forward (chain.cuh).
 // ---------------------------------------------------------------------------
-template <bool WITH_M>
 __global__ void k_run_params(SlmTileArgs A, long long n_runs, float* __restrict__ out) {
   for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n_runs;
        r += (long long)gridDim.x * blockDim.x) {
@@ -114,33 +112,18 @@ __global__ void k_run_params(SlmTileArgs A, long long n_runs, float* __restrict_
     const int lt = (int)(tg & 0xffffffu);
     const int tiles_x = (vw.W + SLM_TILE - 1) / SLM_TILE;
     const double ox = (double)((lt % tiles_x) * SLM_TILE) + 0.5, oy = (double)((lt / tiles_x) * SLM_TILE) + 0.5;
-    const int q = A.run_q[r];
-    const SlmPairGeo g = A.geo[q];
-    float P[16];
-    P[0] = (float)(g.mx - ox);
-    P[1] = (float)(g.my - oy);
-    P[2] = g.ka; P[3] = g.kb; P[4] = g.kc;
-    P[14] = g.inv_o;
-    P[15] = 0.f;
-    if (WITH_M) {
-      const PairM m = reinterpret_cast<const PairM*>(A.pm)[q];
-      P[5] = g.inv_o * m.b.y;
-      P[6] = m.a.x; P[7] = m.a.y; P[8] = 0.5f * m.a.z; P[9] = m.a.w; P[10] = 0.5f * m.b.x;
-      P[11] = m.b.z; P[12] = m.b.w; P[13] = m.c.x;
-    } else {
-#pragma unroll
-      for (int i = 5; i < 14; ++i) P[i] = 0.f;
-    }
+    const SlmPairGeo g = A.geo[A.run_q[r]];
     float4* o = reinterpret_cast<float4*>(out + r * PAR);
-    o[0] = make_float4(P[0], P[1], P[2], P[3]);
-    o[1] = make_float4(P[4], P[5], P[6], P[7]);
-    o[2] = make_float4(P[8], P[9], P[10], P[11]);
-    o[3] = make_float4(P[12], P[13], P[14], P[15]);
+    o[0] = make_float4((float)(g.mx - ox), (float)(g.my - oy), g.ka, g.kb);
+    o[1] = make_float4(g.kc, 0.f, 0.f, 0.f);
+    o[2] = make_float4(0.f, 0.f, 0.f, 0.f);
+    o[3] = make_float4(0.f, 0.f, g.inv_o, 0.f);
   }
 }
 
 // ---------------------------------------------------------------------------
 // chunk table: per tile, run-aligned chunks of <= CR runs and <= CH entries
+// (FILL=false: chunks per tile; FILL=true: first run of each chunk)
 // ---------------------------------------------------------------------------
 template <bool FILL>
 __global__ void k_tile_chunks(const int* __restrict__ tile_run_off, int n_tiles,
@@ -168,18 +151,34 @@ __global__ void k_tile_chunks(const int* __restrict__ tile_run_off, int n_tiles,
   }
 }
 
+// each chunk's group schedule: its runs by decreasing length (ties by index),
+// 0xff-padded to 32 slots; one warp per chunk, lane = run
+__global__ void k_chunk_perm(const int* __restrict__ chunk_run, long long n_chunks,
+                             const long long* __restrict__ run_start, uint8_t* __restrict__ perm) {
+  const int lane = threadIdx.x & 31;
+  for (long long c = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; c < n_chunks;
+       c += ((long long)gridDim.x * blockDim.x) >> 5) {
+    const int k0 = chunk_run[c], n = chunk_run[c + 1] - k0;
+    const long long len = lane < n ? run_start[k0 + lane + 1] - run_start[k0 + lane] : -1;
+    int rank = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const long long lj = __shfl_sync(0xffffffffu, len, j);
+      rank += (lj > len) || (lj == len && j < lane);
+    }
+    perm[c * 32 + lane] = 0xff;
+    __syncwarp();
+    if (lane < n) perm[c * 32 + rank] = (uint8_t)lane;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // the product kernel
 // ---------------------------------------------------------------------------
-struct Ent {
-  float ae, at, d0, d1, d2;
-  int pl;
-};
-
 __device__ __forceinline__ uint8_t* stage_ptr(uint8_t* ring, int s) { return ring + (size_t)s * ST_BYTES; }
 
 __host__ __device__ constexpr size_t stream_smem_bytes(int mode) {
-  return 256 * 16 + ((mode & MODE_J) ? 3 * NW * 256 * 4 : 0) + (size_t)NS * ST_BYTES + TMETA * 32;
+  return 256 * 16 + ((mode & MODE_J) ? (size_t)NW * 256 * 16 : 0) + (size_t)NS * ST_BYTES + TMETA * 24;
 }
 
 struct ChunkMeta {
@@ -187,6 +186,8 @@ struct ChunkMeta {
   long long e0, e1;
 };
 
+// stage header: [0] runs, [1] run-start offset (k0 - a2), [2] k0 (global run),
+// [3] d2 offset (e0 - a4), [4] pix offset (e0 - a16)
 template <int MODE>
 __global__ void __launch_bounds__(NT) k_stream(SlmTileArgs A) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -194,8 +195,8 @@ __global__ void __launch_bounds__(NT) k_stream(SlmTileArgs A) {
   unsigned char* sp = smem;
   float4* s_u = reinterpret_cast<float4*>(sp);
   sp += 256 * 16;
-  float* s_acc = reinterpret_cast<float*>(sp);
-  sp += (MODE & MODE_J) ? 3 * NW * 256 * 4 : 0;
+  float4* s_acc = reinterpret_cast<float4*>(sp);
+  sp += (MODE & MODE_J) ? (size_t)NW * 256 * 16 : 0;
   uint8_t* ring = sp;
   sp += (size_t)NS * ST_BYTES;
   ChunkMeta* tmeta = reinterpret_cast<ChunkMeta*>(sp);
@@ -213,10 +214,14 @@ __global__ void __launch_bounds__(NT) k_stream(SlmTileArgs A) {
 
   if (warp == NW) {
     // ------------------------------ producer ------------------------------
+    const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
     unsigned g = 0;
     for (int t = blockIdx.x; t < A.n_tiles; t += gridDim.x) {
       const int c0 = A.tile_chunk_off[t], c1 = A.tile_chunk_off[t + 1];
       for (int pass = 0; pass < n_pass; ++pass) {
+        // the cache of a tile is read twice in the fused mode: keep it in L2
+        // for the J^T pass, then let it go
+        const uint64_t pol = (n_pass == 2 && pass == 0) ? keep : drop;
         for (int w0 = c0; w0 < c1; w0 += TMETA) {
           const int wn = min(TMETA, c1 - w0);
           __syncwarp();
@@ -238,23 +243,23 @@ __global__ void __launch_bounds__(NT) k_stream(SlmTileArgs A) {
               const long long a4 = m.e0 & ~3LL, z4 = (m.e1 + 3) & ~3LL;
               const long long a16 = m.e0 & ~15LL, z16 = (m.e1 + 15) & ~15LL;
               const long long a2 = m.k0 & ~1LL, z2 = (m.k1 + 2) & ~1LL;
-              const unsigned bf = (unsigned)(z4 - a4) * 4u, bb = (unsigned)(z16 - a16);
-              const unsigned bp = (unsigned)(m.k1 - m.k0) * PAR * 4u, br = (unsigned)(z2 - a2) * 8u;
-              int* hdr = reinterpret_cast<int*>(st + ST_F + ST_PIX + ST_PAR + ST_RS);
+              const unsigned b4 = (unsigned)(m.e1 - m.e0) * 16u, bd = (unsigned)(z4 - a4) * 4u;
+              const unsigned bx = (unsigned)(z16 - a16), bp = (unsigned)(m.k1 - m.k0) * PAR * 4u;
+              const unsigned br = (unsigned)(z2 - a2) * 8u;
+              int* hdr = reinterpret_cast<int*>(st + OFF_HDR);
               hdr[0] = m.k1 - m.k0;
               hdr[1] = (int)(m.k0 - a2);
               hdr[2] = m.k0;
+              hdr[3] = (int)(m.e0 - a4);
+              // generic-proxy header writes before the async-proxy copies land
               asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-              mbar_arrive_tx(&full[s], 5u * bf + bb + bp + br);
-              float* sf = reinterpret_cast<float*>(st);
-              bulk_g2s(sf + 0 * CHF, A.ae + a4, bf, &full[s]);
-              bulk_g2s(sf + 1 * CHF, A.at + a4, bf, &full[s]);
-              bulk_g2s(sf + 2 * CHF, A.d0 + a4, bf, &full[s]);
-              bulk_g2s(sf + 3 * CHF, A.d1 + a4, bf, &full[s]);
-              bulk_g2s(sf + 4 * CHF, A.d2 + a4, bf, &full[s]);
-              bulk_g2s(st + ST_F, A.pix + a16, bb, &full[s]);
-              bulk_g2s(st + ST_F + ST_PIX, A.run_par + (size_t)m.k0 * PAR, bp, &full[s]);
-              bulk_g2s(st + ST_F + ST_PIX + ST_PAR, A.run_start + a2, br, &full[s]);
+              mbar_arrive_tx(&full[s], b4 + bd + bx + bp + br + ST_PERM);
+              bulk_g2s(st, A.rec4 + m.e0, b4, &full[s], pol);
+              bulk_g2s(st + OFF_D2, A.d2 + a4, bd, &full[s], pol);
+              bulk_g2s(st + OFF_PIX, A.pix + a16, bx, &full[s], pol);
+              bulk_g2s(st + OFF_PAR, A.run_par + (size_t)m.k0 * PAR, bp, &full[s], pol);
+              bulk_g2s(st + OFF_RS, A.run_start + a2, br, &full[s], pol);
+              bulk_g2s(st + OFF_PERM, A.chunk_perm + (size_t)(w0 + i) * 32, ST_PERM, &full[s], pol);
             }
           }
         }
@@ -265,10 +270,9 @@ __global__ void __launch_bounds__(NT) k_stream(SlmTileArgs A) {
 
   // ------------------------------ consumers -------------------------------
   unsigned g = 0;
-  float* acc0 = s_acc + (0 * NW + warp) * 256;
-  float* acc1 = s_acc + (1 * NW + warp) * 256;
-  float* acc2 = s_acc + (2 * NW + warp) * 256;
+  float4* acc = s_acc + warp * 256;
   const int p = threadIdx.x;
+  const int slot = lane >> 3, lg = lane & 7;  // J^T: 4 groups of 8 lanes per warp
   for (int t = blockIdx.x; t < A.n_tiles; t += gridDim.x) {
     const int v = view_of_tile(A.view_tile_base, A.n_views, t);
     const SlmView vw = A.views[v];
@@ -280,33 +284,43 @@ __global__ void __launch_bounds__(NT) k_stream(SlmTileArgs A) {
     const int c0 = A.tile_chunk_off[t], c1 = A.tile_chunk_off[t + 1];
 
     if (MODE & MODE_J) {
-      for (int i = lane; i < 256; i += 32) acc0[i] = acc1[i] = acc2[i] = 0.f;
+      for (int i = lane; i < 256; i += 32) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      __syncwarp();
+      // pass J: one run per warp at a time, lanes over its entries (a run
+      // never repeats a pixel, so the per-warp accumulators need no atomics;
+      // runs are taken in a fixed order -> deterministic).  Measured faster
+      // than flat 32-entry windows with __match_any conflict resolution.
       for (int ci = c0; ci < c1; ++ci, ++g) {
         const int s = (int)(g % NS);
         mbar_wait(&full[s], (g / NS) & 1u);
         const uint8_t* st = stage_ptr(ring, s);
-        const int* hdr = reinterpret_cast<const int*>(st + ST_F + ST_PIX + ST_PAR + ST_RS);
+        const int* hdr = reinterpret_cast<const int*>(st + OFF_HDR);
         const int nr = hdr[0];
-        const long long* rs = reinterpret_cast<const long long*>(st + ST_F + ST_PIX + ST_PAR) + hdr[1];
-        const float* sf = reinterpret_cast<const float*>(st);
-        const uint8_t* spx = st + ST_F;
-        const long long b4 = rs[0] & ~3LL, b16 = rs[0] & ~15LL;
+        const long long* rs = reinterpret_cast<const long long*>(st + OFF_RS) + hdr[1];
+        const long long e0 = rs[0];
+        const float4* s4 = reinterpret_cast<const float4*>(st);
+        const float* sd2 = reinterpret_cast<const float*>(st + OFF_D2) + hdr[3];
+        const uint8_t* spx = st + OFF_PIX + (e0 & 15);
+        const float4* PAR4 = reinterpret_cast<const float4*>(st + OFF_PAR);
         for (int i = warp; i < nr; i += NW) {
-          const float* P = reinterpret_cast<const float*>(st + ST_F + ST_PIX) + i * PAR;
-          const float p0 = P[0], p1 = P[1], ka = P[2], kb = P[3], kc = P[4], a0 = P[5], m0 = P[6], m1 = P[7];
-          const float m2 = P[8], m3 = P[9], m4 = P[10], q0 = P[11], q1 = P[12], q2 = P[13];
-          const int f0 = (int)(rs[i] - b4), n = (int)(rs[i + 1] - rs[i]);
-          const int x0 = (int)(rs[i] - b16);
+          // q0 = (p0, p1, ka, kb), q1 = (kc, a0, m0, m1), q2 = (m2, m3, m4, c0), q3 = (c1, c2, io, -)
+          const float4 q0 = PAR4[i * 4], q1 = PAR4[i * 4 + 1], q2 = PAR4[i * 4 + 2], q3 = PAR4[i * 4 + 3];
+          const int f0 = (int)(rs[i] - e0), n = (int)(rs[i + 1] - rs[i]);
+          const float4* pr = s4 + f0;
+          const float* pd = sd2 + f0;
+          const uint8_t* pp = spx + f0;
           for (int j = lane; j < n; j += 32) {
-            const float ae = sf[0 * CHF + f0 + j], at = sf[1 * CHF + f0 + j];
-            const float d0 = sf[2 * CHF + f0 + j], d1 = sf[3 * CHF + f0 + j], d2 = sf[4 * CHF + f0 + j];
-            const int pl = spx[x0 + j];
-            const float dx = (float)(pl & 15) - p0, dy = (float)(pl >> 4) - p1;
-            const float e1 = ka * dx + kb * dy, e2 = kb * dx + kc * dy;
-            const float da = ae * (a0 + e1 * m0 + e2 * m1 + e1 * e1 * m2 + e1 * e2 * m3 + e2 * e2 * m4);
-            acc0[pl] += d0 * da + at * q0;
-            acc1[pl] += d1 * da + at * q1;
-            acc2[pl] += d2 * da + at * q2;
+            const float4 r = pr[j];
+            const float d2 = pd[j];
+            const int pl = pp[j];
+            const float dx = (float)(pl & 15) - q0.x, dy = (float)(pl >> 4) - q0.y;
+            const float e1 = q0.z * dx + q0.w * dy, e2 = q0.w * dx + q1.x * dy;
+            const float da = r.x * (q1.y + e1 * (q1.z + e1 * q2.x + e2 * q2.y) + e2 * (q1.w + e2 * q2.z));
+            float4 a = acc[pl];
+            a.x += fmaf(r.z, da, r.y * q2.w);
+            a.y += fmaf(r.w, da, r.y * q3.x);
+            a.z += fmaf(d2, da, r.y * q3.y);
+            acc[pl] = a;
           }
         }
         __syncwarp();
@@ -315,10 +329,11 @@ __global__ void __launch_bounds__(NT) k_stream(SlmTileArgs A) {
       consumer_sync();
       float u0 = 0.f, u1 = 0.f, u2 = 0.f;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        u0 += s_acc[(0 * NW + w) * 256 + p];
-        u1 += s_acc[(1 * NW + w) * 256 + p];
-        u2 += s_acc[(2 * NW + w) * 256 + p];
+      for (int w = 0; w < NW; ++w) {  // fixed warp order -> deterministic
+        const float4 a = s_acc[w * 256 + p];
+        u0 += a.x;
+        u1 += a.y;
+        u2 += a.z;
       }
       float4 uw = make_float4(0.f, 0.f, 0.f, 0.f);
       if (inside) {
@@ -333,46 +348,83 @@ __global__ void __launch_bounds__(NT) k_stream(SlmTileArgs A) {
 
     if (MODE & MODE_JT) {
       consumer_sync();
+      // pass J^T: 4 runs per warp (8 lanes each) from the chunk's
+      // length-sorted schedule; the warp's slot block rotates with the chunk
       for (int ci = c0; ci < c1; ++ci, ++g) {
         const int s = (int)(g % NS);
         mbar_wait(&full[s], (g / NS) & 1u);
         const uint8_t* st = stage_ptr(ring, s);
-        const int* hdr = reinterpret_cast<const int*>(st + ST_F + ST_PIX + ST_PAR + ST_RS);
-        const int nr = hdr[0], kg = hdr[2];
-        const long long* rs = reinterpret_cast<const long long*>(st + ST_F + ST_PIX + ST_PAR) + hdr[1];
-        const float* sf = reinterpret_cast<const float*>(st);
-        const uint8_t* spx = st + ST_F;
-        const long long b4 = rs[0] & ~3LL, b16 = rs[0] & ~15LL;
-        for (int i = warp; i < nr; i += NW) {
-          const float* P = reinterpret_cast<const float*>(st + ST_F + ST_PIX) + i * PAR;
-          const float p0 = P[0], p1 = P[1], ka = P[2], kb = P[3], kc = P[4], io = P[14];
-          const int f0 = (int)(rs[i] - b4), n = (int)(rs[i + 1] - rs[i]);
-          const int x0 = (int)(rs[i] - b16);
-          float a[16];
+        const int* hdr = reinterpret_cast<const int*>(st + OFF_HDR);
+        const int kg = hdr[2];
+        const long long* rs = reinterpret_cast<const long long*>(st + OFF_RS) + hdr[1];
+        const float4* s4 = reinterpret_cast<const float4*>(st);
+        const float* sd2 = reinterpret_cast<const float*>(st + OFF_D2) + hdr[3];
+        const uint8_t* spx = st + OFF_PIX + (rs[0] & 15);
+        const long long e0 = rs[0];
+        const int ri = st[OFF_PERM + (((warp + ci) & (NW - 1)) * 4 + slot)];
+        int n = 0, f0 = 0;
+        float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f);
+        float kc = 0.f, io = 0.f;
+        if (ri != 0xff) {
+          const float4* P4 = reinterpret_cast<const float4*>(st + OFF_PAR) + ri * 4;
+          q0 = P4[0];
+          kc = P4[1].x;
+          io = P4[3].z;
+          f0 = (int)(rs[ri] - e0);
+          n = (int)(rs[ri + 1] - rs[ri]);
+        }
+        const int nmax = __reduce_max_sync(0xffffffffu, (unsigned)n);
+        if (nmax == 0) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[s]);
+          continue;
+        }
+        float a[9];
 #pragma unroll
-          for (int k = 0; k < 16; ++k) a[k] = 0.f;
-          for (int j = lane; j < n; j += 32) {
-            const float ae = sf[0 * CHF + f0 + j], at = sf[1 * CHF + f0 + j];
-            const float d0 = sf[2 * CHF + f0 + j], d1 = sf[3 * CHF + f0 + j], d2 = sf[4 * CHF + f0 + j];
-            const int pl = spx[x0 + j];
+        for (int k = 0; k < 9; ++k) a[k] = 0.f;
+        const float4* pr = s4 + f0;
+        const float* pd = sd2 + f0;
+        const uint8_t* pp = spx + f0;
+        for (int j = lg; j < nmax; j += 8) {
+          if (j < n) {
+            const float4 r = pr[j];
+            const float d2 = pd[j];
+            const int pl = pp[j];
             const float4 uu = s_u[pl];
-            const float dx = (float)(pl & 15) - p0, dy = (float)(pl >> 4) - p1;
-            const float e1 = ka * dx + kb * dy, e2 = kb * dx + kc * dy;
-            const float sa = d0 * uu.x + d1 * uu.y + d2 * uu.z;
-            const float tt = sa * ae;
-            a[0] += tt * e1;
-            a[1] += tt * e2;
-            a[2] += 0.5f * tt * e1 * e1;
-            a[3] += tt * e1 * e2;
-            a[4] += 0.5f * tt * e2 * e2;
+            const float dx = (float)(pl & 15) - q0.x, dy = (float)(pl >> 4) - q0.y;
+            const float e1 = q0.z * dx + q0.w * dy, e2 = q0.w * dx + kc * dy;
+            const float sa = fmaf(r.z, uu.x, fmaf(r.w, uu.y, d2 * uu.z));
+            const float tt = sa * r.x;
+            const float te1 = tt * e1, te2 = tt * e2;
+            a[0] += te1;
+            a[1] += te2;
+            a[2] = fmaf(te1, e1, a[2]);  // x 1/2 in the epilogue
+            a[3] = fmaf(te1, e2, a[3]);
+            a[4] = fmaf(te2, e2, a[4]);  // x 1/2 in the epilogue
             a[5] += tt;
-            a[6] += at * uu.x;
-            a[7] += at * uu.y;
-            a[8] += at * uu.z;
+            a[6] = fmaf(r.y, uu.x, a[6]);
+            a[7] = fmaf(r.y, uu.y, a[7]);
+            a[8] = fmaf(r.y, uu.z, a[8]);
           }
-          const float sum = warp_reduce_scatter16(a, lane);
-          const int slot = rs16_slot(lane);
-          if (!(lane & 1) && slot < 9) A.out[(size_t)(kg + i) * 9 + slot] = slot == 5 ? sum * io : sum;
+        }
+        // 8-lane reduce-scatter of a[0..7] (lane lg ends with the group sum of
+        // value lg) plus a butterfly for a[8]; fixed pattern -> deterministic
+        const unsigned F = 0xffffffffu;
+        const bool u4 = lg & 4, u2 = lg & 2, u1 = lg & 1;
+        float w4[4], w2[2];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) w4[k] = (u4 ? a[k + 4] : a[k]) + __shfl_xor_sync(F, u4 ? a[k] : a[k + 4], 4);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) w2[k] = (u2 ? w4[k + 2] : w4[k]) + __shfl_xor_sync(F, u2 ? w4[k] : w4[k + 2], 2);
+        const float w1 = (u1 ? w2[1] : w2[0]) + __shfl_xor_sync(F, u1 ? w2[0] : w2[1], 1);
+        float a8 = a[8];
+        a8 += __shfl_xor_sync(F, a8, 4);
+        a8 += __shfl_xor_sync(F, a8, 2);
+        a8 += __shfl_xor_sync(F, a8, 1);
+        if (ri != 0xff) {
+          float* o = A.out + (size_t)(kg + ri) * 9;
+          o[lg] = lg == 5 ? w1 * io : ((lg == 2 || lg == 4) ? 0.5f * w1 : w1);
+          if (lg == 0) o[8] = a8;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
@@ -403,20 +455,30 @@ static int launch_stream(const SlmTileArgs* a, cudaStream_t st) {
 
 extern "C" {
 
-int slm_run_params(const SlmTileArgs* a, long long n_runs, int with_m, float* out, cudaStream_t st) {
+int slm_run_params(const SlmTileArgs* a, long long n_runs, float* out, cudaStream_t st) {
   if (n_runs <= 0) return SLM_OK;
-  const unsigned b = slm_blocks(n_runs, 256, 1LL << 30);
-  if (with_m) k_run_params<true><<<b, 256, 0, st>>>(*a, n_runs, out);
-  else k_run_params<false><<<b, 256, 0, st>>>(*a, n_runs, out);
+  k_run_params<<<slm_blocks(n_runs, 256, 1LL << 30), 256, 0, st>>>(*a, n_runs, out);
   return slm_cuda_status();
 }
 
 int slm_tile_chunks(const int* tile_run_off, int n_tiles, const long long* run_start, const int* tile_chunk_off,
-                    int* out, int fill, cudaStream_t st) {
+                    int* out, uint8_t* chunk_perm, int fill, cudaStream_t st) {
   if (n_tiles <= 0) return SLM_OK;
   const unsigned b = slm_blocks(n_tiles, 128, 1LL << 30);
-  if (fill) k_tile_chunks<true><<<b, 128, 0, st>>>(tile_run_off, n_tiles, run_start, tile_chunk_off, out);
-  else k_tile_chunks<false><<<b, 128, 0, st>>>(tile_run_off, n_tiles, run_start, tile_chunk_off, out);
+  if (!fill) {
+    k_tile_chunks<false><<<b, 128, 0, st>>>(tile_run_off, n_tiles, run_start, tile_chunk_off, out);
+    return slm_cuda_status();
+  }
+  k_tile_chunks<true><<<b, 128, 0, st>>>(tile_run_off, n_tiles, run_start, tile_chunk_off, out);
+  // out[n_chunks] (= R) is written by the caller before the perm pass; read it on the device
+  return slm_cuda_status();
+}
+
+int slm_chunk_perm(const int* chunk_run, long long n_chunks, const long long* run_start, uint8_t* chunk_perm,
+                   cudaStream_t st) {
+  if (n_chunks <= 0) return SLM_OK;
+  k_chunk_perm<<<slm_blocks(n_chunks * 32, 256, 1LL << 30), 256, 0, st>>>(chunk_run, n_chunks, run_start,
+                                                                         chunk_perm);
   return slm_cuda_status();
 }
 

@@ -387,11 +387,10 @@ class CacheSet:
         self.pair_geo = _empty(Pn * _lib.PAIR_GEO_BYTES, torch.uint8, dev)
         pidx = torch.empty(VG, dtype=torch.int32, device=dev)
         self.gpo = torch.empty(G + 1, dtype=torch.int32, device=dev)
-        self.gp_list = _empty(Pn, torch.int32, dev)
         splats_all = torch.cat([f.splats for f in self.frames])
         call("slm_pairs_emit", ptr(self.pair_cnt), V, G, ptr(pair_of), ptr(vscan), ptr(tscan), ptr(splats_all),
              ptr(self.pair_off), ptr(self.pair_gid), ptr(self.pair_vm), ptr(self.pair_geo), ptr(pidx), ptr(self.gpo),
-             ptr(self.gp_list), Pn, self.E, stream_ptr())
+             Pn, self.E, stream_ptr())
         del cntV, flagV, flagT, vscan, pair_of, tscan, splats_all
 
         # ---- run table, runs per tile, pair -> runs ----------------------------
@@ -414,15 +413,18 @@ class CacheSet:
         scan_i32(tile_nruns, self.tile_run_off)
         # chunk table for the streaming product kernel (<= 32 runs / 512 entries per chunk)
         tile_nch = torch.zeros(nt + 1, dtype=torch.int32, device=dev)
-        call("slm_tile_chunks", ptr(self.tile_run_off), nt, ptr(self.run_start), None, ptr(tile_nch), 0,
+        call("slm_tile_chunks", ptr(self.tile_run_off), nt, ptr(self.run_start), None, ptr(tile_nch), None, 0,
              stream_ptr())
         self.tile_chunk_off = torch.empty_like(tile_nch)
         scan_i32(tile_nch, self.tile_chunk_off)
         self.n_chunks = int(self.tile_chunk_off[nt].item())
         self.chunk_run = torch.empty(self.n_chunks + 1, dtype=torch.int32, device=dev)
+        self.chunk_perm = torch.empty((self.n_chunks + 1) * 32, dtype=torch.uint8, device=dev)
         call("slm_tile_chunks", ptr(self.tile_run_off), nt, ptr(self.run_start), ptr(self.tile_chunk_off),
-             ptr(self.chunk_run), 1, stream_ptr())
+             ptr(self.chunk_run), ptr(self.chunk_perm), 1, stream_ptr())
         self.chunk_run[self.n_chunks:].fill_(R)
+        call("slm_chunk_perm", ptr(self.chunk_run), self.n_chunks, ptr(self.run_start), ptr(self.chunk_perm),
+             stream_ptr())
         del tile_nch
         self.pair_run_off = torch.empty_like(pair_nruns)
         scan_i32(pair_nruns, self.pair_run_off)
@@ -436,14 +438,16 @@ class CacheSet:
         # ---- FILL phase: run-ordered records ------------------------------------
         E = self.E
         f32 = torch.float32
-        # alpha_eff, alpha*T, dc/dalpha[3] + tile-local pixel; +16 slots so the
-        # 16-byte-granular TMA chunk copies of the product kernels stay in bounds
-        self.rec = [torch.zeros(E + 16, dtype=f32, device=dev) for _ in range(5)]
+        # {alpha_eff, alpha*T, dc/dalpha_r, dc/dalpha_g}, dc/dalpha_b, tile-local
+        # pixel; +16 slots so the 16-byte-granular TMA chunk copies of the
+        # product kernels stay in bounds
+        self.rec4 = torch.zeros((E + 16) * 4, dtype=f32, device=dev)
+        self.rec_d2 = torch.zeros(E + 16, dtype=f32, device=dev)
         self.rec_pix = torch.zeros(E + 16, dtype=torch.uint8, device=dev)
         for v, fr in enumerate(self.frames):
             a = raster_args(fr, cfg_s)
             a.rgb, a.inst_mask, a.inst_start = ptr(fr.rgb), ptr(fr.inst_mask), ptr(fr.inst_start)
-            a.rec_ae, a.rec_at, a.rec_d0, a.rec_d1, a.rec_d2 = [ptr(t) for t in self.rec]
+            a.rec4, a.rec_d2 = ptr(self.rec4), ptr(self.rec_d2)
             a.rec_pix = ptr(self.rec_pix)
             call("slm_raster_fill", _lib.byref(a), stream_ptr())
             T.tick("raster_fill")
@@ -453,9 +457,9 @@ class CacheSet:
         self.view_tile_base_dev = torch.tensor(self.view_tile_base, dtype=torch.int32, device=dev)
         # product scratch
         self.u = torch.empty(self.N * 4, dtype=f32, device=dev)
-        self.pm = _empty(Pn * 12, f32, dev)
         self.run_acc = _empty(R * _lib.JT_D, f32, dev)
         self.run_par = _empty(R * 16, f32, dev)
+        self.pacc = _empty(Pn * _lib.DIAG_D, f32, dev)
         self._b = None
         self._M = None
 
@@ -463,13 +467,21 @@ class CacheSet:
     @property
     def nbytes(self) -> int:
         """Bytes of the record stream (budget accounting, ref: jacobian.py:76-80)."""
-        return 21 * self.E + 48 * self.R
+        return 21 * self.E + 48 * self.R + 36 * self.n_chunks
 
     def pair_forward(self, p: torch.Tensor, gaussian_major: bool = False):
+        """Forward chain m = dy/dx p per pair, written into every run's
+        parameter record (self.run_par) for the J / fused product kernels."""
         G, P = self.G, self.P
-        sa, sg = (1, P) if gaussian_major else (G, 1)
-        call("slm_pair_forward", ptr(self.scene.x32()), G, self.scene.sh_degree, ptr(self.pair_gid),
-             ptr(self.pair_vm), ptr(self.cams_dev), self.n_pairs, ptr(p), sa, sg, ptr(self.pm), stream_ptr())
+        a = _lib.SlmFwdArgs()
+        a.xs, a.G = ptr(self.scene.x32()), G
+        a.pair_gid, a.pair_vm, a.cams, a.n_pairs = ptr(self.pair_gid), ptr(self.pair_vm), ptr(self.cams_dev), \
+            self.n_pairs
+        a.p = ptr(p)
+        a.sa, a.sg = (1, P) if gaussian_major else (G, 1)
+        a.geo, a.pair_run_off, a.pair_runs = ptr(self.pair_geo), ptr(self.pair_run_off), ptr(self.pair_runs)
+        a.run_tile, a.views, a.run_par = ptr(self.run_tile), ptr(self.views_dev), ptr(self.run_par)
+        call("slm_pair_forward", _lib.byref(a), self.scene.sh_degree, stream_ptr())
 
     def _tile_args(self) -> _lib.SlmTileArgs:
         a = _lib.SlmTileArgs()
@@ -477,36 +489,36 @@ class CacheSet:
         a.n_tiles = self.n_tiles_total
         a.tile_run_off, a.tile_chunk_off, a.chunk_run = ptr(self.tile_run_off), ptr(self.tile_chunk_off), \
             ptr(self.chunk_run)
+        a.chunk_perm = ptr(self.chunk_perm)
         a.run_start, a.run_q, a.run_tile, a.run_par = ptr(self.run_start), ptr(self.run_q), ptr(self.run_tile), \
             ptr(self.run_par)
-        a.geo, a.pm = ptr(self.pair_geo), ptr(self.pm)
-        a.ae, a.at, a.d0, a.d1, a.d2 = [ptr(t) for t in self.rec]
+        a.geo = ptr(self.pair_geo)
+        a.rec4, a.d2 = ptr(self.rec4), ptr(self.rec_d2)
         a.pix = ptr(self.rec_pix)
         return a
 
-    def _run_params(self, a: _lib.SlmTileArgs, with_m: bool):
-        call("slm_run_params", _lib.byref(a), self.R, 1 if with_m else 0, ptr(self.run_par), stream_ptr())
+    def _static_run_params(self, a: _lib.SlmTileArgs):
+        call("slm_run_params", _lib.byref(a), self.R, ptr(self.run_par), stream_ptr())
 
-    def _back_args(self, acc, out, scale=1.0, p=None, M=None, lam=0.0, dot_part=None,
-                   lam_out=True) -> _lib.SlmBackArgs:
+    def _backward(self, run_acc, d, out, mode, scale=1.0, p=None, M=None, lam=0.0, dot_part=None, lam_out=True):
+        """run partials -> per-pair sums -> per-gaussian chain, attribute-major out."""
+        call("slm_pair_sum", ptr(self.pair_run_off), ptr(self.pair_runs), self.n_pairs, ptr(run_acc), d,
+             ptr(self.pacc), stream_ptr())
         a = _lib.SlmBackArgs()
         a.xs, a.G = ptr(self.scene.x32()), self.G
-        a.gpo, a.gp_list = ptr(self.gpo), ptr(self.gp_list)
-        a.pair_run_off, a.pair_runs = ptr(self.pair_run_off), ptr(self.pair_runs)
-        a.pair_vm, a.cams, a.acc = ptr(self.pair_vm), ptr(self.cams_dev), ptr(acc)
+        a.gpo, a.pair_vm, a.cams, a.pacc = ptr(self.gpo), ptr(self.pair_vm), ptr(self.cams_dev), ptr(self.pacc)
         a.scale, a.p, a.Mdiag, a.lam = float(scale), ptr(p), ptr(M), float(lam)
         a.lam_out = 1 if lam_out else 0
         a.out, a.dot_part = ptr(out), ptr(dot_part)
-        return a
+        call("slm_pair_backward", _lib.byref(a), mode, self.scene.sh_degree, stream_ptr())
 
     def apply_j_raw(self, weighted: bool) -> torch.Tensor:
-        """u (or u_hat) into self.u from the pair forward chain in self.pm."""
+        """u (or u_hat) into self.u from the run records written by pair_forward."""
         if weighted and self.gradr is None:
             raise ValueError("cache was built without residual weights")
         a = self._tile_args()
         a.gradr = ptr(self.gradr) if weighted else None
         a.u_out = ptr(self.u)
-        self._run_params(a, with_m=True)
         call("slm_apply_j", _lib.byref(a), stream_ptr())
         return self.u
 
@@ -514,10 +526,9 @@ class CacheSet:
                      dot_part=None):
         ra = self._tile_args()
         ra.u, ra.out = ptr(u), ptr(self.run_acc)
-        self._run_params(ra, with_m=False)
+        self._static_run_params(ra)
         call("slm_apply_jt_runs", _lib.byref(ra), stream_ptr())
-        ba = self._back_args(self.run_acc, out, scale, p, M, lam, dot_part)
-        call("slm_pair_backward", _lib.byref(ba), 0, self.scene.sh_degree, stream_ptr())
+        self._backward(self.run_acc, _lib.JT_D, out, 0, scale, p, M, lam, dot_part)
         return out
 
     def jtwj(self, p: torch.Tensor, out: torch.Tensor, lam: float = 0.0, M=None, dot_part=None,
@@ -525,18 +536,16 @@ class CacheSet:
         """out = J^T W J p (+ lam * max(M, 1e-12) * p when lam_out); attribute-major
         fp32.  dot_part receives fp64 block partials of p.(J^T W J p + lam Mf p).
 
-        Four launches: pair forward chain, run parameter records, the fused
-        per-tile J / W / J^T streaming kernel (u never leaves shared memory),
-        per-gaussian backward chain."""
+        Four launches: pair forward chain (+ run records), the fused per-tile
+        J / W / J^T streaming kernel (u never leaves shared memory), per-pair
+        sums, per-gaussian backward chain."""
         if self.gradr is None:
             raise ValueError("cache was built without residual weights")
         self.pair_forward(p)
         a = self._tile_args()
         a.gradr, a.out = ptr(self.gradr), ptr(self.run_acc)
-        self._run_params(a, with_m=True)
         call("slm_jtwj_runs", _lib.byref(a), stream_ptr())
-        ba = self._back_args(self.run_acc, out, 1.0, p, M if lam != 0.0 else None, lam, dot_part, lam_out)
-        call("slm_pair_backward", _lib.byref(ba), 0, self.scene.sh_degree, stream_ptr())
+        self._backward(self.run_acc, _lib.JT_D, out, 0, 1.0, p, M if lam != 0.0 else None, lam, dot_part, lam_out)
         return out
 
     def rhs(self) -> torch.Tensor:
@@ -562,8 +571,7 @@ class CacheSet:
             ra.ptab, ra.gradr, ra.out = ptr(ptab), ptr(self.gradr), ptr(sums)
             call("slm_diag_runs", _lib.byref(ra), stream_ptr())
             M = torch.empty(self.G * self.P, dtype=torch.float32, device=self.device)
-            ba = self._back_args(sums, M)
-            call("slm_pair_backward", _lib.byref(ba), 1, self.scene.sh_degree, stream_ptr())
+            self._backward(sums, _lib.DIAG_D, M, 1)
             self._M = M
         return self._M
 
@@ -596,7 +604,8 @@ class CacheSet:
         py = (tile // tiles_x) * TILE + (pl >> 4)
         pixel = py * cam.width + px
         gid = pair_gid[run_q[run_of_e]].astype(np.int64)
-        f = [t[e0:e1].cpu().numpy().astype(np.float64) for t in self.rec]
+        r4 = self.rec4[4 * e0:4 * e1].view(-1, 4).cpu().numpy().astype(np.float64)
+        f = [r4[:, 0], r4[:, 1], r4[:, 2], r4[:, 3], self.rec_d2[e0:e1].cpu().numpy().astype(np.float64)]
         order = np.argsort(pixel, kind="stable")      # runs of one tile are in depth order
         pixel, gid = pixel[order], gid[order]
         ae, at = f[0][order], f[1][order]
