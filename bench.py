@@ -282,7 +282,7 @@ def cpu_sample(cfg):
 
     from paper_2409_12892_b200 import synthetic as S
     G = cfg["G"]
-    Gs = min(G, 8000)
+    Gs = min(G, 16000)
     scale = np.sqrt(Gs / G)
     W = max(16, int(round(cfg["W"] * scale)))
     H = max(16, int(round(cfg["H"] * scale)))

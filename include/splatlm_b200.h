@@ -141,6 +141,7 @@ typedef struct {
   const int* tile_chunk_off; /* [n_tiles+1] chunk table (slm_tile_chunks) */
   const int* chunk_run;      /* [n_chunks+1] first run of each chunk */
   const uint8_t* chunk_perm; /* [n_chunks*32] J^T schedule: chunk-local runs by decreasing length */
+  const int* run_slot;       /* [R] position of each run in pair_runs (J^T outputs go there) */
   const long long* run_start;/* [R+1] (+2 padding slots) */
   const int* run_q;          /* pair of each run */
   const uint32_t* run_tile;  /* view << 24 | tile */
@@ -181,7 +182,10 @@ typedef struct {
   const int* gpo;           /* [G+1] gaussian -> pairs (pairs are (gid, view)-numbered) */
   const uint32_t* pair_vm;  /* view | clamp bits << 16 */
   const SlmCamera* cams;
-  const float* pacc;        /* per-pair sums (9 or 14 per pair, slm_pair_sum) */
+  const float* pacc;        /* pair_run_off == NULL: per-pair sums (slm_pair_sum);
+                               else per-run partials in pair-run-slot order (the
+                               J^T kernels write run r to its slot in pair_runs) */
+  const int* pair_run_off;  /* [P+1] pair -> run slots, or NULL */
   float scale;
   const float* p;           /* optional: fp64 partials of p.(out + lam * max(M,1e-12) * p) */
   const float* Mdiag;

@@ -58,7 +58,7 @@ class SlmResidArgs(C.Structure):
 
 class SlmTileArgs(C.Structure):
     _fields_ = [("views", c_vp), ("view_tile_base", c_vp), ("n_views", c_i), ("n_tiles", c_i),
-                ("tile_run_off", c_vp), ("tile_chunk_off", c_vp), ("chunk_run", c_vp), ("chunk_perm", c_vp),
+                ("tile_run_off", c_vp), ("tile_chunk_off", c_vp), ("chunk_run", c_vp), ("chunk_perm", c_vp), ("run_slot", c_vp),
                 ("run_start", c_vp), ("run_q", c_vp), ("run_tile", c_vp), ("run_par", c_vp),
                 ("geo", c_vp), ("ptab", c_vp),
                 ("rec4", c_vp), ("d2", c_vp), ("pix", c_vp),
@@ -73,6 +73,7 @@ class SlmFwdArgs(C.Structure):
 
 class SlmBackArgs(C.Structure):
     _fields_ = [("xs", c_vp), ("G", c_ll), ("gpo", c_vp), ("pair_vm", c_vp), ("cams", c_vp), ("pacc", c_vp),
+                ("pair_run_off", c_vp),
                 ("scale", c_f),
                 ("p", c_vp), ("Mdiag", c_vp), ("lam", c_d), ("lam_out", c_i), ("out", c_vp), ("dot_part", c_vp)]
 

@@ -162,7 +162,7 @@ __device__ __forceinline__ void pair_tab(const float* __restrict__ xs, long long
 // so consecutive threads share the gaussian's parameters):
 //   P[0..1] splat centre minus the tile's pixel-centre origin, P[2..4] conic,
 //   P[5] inv_o * m_opa, P[6..10] m_mu0, m_mu1, m_cov0/2, m_cov1, m_cov2/2,
-//   P[11..13] m_col, P[14] inv_o, P[15] 0.
+//   P[11..13] m_col, P[14] inv_o, P[15] the run's slot in pair_runs (int bits).
 // p is read with strides so both layouts work: p[a * sa + g * sg].
 template <int K>
 __global__ void __launch_bounds__(128) k_pair_forward(SlmFwdArgs A) {
@@ -199,7 +199,6 @@ __global__ void __launch_bounds__(128) k_pair_forward(SlmFwdArgs A) {
     const int tiles_x = (vw.W + SLM_TILE - 1) / SLM_TILE;
     const float4 r1 = make_float4(ge.kc, ge.inv_o * mopa, mmu0, mmu1);
     const float4 r2 = make_float4(0.5f * mc[0], mc[1], 0.5f * mc[2], mcol[0]);
-    const float4 r3 = make_float4(mcol[1], mcol[2], ge.inv_o, 0.f);
     for (int rr = A.pair_run_off[q]; rr < A.pair_run_off[q + 1]; ++rr) {
       const int r = A.pair_runs[rr];
       const int lt = (int)(A.run_tile[r] & 0xffffffu);
@@ -208,7 +207,7 @@ __global__ void __launch_bounds__(128) k_pair_forward(SlmFwdArgs A) {
       o[0] = make_float4((float)(ge.mx - ox), (float)(ge.my - oy), ge.ka, ge.kb);
       o[1] = r1;
       o[2] = r2;
-      o[3] = r3;
+      o[3] = make_float4(mcol[1], mcol[2], ge.inv_o, __int_as_float(rr));
     }
   }
 }

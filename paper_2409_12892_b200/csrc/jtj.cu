@@ -141,22 +141,30 @@ __global__ void __launch_bounds__(256) k_diag_tile(SlmTileArgs A) {
         const float e2 = kb * dx + kc * dy;
         const float w0 = ae * e1, w1 = ae * e2, w2 = 0.5f * ae * e1 * e1, w3 = ae * e1 * e2;
         const float w4 = 0.5f * ae * e2 * e2;
+        // sum_ch grad_r_sq_ch * (dc_ch/dx_k)^2 with dc_ch/dx_k = d_ch * dalpha_k (+ at * dcol_ch,k
+        // for the 3 position params): for k >= 3 it is dalpha_k^2 * Aw, Aw = sum_ch gr_ch d_ch^2
+        // (exact, no cancellation); the position params keep the per-channel squares
+        const float Aw = grc[0] * dd[0] * dd[0] + grc[1] * dd[1] * dd[1] + grc[2] * dd[2] * dd[2];
 #pragma unroll
-        for (int kk = 0; kk < 11; ++kk) {
-          float da;
-          if (kk < 3)
-            da = w0 * D[kk * 5] + w1 * D[kk * 5 + 1] + w2 * D[kk * 5 + 2] + w3 * D[kk * 5 + 3] + w4 * D[kk * 5 + 4];
-          else if (kk < 10)
-            da = w2 * D[15 + (kk - 3) * 3] + w3 * D[16 + (kk - 3) * 3] + w4 * D[17 + (kk - 3) * 3];
-          else
-            da = ae * io * D[36];
-          float s = 0.f;
+        for (int kk = 0; kk < 3; ++kk) {
+          const float da = w0 * D[kk * 5] + w1 * D[kk * 5 + 1] + w2 * D[kk * 5 + 2] + w3 * D[kk * 5 + 3] +
+                           w4 * D[kk * 5 + 4];
+          float sq = 0.f;
 #pragma unroll
           for (int ch = 0; ch < 3; ++ch) {
-            const float dc = dd[ch] * da + (kk < 3 ? at * D[37 + ch * 3 + kk] : 0.f);
-            s += grc[ch] * dc * dc;
+            const float dc = fmaf(dd[ch], da, at * D[37 + ch * 3 + kk]);
+            sq = fmaf(grc[ch] * dc, dc, sq);
           }
-          a[kk] += s;
+          a[kk] += sq;
+        }
+#pragma unroll
+        for (int kk = 3; kk < 10; ++kk) {
+          const float da = w2 * D[15 + (kk - 3) * 3] + w3 * D[16 + (kk - 3) * 3] + w4 * D[17 + (kk - 3) * 3];
+          a[kk] = fmaf(da * da, Aw, a[kk]);
+        }
+        {
+          const float da = ae * io * D[36];
+          a[10] = fmaf(da * da, Aw, a[10]);
         }
         const float at2 = at * at;
         a[11] += grc[0] * at2;
@@ -217,8 +225,17 @@ __global__ void __launch_bounds__(128) k_gauss_backward(SlmBackArgs A) {
     const int k0 = A.gpo[g], k1 = A.gpo[g + 1];
     for (int q = k0; q < k1; ++q) {  // this gaussian's pairs, in view order
       float a[D];
+      if (A.pair_run_off) {  // per-run partials in slot order: this pair's runs are contiguous
 #pragma unroll
-      for (int j = 0; j < D; ++j) a[j] = A.pacc[(size_t)q * D + j];
+        for (int j = 0; j < D; ++j) a[j] = 0.f;
+        for (int rr = A.pair_run_off[q]; rr < A.pair_run_off[q + 1]; ++rr) {
+#pragma unroll
+          for (int j = 0; j < D; ++j) a[j] += A.pacc[(size_t)rr * D + j];
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < D; ++j) a[j] = A.pacc[(size_t)q * D + j];
+      }
       const uint32_t vm = A.pair_vm[q];
       Tab<K> T;
       pair_tab<K>(A.xs, G, g, A.cams[vm & 0xffffu], vm >> 16, T);

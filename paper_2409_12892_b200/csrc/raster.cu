@@ -243,20 +243,22 @@ __global__ void k_runs_emit(const uint32_t* __restrict__ mask, const uint32_t* _
   }
 }
 
-// per tile of one view: its run count and each run's (view, tile) tag
+// per tile of one view: its run count and each run's (view, tile) tag; one
+// warp per tile (the tile's instances are contiguous)
 __global__ void k_tile_runs(const slm_u2* __restrict__ ranges, int n_tiles, const int* __restrict__ used,
                             const int* __restrict__ run_of, long long ibase, int view, int* __restrict__ tile_nruns,
                             uint32_t* __restrict__ run_tile) {
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_tiles; t += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n_tiles; t += (gridDim.x * blockDim.x) >> 5) {
     const slm_u2 rg = ranges[t];
     int c = 0;
-    for (uint32_t j = rg.x; j < rg.y; ++j) {
-      if (used[ibase + j]) {
-        run_tile[run_of[ibase + j]] = ((uint32_t)view << 24) | (uint32_t)t;
-        ++c;
-      }
+    for (uint32_t j0 = rg.x; j0 < rg.y; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      const bool u = j < rg.y && used[ibase + j];
+      if (u) run_tile[run_of[ibase + j]] = ((uint32_t)view << 24) | (uint32_t)t;
+      c += __popc(__ballot_sync(0xffffffffu, u));
     }
-    tile_nruns[t] = c;
+    if (lane == 0) tile_nruns[t] = c;
   }
 }
 
@@ -311,7 +313,7 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
   __shared__ double s_c0[RB], s_c1[RB], s_c2[RB];
   __shared__ int4 s_box[RB];
   __shared__ uint32_t s_gid[RB];
-  __shared__ uint32_t s_mask[FILL ? 1 : RB * RW];   // COUNT: keep masks of the batch
+  __shared__ uint32_t s_mask[RB * RW];              // keep masks of the batch (COUNT out, FILL in)
   __shared__ long long s_start[FILL ? RB : 1];      // FILL: first entry of each instance's run
   __shared__ uint8_t s_pre[FILL ? RB * RW : 1];     // FILL: keepers in lower warps, per instance
 
@@ -328,6 +330,7 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const unsigned lanes_below = (1u << lane) - 1u;
+  const int row0 = ty * SLM_TILE + 2 * warp;  // the warp's two pixel rows
 
   double T = 1.0, C0 = 0.0, C1 = 0.0, C2 = 0.0;
   uint32_t cnt = 0;
@@ -353,15 +356,17 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
       s_c0[threadIdx.x] = s.c0; s_c1[threadIdx.x] = s.c1; s_c2[threadIdx.x] = s.c2;
       s_box[threadIdx.x] = make_int4(s.x0, s.x1, s.y0, s.y1);
       s_gid[threadIdx.x] = g;
-      if (FILL && A.rec4) {
-        s_start[threadIdx.x] = A.inst_start[j];
+      if (FILL) {
         const uint32_t* mk = A.inst_mask + (size_t)j * RW;
         int acc = 0;
 #pragma unroll
         for (int w = 0; w < RW; ++w) {
+          const uint32_t mw = mk[w];
+          s_mask[threadIdx.x * RW + w] = mw;
           s_pre[threadIdx.x * RW + w] = (uint8_t)acc;
-          acc += __popc(mk[w]);
+          acc += __popc(mw);
         }
+        if (A.rec4) s_start[threadIdx.x] = A.inst_start[j];
       }
     }
     __syncthreads();
@@ -369,8 +374,17 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
     for (int k = 0; k < nb; ++k) {
       bool keep = false;
       double a = 0.0;
+      // FILL: the COUNT pass's keep mask says which pixels keep instance k;
+      // warps with none skip it (same fp64 alpha arithmetic for the keepers)
+      if (FILL && s_mask[k * RW + warp] == 0u) continue;
       const int4 bx = s_box[k];
-      if (!done && px >= bx.x && px <= bx.y && py >= bx.z && py <= bx.w) {
+      if (!FILL && (bx.w < row0 || bx.z > row0 + 1)) {  // warp-uniform: bbox misses the warp's two rows
+        if (lane == 0) s_mask[k * RW + warp] = 0u;
+        continue;
+      }
+      bool inb = !done && (!FILL || ((s_mask[k * RW + warp] >> lane) & 1u)) && px >= bx.x && px <= bx.y &&
+                 py >= bx.z && py <= bx.w;
+      if (inb) {
         // -(1/2) d^T conic d in the reference's evaluation order
         double dx = __dsub_rn(dxp, s_mx[k]);
         double dy = __dsub_rn(dyp, s_my[k]);
@@ -380,7 +394,7 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
         a = a < aclamp ? a : aclamp;
         keep = (a >= amin) && (a > 0.0) && (T >= tstop);
       }
-      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      const unsigned m = FILL ? s_mask[k * RW + warp] : __ballot_sync(0xffffffffu, keep);
       if (!FILL && lane == 0) s_mask[k * RW + warp] = m;
       if (keep) {
         const double wgt = __dmul_rn(a, T);
@@ -388,11 +402,11 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
         C1 = __dadd_rn(C1, __dmul_rn(wgt, s_c1[k]));
         C2 = __dadd_rn(C2, __dmul_rn(wgt, s_c2[k]));
         if (FILL && A.rec4) {
-          const double om = 1.0 - a;
+          const double iom = 1.0 / (1.0 - a);  // stored values are fp32: one fp64 reciprocal suffices
           const long long dest = s_start[k] + s_pre[k * RW + warp] + __popc(m & lanes_below);
           A.rec4[dest] = make_float4(a < aclamp ? (float)a : 0.0f, (float)wgt,
-                                     (float)(s_c0[k] * T - (tot0 - C0) / om), (float)(s_c1[k] * T - (tot1 - C1) / om));
-          A.rec_d2[dest] = (float)(s_c2[k] * T - (tot2 - C2) / om);
+                                     (float)(s_c0[k] * T - (tot0 - C0) * iom), (float)(s_c1[k] * T - (tot1 - C1) * iom));
+          A.rec_d2[dest] = (float)(s_c2[k] * T - (tot2 - C2) * iom);
           A.rec_pix[dest] = (uint8_t)threadIdx.x;
         }
         if (FILL) {
@@ -505,8 +519,8 @@ int slm_runs_emit(const uint32_t* mask, const uint32_t* inst_gid, const int* use
 
 int slm_tile_runs(const slm_u2* ranges, int n_tiles, const int* used, const int* run_of, long long ibase, int view,
                   int* tile_nruns, uint32_t* run_tile, cudaStream_t stream) {
-  k_tile_runs<<<slm_blocks(n_tiles, 128), 128, 0, stream>>>(ranges, n_tiles, used, run_of, ibase, view, tile_nruns,
-                                                             run_tile);
+  k_tile_runs<<<slm_blocks((long long)n_tiles * 32, 256), 256, 0, stream>>>(ranges, n_tiles, used, run_of, ibase, view,
+                                                                             tile_nruns, run_tile);
   return slm_cuda_status();
 }
 
@@ -532,6 +546,7 @@ int slm_raster_count(const RasterArgs* a, cudaStream_t stream) {
 }
 
 int slm_raster_fill(const RasterArgs* a, cudaStream_t stream) {
+  if (!a->inst_mask) return SLM_ERR_ARG;  // FILL replays the COUNT pass's keep masks
   int tiles_y = (a->H + SLM_TILE - 1) / SLM_TILE;
   k_raster<true><<<a->tiles_x * tiles_y, RB, 0, stream>>>(*a);
   return slm_cuda_status();

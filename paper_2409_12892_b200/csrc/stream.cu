@@ -117,7 +117,7 @@ __global__ void k_run_params(SlmTileArgs A, long long n_runs, float* __restrict_
     o[0] = make_float4((float)(g.mx - ox), (float)(g.my - oy), g.ka, g.kb);
     o[1] = make_float4(g.kc, 0.f, 0.f, 0.f);
     o[2] = make_float4(0.f, 0.f, 0.f, 0.f);
-    o[3] = make_float4(0.f, 0.f, g.inv_o, 0.f);
+    o[3] = make_float4(0.f, 0.f, g.inv_o, __int_as_float(A.run_slot[r]));
   }
 }
 
@@ -365,11 +365,14 @@ __global__ void __launch_bounds__(NT) k_stream(SlmTileArgs A) {
         int n = 0, f0 = 0;
         float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f);
         float kc = 0.f, io = 0.f;
+        int slot = 0;
         if (ri != 0xff) {
           const float4* P4 = reinterpret_cast<const float4*>(st + OFF_PAR) + ri * 4;
           q0 = P4[0];
           kc = P4[1].x;
-          io = P4[3].z;
+          const float4 q3 = P4[3];
+          io = q3.z;
+          slot = __float_as_int(q3.w);
           f0 = (int)(rs[ri] - e0);
           n = (int)(rs[ri + 1] - rs[ri]);
         }
@@ -422,7 +425,7 @@ __global__ void __launch_bounds__(NT) k_stream(SlmTileArgs A) {
         a8 += __shfl_xor_sync(F, a8, 2);
         a8 += __shfl_xor_sync(F, a8, 1);
         if (ri != 0xff) {
-          float* o = A.out + (size_t)(kg + ri) * 9;
+          float* o = A.out + (size_t)slot * 9;  // pair-run-slot order (read contiguously by the backward)
           o[lg] = lg == 5 ? w1 * io : ((lg == 2 || lg == 4) ? 0.5f * w1 : w1);
           if (lg == 0) o[8] = a8;
         }

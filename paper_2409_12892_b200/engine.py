@@ -433,6 +433,12 @@ class CacheSet:
             call("slm_pair_runs", ptr(fr.sorted_gid), ptr(fr.inst_off), G, ptr(fr.post_of_pre), ptr(inst_used),
                  ptr(run_of), ibases[v], off(pidx, v * G), ptr(self.pair_run_off), ptr(self.pair_runs), stream_ptr())
         del pidx, pair_nruns, tile_nruns, inst_used, run_of, ent_of
+        # slot of each run in pair_runs: J^T kernels write run partials there so
+        # the per-gaussian backward reads its pairs' runs contiguously
+        self.run_slot = torch.empty(max(R, 1), dtype=torch.int32, device=dev)
+        if R:
+            self.run_slot.index_copy_(0, self.pair_runs[:R].long(),
+                                       torch.arange(R, dtype=torch.int32, device=dev))
         T.tick("runs_pairs")
 
         # ---- FILL phase: run-ordered records ------------------------------------
@@ -489,7 +495,7 @@ class CacheSet:
         a.n_tiles = self.n_tiles_total
         a.tile_run_off, a.tile_chunk_off, a.chunk_run = ptr(self.tile_run_off), ptr(self.tile_chunk_off), \
             ptr(self.chunk_run)
-        a.chunk_perm = ptr(self.chunk_perm)
+        a.chunk_perm, a.run_slot = ptr(self.chunk_perm), ptr(self.run_slot)
         a.run_start, a.run_q, a.run_tile, a.run_par = ptr(self.run_start), ptr(self.run_q), ptr(self.run_tile), \
             ptr(self.run_par)
         a.geo = ptr(self.pair_geo)
@@ -500,13 +506,20 @@ class CacheSet:
     def _static_run_params(self, a: _lib.SlmTileArgs):
         call("slm_run_params", _lib.byref(a), self.R, ptr(self.run_par), stream_ptr())
 
-    def _backward(self, run_acc, d, out, mode, scale=1.0, p=None, M=None, lam=0.0, dot_part=None, lam_out=True):
-        """run partials -> per-pair sums -> per-gaussian chain, attribute-major out."""
-        call("slm_pair_sum", ptr(self.pair_run_off), ptr(self.pair_runs), self.n_pairs, ptr(run_acc), d,
-             ptr(self.pacc), stream_ptr())
+    def _backward(self, run_acc, d, out, mode, scale=1.0, p=None, M=None, lam=0.0, dot_part=None, lam_out=True,
+                  slot_order=False):
+        """run partials -> per-gaussian chain, attribute-major out.  slot_order:
+        run_acc is already in pair-run-slot order (J^T kernels); otherwise it is
+        run-indexed and first reduced to per-pair sums."""
         a = _lib.SlmBackArgs()
+        if slot_order:
+            a.pacc, a.pair_run_off = ptr(run_acc), ptr(self.pair_run_off)
+        else:
+            call("slm_pair_sum", ptr(self.pair_run_off), ptr(self.pair_runs), self.n_pairs, ptr(run_acc), d,
+                 ptr(self.pacc), stream_ptr())
+            a.pacc, a.pair_run_off = ptr(self.pacc), None
         a.xs, a.G = ptr(self.scene.x32()), self.G
-        a.gpo, a.pair_vm, a.cams, a.pacc = ptr(self.gpo), ptr(self.pair_vm), ptr(self.cams_dev), ptr(self.pacc)
+        a.gpo, a.pair_vm, a.cams = ptr(self.gpo), ptr(self.pair_vm), ptr(self.cams_dev)
         a.scale, a.p, a.Mdiag, a.lam = float(scale), ptr(p), ptr(M), float(lam)
         a.lam_out = 1 if lam_out else 0
         a.out, a.dot_part = ptr(out), ptr(dot_part)
@@ -528,7 +541,7 @@ class CacheSet:
         ra.u, ra.out = ptr(u), ptr(self.run_acc)
         self._static_run_params(ra)
         call("slm_apply_jt_runs", _lib.byref(ra), stream_ptr())
-        self._backward(self.run_acc, _lib.JT_D, out, 0, scale, p, M, lam, dot_part)
+        self._backward(self.run_acc, _lib.JT_D, out, 0, scale, p, M, lam, dot_part, slot_order=True)
         return out
 
     def jtwj(self, p: torch.Tensor, out: torch.Tensor, lam: float = 0.0, M=None, dot_part=None,
@@ -545,7 +558,8 @@ class CacheSet:
         a = self._tile_args()
         a.gradr, a.out = ptr(self.gradr), ptr(self.run_acc)
         call("slm_jtwj_runs", _lib.byref(a), stream_ptr())
-        self._backward(self.run_acc, _lib.JT_D, out, 0, 1.0, p, M if lam != 0.0 else None, lam, dot_part, lam_out)
+        self._backward(self.run_acc, _lib.JT_D, out, 0, 1.0, p, M if lam != 0.0 else None, lam, dot_part, lam_out,
+                       slot_order=True)
         return out
 
     def rhs(self) -> torch.Tensor:

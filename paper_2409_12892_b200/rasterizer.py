@@ -117,6 +117,8 @@ def render(scene: GaussianScene, camera: Camera, config: RenderConfig = DEFAULT_
     fr.t_final = torch.empty(hw, dtype=torch.float64, device=dev)
     a = raster_args(fr, cfg_s)
     a.px_count, a.rgb, a.t_final = ptr(cnt), ptr(fr.rgb), ptr(fr.t_final)
+    inst_mask = torch.zeros(max(fr.n_inst, 1) * 8, dtype=torch.int32, device=dev) if traversals else None
+    a.inst_mask = ptr(inst_mask)
     call("slm_raster_count", _lib.byref(a), stream_ptr())
     splats = ProjectedSplats.from_bytes(fr.splats, G)
     image = fr.rgb.view(camera.height, camera.width, 3)
@@ -130,7 +132,7 @@ def render(scene: GaussianScene, camera: Camera, config: RenderConfig = DEFAULT_
     ta = torch.empty(max(E, 1), dtype=torch.float64, device=dev)
     tt = torch.empty(max(E, 1), dtype=torch.float64, device=dev)
     a = raster_args(fr, cfg_s)
-    a.rgb, a.pix_off = ptr(fr.rgb), ptr(off)
+    a.rgb, a.pix_off, a.inst_mask = ptr(fr.rgb), ptr(off), ptr(inst_mask)
     a.trav_gid, a.trav_alpha, a.trav_T = ptr(tg), ptr(ta), ptr(tt)
     call("slm_raster_fill", _lib.byref(a), stream_ptr())
     pix = torch.repeat_interleave(torch.arange(hw, device=dev), (off[1:] - off[:-1]))
