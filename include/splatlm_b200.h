@@ -293,6 +293,9 @@ int slm_chunk_perm(const int* chunk_run, long long n_chunks, const long long* ru
 int slm_pair_tables(const float* xs, long long G, int sh_degree, const int* pair_gid, const uint32_t* pair_vm,
                     const SlmCamera* cams, int n_pairs, float* tab, cudaStream_t s);
 int slm_diag_runs(const SlmTileArgs* a, cudaStream_t s);
+/* the same 14 sums per run on the streaming kernel, written in pair-run-slot
+ * order (run records from slm_run_params, a->ptab from slm_pair_tables) */
+int slm_diag_stream(const SlmTileArgs* a, cudaStream_t s);
 /* forward chain m = dy/dx p per pair (jacobian.py:434-443), written as the
  * 64-byte parameter record of every run of the pair */
 int slm_pair_forward(const SlmFwdArgs* a, int sh_degree, cudaStream_t s);

@@ -124,6 +124,7 @@ _SIGS = {
     "slm_tile_chunks": (c_i, [c_vp, c_i, c_vp, c_vp, c_vp, c_vp, c_i, c_vp]),
     "slm_pair_tables": (c_i, [c_vp, c_ll, c_i, c_vp, c_vp, c_vp, c_i, c_vp, c_vp]),
     "slm_diag_runs": (c_i, [c_vp, c_vp]),
+    "slm_diag_stream": (c_i, [c_vp, c_vp]),
     "slm_pair_forward": (c_i, [c_vp, c_i, c_vp]),
     "slm_pair_sum": (c_i, [c_vp, c_vp, c_i, c_vp, c_i, c_vp, c_vp]),
     "slm_backward_blocks": (c_i, [c_ll]),

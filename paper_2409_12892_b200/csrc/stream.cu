@@ -34,6 +34,9 @@
 #define MODE_J 1
 #define MODE_WRITEU 2
 #define MODE_JT 4
+#define MODE_DIAG 8
+#define DIAG_TAB 48      // floats per pair coefficient table (k_pair_tables)
+#define DIAG_D 14        // diag sums per run
 
 // one ring stage: rec4 | d2 | pix | run params | run starts | J^T schedule | header
 #define ST_R4 (CH * 16)
@@ -115,7 +118,7 @@ __global__ void k_run_params(SlmTileArgs A, long long n_runs, float* __restrict_
     const SlmPairGeo g = A.geo[A.run_q[r]];
     float4* o = reinterpret_cast<float4*>(out + r * PAR);
     o[0] = make_float4((float)(g.mx - ox), (float)(g.my - oy), g.ka, g.kb);
-    o[1] = make_float4(g.kc, 0.f, 0.f, 0.f);
+    o[1] = make_float4(g.kc, __int_as_float(A.run_q[r]), 0.f, 0.f);  // P[5] = pair (diag mode)
     o[2] = make_float4(0.f, 0.f, 0.f, 0.f);
     o[3] = make_float4(0.f, 0.f, g.inv_o, __int_as_float(A.run_slot[r]));
   }
@@ -189,7 +192,7 @@ struct ChunkMeta {
 // stage header: [0] runs, [1] run-start offset (k0 - a2), [2] k0 (global run),
 // [3] d2 offset (e0 - a4), [4] pix offset (e0 - a16)
 template <int MODE>
-__global__ void __launch_bounds__(NT) k_stream(SlmTileArgs A) {
+__global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t full[NS], empty[NS];
   unsigned char* sp = smem;
@@ -210,7 +213,7 @@ __global__ void __launch_bounds__(NT) k_stream(SlmTileArgs A) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const int n_pass = ((MODE & MODE_J) ? 1 : 0) + ((MODE & MODE_JT) ? 1 : 0);
+  const int n_pass = ((MODE & MODE_J) ? 1 : 0) + ((MODE & (MODE_JT | MODE_DIAG)) ? 1 : 0);
 
   if (warp == NW) {
     // ------------------------------ producer ------------------------------
@@ -343,7 +346,128 @@ __global__ void __launch_bounds__(NT) k_stream(SlmTileArgs A) {
       }
       s_u[p] = uw;
     } else {
-      s_u[p] = inside ? A.u[gp] : make_float4(0.f, 0.f, 0.f, 0.f);
+      // J^T: u per pixel; diag: grad_r_sq per pixel
+      const slm_f4* src = (MODE & MODE_DIAG) ? A.gradr : A.u;
+      s_u[p] = inside ? src[gp] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+
+    if (MODE & MODE_DIAG) {
+      consumer_sync();
+      // diag(J^T W J) sums per run (ref: jacobian.py:486-512): same 8-lane
+      // groups / schedule as J^T; each group holds its pair's 48-float chain
+      // table in registers (run record P[5] = pair index, from L2)
+      for (int ci = c0; ci < c1; ++ci, ++g) {
+        const int s = (int)(g % NS);
+        mbar_wait(&full[s], (g / NS) & 1u);
+        const uint8_t* st = stage_ptr(ring, s);
+        const int* hdr = reinterpret_cast<const int*>(st + OFF_HDR);
+        const long long* rs = reinterpret_cast<const long long*>(st + OFF_RS) + hdr[1];
+        const float4* s4 = reinterpret_cast<const float4*>(st);
+        const float* sd2 = reinterpret_cast<const float*>(st + OFF_D2) + hdr[3];
+        const uint8_t* spx = st + OFF_PIX + (rs[0] & 15);
+        const long long e0 = rs[0];
+        const int ri = st[OFF_PERM + (((warp + ci) & (NW - 1)) * 4 + slot)];
+        int n = 0, f0 = 0, sl = 0;
+        float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f);
+        float kc = 0.f, io = 0.f;
+        float D[DIAG_TAB];
+        if (ri != 0xff) {
+          const float4* P4 = reinterpret_cast<const float4*>(st + OFF_PAR) + ri * 4;
+          q0 = P4[0];
+          const float4 q1 = P4[1], q3 = P4[3];
+          kc = q1.x;
+          io = q3.z;
+          sl = __float_as_int(q3.w);
+          const float4* tq = reinterpret_cast<const float4*>(A.ptab + (size_t)__float_as_int(q1.y) * DIAG_TAB);
+#pragma unroll
+          for (int k = 0; k < DIAG_TAB / 4; ++k) {
+            const float4 v = __ldg(tq + k);
+            D[4 * k] = v.x;
+            D[4 * k + 1] = v.y;
+            D[4 * k + 2] = v.z;
+            D[4 * k + 3] = v.w;
+          }
+          f0 = (int)(rs[ri] - e0);
+          n = (int)(rs[ri + 1] - rs[ri]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < DIAG_TAB; ++k) D[k] = 0.f;
+        }
+        const int nmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)n);
+        if (nmax == 0) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[s]);
+          continue;
+        }
+        const float dop = io * D[36];
+        float a[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) a[k] = 0.f;
+        const float4* pr = s4 + f0;
+        const float* pd = sd2 + f0;
+        const uint8_t* pp = spx + f0;
+        for (int j = lg; j < nmax; j += 8) {
+          if (j < n) {
+            const float4 r = pr[j];
+            const float dd[3] = {r.z, r.w, pd[j]};
+            const int pl = pp[j];
+            const float4 gr = s_u[pl];
+            const float grc[3] = {gr.x, gr.y, gr.z};
+            const float ae = r.x, at = r.y;
+            const float dx = (float)(pl & 15) - q0.x, dy = (float)(pl >> 4) - q0.y;
+            const float e1 = q0.z * dx + q0.w * dy, e2 = q0.w * dx + kc * dy;
+            const float w0 = ae * e1, w1 = ae * e2, w2 = 0.5f * w0 * e1, w3 = w0 * e2, w4 = 0.5f * w1 * e2;
+            // sum_ch gr_ch (dc_ch/dx_k)^2: dalpha_k^2 * Aw for k >= 3 (exact),
+            // per-channel squares for the position params (dc also has at * dcol)
+            const float Aw = grc[0] * dd[0] * dd[0] + grc[1] * dd[1] * dd[1] + grc[2] * dd[2] * dd[2];
+#pragma unroll
+            for (int kk = 0; kk < 3; ++kk) {
+              const float da = w0 * D[kk * 5] + w1 * D[kk * 5 + 1] + w2 * D[kk * 5 + 2] + w3 * D[kk * 5 + 3] +
+                               w4 * D[kk * 5 + 4];
+              float sq = 0.f;
+#pragma unroll
+              for (int ch = 0; ch < 3; ++ch) {
+                const float dc = fmaf(dd[ch], da, at * D[37 + ch * 3 + kk]);
+                sq = fmaf(grc[ch] * dc, dc, sq);
+              }
+              a[kk] += sq;
+            }
+#pragma unroll
+            for (int kk = 3; kk < 10; ++kk) {
+              const float da = w2 * D[15 + (kk - 3) * 3] + w3 * D[16 + (kk - 3) * 3] + w4 * D[17 + (kk - 3) * 3];
+              a[kk] = fmaf(da * da, Aw, a[kk]);
+            }
+            const float dao = ae * dop;
+            a[10] = fmaf(dao * dao, Aw, a[10]);
+            const float at2 = at * at;
+            a[11] = fmaf(grc[0], at2, a[11]);
+            a[12] = fmaf(grc[1], at2, a[12]);
+            a[13] = fmaf(grc[2], at2, a[13]);
+          }
+        }
+        // two 8-lane reduce-scatters: lane lg ends with the group sums of
+        // values lg and 8 + lg (fixed pattern -> deterministic)
+        const unsigned F = 0xffffffffu;
+        const bool u4 = lg & 4, u2 = lg & 2, u1 = lg & 1;
+        float res[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const float* v = a + 8 * h;
+          float w4[4], w2[2];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) w4[k] = (u4 ? v[k + 4] : v[k]) + __shfl_xor_sync(F, u4 ? v[k] : v[k + 4], 4);
+#pragma unroll
+          for (int k = 0; k < 2; ++k) w2[k] = (u2 ? w4[k + 2] : w4[k]) + __shfl_xor_sync(F, u2 ? w4[k] : w4[k + 2], 2);
+          res[h] = (u1 ? w2[1] : w2[0]) + __shfl_xor_sync(F, u1 ? w2[0] : w2[1], 1);
+        }
+        if (ri != 0xff) {
+          float* o = A.out + (size_t)sl * DIAG_D;  // pair-run-slot order
+          o[lg] = res[0];
+          if (lg < DIAG_D - 8) o[8 + lg] = res[1];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
     }
 
     if (MODE & MODE_JT) {
@@ -487,6 +611,10 @@ int slm_chunk_perm(const int* chunk_run, long long n_chunks, const long long* ru
 
 // u = J p (a->gradr weights it) written to a->u_out
 int slm_apply_j(const SlmTileArgs* a, cudaStream_t st) { return launch_stream<MODE_J | MODE_WRITEU>(a, st); }
+
+// diag(J^T W J) sums per run (14, pair-run-slot order) from a->gradr and the
+// per-pair tables a->ptab; run records must come from slm_run_params
+int slm_diag_stream(const SlmTileArgs* a, cudaStream_t st) { return launch_stream<MODE_DIAG>(a, st); }
 
 // J^T partials per run from the per-pixel a->u
 int slm_apply_jt_runs(const SlmTileArgs* a, cudaStream_t st) { return launch_stream<MODE_JT>(a, st); }

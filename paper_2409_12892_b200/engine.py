@@ -583,9 +583,10 @@ class CacheSet:
                  ptr(self.pair_vm), ptr(self.cams_dev), self.n_pairs, ptr(ptab), stream_ptr())
             ra = self._tile_args()
             ra.ptab, ra.gradr, ra.out = ptr(ptab), ptr(self.gradr), ptr(sums)
-            call("slm_diag_runs", _lib.byref(ra), stream_ptr())
+            self._static_run_params(ra)
+            call("slm_diag_stream", _lib.byref(ra), stream_ptr())
             M = torch.empty(self.G * self.P, dtype=torch.float32, device=self.device)
-            self._backward(sums, _lib.DIAG_D, M, 1)
+            self._backward(sums, _lib.DIAG_D, M, 1, slot_order=True)
             self._M = M
         return self._M
 
