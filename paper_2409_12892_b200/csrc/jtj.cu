@@ -208,66 +208,98 @@ __global__ void k_pair_sum(const int* __restrict__ pair_run_off, const int* __re
 // optional fp64 partials of p.(out + lam * max(M, 1e-12) * p) (PCG), and
 // out += lam * max(M, 1e-12) * p when lam_out
 // ---------------------------------------------------------------------------
+// sum of one pair's run partials (slot order) or its precomputed pair sum
+template <int D, int J0, int J1>
+__device__ __forceinline__ void pair_partials(const SlmBackArgs& A, int q, float (&a)[J1 - J0]) {
+#pragma unroll
+  for (int j = 0; j < J1 - J0; ++j) a[j] = 0.f;
+  if (A.pair_run_off) {
+    for (int rr = A.pair_run_off[q]; rr < A.pair_run_off[q + 1]; ++rr) {
+#pragma unroll
+      for (int j = 0; j < J1 - J0; ++j) a[j] += A.pacc[(size_t)rr * D + J0 + j];
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < J1 - J0; ++j) a[j] = A.pacc[(size_t)q * D + J0 + j];
+  }
+}
+
+// Two sweeps over the gaussian's pairs keep the live state small (geometry
+// accumulators + chain, then the 3 x K SH accumulators + basis) so the kernel
+// runs at 4 blocks / SM without spills.
 template <int K, int MODE>
-__global__ void __launch_bounds__(128) k_gauss_backward(SlmBackArgs A) {
+__global__ void __launch_bounds__(128, 3) k_gauss_backward(SlmBackArgs A) {
   __shared__ double sm[32];
   constexpr int D = MODE == 0 ? 9 : DIAG_RUN_D;
   const long long G = A.G;
   double dot = 0.0;
   for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < G; g += (long long)gridDim.x * blockDim.x) {
-    float og[11], osh[3][K];
+    const int k0 = A.gpo[g], k1 = A.gpo[g + 1];
+    // ---- sweep 1: the 11 geometry parameters
+    float og[11];
 #pragma unroll
     for (int j = 0; j < 11; ++j) og[j] = 0.f;
+    for (int q = k0; q < k1; ++q) {  // this gaussian's pairs, in view order
+      if (MODE == 0) {
+        float a[9];
+        pair_partials<D, 0, 9>(A, q, a);
+        const uint32_t vm = A.pair_vm[q];
+        Tab<K> T;
+        pair_tab<K>(A.xs, G, g, A.cams[vm & 0xffffu], vm >> 16, T);
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          og[j] += T.dmu[0][j] * a[0] + T.dmu[1][j] * a[1] + T.dcol[0][j] * a[6] + T.dcol[1][j] * a[7] +
+                   T.dcol[2][j] * a[8];
+#pragma unroll
+        for (int j = 0; j < 10; ++j) og[j] += T.dcov[0][j] * a[2] + T.dcov[1][j] * a[3] + T.dcov[2][j] * a[4];
+        og[10] += T.dopa * a[5];
+      } else {
+        float a[11];
+        pair_partials<D, 0, 11>(A, q, a);
+#pragma unroll
+        for (int j = 0; j < 11; ++j) og[j] += a[j];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 11; ++j) {
+      float v = A.scale * og[j];
+      const long long i = (long long)j * G + g;
+      if (A.p) {
+        const double pv = (double)A.p[i];
+        const double lt = A.Mdiag ? A.lam * (double)fmaxf(A.Mdiag[i], 1e-12f) * pv : 0.0;
+        dot += pv * ((double)v + lt);
+        if (A.lam_out) v = (float)((double)v + lt);
+      }
+      A.out[i] = v;
+    }
+    // ---- sweep 2: the SH block, (colour partial * clamp mask) x basis (MODE 0)
+    // or (colour sum * clamp mask) x basis^2 (MODE 1)
+    float osh[3][K];
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch)
 #pragma unroll
       for (int k = 0; k < K; ++k) osh[ch][k] = 0.f;
-    const int k0 = A.gpo[g], k1 = A.gpo[g + 1];
-    for (int q = k0; q < k1; ++q) {  // this gaussian's pairs, in view order
-      float a[D];
-      if (A.pair_run_off) {  // per-run partials in slot order: this pair's runs are contiguous
-#pragma unroll
-        for (int j = 0; j < D; ++j) a[j] = 0.f;
-        for (int rr = A.pair_run_off[q]; rr < A.pair_run_off[q + 1]; ++rr) {
-#pragma unroll
-          for (int j = 0; j < D; ++j) a[j] += A.pacc[(size_t)rr * D + j];
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < D; ++j) a[j] = A.pacc[(size_t)q * D + j];
-      }
+    const float px = A.xs[g], py = A.xs[G + g], pz = A.xs[2 * G + g];
+    for (int q = k0; q < k1; ++q) {
+      float c[3];
+      if (MODE == 0) pair_partials<D, 6, 9>(A, q, c);
+      else pair_partials<D, 11, 14>(A, q, c);
       const uint32_t vm = A.pair_vm[q];
-      Tab<K> T;
-      pair_tab<K>(A.xs, G, g, A.cams[vm & 0xffffu], vm >> 16, T);
-      if (MODE == 0) {
-        const float col[3] = {a[6], a[7], a[8]};
+      const SlmCamera& cam = A.cams[vm & 0xffffu];
+      const float v0 = px - (float)cam.C[0], v1 = py - (float)cam.C[1], v2 = pz - (float)cam.C[2];
+      const float ivn = 1.f / sqrtf(v0 * v0 + v1 * v1 + v2 * v2);
+      float Y[K];
+      sh_basis<float, K>(v0 * ivn, v1 * ivn, v2 * ivn, Y);
 #pragma unroll
-        for (int j = 0; j < 3; ++j)
-          og[j] += T.dmu[0][j] * a[0] + T.dmu[1][j] * a[1] + T.dcol[0][j] * col[0] + T.dcol[1][j] * col[1] +
-                   T.dcol[2][j] * col[2];
+      for (int ch = 0; ch < 3; ++ch) {
+        const float s = ((vm >> (16 + ch)) & 1u) ? 0.f : c[ch];
 #pragma unroll
-        for (int j = 0; j < 10; ++j) og[j] += T.dcov[0][j] * a[2] + T.dcov[1][j] * a[3] + T.dcov[2][j] * a[4];
-        og[10] += T.dopa * a[5];
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-          const float s = col[ch] * T.mask[ch];
-#pragma unroll
-          for (int k = 0; k < K; ++k) osh[ch][k] += s * T.Y[k];
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 11; ++j) og[j] += a[j];
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-          const float s = a[11 + ch] * T.mask[ch];
-#pragma unroll
-          for (int k = 0; k < K; ++k) osh[ch][k] += s * T.Y[k] * T.Y[k];
-        }
+        for (int k = 0; k < K; ++k) osh[ch][k] += MODE == 0 ? s * Y[k] : s * Y[k] * Y[k];
       }
     }
 #pragma unroll
-    for (int a = 0; a < 11 + 3 * K; ++a) {
-      float v = A.scale * (a < 11 ? og[a] : osh[(a - 11) / K][(a - 11) % K]);
+    for (int a = 11; a < 11 + 3 * K; ++a) {
+      float v = A.scale * osh[(a - 11) / K][(a - 11) % K];
       const long long i = (long long)a * G + g;
       if (A.p) {
         const double pv = (double)A.p[i];
