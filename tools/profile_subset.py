@@ -81,6 +81,27 @@ def main():
             f.append((f0, f1))
         torch.cuda.synchronize()
         phases["fused_jtwj_product"] = f[-1][0].elapsed_time(f[-1][1])
+        # the fused product's launches timed one by one
+        from paper_2409_12892_b200 import _lib
+        from paper_2409_12892_b200._lib import call, ptr, stream_ptr
+        dp = torch.zeros(_lib.load().slm_backward_blocks(cs.G), dtype=torch.float64, device=dev)
+        ks = []
+        for _ in range(3):
+            t0 = ev()
+            cs.pair_forward(p)
+            t1 = ev()
+            a = cs._tile_args()
+            a.gradr, a.out = ptr(cs.gradr), ptr(cs.run_acc)
+            call("slm_jtwj_runs", _lib.byref(a), stream_ptr())
+            t2 = ev()
+            cs._backward(cs.run_acc, _lib.JT_D, g, 0, 1.0, p, M, 1e-4, dp, False, slot_order=True)
+            t3 = ev()
+            ks.append((t0, t1, t2, t3))
+        torch.cuda.synchronize()
+        t0, t1, t2, t3 = ks[-1]
+        phases["k_pair_forward"] = t0.elapsed_time(t1)
+        phases["k_stream_fused"] = t1.elapsed_time(t2)
+        phases["k_backward"] = t2.elapsed_time(t3)
         if not args.skip_pcg:
             s0 = ev()
             pcg_run(cs, b, M, 1e-4, cfg["iters"])
