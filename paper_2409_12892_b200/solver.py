@@ -208,7 +208,8 @@ def lm_direction(scene, cameras, gts, schedule: BatchSchedule = BatchSchedule(),
             continue
         pcg_stats.append(st)
         comb.add(d, M)
-        if keep_caches:
+        if keep_caches and not caches:  # the first accepted batch (rho's frozen caches)
+            cs.view_ids = list(views)
             caches.append(cs)
         del cs
     comb.allreduce()
