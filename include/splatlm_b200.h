@@ -173,6 +173,11 @@ typedef struct {
   const uint32_t* run_tile; /* view << 24 | tile */
   const SlmView* views;
   float* run_par;           /* [R*16] out */
+  /* split form (pm != NULL): per-pair m scratch [P*12] then per-run records */
+  void* pm;
+  const int* run_q;
+  const int* run_slot;
+  long long n_runs;
 } SlmFwdArgs;
 
 /* per-gaussian backward chain */

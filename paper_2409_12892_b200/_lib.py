@@ -68,7 +68,8 @@ class SlmTileArgs(C.Structure):
 class SlmFwdArgs(C.Structure):
     _fields_ = [("xs", c_vp), ("G", c_ll), ("pair_gid", c_vp), ("pair_vm", c_vp), ("cams", c_vp), ("n_pairs", c_i),
                 ("p", c_vp), ("sa", c_ll), ("sg", c_ll), ("geo", c_vp), ("pair_run_off", c_vp), ("pair_runs", c_vp),
-                ("run_tile", c_vp), ("views", c_vp), ("run_par", c_vp)]
+                ("run_tile", c_vp), ("views", c_vp), ("run_par", c_vp), ("pm", c_vp), ("run_q", c_vp),
+                ("run_slot", c_vp), ("n_runs", c_ll)]
 
 
 class SlmBackArgs(C.Structure):

@@ -479,7 +479,6 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
         mbar_wait(&full[s], (g / NS) & 1u);
         const uint8_t* st = stage_ptr(ring, s);
         const int* hdr = reinterpret_cast<const int*>(st + OFF_HDR);
-        const int kg = hdr[2];
         const long long* rs = reinterpret_cast<const long long*>(st + OFF_RS) + hdr[1];
         const float4* s4 = reinterpret_cast<const float4*>(st);
         const float* sd2 = reinterpret_cast<const float*>(st + OFF_D2) + hdr[3];

@@ -466,6 +466,8 @@ class CacheSet:
         self.run_acc = _empty(R * _lib.JT_D, f32, dev)
         self.run_par = _empty(R * 16, f32, dev)
         self.pacc = _empty(Pn * _lib.DIAG_D, f32, dev)
+        self.split_forward = True
+        self.pm = _empty(Pn * 12, f32, dev)
         self._b = None
         self._M = None
 
@@ -487,6 +489,8 @@ class CacheSet:
         a.sa, a.sg = (1, P) if gaussian_major else (G, 1)
         a.geo, a.pair_run_off, a.pair_runs = ptr(self.pair_geo), ptr(self.pair_run_off), ptr(self.pair_runs)
         a.run_tile, a.views, a.run_par = ptr(self.run_tile), ptr(self.views_dev), ptr(self.run_par)
+        if self.split_forward:
+            a.pm, a.run_q, a.run_slot, a.n_runs = ptr(self.pm), ptr(self.run_q), ptr(self.run_slot), self.R
         call("slm_pair_forward", _lib.byref(a), self.scene.sh_degree, stream_ptr())
 
     def _tile_args(self) -> _lib.SlmTileArgs:
