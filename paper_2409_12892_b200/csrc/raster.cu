@@ -316,6 +316,7 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
   __shared__ uint32_t s_mask[RB * RW];              // keep masks of the batch (COUNT out, FILL in)
   __shared__ long long s_start[FILL ? RB : 1];      // FILL: first entry of each instance's run
   __shared__ uint8_t s_pre[FILL ? RB * RW : 1];     // FILL: keepers in lower warps, per instance
+  __shared__ uint8_t s_list[RW][RB];                // per warp: batch instances that concern it
 
   const int tiles_x = A.tiles_x;
   const int tile = blockIdx.x;
@@ -371,17 +372,32 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
     }
     __syncthreads();
     const int nb = min((unsigned)RB, rng.y - base);
-    for (int k = 0; k < nb; ++k) {
+    // each warp compacts the batch's instances that concern its two pixel rows:
+    // COUNT -- bbox meets the rows (the others get an empty keep mask);
+    // FILL  -- the COUNT pass kept at least one of the warp's pixels
+    int nrel = 0;
+    for (int k0 = 0; k0 < nb; k0 += 32) {
+      const int k = k0 + lane;
+      bool rel = false;
+      if (k < nb) {
+        if (FILL) {
+          rel = s_mask[k * RW + warp] != 0u;
+        } else {
+          const int4 bx = s_box[k];
+          rel = !(bx.w < row0 || bx.z > row0 + 1);
+          if (!rel) s_mask[k * RW + warp] = 0u;
+        }
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, rel);
+      if (rel) s_list[warp][nrel + __popc(bal & lanes_below)] = (uint8_t)k;
+      nrel += __popc(bal);
+    }
+    __syncwarp();
+    for (int ki = 0; ki < nrel; ++ki) {
+      const int k = s_list[warp][ki];
       bool keep = false;
       double a = 0.0;
-      // FILL: the COUNT pass's keep mask says which pixels keep instance k;
-      // warps with none skip it (same fp64 alpha arithmetic for the keepers)
-      if (FILL && s_mask[k * RW + warp] == 0u) continue;
       const int4 bx = s_box[k];
-      if (!FILL && (bx.w < row0 || bx.z > row0 + 1)) {  // warp-uniform: bbox misses the warp's two rows
-        if (lane == 0) s_mask[k * RW + warp] = 0u;
-        continue;
-      }
       bool inb = !done && (!FILL || ((s_mask[k * RW + warp] >> lane) & 1u)) && px >= bx.x && px <= bx.y &&
                  py >= bx.z && py <= bx.w;
       if (inb) {
