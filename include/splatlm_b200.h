@@ -191,6 +191,11 @@ typedef struct {
                                else per-run partials in pair-run-slot order (the
                                J^T kernels write run r to its slot in pair_runs) */
   const int* pair_run_off;  /* [P+1] pair -> run slots, or NULL */
+  const int* warp_g0;       /* packed form: first gaussian of each 32-pair window
+                               (slm_warp_bounds), or NULL for thread-per-gaussian */
+  const int* pair_gid;
+  long long n_pairs;
+  float* gm;                /* packed form: [G*P] gaussian-major scratch */
   float scale;
   const float* p;           /* optional: fp64 partials of p.(out + lam * max(M,1e-12) * p) */
   const float* Mdiag;
@@ -310,6 +315,7 @@ int slm_pair_sum(const int* pair_run_off, const int* pair_runs, int n_pairs, con
 /* backward chain per gaussian, attribute-major out (jacobian.py:314-353):
  * mode 0 from J^T pair sums, mode 1 from diag pair sums */
 int slm_backward_blocks(long long G);
+int slm_warp_bounds(const int* gpo, long long G, int n_pairs, int* warp_g0, cudaStream_t s);
 int slm_pair_backward(const SlmBackArgs* a, int mode, int sh_degree, cudaStream_t s);
 
 /* ---- PCG (Alg. 1; SPEC pcg_solve 391-399) ------------------ */

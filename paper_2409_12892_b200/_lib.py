@@ -74,7 +74,7 @@ class SlmFwdArgs(C.Structure):
 
 class SlmBackArgs(C.Structure):
     _fields_ = [("xs", c_vp), ("G", c_ll), ("gpo", c_vp), ("pair_vm", c_vp), ("cams", c_vp), ("pacc", c_vp),
-                ("pair_run_off", c_vp),
+                ("pair_run_off", c_vp), ("warp_g0", c_vp), ("pair_gid", c_vp), ("n_pairs", c_ll), ("gm", c_vp),
                 ("scale", c_f),
                 ("p", c_vp), ("Mdiag", c_vp), ("lam", c_d), ("lam_out", c_i), ("out", c_vp), ("dot_part", c_vp)]
 
@@ -129,6 +129,7 @@ _SIGS = {
     "slm_pair_forward": (c_i, [c_vp, c_i, c_vp]),
     "slm_pair_sum": (c_i, [c_vp, c_vp, c_i, c_vp, c_i, c_vp, c_vp]),
     "slm_backward_blocks": (c_i, [c_ll]),
+    "slm_warp_bounds": (c_i, [c_vp, c_ll, c_i, c_vp, c_vp]),
     "slm_pair_backward": (c_i, [c_vp, c_i, c_i, c_vp]),
     "slm_vec_blocks": (c_i, []),
     "slm_pcg_pinit": (c_i, [c_vp, c_vp, c_vp, c_ll, c_vp]),

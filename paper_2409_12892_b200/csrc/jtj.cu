@@ -317,6 +317,146 @@ __global__ void __launch_bounds__(128, 3) k_gauss_backward(SlmBackArgs A) {
 }
 
 // ---------------------------------------------------------------------------
+// Packed per-gaussian backward: warp w owns the gaussians whose first pair
+// falls in pairs [32w, 32w + 32) (warp_g0 from k_warp_bounds), lane = pair.
+// Each lane sums its pair's run partials (contiguous slots), applies its
+// view's 9 -> 59 chain and writes the row to a per-warp shared tile; the lanes
+// then walk the rows in pair order summing columns j = lane, lane + 32 per
+// gaussian (fixed order -> deterministic).  Loads are coalesced across lanes
+// and there is no per-thread serial loop over a gaussian's pairs.
+// ---------------------------------------------------------------------------
+__global__ void k_warp_bounds(const int* __restrict__ gpo, long long G, int n_warps, int* __restrict__ warp_g0) {
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g <= G; g += (long long)gridDim.x * blockDim.x) {
+    const int hi = g < G ? (gpo[g] >> 5) : n_warps;
+    const int lo = g == 0 ? -1 : (gpo[g - 1] >> 5);
+    for (int w = lo + 1; w <= hi && w <= n_warps; ++w) warp_g0[w] = (int)g;
+  }
+}
+
+#define PK_WARPS 4
+template <int K, int MODE>
+__global__ void __launch_bounds__(32 * PK_WARPS) k_gauss_backward_packed(SlmBackArgs A, const int* __restrict__ warp_g0,
+                                                                       int n_warps) {
+  constexpr int P = 11 + 3 * K;
+  constexpr int PP = P | 1;  // odd row stride: conflict-free row writes and column reads
+  constexpr int D = MODE == 0 ? 9 : DIAG_RUN_D;
+  __shared__ float s_v[PK_WARPS][32 * PP];
+  __shared__ int s_g[PK_WARPS][32];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const long long G = A.G;
+  // gaussian-major scratch row (contiguous, coalesced); k_gm_to_am writes the
+  // attribute-major output with the scale / lambda / dot epilogue
+  auto flush = [&](long long g, float c0, float c1) {
+    float* o = A.gm + (size_t)g * P;
+    o[lane] = c0;
+    if (lane + 32 < P) o[lane + 32] = c1;
+  };
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n_warps; w += (gridDim.x * blockDim.x) >> 5) {
+    const int ga = warp_g0[w], gb = warp_g0[w + 1];
+    if (ga >= gb) continue;
+    const int q0 = A.gpo[ga], q1 = A.gpo[gb];
+    long long cur = ga;  // gaussian being accumulated
+    float c0 = 0.f, c1 = 0.f;
+    for (int base = q0; base < q1; base += 32) {
+      const int q = base + lane;
+      if (q < q1) {
+        const long long g = A.pair_gid[q];
+        s_g[wl][lane] = (int)g;
+        float* row = s_v[wl] + lane * PP;
+        float a[D];
+        pair_partials<D, 0, D>(A, q, a);
+        const uint32_t vm = A.pair_vm[q];
+        if (MODE == 0) {
+          Tab<K> T;
+          pair_tab<K>(A.xs, G, g, A.cams[vm & 0xffffu], vm >> 16, T);
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+            row[j] = T.dmu[0][j] * a[0] + T.dmu[1][j] * a[1] + T.dcol[0][j] * a[6] + T.dcol[1][j] * a[7] +
+                     T.dcol[2][j] * a[8] + T.dcov[0][j] * a[2] + T.dcov[1][j] * a[3] + T.dcov[2][j] * a[4];
+#pragma unroll
+          for (int j = 3; j < 10; ++j) row[j] = T.dcov[0][j] * a[2] + T.dcov[1][j] * a[3] + T.dcov[2][j] * a[4];
+          row[10] = T.dopa * a[5];
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            const float sc = a[6 + ch] * T.mask[ch];
+#pragma unroll
+            for (int k = 0; k < K; ++k) row[11 + ch * K + k] = sc * T.Y[k];
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 11; ++j) row[j] = a[j];
+          const SlmCamera& cam = A.cams[vm & 0xffffu];
+          const float v0 = A.xs[g] - (float)cam.C[0], v1 = A.xs[G + g] - (float)cam.C[1];
+          const float v2 = A.xs[2 * G + g] - (float)cam.C[2];
+          const float ivn = 1.f / sqrtf(v0 * v0 + v1 * v1 + v2 * v2);
+          float Y[K];
+          sh_basis<float, K>(v0 * ivn, v1 * ivn, v2 * ivn, Y);
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            const float sc = ((vm >> (16 + ch)) & 1u) ? 0.f : a[11 + ch];
+#pragma unroll
+            for (int k = 0; k < K; ++k) row[11 + ch * K + k] = sc * Y[k] * Y[k];
+          }
+        }
+      }
+      __syncwarp();
+      const int nr = min(32, q1 - base);
+      for (int i = 0; i < nr; ++i) {  // rows in pair order
+        const int gi = s_g[wl][i];
+        while (cur < gi) {  // finish cur (and any pair-less gaussians before gi)
+          flush(cur, c0, c1);
+          c0 = c1 = 0.f;
+          ++cur;
+        }
+        const float* r = s_v[wl] + i * PP;
+        c0 += r[lane];
+        if (lane + 32 < P) c1 += r[lane + 32];
+      }
+      __syncwarp();
+    }
+    while (cur < gb) {
+      flush(cur, c0, c1);
+      c0 = c1 = 0.f;
+      ++cur;
+    }
+  }
+}
+
+// gaussian-major scratch -> attribute-major out (tiled transpose, 32 gaussians
+// per tile) with out = scale * v (+ lam * max(M, 1e-12) * p) and fp64 partials
+// of p.(v + lam Mf p)
+template <int P>
+__global__ void __launch_bounds__(256) k_gm_to_am(SlmBackArgs A) {
+  __shared__ float t[32][P + 1];
+  __shared__ double sm[32];
+  const long long G = A.G;
+  double dot = 0.0;
+  for (long long g0 = (long long)blockIdx.x * 32; g0 < G; g0 += (long long)gridDim.x * 32) {
+    const int ng = (int)min((long long)32, G - g0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < ng * P; i += blockDim.x) t[i / P][i % P] = A.gm[(size_t)g0 * P + i];
+    __syncthreads();
+    for (int i = threadIdx.x; i < 32 * P; i += blockDim.x) {
+      const int a = i >> 5, gl = i & 31;
+      if (gl >= ng) continue;
+      float v = A.scale * t[gl][a];
+      const long long idx = (long long)a * G + g0 + gl;
+      if (A.p) {
+        const double pv = (double)A.p[idx];
+        const double lt = A.Mdiag ? A.lam * (double)fmaxf(A.Mdiag[idx], 1e-12f) * pv : 0.0;
+        dot += pv * ((double)v + lt);
+        if (A.lam_out) v = (float)((double)v + lt);
+      }
+      A.out[idx] = v;
+    }
+  }
+  if (A.dot_part) {
+    double tt = block_sum_d(dot, sm);
+    if (threadIdx.x == 0) A.dot_part[blockIdx.x] = tt;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // C-ABI
 // ---------------------------------------------------------------------------
 extern "C" {
@@ -384,8 +524,32 @@ int slm_pair_sum(const int* pair_run_off, const int* pair_runs, int n_pairs, con
 
 int slm_backward_blocks(long long G) { return (int)slm_blocks(G, 128, 148LL * 16); }
 
+int slm_warp_bounds(const int* gpo, long long G, int n_pairs, int* warp_g0, cudaStream_t st) {
+  const int n_warps = (n_pairs >> 5) + 1;
+  k_warp_bounds<<<slm_blocks(G + 1, 256), 256, 0, st>>>(gpo, G, n_warps, warp_g0);
+  return slm_cuda_status();
+}
+
 int slm_pair_backward(const SlmBackArgs* a, int mode, int sh_degree, cudaStream_t st) {
   unsigned b = (unsigned)slm_backward_blocks(a->G);
+  if (a->warp_g0) {  // packed: warp per 32-pair window of gaussians
+    const int nw = (int)((a->n_pairs >> 5) + 1);
+#define SLM_PK(KK)                                                                         \
+  if (mode == 0)                                                                           \
+    k_gauss_backward_packed<KK, 0><<<b, 32 * PK_WARPS, 0, st>>>(*a, a->warp_g0, nw);       \
+  else                                                                                     \
+    k_gauss_backward_packed<KK, 1><<<b, 32 * PK_WARPS, 0, st>>>(*a, a->warp_g0, nw);       \
+  k_gm_to_am<11 + 3 * KK><<<b, 256, 0, st>>>(*a);
+    switch (sh_degree) {
+      case 0: SLM_PK(1) break;
+      case 1: SLM_PK(4) break;
+      case 2: SLM_PK(9) break;
+      case 3: SLM_PK(16) break;
+      default: return SLM_ERR_ARG;
+    }
+#undef SLM_PK
+    return slm_cuda_status();
+  }
 #define SLM_BW(KK)                                  \
   if (mode == 0)                                    \
     k_gauss_backward<KK, 0><<<b, 128, 0, st>>>(*a); \

@@ -467,6 +467,10 @@ class CacheSet:
         self.run_par = _empty(R * 16, f32, dev)
         self.pacc = _empty(Pn * _lib.DIAG_D, f32, dev)
         self.split_forward = True
+        self.packed_backward = True
+        self.warp_g0 = torch.empty((Pn >> 5) + 2, dtype=torch.int32, device=dev)
+        self.gm = torch.empty(G * self.P, dtype=torch.float32, device=dev)
+        call("slm_warp_bounds", ptr(self.gpo), G, Pn, ptr(self.warp_g0), stream_ptr())
         self.pm = _empty(Pn * 12, f32, dev)
         self._b = None
         self._M = None
@@ -524,6 +528,9 @@ class CacheSet:
             a.pacc, a.pair_run_off = ptr(self.pacc), None
         a.xs, a.G = ptr(self.scene.x32()), self.G
         a.gpo, a.pair_vm, a.cams = ptr(self.gpo), ptr(self.pair_vm), ptr(self.cams_dev)
+        if self.packed_backward:
+            a.warp_g0, a.pair_gid, a.n_pairs = ptr(self.warp_g0), ptr(self.pair_gid), self.n_pairs
+            a.gm = ptr(self.gm)
         a.scale, a.p, a.Mdiag, a.lam = float(scale), ptr(p), ptr(M), float(lam)
         a.lam_out = 1 if lam_out else 0
         a.out, a.dot_part = ptr(out), ptr(dot_part)
