@@ -145,7 +145,8 @@ typedef struct {
   const long long* run_start;/* [R+1] (+2 padding slots) */
   const int* run_q;          /* pair of each run */
   const uint32_t* run_tile;  /* view << 24 | tile */
-  const float* run_par;      /* [R*16] run parameter records (slm_pair_forward / slm_run_params) */
+  const float* run_static;   /* [R*8] static run records (slm_run_static) */
+  const void* pm;            /* [P*12] per-pair forward chain m (slm_pair_forward); NULL: J^T / diag only */
   const SlmPairGeo* geo;
   const float* ptab;         /* diag: per-pair coefficient tables (slm_pair_tables) */
   const slm_f4* rec4;
@@ -157,7 +158,7 @@ typedef struct {
   float* out;                /* applyJT [R*9] / diag [R*14] run partials */
 } SlmTileArgs;
 
-/* per-pair forward chain + per-run parameter records (applyJ) */
+/* per-pair forward chain (applyJ) */
 typedef struct {
   const float* xs;          /* scene, attribute-major fp32 */
   long long G;
@@ -167,17 +168,7 @@ typedef struct {
   int n_pairs;
   const float* p;           /* direction, p[a * sa + g * sg] (either layout) */
   long long sa, sg;
-  const SlmPairGeo* geo;
-  const int* pair_run_off;  /* [P+1] pair -> runs CSR */
-  const int* pair_runs;
-  const uint32_t* run_tile; /* view << 24 | tile */
-  const SlmView* views;
-  float* run_par;           /* [R*16] out */
-  /* split form (pm != NULL): per-pair m scratch [P*12] then per-run records */
-  void* pm;
-  const int* run_q;
-  const int* run_slot;
-  long long n_runs;
+  void* pm;                 /* [P*12] out: m = dy/dx p per pair (3 float4) */
 } SlmFwdArgs;
 
 /* per-gaussian backward chain */
@@ -290,10 +281,11 @@ int slm_apply_jt_runs(const SlmTileArgs* a, cudaStream_t s);
 /* fused apply_jt(weight_residuals(apply_j(p))) first half, tile by tile: u
  * stays in shared memory, the cache is streamed from HBM once */
 int slm_jtwj_runs(const SlmTileArgs* a, cudaStream_t s);
-/* static run parameter records for the J^T-only mode, and the per-tile chunk
- * table (fill=0: counts per tile, fill=1: chunk_run) + the per-chunk J^T
- * schedule (runs by decreasing length, slm_chunk_perm) */
-int slm_run_params(const SlmTileArgs* a, long long n_runs, float* out, cudaStream_t s);
+/* static run records (once per cache): centre relative to the tile, conic,
+ * 1/opacity, pair-run slot, pair; and the per-tile chunk table (fill=0:
+ * counts per tile, fill=1: chunk_run) + the per-chunk J^T schedule (runs by
+ * decreasing length, slm_chunk_perm) */
+int slm_run_static(const SlmTileArgs* a, long long n_runs, const int* run_slot, float* out, cudaStream_t s);
 int slm_tile_chunks(const int* tile_run_off, int n_tiles, const long long* run_start, const int* tile_chunk_off,
                     int* out, uint8_t* chunk_perm, int fill, cudaStream_t s);
 int slm_chunk_perm(const int* chunk_run, long long n_chunks, const long long* run_start, uint8_t* chunk_perm,
@@ -304,10 +296,9 @@ int slm_pair_tables(const float* xs, long long G, int sh_degree, const int* pair
                     const SlmCamera* cams, int n_pairs, float* tab, cudaStream_t s);
 int slm_diag_runs(const SlmTileArgs* a, cudaStream_t s);
 /* the same 14 sums per run on the streaming kernel, written in pair-run-slot
- * order (run records from slm_run_params, a->ptab from slm_pair_tables) */
+ * order (a->ptab from slm_pair_tables) */
 int slm_diag_stream(const SlmTileArgs* a, cudaStream_t s);
-/* forward chain m = dy/dx p per pair (jacobian.py:434-443), written as the
- * 64-byte parameter record of every run of the pair */
+/* forward chain m = dy/dx p per pair (jacobian.py:434-443), 48 B per pair */
 int slm_pair_forward(const SlmFwdArgs* a, int sh_degree, cudaStream_t s);
 /* per-pair sums of run partials (d = 9 J^T partials or 14 diag sums) */
 int slm_pair_sum(const int* pair_run_off, const int* pair_runs, int n_pairs, const float* run_acc, int d,

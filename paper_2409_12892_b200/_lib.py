@@ -15,7 +15,8 @@ import torch
 from .errors import CacheOrderError, ImageSizeError, LayoutError, SplatLMError
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libsplatlm_b200.so"
+# SLM_LIB overrides the library path (A/B builds of tuning variants)
+LIB_PATH = Path(os.environ["SLM_LIB"]) if os.environ.get("SLM_LIB") else _HERE / "libsplatlm_b200.so"
 
 c_vp = C.c_void_p
 c_ll = C.c_longlong
@@ -59,7 +60,7 @@ class SlmResidArgs(C.Structure):
 class SlmTileArgs(C.Structure):
     _fields_ = [("views", c_vp), ("view_tile_base", c_vp), ("n_views", c_i), ("n_tiles", c_i),
                 ("tile_run_off", c_vp), ("tile_chunk_off", c_vp), ("chunk_run", c_vp), ("chunk_perm", c_vp), ("run_slot", c_vp),
-                ("run_start", c_vp), ("run_q", c_vp), ("run_tile", c_vp), ("run_par", c_vp),
+                ("run_start", c_vp), ("run_q", c_vp), ("run_tile", c_vp), ("run_static", c_vp), ("pm", c_vp),
                 ("geo", c_vp), ("ptab", c_vp),
                 ("rec4", c_vp), ("d2", c_vp), ("pix", c_vp),
                 ("gradr", c_vp), ("u", c_vp), ("u_out", c_vp), ("out", c_vp)]
@@ -67,9 +68,7 @@ class SlmTileArgs(C.Structure):
 
 class SlmFwdArgs(C.Structure):
     _fields_ = [("xs", c_vp), ("G", c_ll), ("pair_gid", c_vp), ("pair_vm", c_vp), ("cams", c_vp), ("n_pairs", c_i),
-                ("p", c_vp), ("sa", c_ll), ("sg", c_ll), ("geo", c_vp), ("pair_run_off", c_vp), ("pair_runs", c_vp),
-                ("run_tile", c_vp), ("views", c_vp), ("run_par", c_vp), ("pm", c_vp), ("run_q", c_vp),
-                ("run_slot", c_vp), ("n_runs", c_ll)]
+                ("p", c_vp), ("sa", c_ll), ("sg", c_ll), ("pm", c_vp)]
 
 
 class SlmBackArgs(C.Structure):
@@ -120,7 +119,7 @@ _SIGS = {
     "slm_apply_j": (c_i, [c_vp, c_vp]),
     "slm_apply_jt_runs": (c_i, [c_vp, c_vp]),
     "slm_jtwj_runs": (c_i, [c_vp, c_vp]),
-    "slm_run_params": (c_i, [c_vp, c_ll, c_vp, c_vp]),
+    "slm_run_static": (c_i, [c_vp, c_ll, c_vp, c_vp, c_vp]),
     "slm_chunk_perm": (c_i, [c_vp, c_ll, c_vp, c_vp, c_vp]),
     "slm_tile_chunks": (c_i, [c_vp, c_i, c_vp, c_vp, c_vp, c_vp, c_i, c_vp]),
     "slm_pair_tables": (c_i, [c_vp, c_ll, c_i, c_vp, c_vp, c_vp, c_i, c_vp, c_vp]),

@@ -156,66 +156,10 @@ __device__ __forceinline__ void pair_tab(const float* __restrict__ xs, long long
   T.dopa = o * (Rt(1) - o);
 }
 
-// Forward chain of applyJ (ref: jacobian.py:434-443) fused with the per-run
-// parameter records of the product kernel: per pair, m = dy/dx p (9 numbers),
-// then one 64-byte record per run of the pair (pairs are numbered (gid, view),
-// so consecutive threads share the gaussian's parameters):
-//   P[0..1] splat centre minus the tile's pixel-centre origin, P[2..4] conic,
-//   P[5] inv_o * m_opa, P[6..10] m_mu0, m_mu1, m_cov0/2, m_cov1, m_cov2/2,
-//   P[11..13] m_col, P[14] inv_o, P[15] the run's slot in pair_runs (int bits).
-// p is read with strides so both layouts work: p[a * sa + g * sg].
-template <int K>
-__global__ void __launch_bounds__(128) k_pair_forward(SlmFwdArgs A) {
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < A.n_pairs; q += gridDim.x * blockDim.x) {
-    const long long g = A.pair_gid[q];
-    const uint32_t vm = A.pair_vm[q];
-    const long long sa = A.sa, sg = A.sg;
-    const float* __restrict__ p = A.p;
-    Tab<K> T;
-    pair_tab<K>(A.xs, A.G, g, A.cams[vm & 0xffffu], vm >> 16, T);
-    float pg[11];
-#pragma unroll
-    for (int a = 0; a < 11; ++a) pg[a] = p[a * sa + g * sg];
-    float mmu0 = 0.f, mmu1 = 0.f, mc[3] = {0.f, 0.f, 0.f}, mcol[3];
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      mmu0 += T.dmu[0][j] * pg[j];
-      mmu1 += T.dmu[1][j] * pg[j];
-    }
-#pragma unroll
-    for (int k = 0; k < 3; ++k)
-#pragma unroll
-      for (int j = 0; j < 10; ++j) mc[k] += T.dcov[k][j] * pg[j];
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      float s = 0.f;
-#pragma unroll
-      for (int k = 0; k < K; ++k) s += T.Y[k] * p[(11 + ch * K + k) * sa + g * sg];
-      mcol[ch] = T.dcol[ch][0] * pg[0] + T.dcol[ch][1] * pg[1] + T.dcol[ch][2] * pg[2] + T.mask[ch] * s;
-    }
-    const float mopa = T.dopa * pg[10];
-    const SlmPairGeo ge = A.geo[q];
-    const SlmView vw = A.views[vm & 0xffffu];
-    const int tiles_x = (vw.W + SLM_TILE - 1) / SLM_TILE;
-    const float4 r1 = make_float4(ge.kc, ge.inv_o * mopa, mmu0, mmu1);
-    const float4 r2 = make_float4(0.5f * mc[0], mc[1], 0.5f * mc[2], mcol[0]);
-    for (int rr = A.pair_run_off[q]; rr < A.pair_run_off[q + 1]; ++rr) {
-      const int r = A.pair_runs[rr];
-      const int lt = (int)(A.run_tile[r] & 0xffffffu);
-      const double ox = (double)((lt % tiles_x) * SLM_TILE) + 0.5, oy = (double)((lt / tiles_x) * SLM_TILE) + 0.5;
-      float4* o = reinterpret_cast<float4*>(A.run_par + (size_t)r * 16);
-      o[0] = make_float4((float)(ge.mx - ox), (float)(ge.my - oy), ge.ka, ge.kb);
-      o[1] = r1;
-      o[2] = r2;
-      o[3] = make_float4(mcol[1], mcol[2], ge.inv_o, __int_as_float(rr));
-    }
-  }
-}
-
-// Split form of the forward (selected when SlmFwdArgs.pm != NULL):
-// k_pair_m: thread per pair, m = dy/dx p packed as 3 float4 (48 B, contiguous)
-// k_run_records: thread per run, gathers its pair's geometry and m and writes
-// the 64-byte record at its own (coalesced) position.
+// Forward chain of applyJ (ref: jacobian.py:434-443): thread per pair (pairs
+// are (gid, view)-numbered, so neighbouring threads share the gaussian's
+// parameters), m = dy/dx p packed as 3 float4 (48 B).  The product kernel's
+// producer warp gathers it per run (cp.async) next to the static run records.
 template <int K>
 __global__ void __launch_bounds__(128) k_pair_m(SlmFwdArgs A) {
   float4* __restrict__ pm = reinterpret_cast<float4*>(A.pm);
@@ -251,25 +195,5 @@ __global__ void __launch_bounds__(128) k_pair_m(SlmFwdArgs A) {
     pm[(size_t)q * 3 + 0] = make_float4(T.dopa * pg[10], mmu0, mmu1, 0.5f * mc[0]);
     pm[(size_t)q * 3 + 1] = make_float4(mc[1], 0.5f * mc[2], mcol[0], mcol[1]);
     pm[(size_t)q * 3 + 2] = make_float4(mcol[2], 0.f, 0.f, 0.f);
-  }
-}
-
-static __global__ void __launch_bounds__(256) k_run_records(SlmFwdArgs A) {
-  const float4* __restrict__ pm = reinterpret_cast<const float4*>(A.pm);
-  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < A.n_runs;
-       r += (long long)gridDim.x * blockDim.x) {
-    const int q = A.run_q[r];
-    const uint32_t tg = A.run_tile[r];
-    const SlmView vw = A.views[tg >> 24];
-    const int lt = (int)(tg & 0xffffffu);
-    const int tiles_x = (vw.W + SLM_TILE - 1) / SLM_TILE;
-    const double ox = (double)((lt % tiles_x) * SLM_TILE) + 0.5, oy = (double)((lt / tiles_x) * SLM_TILE) + 0.5;
-    const SlmPairGeo ge = A.geo[q];
-    const float4 m0 = pm[(size_t)q * 3], m1 = pm[(size_t)q * 3 + 1], m2 = pm[(size_t)q * 3 + 2];
-    float4* o = reinterpret_cast<float4*>(A.run_par + (size_t)r * 16);
-    o[0] = make_float4((float)(ge.mx - ox), (float)(ge.my - oy), ge.ka, ge.kb);
-    o[1] = make_float4(ge.kc, ge.inv_o * m0.x, m0.y, m0.z);
-    o[2] = make_float4(m0.w, m1.x, m1.y, m1.z);
-    o[3] = make_float4(m1.w, m2.x, ge.inv_o, __int_as_float(A.run_slot[r]));
   }
 }

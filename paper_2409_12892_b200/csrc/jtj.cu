@@ -490,23 +490,13 @@ int slm_fwd_args_size() { return (int)sizeof(SlmFwdArgs); }
 
 int slm_pair_forward(const SlmFwdArgs* a, int sh_degree, cudaStream_t st) {
   if (a->n_pairs <= 0) return SLM_OK;
+  if (!a->pm) return SLM_ERR_ARG;
   unsigned b = slm_blocks(a->n_pairs, 128, 1LL << 30);
-  if (a->pm) {  // split form: per-pair m, then coalesced per-run records
-    switch (sh_degree) {
-      case 0: k_pair_m<1><<<b, 128, 0, st>>>(*a); break;
-      case 1: k_pair_m<4><<<b, 128, 0, st>>>(*a); break;
-      case 2: k_pair_m<9><<<b, 128, 0, st>>>(*a); break;
-      case 3: k_pair_m<16><<<b, 128, 0, st>>>(*a); break;
-      default: return SLM_ERR_ARG;
-    }
-    if (a->n_runs > 0) k_run_records<<<slm_blocks(a->n_runs, 256, 1LL << 30), 256, 0, st>>>(*a);
-    return slm_cuda_status();
-  }
   switch (sh_degree) {
-    case 0: k_pair_forward<1><<<b, 128, 0, st>>>(*a); break;
-    case 1: k_pair_forward<4><<<b, 128, 0, st>>>(*a); break;
-    case 2: k_pair_forward<9><<<b, 128, 0, st>>>(*a); break;
-    case 3: k_pair_forward<16><<<b, 128, 0, st>>>(*a); break;
+    case 0: k_pair_m<1><<<b, 128, 0, st>>>(*a); break;
+    case 1: k_pair_m<4><<<b, 128, 0, st>>>(*a); break;
+    case 2: k_pair_m<9><<<b, 128, 0, st>>>(*a); break;
+    case 3: k_pair_m<16><<<b, 128, 0, st>>>(*a); break;
     default: return SLM_ERR_ARG;
   }
   return slm_cuda_status();

@@ -25,9 +25,15 @@
 
 #define NW 8
 #define NT (32 * (NW + 1))
-#define CH 1024          // max entries per chunk
+#ifndef SLM_CH
+#define SLM_CH 1024
+#endif
+#ifndef SLM_NS
+#define SLM_NS 3
+#endif
+#define CH SLM_CH        // max entries per chunk
 #define CR 32            // max runs per chunk
-#define NS 3             // ring stages
+#define NS SLM_NS        // ring stages
 #define PAR 16           // floats per run parameter record
 #define TMETA 64         // producer chunk-metadata window
 
@@ -42,18 +48,23 @@
 #define ST_R4 (CH * 16)
 #define ST_D2 ((CH + 8) * 4)
 #define ST_PIX (CH + 32)
-#define ST_PAR (CR * PAR * 4)
+#define ST_PST (CR * 32)   // static run records (TMA)
+#define ST_PDY (CR * 48)   // per-product pair m, gathered per run (cp.async)
+#define ST_PAR (ST_PST + ST_PDY)
 #define ST_RS ((CR + 4) * 8)
 #define ST_PERM 32
 #define ST_HDR 16
 #define OFF_D2 ST_R4
 #define OFF_PIX (OFF_D2 + ST_D2)
 #define OFF_PAR (OFF_PIX + ST_PIX)
+#define OFF_PST OFF_PAR
+#define OFF_PDY (OFF_PAR + ST_PST)
 #define OFF_RS (OFF_PAR + ST_PAR)
 #define OFF_PERM (OFF_RS + ST_RS)
 #define OFF_HDR (OFF_PERM + ST_PERM)
 #define ST_BYTES (OFF_HDR + ST_HDR)
-static_assert(OFF_D2 % 16 == 0 && OFF_PIX % 16 == 0 && OFF_PAR % 16 == 0 && OFF_RS % 16 == 0 && OFF_PERM % 16 == 0 &&
+static_assert(OFF_D2 % 16 == 0 && OFF_PIX % 16 == 0 && OFF_PAR % 16 == 0 && OFF_PDY % 16 == 0 && OFF_RS % 16 == 0 &&
+                  OFF_PERM % 16 == 0 &&
                   OFF_HDR % 16 == 0 && ST_BYTES % 16 == 0,
               "stage sections must stay 16-byte aligned for cp.async.bulk");
 
@@ -94,6 +105,13 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+// arrive on the mbarrier once this thread's prior cp.async copies have landed
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory"); }
 
 __device__ __forceinline__ int view_of_tile(const int* __restrict__ vtb, int n_views, int t) {
@@ -103,11 +121,15 @@ __device__ __forceinline__ int view_of_tile(const int* __restrict__ vtb, int n_v
 }
 
 // ---------------------------------------------------------------------------
-// static run parameter records for the J^T-only mode (centre relative to the
-// tile origin, conic, inv_o; the forward-chain slots are zero).  The J and
-// fused modes get full records from slm_pair_forward (chain.cuh).
+// static run records (once per cache; the scene is fixed during a solve):
+//   (p0, p1, ka, kb) splat centre relative to the tile's pixel-centre origin
+//   and conic, (kc, inv_o, slot, pair) -- slot = the run's position in
+//   pair_runs (J^T / diag outputs go there), pair = its (gid, view) pair.
+// The per-product forward chain m of the run's pair is gathered per chunk by
+// the producer warp (cp.async from the per-pair m of slm_pair_forward).
 // ---------------------------------------------------------------------------
-__global__ void k_run_params(SlmTileArgs A, long long n_runs, float* __restrict__ out) {
+__global__ void k_run_static(SlmTileArgs A, long long n_runs, const int* __restrict__ run_slot,
+                             float* __restrict__ out) {
   for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n_runs;
        r += (long long)gridDim.x * blockDim.x) {
     const uint32_t tg = A.run_tile[r];
@@ -115,12 +137,11 @@ __global__ void k_run_params(SlmTileArgs A, long long n_runs, float* __restrict_
     const int lt = (int)(tg & 0xffffffu);
     const int tiles_x = (vw.W + SLM_TILE - 1) / SLM_TILE;
     const double ox = (double)((lt % tiles_x) * SLM_TILE) + 0.5, oy = (double)((lt / tiles_x) * SLM_TILE) + 0.5;
-    const SlmPairGeo g = A.geo[A.run_q[r]];
-    float4* o = reinterpret_cast<float4*>(out + r * PAR);
+    const int q = A.run_q[r];
+    const SlmPairGeo g = A.geo[q];
+    float4* o = reinterpret_cast<float4*>(out + r * 8);
     o[0] = make_float4((float)(g.mx - ox), (float)(g.my - oy), g.ka, g.kb);
-    o[1] = make_float4(g.kc, __int_as_float(A.run_q[r]), 0.f, 0.f);  // P[5] = pair (diag mode)
-    o[2] = make_float4(0.f, 0.f, 0.f, 0.f);
-    o[3] = make_float4(0.f, 0.f, g.inv_o, __int_as_float(A.run_slot[r]));
+    o[1] = make_float4(g.kc, g.inv_o, __int_as_float(run_slot[r]), __int_as_float(q));
   }
 }
 
@@ -207,7 +228,7 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], 1 + 32);  // producer lane 0 (expect_tx) + 32 cp.async arrivals
       mbar_init(&empty[s], NW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -237,17 +258,28 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
             tmeta[i] = m;
           }
           __syncwarp();
-          if (lane == 0) {
-            for (int i = 0; i < wn; ++i, ++g) {
-              const int s = (int)(g % NS);
-              if (g >= NS) mbar_wait(&empty[s], ((g / NS) - 1) & 1u);
-              const ChunkMeta m = tmeta[i];
-              uint8_t* st = stage_ptr(ring, s);
+          for (int i = 0; i < wn; ++i, ++g) {
+            const int s = (int)(g % NS);
+            if (g >= NS) mbar_wait(&empty[s], ((g / NS) - 1) & 1u);
+            const ChunkMeta m = tmeta[i];
+            uint8_t* st = stage_ptr(ring, s);
+            // per-run forward-chain m of the run's pair: one lane per run
+            if (A.pm && lane < m.k1 - m.k0) {
+              const int q = A.run_q[m.k0 + lane];
+              const uint8_t* src = reinterpret_cast<const uint8_t*>(A.pm) + (size_t)q * 48;
+              uint8_t* dst = st + OFF_PDY + lane * 48;
+              cp_async16(dst, src);
+              cp_async16(dst + 16, src + 16);
+              cp_async16(dst + 32, src + 32);
+            }
+            cp_async_mbar_arrive(&full[s]);
+            __syncwarp();
+            if (lane == 0) {
               const long long a4 = m.e0 & ~3LL, z4 = (m.e1 + 3) & ~3LL;
               const long long a16 = m.e0 & ~15LL, z16 = (m.e1 + 15) & ~15LL;
               const long long a2 = m.k0 & ~1LL, z2 = (m.k1 + 2) & ~1LL;
               const unsigned b4 = (unsigned)(m.e1 - m.e0) * 16u, bd = (unsigned)(z4 - a4) * 4u;
-              const unsigned bx = (unsigned)(z16 - a16), bp = (unsigned)(m.k1 - m.k0) * PAR * 4u;
+              const unsigned bx = (unsigned)(z16 - a16), bp = (unsigned)(m.k1 - m.k0) * 32u;
               const unsigned br = (unsigned)(z2 - a2) * 8u;
               int* hdr = reinterpret_cast<int*>(st + OFF_HDR);
               hdr[0] = m.k1 - m.k0;
@@ -260,10 +292,11 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
               bulk_g2s(st, A.rec4 + m.e0, b4, &full[s], pol);
               bulk_g2s(st + OFF_D2, A.d2 + a4, bd, &full[s], pol);
               bulk_g2s(st + OFF_PIX, A.pix + a16, bx, &full[s], pol);
-              bulk_g2s(st + OFF_PAR, A.run_par + (size_t)m.k0 * PAR, bp, &full[s], pol);
+              bulk_g2s(st + OFF_PST, A.run_static + (size_t)m.k0 * 8, bp, &full[s], pol);
               bulk_g2s(st + OFF_RS, A.run_start + a2, br, &full[s], pol);
               bulk_g2s(st + OFF_PERM, A.chunk_perm + (size_t)(w0 + i) * 32, ST_PERM, &full[s], pol);
             }
+            __syncwarp();
           }
         }
       }
@@ -304,10 +337,15 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
         const float4* s4 = reinterpret_cast<const float4*>(st);
         const float* sd2 = reinterpret_cast<const float*>(st + OFF_D2) + hdr[3];
         const uint8_t* spx = st + OFF_PIX + (e0 & 15);
-        const float4* PAR4 = reinterpret_cast<const float4*>(st + OFF_PAR);
+        const float4* PST = reinterpret_cast<const float4*>(st + OFF_PST);
+        const float4* PDY = reinterpret_cast<const float4*>(st + OFF_PDY);
         for (int i = warp; i < nr; i += NW) {
-          // q0 = (p0, p1, ka, kb), q1 = (kc, a0, m0, m1), q2 = (m2, m3, m4, c0), q3 = (c1, c2, io, -)
-          const float4 q0 = PAR4[i * 4], q1 = PAR4[i * 4 + 1], q2 = PAR4[i * 4 + 2], q3 = PAR4[i * 4 + 3];
+          // static: q0 = (p0, p1, ka, kb), s1 = (kc, io, slot, pair)
+          // pair m:  d0 = (m_opa, m0, m1, m2), d1 = (m3, m4, c0, c1), d2m = (c2, -, -, -)
+          const float4 q0 = PST[i * 2], s1 = PST[i * 2 + 1];
+          const float4 d0 = PDY[i * 3], d1 = PDY[i * 3 + 1];
+          const float c2m = PDY[i * 3 + 2].x;
+          const float a0 = s1.y * d0.x;
           const int f0 = (int)(rs[i] - e0), n = (int)(rs[i + 1] - rs[i]);
           const float4* pr = s4 + f0;
           const float* pd = sd2 + f0;
@@ -317,12 +355,12 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
             const float d2 = pd[j];
             const int pl = pp[j];
             const float dx = (float)(pl & 15) - q0.x, dy = (float)(pl >> 4) - q0.y;
-            const float e1 = q0.z * dx + q0.w * dy, e2 = q0.w * dx + q1.x * dy;
-            const float da = r.x * (q1.y + e1 * (q1.z + e1 * q2.x + e2 * q2.y) + e2 * (q1.w + e2 * q2.z));
+            const float e1 = q0.z * dx + q0.w * dy, e2 = q0.w * dx + s1.x * dy;
+            const float da = r.x * (a0 + e1 * (d0.y + e1 * d0.w + e2 * d1.x) + e2 * (d0.z + e2 * d1.y));
             float4 a = acc[pl];
-            a.x += fmaf(r.z, da, r.y * q2.w);
-            a.y += fmaf(r.w, da, r.y * q3.x);
-            a.z += fmaf(d2, da, r.y * q3.y);
+            a.x += fmaf(r.z, da, r.y * d1.z);
+            a.y += fmaf(r.w, da, r.y * d1.w);
+            a.z += fmaf(d2, da, r.y * c2m);
             acc[pl] = a;
           }
         }
@@ -372,13 +410,13 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
         float kc = 0.f, io = 0.f;
         float D[DIAG_TAB];
         if (ri != 0xff) {
-          const float4* P4 = reinterpret_cast<const float4*>(st + OFF_PAR) + ri * 4;
+          const float4* P4 = reinterpret_cast<const float4*>(st + OFF_PST) + ri * 2;
           q0 = P4[0];
-          const float4 q1 = P4[1], q3 = P4[3];
-          kc = q1.x;
-          io = q3.z;
-          sl = __float_as_int(q3.w);
-          const float4* tq = reinterpret_cast<const float4*>(A.ptab + (size_t)__float_as_int(q1.y) * DIAG_TAB);
+          const float4 s1 = P4[1];
+          kc = s1.x;
+          io = s1.y;
+          sl = __float_as_int(s1.z);
+          const float4* tq = reinterpret_cast<const float4*>(A.ptab + (size_t)__float_as_int(s1.w) * DIAG_TAB);
 #pragma unroll
           for (int k = 0; k < DIAG_TAB / 4; ++k) {
             const float4 v = __ldg(tq + k);
@@ -490,12 +528,12 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
         float kc = 0.f, io = 0.f;
         int slot = 0;
         if (ri != 0xff) {
-          const float4* P4 = reinterpret_cast<const float4*>(st + OFF_PAR) + ri * 4;
+          const float4* P4 = reinterpret_cast<const float4*>(st + OFF_PST) + ri * 2;
           q0 = P4[0];
-          kc = P4[1].x;
-          const float4 q3 = P4[3];
-          io = q3.z;
-          slot = __float_as_int(q3.w);
+          const float4 s1 = P4[1];
+          kc = s1.x;
+          io = s1.y;
+          slot = __float_as_int(s1.z);
           f0 = (int)(rs[ri] - e0);
           n = (int)(rs[ri + 1] - rs[ri]);
         }
@@ -581,9 +619,9 @@ static int launch_stream(const SlmTileArgs* a, cudaStream_t st) {
 
 extern "C" {
 
-int slm_run_params(const SlmTileArgs* a, long long n_runs, float* out, cudaStream_t st) {
+int slm_run_static(const SlmTileArgs* a, long long n_runs, const int* run_slot, float* out, cudaStream_t st) {
   if (n_runs <= 0) return SLM_OK;
-  k_run_params<<<slm_blocks(n_runs, 256, 1LL << 30), 256, 0, st>>>(*a, n_runs, out);
+  k_run_static<<<slm_blocks(n_runs, 256, 1LL << 30), 256, 0, st>>>(*a, n_runs, run_slot, out);
   return slm_cuda_status();
 }
 
@@ -612,7 +650,7 @@ int slm_chunk_perm(const int* chunk_run, long long n_chunks, const long long* ru
 int slm_apply_j(const SlmTileArgs* a, cudaStream_t st) { return launch_stream<MODE_J | MODE_WRITEU>(a, st); }
 
 // diag(J^T W J) sums per run (14, pair-run-slot order) from a->gradr and the
-// per-pair tables a->ptab; run records must come from slm_run_params
+// per-pair tables a->ptab
 int slm_diag_stream(const SlmTileArgs* a, cudaStream_t st) { return launch_stream<MODE_DIAG>(a, st); }
 
 // J^T partials per run from the per-pixel a->u

@@ -464,14 +464,15 @@ class CacheSet:
         # product scratch
         self.u = torch.empty(self.N * 4, dtype=f32, device=dev)
         self.run_acc = _empty(R * _lib.JT_D, f32, dev)
-        self.run_par = _empty(R * 16, f32, dev)
+        self.run_static = _empty(R * 8, f32, dev)
         self.pacc = _empty(Pn * _lib.DIAG_D, f32, dev)
-        self.split_forward = True
         self.packed_backward = True
         self.warp_g0 = torch.empty((Pn >> 5) + 2, dtype=torch.int32, device=dev)
         self.gm = torch.empty(G * self.P, dtype=torch.float32, device=dev)
         call("slm_warp_bounds", ptr(self.gpo), G, Pn, ptr(self.warp_g0), stream_ptr())
         self.pm = _empty(Pn * 12, f32, dev)
+        call("slm_run_static", _lib.byref(self._tile_args()), R, ptr(self.run_slot), ptr(self.run_static),
+             stream_ptr())
         self._b = None
         self._M = None
 
@@ -482,8 +483,8 @@ class CacheSet:
         return 21 * self.E + 48 * self.R + 36 * self.n_chunks
 
     def pair_forward(self, p: torch.Tensor, gaussian_major: bool = False):
-        """Forward chain m = dy/dx p per pair, written into every run's
-        parameter record (self.run_par) for the J / fused product kernels."""
+        """Forward chain m = dy/dx p per pair into self.pm (48 B per pair); the
+        J / fused product kernels gather it per run."""
         G, P = self.G, self.P
         a = _lib.SlmFwdArgs()
         a.xs, a.G = ptr(self.scene.x32()), G
@@ -491,28 +492,23 @@ class CacheSet:
             self.n_pairs
         a.p = ptr(p)
         a.sa, a.sg = (1, P) if gaussian_major else (G, 1)
-        a.geo, a.pair_run_off, a.pair_runs = ptr(self.pair_geo), ptr(self.pair_run_off), ptr(self.pair_runs)
-        a.run_tile, a.views, a.run_par = ptr(self.run_tile), ptr(self.views_dev), ptr(self.run_par)
-        if self.split_forward:
-            a.pm, a.run_q, a.run_slot, a.n_runs = ptr(self.pm), ptr(self.run_q), ptr(self.run_slot), self.R
+        a.pm = ptr(self.pm)
         call("slm_pair_forward", _lib.byref(a), self.scene.sh_degree, stream_ptr())
 
-    def _tile_args(self) -> _lib.SlmTileArgs:
+    def _tile_args(self, with_m: bool = False) -> _lib.SlmTileArgs:
         a = _lib.SlmTileArgs()
         a.views, a.view_tile_base, a.n_views = ptr(self.views_dev), ptr(self.view_tile_base_dev), self.V
         a.n_tiles = self.n_tiles_total
         a.tile_run_off, a.tile_chunk_off, a.chunk_run = ptr(self.tile_run_off), ptr(self.tile_chunk_off), \
             ptr(self.chunk_run)
         a.chunk_perm, a.run_slot = ptr(self.chunk_perm), ptr(self.run_slot)
-        a.run_start, a.run_q, a.run_tile, a.run_par = ptr(self.run_start), ptr(self.run_q), ptr(self.run_tile), \
-            ptr(self.run_par)
+        a.run_start, a.run_q, a.run_tile, a.run_static = ptr(self.run_start), ptr(self.run_q), ptr(self.run_tile), \
+            ptr(self.run_static)
+        a.pm = ptr(self.pm) if with_m else None
         a.geo = ptr(self.pair_geo)
         a.rec4, a.d2 = ptr(self.rec4), ptr(self.rec_d2)
         a.pix = ptr(self.rec_pix)
         return a
-
-    def _static_run_params(self, a: _lib.SlmTileArgs):
-        call("slm_run_params", _lib.byref(a), self.R, ptr(self.run_par), stream_ptr())
 
     def _backward(self, run_acc, d, out, mode, scale=1.0, p=None, M=None, lam=0.0, dot_part=None, lam_out=True,
                   slot_order=False):
@@ -540,7 +536,7 @@ class CacheSet:
         """u (or u_hat) into self.u from the run records written by pair_forward."""
         if weighted and self.gradr is None:
             raise ValueError("cache was built without residual weights")
-        a = self._tile_args()
+        a = self._tile_args(with_m=True)
         a.gradr = ptr(self.gradr) if weighted else None
         a.u_out = ptr(self.u)
         call("slm_apply_j", _lib.byref(a), stream_ptr())
@@ -550,7 +546,6 @@ class CacheSet:
                      dot_part=None):
         ra = self._tile_args()
         ra.u, ra.out = ptr(u), ptr(self.run_acc)
-        self._static_run_params(ra)
         call("slm_apply_jt_runs", _lib.byref(ra), stream_ptr())
         self._backward(self.run_acc, _lib.JT_D, out, 0, scale, p, M, lam, dot_part, slot_order=True)
         return out
@@ -566,7 +561,7 @@ class CacheSet:
         if self.gradr is None:
             raise ValueError("cache was built without residual weights")
         self.pair_forward(p)
-        a = self._tile_args()
+        a = self._tile_args(with_m=True)
         a.gradr, a.out = ptr(self.gradr), ptr(self.run_acc)
         call("slm_jtwj_runs", _lib.byref(a), stream_ptr())
         self._backward(self.run_acc, _lib.JT_D, out, 0, 1.0, p, M if lam != 0.0 else None, lam, dot_part, lam_out,
@@ -594,7 +589,6 @@ class CacheSet:
                  ptr(self.pair_vm), ptr(self.cams_dev), self.n_pairs, ptr(ptab), stream_ptr())
             ra = self._tile_args()
             ra.ptab, ra.gradr, ra.out = ptr(ptab), ptr(self.gradr), ptr(sums)
-            self._static_run_params(ra)
             call("slm_diag_stream", _lib.byref(ra), stream_ptr())
             M = torch.empty(self.G * self.P, dtype=torch.float32, device=self.device)
             self._backward(sums, _lib.DIAG_D, M, 1, slot_order=True)

@@ -90,7 +90,7 @@ def main():
             t0 = ev()
             cs.pair_forward(p)
             t1 = ev()
-            a = cs._tile_args()
+            a = cs._tile_args(with_m=True)
             a.gradr, a.out = ptr(cs.gradr), ptr(cs.run_acc)
             call("slm_jtwj_runs", _lib.byref(a), stream_ptr())
             t2 = ev()
@@ -102,14 +102,7 @@ def main():
         phases["k_pair_forward"] = t0.elapsed_time(t1)
         phases["k_stream_fused"] = t1.elapsed_time(t2)
         phases["k_backward"] = t2.elapsed_time(t3)
-        cs.split_forward = not cs.split_forward
-        for _ in range(3):
-            t0 = ev()
-            cs.pair_forward(p)
-            t1 = ev()
-        torch.cuda.synchronize()
-        phases["k_pair_forward_alt(split=%d)" % cs.split_forward] = t0.elapsed_time(t1)
-        cs.split_forward = not cs.split_forward
+
         if not args.skip_pcg:
             s0 = ev()
             pcg_run(cs, b, M, 1e-4, cfg["iters"])
