@@ -263,8 +263,8 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
             if (g >= NS) mbar_wait(&empty[s], ((g / NS) - 1) & 1u);
             const ChunkMeta m = tmeta[i];
             uint8_t* st = stage_ptr(ring, s);
-            // per-run forward-chain m of the run's pair: one lane per run
-            if (A.pm && lane < m.k1 - m.k0) {
+            // per-run forward-chain m of the run's pair (J pass only): one lane per run
+            if ((MODE & MODE_J) && pass == 0 && A.pm && lane < m.k1 - m.k0) {
               const int q = A.run_q[m.k0 + lane];
               const uint8_t* src = reinterpret_cast<const uint8_t*>(A.pm) + (size_t)q * 48;
               uint8_t* dst = st + OFF_PDY + lane * 48;
