@@ -258,14 +258,19 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
             tmeta[i] = m;
           }
           __syncwarp();
+          const bool gather = (MODE & MODE_J) && pass == 0 && A.pm;
+          int qn = 0;  // pair of this lane's run in the next chunk (prefetched)
+          if (gather && lane < tmeta[0].k1 - tmeta[0].k0) qn = A.run_q[tmeta[0].k0 + lane];
           for (int i = 0; i < wn; ++i, ++g) {
             const int s = (int)(g % NS);
+            const int q = qn;
+            if (gather && i + 1 < wn && lane < tmeta[i + 1].k1 - tmeta[i + 1].k0)
+              qn = A.run_q[tmeta[i + 1].k0 + lane];
             if (g >= NS) mbar_wait(&empty[s], ((g / NS) - 1) & 1u);
             const ChunkMeta m = tmeta[i];
             uint8_t* st = stage_ptr(ring, s);
             // per-run forward-chain m of the run's pair (J pass only): one lane per run
-            if ((MODE & MODE_J) && pass == 0 && A.pm && lane < m.k1 - m.k0) {
-              const int q = A.run_q[m.k0 + lane];
+            if (gather && lane < m.k1 - m.k0) {
               const uint8_t* src = reinterpret_cast<const uint8_t*>(A.pm) + (size_t)q * 48;
               uint8_t* dst = st + OFF_PDY + lane * 48;
               cp_async16(dst, src);
