@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(128) k_pair_tables(const float* __restrict__ x
     const uint32_t vm = pair_vm[q];
     Tab<K> T;
     pair_tab<K>(xs, G, pair_gid[q], cams[vm & 0xffffu], vm >> 16, T);
-    float* o = tab + (size_t)q * DIAG_TAB;
+    float o[DIAG_TAB];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       o[k * 5 + 0] = T.dmu[0][k];
@@ -74,6 +74,9 @@ __global__ void __launch_bounds__(128) k_pair_tables(const float* __restrict__ x
       for (int j = 0; j < 3; ++j) o[37 + ch * 3 + j] = T.dcol[ch][j];
     o[46] = 0.f;
     o[47] = 0.f;
+    float4* dst = reinterpret_cast<float4*>(tab + (size_t)q * DIAG_TAB);  // 16-byte stores
+#pragma unroll
+    for (int k = 0; k < DIAG_TAB / 4; ++k) dst[k] = make_float4(o[4 * k], o[4 * k + 1], o[4 * k + 2], o[4 * k + 3]);
   }
 }
 

@@ -102,6 +102,31 @@ def ssim_host_tables(H, W, window, sigma):
     return k, cw(H), cw(W)
 
 
+_SSIM_CACHE: dict = {}
+_SCRATCH: dict = {}
+
+
+def _ssim_tables(H, W, window, sigma, dev):
+    """Device copies of the SSIM taps / centre weights, cached per shape."""
+    key = (H, W, window, float(sigma), str(dev))
+    t = _SSIM_CACHE.get(key)
+    if t is None:
+        taps, cwy, cwx = ssim_host_tables(H, W, window, sigma)
+        t = tuple(torch.from_numpy(a).to(dev) for a in (taps, cwy, cwx))
+        _SSIM_CACHE[key] = t
+    return t
+
+
+def _scratch(n, dev):
+    """Reusable fp64 scratch of the residual kernels (stream-ordered reuse)."""
+    key = str(dev)
+    t = _SCRATCH.get(key)
+    if t is None or t.numel() < n:
+        t = torch.empty(max(int(n), 1), dtype=torch.float64, device=dev)
+        _SCRATCH[key] = t
+    return t
+
+
 class PhaseTimer:
     """CUDA-event phase accounting on the current stream: tick(name) charges the
     time since the previous tick to `name`."""
@@ -226,12 +251,9 @@ def residual_pass(frame: ViewFrame, gt: torch.Tensor, loss: LossConfig, gradr: t
         raise ValueError("ground truth must be float32 or float64")
     dev = gt.device
     gt = gt.contiguous()
-    taps, cwy, cwx = ssim_host_tables(H, W, loss.window, loss.sigma)
-    taps_t = torch.from_numpy(taps).to(dev)
-    cwy_t = torch.from_numpy(cwy).to(dev)
-    cwx_t = torch.from_numpy(cwx).to(dev)
+    taps_t, cwy_t, cwx_t = _ssim_tables(H, W, loss.window, loss.sigma, dev)
     need_ssim = loss.mode == "l1ssim" and loss.lambda2 > 0
-    tmp = _empty(H * W * 15 if need_ssim else 1, torch.float64, dev)
+    tmp = _scratch(H * W * 15 if need_ssim else 1, dev)
     blocks = int(min(max((H * W + 255) // 256, 1), 148 * 8))
     part = torch.empty(blocks, dtype=torch.float64, device=dev)
     a = _lib.SlmResidArgs()
