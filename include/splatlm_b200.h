@@ -246,10 +246,24 @@ int slm_runs_emit(const uint32_t* mask, const uint32_t* inst_gid, const int* use
                   const long long* ent_of, long long ibase, long long n, const int* pidx, long long* run_start,
                   int* run_q, uint32_t* run_mask, int* pair_nruns, long long* inst_start, cudaStream_t s);
 int slm_tile_runs(const slm_u2* ranges, int n_tiles, const int* used, const int* run_of, long long ibase, int view,
-                  int* tile_nruns, uint32_t* run_tile, cudaStream_t s);
+                  int* tile_nruns, uint32_t* run_tile, const int* view_tile_base, int n_views, cudaStream_t s);
 int slm_pair_runs(const uint32_t* sorted_gid, const unsigned long long* inst_off, long long G,
                   const uint32_t* post_of_pre, const int* used, const int* run_of, long long ibase, const int* pidx,
-                  const int* pair_run_off, int* pair_runs, cudaStream_t s);
+                  const int* pair_run_off, int* pair_runs, long long n, int batched, cudaStream_t s);
+/* subset-batched projection and binning (all V views of a cache subset per
+ * launch): element v * G + g, sorted value (v << 24) | g, global tiles
+ * view_tile_base[v] + ty * tiles_x + tx */
+int slm_preprocess_views(const double* x, long long G, int sh_degree, const SlmCamera* cams_dev, int V,
+                         const SlmRastCfg* cfg, SlmSplat* out, unsigned long long* depth_key, uint32_t* order_val,
+                         int* err, cudaStream_t s);
+int slm_tile_count_v(const uint32_t* sv, long long n, long long G, const SlmSplat* splats, const SlmView* views,
+                     unsigned long long* n_inst, cudaStream_t s);
+int slm_tile_emit_v(const uint32_t* sv, const unsigned long long* inst_off, long long n, long long G,
+                    const SlmSplat* splats, const SlmView* views, const int* view_tile_base, int rank_bits,
+                    unsigned long long* keys, uint32_t* vals, uint32_t* inst_s_pre, cudaStream_t s);
+long long slm_sort_keys_u32_workspace(long long n);
+int slm_sort_keys_u32(void* ws, long long ws_bytes, const uint32_t* kin, uint32_t* kout, long long n, int begin_bit,
+                      int end_bit, cudaStream_t s);
 
 /* ---- residuals: compute_residuals (residuals.py:249-296) ----------------- */
 int slm_residuals(const SlmResidArgs* a, int blocks, cudaStream_t s);

@@ -13,11 +13,10 @@
 // projection (ref: rasterizer.py:78-165)
 // ---------------------------------------------------------------------------
 template <int K>
-__global__ void k_preprocess(const double* __restrict__ x, long long G, SlmCamera cam, SlmRastCfg cfg,
-                             SlmSplat* __restrict__ out, unsigned long long* __restrict__ depth_key,
-                             uint32_t* __restrict__ order_val, int* __restrict__ err) {
-  long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  for (; g < G; g += (long long)gridDim.x * blockDim.x) {
+__device__ __forceinline__ void preprocess_one(const double* __restrict__ x, long long G, long long g,
+                                               const SlmCamera& cam, const SlmRastCfg& cfg, SlmSplat& s_out,
+                                               unsigned long long& key_out, int* __restrict__ err) {
+  {
     double p0 = x[g], p1 = x[G + g], p2 = x[2 * G + g];
     double qw = x[3 * G + g], qx = x[4 * G + g], qy = x[5 * G + g], qz = x[6 * G + g];
     double l0 = x[7 * G + g], l1 = x[8 * G + g], l2 = x[9 * G + g];
@@ -123,9 +122,33 @@ __global__ void k_preprocess(const double* __restrict__ x, long long G, SlmCamer
     s.x0 = x0; s.x1 = x1; s.y0 = y0; s.y1 = y1;
     s.flags = (valid ? SLM_FLAG_VALID : 0u) | clampbits;
     s.pad = 0;
-    out[g] = s;
-    depth_key[g] = valid ? (unsigned long long)__double_as_longlong(X2) : ~0ull;
+    s_out = s;
+    key_out = valid ? (unsigned long long)__double_as_longlong(X2) : ~0ull;
+  }
+}
+
+template <int K>
+__global__ void k_preprocess(const double* __restrict__ x, long long G, SlmCamera cam, SlmRastCfg cfg,
+                             SlmSplat* __restrict__ out, unsigned long long* __restrict__ depth_key,
+                             uint32_t* __restrict__ order_val, int* __restrict__ err) {
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < G; g += (long long)gridDim.x * blockDim.x) {
+    preprocess_one<K>(x, G, g, cam, cfg, out[g], depth_key[g], err);
     order_val[g] = (uint32_t)g;
+  }
+}
+
+// all views of a subset in one launch: element i = v * G + g, value (v << 24) | g
+template <int K>
+__global__ void k_preprocess_views(const double* __restrict__ x, long long G, const SlmCamera* __restrict__ cams,
+                                   int V, SlmRastCfg cfg, SlmSplat* __restrict__ out,
+                                   unsigned long long* __restrict__ depth_key, uint32_t* __restrict__ order_val,
+                                   int* __restrict__ err) {
+  const long long n = G * V;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int v = (int)(i / G);
+    const long long g = i - (long long)v * G;
+    preprocess_one<K>(x, G, g, cams[v], cfg, out[i], depth_key[i], err);
+    order_val[i] = ((uint32_t)v << 24) | (uint32_t)g;
   }
 }
 
@@ -177,6 +200,56 @@ __global__ void k_tile_emit(const uint32_t* __restrict__ sorted_gid, const unsig
         keys[k] = ((unsigned long long)(ty * tiles_x + tx) << rank_bits) | (unsigned long long)i;
         vals[k] = (uint32_t)k;
         inst_g_pre[k] = g;
+        ++k;
+      }
+  }
+}
+
+// ---- subset-batched binning (all views in one launch each) -----------------
+// sorted element i (view-major, depth order within the view) carries
+// sv = (v << 24) | g; its global splat index is v * G + g; tiles are numbered
+// globally (view_tile_base[v] + ty * tiles_x + tx)
+__device__ __forceinline__ int tiles_x_of(const SlmView& vw) { return (vw.W + SLM_TILE - 1) / SLM_TILE; }
+__device__ __forceinline__ int tiles_y_of(const SlmView& vw) { return (vw.H + SLM_TILE - 1) / SLM_TILE; }
+
+__global__ void k_tile_count_v(const uint32_t* __restrict__ sv, long long n, long long G,
+                               const SlmSplat* __restrict__ splats, const SlmView* __restrict__ views,
+                               unsigned long long* __restrict__ n_inst) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const uint32_t e = sv[i];
+    const int v = (int)(e >> 24);
+    const SlmView vw = views[v];
+    unsigned long long c = 0;
+    int tx0, tx1, ty0, ty1;
+    if (splat_tiles(splats[(long long)v * G + (e & 0xffffffu)], tiles_x_of(vw), tiles_y_of(vw), tx0, tx1, ty0, ty1))
+      c = (unsigned long long)(tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+    n_inst[i] = c;
+  }
+}
+
+__global__ void k_tile_emit_v(const uint32_t* __restrict__ sv, const unsigned long long* __restrict__ inst_off,
+                              long long n, long long G, const SlmSplat* __restrict__ splats,
+                              const SlmView* __restrict__ views, const int* __restrict__ view_tile_base,
+                              int rank_bits, unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals,
+                              uint32_t* __restrict__ inst_s_pre) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long beg = inst_off[i], end = inst_off[i + 1];
+    if (beg == end) continue;
+    const uint32_t e = sv[i];
+    const int v = (int)(e >> 24);
+    const long long gs = (long long)v * G + (e & 0xffffffu);
+    const long long rank = i - (long long)v * G;
+    const SlmView vw = views[v];
+    const int tiles_x = tiles_x_of(vw);
+    int tx0, tx1, ty0, ty1;
+    splat_tiles(splats[gs], tiles_x, tiles_y_of(vw), tx0, tx1, ty0, ty1);
+    unsigned long long k = beg;
+    for (int ty = ty0; ty <= ty1; ++ty)
+      for (int tx = tx0; tx <= tx1; ++tx) {
+        keys[k] = ((unsigned long long)(view_tile_base[v] + ty * tiles_x + tx) << rank_bits) |
+                  (unsigned long long)rank;
+        vals[k] = (uint32_t)k;
+        inst_s_pre[k] = (uint32_t)gs;
         ++k;
       }
   }
@@ -243,19 +316,26 @@ __global__ void k_runs_emit(const uint32_t* __restrict__ mask, const uint32_t* _
   }
 }
 
-// per tile of one view: its run count and each run's (view, tile) tag; one
-// warp per tile (the tile's instances are contiguous)
+// per tile: its run count and each run's (view, tile) tag; one warp per tile
+// (the tile's instances are contiguous).  Tiles are global when
+// view_tile_base != NULL (subset-batched), else local to `view`.
 __global__ void k_tile_runs(const slm_u2* __restrict__ ranges, int n_tiles, const int* __restrict__ used,
                             const int* __restrict__ run_of, long long ibase, int view, int* __restrict__ tile_nruns,
-                            uint32_t* __restrict__ run_tile) {
+                            uint32_t* __restrict__ run_tile, const int* __restrict__ view_tile_base, int n_views) {
   const int lane = threadIdx.x & 31;
   for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n_tiles; t += (gridDim.x * blockDim.x) >> 5) {
     const slm_u2 rg = ranges[t];
+    int vv = view, lt = t;
+    if (view_tile_base) {
+      vv = 0;
+      while (vv + 1 < n_views && view_tile_base[vv + 1] <= t) ++vv;
+      lt = t - view_tile_base[vv];
+    }
     int c = 0;
     for (uint32_t j0 = rg.x; j0 < rg.y; j0 += 32) {
       const uint32_t j = j0 + lane;
       const bool u = j < rg.y && used[ibase + j];
-      if (u) run_tile[run_of[ibase + j]] = ((uint32_t)view << 24) | (uint32_t)t;
+      if (u) run_tile[run_of[ibase + j]] = ((uint32_t)vv << 24) | (uint32_t)lt;
       c += __popc(__ballot_sync(0xffffffffu, u));
     }
     if (lane == 0) tile_nruns[t] = c;
@@ -267,11 +347,13 @@ __global__ void k_tile_runs(const slm_u2* __restrict__ ranges, int n_tiles, cons
 __global__ void k_pair_runs(const uint32_t* __restrict__ sorted_gid, const unsigned long long* __restrict__ inst_off,
                             long long G, const uint32_t* __restrict__ post_of_pre, const int* __restrict__ used,
                             const int* __restrict__ run_of, long long ibase, const int* __restrict__ pidx,
-                            const int* __restrict__ pair_run_off, int* __restrict__ pair_runs) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < G; i += (long long)gridDim.x * blockDim.x) {
+                            const int* __restrict__ pair_run_off, int* __restrict__ pair_runs, long long n,
+                            int batched) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     unsigned long long beg = inst_off[i], end = inst_off[i + 1];
     if (beg == end) continue;
-    const int q = pidx[sorted_gid[i]];
+    const uint32_t e = sorted_gid[i];
+    const int q = batched ? pidx[(long long)(e >> 24) * G + (e & 0xffffffu)] : pidx[e];
     if (q < 0) continue;
     int k = pair_run_off[q];
     for (unsigned long long pre = beg; pre < end; ++pre) {
@@ -474,6 +556,54 @@ int slm_preprocess(const double* x, long long G, int sh_degree, const SlmCamera*
   return slm_cuda_status();
 }
 
+int slm_preprocess_views(const double* x, long long G, int sh_degree, const SlmCamera* cams_dev, int V,
+                         const SlmRastCfg* cfg, SlmSplat* out, unsigned long long* depth_key, uint32_t* order_val,
+                         int* err, cudaStream_t stream) {
+  if (G <= 0 || V <= 0 || G >= (1LL << 24) || V > 255) return SLM_ERR_ARG;
+  unsigned blocks = slm_blocks(G * V, 256);
+  switch (sh_degree) {
+    case 0: k_preprocess_views<1><<<blocks, 256, 0, stream>>>(x, G, cams_dev, V, *cfg, out, depth_key, order_val, err); break;
+    case 1: k_preprocess_views<4><<<blocks, 256, 0, stream>>>(x, G, cams_dev, V, *cfg, out, depth_key, order_val, err); break;
+    case 2: k_preprocess_views<9><<<blocks, 256, 0, stream>>>(x, G, cams_dev, V, *cfg, out, depth_key, order_val, err); break;
+    case 3: k_preprocess_views<16><<<blocks, 256, 0, stream>>>(x, G, cams_dev, V, *cfg, out, depth_key, order_val, err); break;
+    default: return SLM_ERR_ARG;
+  }
+  return slm_cuda_status();
+}
+
+int slm_tile_count_v(const uint32_t* sv, long long n, long long G, const SlmSplat* splats, const SlmView* views,
+                     unsigned long long* n_inst, cudaStream_t stream) {
+  if (n <= 0) return SLM_OK;
+  k_tile_count_v<<<slm_blocks(n, 256), 256, 0, stream>>>(sv, n, G, splats, views, n_inst);
+  return slm_cuda_status();
+}
+
+int slm_tile_emit_v(const uint32_t* sv, const unsigned long long* inst_off, long long n, long long G,
+                    const SlmSplat* splats, const SlmView* views, const int* view_tile_base, int rank_bits,
+                    unsigned long long* keys, uint32_t* vals, uint32_t* inst_s_pre, cudaStream_t stream) {
+  if (n <= 0) return SLM_OK;
+  k_tile_emit_v<<<slm_blocks(n, 256), 256, 0, stream>>>(sv, inst_off, n, G, splats, views, view_tile_base, rank_bits,
+                                                         keys, vals, inst_s_pre);
+  return slm_cuda_status();
+}
+
+// radix sort of u32 keys on bits [begin_bit, end_bit) (stable): the per-view
+// grouping pass after the subset-wide depth sort
+long long slm_sort_keys_u32_workspace(long long n) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n);
+  return (long long)bytes;
+}
+
+int slm_sort_keys_u32(void* ws, long long ws_bytes, const uint32_t* kin, uint32_t* kout, long long n, int begin_bit,
+                      int end_bit, cudaStream_t stream) {
+  if (n <= 0) return SLM_OK;
+  if (n > 0x7fffffffLL) return SLM_ERR_SIZE;
+  size_t bytes = (size_t)ws_bytes;
+  cudaError_t e = cub::DeviceRadixSort::SortKeys(ws, bytes, kin, kout, (int)n, begin_bit, end_bit, stream);
+  return e == cudaSuccess ? SLM_OK : SLM_ERR_CUDA;
+}
+
 // stable (depth, gid) order of the valid splats: CUB radix sort over the
 // fp64 depth bit patterns (positive doubles order like their bits)
 long long slm_sort_pairs_u64_workspace(long long n) {
@@ -534,17 +664,18 @@ int slm_runs_emit(const uint32_t* mask, const uint32_t* inst_gid, const int* use
 }
 
 int slm_tile_runs(const slm_u2* ranges, int n_tiles, const int* used, const int* run_of, long long ibase, int view,
-                  int* tile_nruns, uint32_t* run_tile, cudaStream_t stream) {
+                  int* tile_nruns, uint32_t* run_tile, const int* view_tile_base, int n_views, cudaStream_t stream) {
   k_tile_runs<<<slm_blocks((long long)n_tiles * 32, 256), 256, 0, stream>>>(ranges, n_tiles, used, run_of, ibase, view,
-                                                                             tile_nruns, run_tile);
+                                                                             tile_nruns, run_tile, view_tile_base,
+                                                                             n_views);
   return slm_cuda_status();
 }
 
 int slm_pair_runs(const uint32_t* sorted_gid, const unsigned long long* inst_off, long long G,
                   const uint32_t* post_of_pre, const int* used, const int* run_of, long long ibase, const int* pidx,
-                  const int* pair_run_off, int* pair_runs, cudaStream_t stream) {
-  k_pair_runs<<<slm_blocks(G, 128), 128, 0, stream>>>(sorted_gid, inst_off, G, post_of_pre, used, run_of, ibase, pidx,
-                                                       pair_run_off, pair_runs);
+                  const int* pair_run_off, int* pair_runs, long long n, int batched, cudaStream_t stream) {
+  k_pair_runs<<<slm_blocks(n, 128), 128, 0, stream>>>(sorted_gid, inst_off, G, post_of_pre, used, run_of, ibase, pidx,
+                                                       pair_run_off, pair_runs, n, batched);
   return slm_cuda_status();
 }
 

@@ -339,17 +339,68 @@ class CacheSet:
         self.frames: list[ViewFrame] = []
         self.residual_exports = [] if residual_exports else None
         energy_parts = []
+        # ---- subset-batched projection, (view, depth, gid) order, binning ----
+        VG = V * G
+        tbases, nt = [], 0
+        for c in self.cameras:
+            tbases.append(nt)
+            nt += ((c.width + TILE - 1) // TILE) * ((c.height + TILE - 1) // TILE)
+        self.n_tiles_total = nt
+        self.view_tile_base = tbases + [nt]
+        self.view_tile_base_dev = torch.tensor(self.view_tile_base, dtype=torch.int32, device=dev)
+        splats_all = torch.empty(VG * _lib.SPLAT_BYTES, dtype=torch.uint8, device=dev)
+        keys = torch.empty(VG, dtype=torch.int64, device=dev)
+        vals = torch.empty(VG, dtype=torch.int32, device=dev)
+        call("slm_preprocess_views", ptr(scene.x), G, scene.sh_degree, ptr(self.cams_dev), V, _lib.byref(cfg_s),
+             ptr(splats_all), ptr(keys), ptr(vals), ptr(err), stream_ptr())
+        skeys = torch.empty_like(keys)
+        sv0 = torch.empty_like(vals)
+        sort_u64(keys, skeys, vals, sv0, VG, 0, 64)           # depth (fp64 bits), ties by (view, gid)
+        del keys, vals, skeys
+        sv = torch.empty_like(sv0)
+        ws = _empty(_lib.load().slm_sort_keys_u32_workspace(VG), torch.uint8, dev)
+        call("slm_sort_keys_u32", ptr(ws), ws.numel(), ptr(sv0), ptr(sv), VG, 24, 32, stream_ptr())  # by view (stable)
+        del sv0, ws
+        n_inst = torch.zeros(VG + 1, dtype=torch.int64, device=dev)
+        call("slm_tile_count_v", ptr(sv), VG, G, ptr(splats_all), ptr(self.views_dev), ptr(n_inst), stream_ptr())
+        inst_off = torch.empty_like(n_inst)
+        scan_i64(n_inst, inst_off)
+        del n_inst
+        ni = int(inst_off[VG].item())
+        self.n_inst_total = ni
+        rank_bits = _bits(G)
+        ik = _empty(ni, torch.int64, dev)
+        iv = _empty(ni, torch.int32, dev)
+        ig = _empty(ni, torch.int32, dev)
+        call("slm_tile_emit_v", ptr(sv), ptr(inst_off), VG, G, ptr(splats_all), ptr(self.views_dev),
+             ptr(self.view_tile_base_dev), rank_bits, ptr(ik), ptr(iv), ptr(ig), stream_ptr())
+        sk = torch.empty_like(ik)
+        siv = torch.empty_like(iv)
+        sort_u64(ik, sk, iv, siv, ni, 0, rank_bits + _bits(nt))
+        del ik, iv
+        ranges = torch.empty(2 * nt, dtype=torch.int32, device=dev)
+        call("slm_tile_ranges", ptr(sk), ni, rank_bits, ptr(ranges), nt, stream_ptr())
+        del sk
+        inst_gid = _empty(ni, torch.int32, dev)      # global splat index v * G + g per instance
+        post_of_pre = _empty(ni, torch.int32, dev)
+        call("slm_tile_post", ptr(siv), ptr(ig), ni, ptr(inst_gid), ptr(post_of_pre), stream_ptr())
+        del siv, ig
+        inst_mask = torch.zeros(max(ni, 1) * MASK_WORDS, dtype=torch.int32, device=dev)
+        T.tick("project_sort_bin")
+
+        # ---- COUNT pass + residuals, per view -----------------------------------
         for v, cam in enumerate(self.cameras):
             fr = ViewFrame(cam, self.pix_bases[v])
-            project_and_bin(scene, fr, cfg_s, err)
-            T.tick("project_sort_bin")
             hw = cam.num_pixels
             fr.rgb = torch.empty(hw * 3, dtype=torch.float64, device=dev)
             fr.t_final = torch.empty(hw, dtype=torch.float64, device=dev)
-            fr.inst_mask = torch.zeros(max(fr.n_inst, 1) * MASK_WORDS, dtype=torch.int32, device=dev)
-            a = raster_args(fr, cfg_s)
+            a = _lib.SlmRasterArgs()
+            a.tile_range = off(ranges, 2 * tbases[v])
+            a.inst_gid, a.splats = ptr(inst_gid), ptr(splats_all)
+            a.W, a.H, a.tiles_x = cam.width, cam.height, fr.tiles_x
+            a.pix_base, a.cfg = fr.pix_base, cfg_s
             a.px_count = off(self.px_count, fr.pix_base)
-            a.rgb, a.t_final, a.inst_mask = ptr(fr.rgb), ptr(fr.t_final), ptr(fr.inst_mask)
+            a.rgb, a.t_final, a.inst_mask = ptr(fr.rgb), ptr(fr.t_final), ptr(inst_mask)
             call("slm_raster_count", _lib.byref(a), stream_ptr())
             T.tick("raster_count")
             if have_res:
@@ -367,20 +418,10 @@ class CacheSet:
         self.energies = [float(p.sum().item()) for p in energy_parts] if have_res else None
 
         # ---- instances -> runs ---------------------------------------------
-        ibases, tbases = [], []
-        ni = nt = 0
-        for fr in self.frames:
-            ibases.append(ni)
-            tbases.append(nt)
-            ni += fr.n_inst
-            nt += fr.n_tiles
-        self.n_inst_total, self.n_tiles_total = ni, nt
-        self.view_tile_base = tbases + [nt]
         inst_cnt = torch.zeros(ni + 1, dtype=torch.int64, device=dev)
         inst_used = torch.zeros(ni + 1, dtype=torch.int32, device=dev)
-        for v, fr in enumerate(self.frames):
-            call("slm_inst_count", ptr(fr.inst_mask), ptr(fr.inst_gid), fr.n_inst, off(inst_cnt, ibases[v]),
-                 off(inst_used, ibases[v]), off(self.pair_cnt, v * G), stream_ptr())
+        call("slm_inst_count", ptr(inst_mask), ptr(inst_gid), ni, ptr(inst_cnt), ptr(inst_used), ptr(self.pair_cnt),
+             stream_ptr())
         ent_of = torch.empty_like(inst_cnt)
         scan_i64(inst_cnt, ent_of)
         run_of = torch.empty_like(inst_used)
@@ -390,7 +431,6 @@ class CacheSet:
         del inst_cnt
 
         # ---- pairs (view, gaussian) ------------------------------------------
-        VG = V * G
         cntV = torch.zeros(VG + 1, dtype=torch.int64, device=dev)
         flagV = torch.zeros(VG + 1, dtype=torch.int32, device=dev)
         flagT = torch.zeros(VG + 1, dtype=torch.int32, device=dev)
@@ -409,11 +449,10 @@ class CacheSet:
         self.pair_geo = _empty(Pn * _lib.PAIR_GEO_BYTES, torch.uint8, dev)
         pidx = torch.empty(VG, dtype=torch.int32, device=dev)
         self.gpo = torch.empty(G + 1, dtype=torch.int32, device=dev)
-        splats_all = torch.cat([f.splats for f in self.frames])
         call("slm_pairs_emit", ptr(self.pair_cnt), V, G, ptr(pair_of), ptr(vscan), ptr(tscan), ptr(splats_all),
              ptr(self.pair_off), ptr(self.pair_gid), ptr(self.pair_vm), ptr(self.pair_geo), ptr(pidx), ptr(self.gpo),
              Pn, self.E, stream_ptr())
-        del cntV, flagV, flagT, vscan, pair_of, tscan, splats_all
+        del cntV, flagV, flagT, vscan, pair_of, tscan
 
         # ---- run table, runs per tile, pair -> runs ----------------------------
         R = self.R
@@ -423,13 +462,12 @@ class CacheSet:
         self.run_tile = _empty(R, torch.int32, dev)
         pair_nruns = torch.zeros(Pn + 1, dtype=torch.int32, device=dev)
         tile_nruns = torch.zeros(nt + 1, dtype=torch.int32, device=dev)
-        for v, fr in enumerate(self.frames):
-            fr.inst_start = _empty(fr.n_inst, torch.int64, dev)
-            call("slm_runs_emit", ptr(fr.inst_mask), ptr(fr.inst_gid), ptr(inst_used), ptr(run_of), ptr(ent_of),
-                 ibases[v], fr.n_inst, off(pidx, v * G), ptr(self.run_start), ptr(self.run_q), ptr(self.run_mask),
-                 ptr(pair_nruns), ptr(fr.inst_start), stream_ptr())
-            call("slm_tile_runs", ptr(fr.ranges), fr.n_tiles, ptr(inst_used), ptr(run_of), ibases[v], v,
-                 off(tile_nruns, tbases[v]), ptr(self.run_tile), stream_ptr())
+        inst_start = _empty(ni, torch.int64, dev)
+        call("slm_runs_emit", ptr(inst_mask), ptr(inst_gid), ptr(inst_used), ptr(run_of), ptr(ent_of), 0, ni,
+             ptr(pidx), ptr(self.run_start), ptr(self.run_q), ptr(self.run_mask), ptr(pair_nruns), ptr(inst_start),
+             stream_ptr())
+        call("slm_tile_runs", ptr(ranges), nt, ptr(inst_used), ptr(run_of), 0, 0, ptr(tile_nruns), ptr(self.run_tile),
+             ptr(self.view_tile_base_dev), V, stream_ptr())
         self.run_start[R:].fill_(self.E)
         self.tile_run_off = torch.empty_like(tile_nruns)
         scan_i32(tile_nruns, self.tile_run_off)
@@ -451,9 +489,9 @@ class CacheSet:
         self.pair_run_off = torch.empty_like(pair_nruns)
         scan_i32(pair_nruns, self.pair_run_off)
         self.pair_runs = _empty(R, torch.int32, dev)
-        for v, fr in enumerate(self.frames):
-            call("slm_pair_runs", ptr(fr.sorted_gid), ptr(fr.inst_off), G, ptr(fr.post_of_pre), ptr(inst_used),
-                 ptr(run_of), ibases[v], off(pidx, v * G), ptr(self.pair_run_off), ptr(self.pair_runs), stream_ptr())
+        call("slm_pair_runs", ptr(sv), ptr(inst_off), G, ptr(post_of_pre), ptr(inst_used), ptr(run_of), 0, ptr(pidx),
+             ptr(self.pair_run_off), ptr(self.pair_runs), VG, 1, stream_ptr())
+        del sv, inst_off, post_of_pre
         del pidx, pair_nruns, tile_nruns, inst_used, run_of, ent_of
         # slot of each run in pair_runs: J^T kernels write run partials there so
         # the per-gaussian backward reads its pairs' runs contiguously
@@ -473,16 +511,18 @@ class CacheSet:
         self.rec_d2 = torch.zeros(E + 16, dtype=f32, device=dev)
         self.rec_pix = torch.zeros(E + 16, dtype=torch.uint8, device=dev)
         for v, fr in enumerate(self.frames):
-            a = raster_args(fr, cfg_s)
-            a.rgb, a.inst_mask, a.inst_start = ptr(fr.rgb), ptr(fr.inst_mask), ptr(fr.inst_start)
+            cam = fr.cam
+            a = _lib.SlmRasterArgs()
+            a.tile_range = off(ranges, 2 * tbases[v])
+            a.inst_gid, a.splats = ptr(inst_gid), ptr(splats_all)
+            a.W, a.H, a.tiles_x = cam.width, cam.height, fr.tiles_x
+            a.pix_base, a.cfg = fr.pix_base, cfg_s
+            a.rgb, a.inst_mask, a.inst_start = ptr(fr.rgb), ptr(inst_mask), ptr(inst_start)
             a.rec4, a.rec_d2 = ptr(self.rec4), ptr(self.rec_d2)
             a.rec_pix = ptr(self.rec_pix)
             call("slm_raster_fill", _lib.byref(a), stream_ptr())
             T.tick("raster_fill")
-        for fr in self.frames:  # keep the images (exports); binning state is no longer needed
-            fr.inst_gid = fr.ranges = fr.post_of_pre = fr.inst_off = fr.sorted_gid = None
-            fr.inst_mask = fr.inst_start = None
-        self.view_tile_base_dev = torch.tensor(self.view_tile_base, dtype=torch.int32, device=dev)
+        del inst_mask, inst_start, inst_gid, ranges, splats_all
         # product scratch
         self.u = torch.empty(self.N * 4, dtype=f32, device=dev)
         self.run_acc = _empty(R * _lib.JT_D, f32, dev)
