@@ -137,18 +137,20 @@ __global__ void k_preprocess(const double* __restrict__ x, long long G, SlmCamer
   }
 }
 
-// all views of a subset in one launch: element i = v * G + g, value (v << 24) | g
+// all views of a subset in one launch: thread per gaussian looping over the
+// views (its parameters stay in L1 across views), element i = v * G + g,
+// value (v << 24) | g
 template <int K>
 __global__ void k_preprocess_views(const double* __restrict__ x, long long G, const SlmCamera* __restrict__ cams,
                                    int V, SlmRastCfg cfg, SlmSplat* __restrict__ out,
                                    unsigned long long* __restrict__ depth_key, uint32_t* __restrict__ order_val,
                                    int* __restrict__ err) {
-  const long long n = G * V;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const int v = (int)(i / G);
-    const long long g = i - (long long)v * G;
-    preprocess_one<K>(x, G, g, cams[v], cfg, out[i], depth_key[i], err);
-    order_val[i] = ((uint32_t)v << 24) | (uint32_t)g;
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < G; g += (long long)gridDim.x * blockDim.x) {
+    for (int v = 0; v < V; ++v) {
+      const long long i = (long long)v * G + g;
+      preprocess_one<K>(x, G, g, cams[v], cfg, out[i], depth_key[i], err);
+      order_val[i] = ((uint32_t)v << 24) | (uint32_t)g;
+    }
   }
 }
 
@@ -560,12 +562,12 @@ int slm_preprocess_views(const double* x, long long G, int sh_degree, const SlmC
                          const SlmRastCfg* cfg, SlmSplat* out, unsigned long long* depth_key, uint32_t* order_val,
                          int* err, cudaStream_t stream) {
   if (G <= 0 || V <= 0 || G >= (1LL << 24) || V > 255) return SLM_ERR_ARG;
-  unsigned blocks = slm_blocks(G * V, 256);
+  unsigned blocks = slm_blocks(G, 128, 1LL << 30);
   switch (sh_degree) {
-    case 0: k_preprocess_views<1><<<blocks, 256, 0, stream>>>(x, G, cams_dev, V, *cfg, out, depth_key, order_val, err); break;
-    case 1: k_preprocess_views<4><<<blocks, 256, 0, stream>>>(x, G, cams_dev, V, *cfg, out, depth_key, order_val, err); break;
-    case 2: k_preprocess_views<9><<<blocks, 256, 0, stream>>>(x, G, cams_dev, V, *cfg, out, depth_key, order_val, err); break;
-    case 3: k_preprocess_views<16><<<blocks, 256, 0, stream>>>(x, G, cams_dev, V, *cfg, out, depth_key, order_val, err); break;
+    case 0: k_preprocess_views<1><<<blocks, 128, 0, stream>>>(x, G, cams_dev, V, *cfg, out, depth_key, order_val, err); break;
+    case 1: k_preprocess_views<4><<<blocks, 128, 0, stream>>>(x, G, cams_dev, V, *cfg, out, depth_key, order_val, err); break;
+    case 2: k_preprocess_views<9><<<blocks, 128, 0, stream>>>(x, G, cams_dev, V, *cfg, out, depth_key, order_val, err); break;
+    case 3: k_preprocess_views<16><<<blocks, 128, 0, stream>>>(x, G, cams_dev, V, *cfg, out, depth_key, order_val, err); break;
     default: return SLM_ERR_ARG;
   }
   return slm_cuda_status();
