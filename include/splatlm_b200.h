@@ -108,6 +108,12 @@ typedef struct {
   long long* trav_gid;
   double* trav_alpha;
   double* trav_T;
+  /* batched mode (views != NULL): one launch over all n_tiles tiles of the
+   * subset's views; tile_range / px_count / rgb / t_final are subset-global */
+  const SlmView* views;
+  const int* view_tile_base;
+  int n_views;
+  int n_tiles;
 } SlmRasterArgs;
 
 /* residual weights (residuals.py:249-296) */

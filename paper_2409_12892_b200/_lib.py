@@ -45,7 +45,7 @@ class SlmRasterArgs(C.Structure):
                 ("px_count", c_vp), ("rgb", c_vp), ("t_final", c_vp), ("inst_mask", c_vp),
                 ("inst_start", c_vp), ("rec4", c_vp), ("rec_d2", c_vp), ("rec_pix", c_vp),
                 ("pix_off", c_vp), ("view_entry_base", c_ll), ("trav_gid", c_vp), ("trav_alpha", c_vp),
-                ("trav_T", c_vp)]
+                ("trav_T", c_vp), ("views", c_vp), ("view_tile_base", c_vp), ("n_views", c_i), ("n_tiles", c_i)]
 
 
 class SlmResidArgs(C.Structure):

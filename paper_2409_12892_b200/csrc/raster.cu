@@ -402,14 +402,26 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
   __shared__ uint8_t s_pre[FILL ? RB * RW : 1];     // FILL: keepers in lower warps, per instance
   __shared__ uint8_t s_list[RW][RB];                // per warp: batch instances that concern it
 
-  const int tiles_x = A.tiles_x;
-  const int tile = blockIdx.x;
+  // batched (A.views != NULL): one launch over the tiles of all the subset's
+  // views; pixel buffers are subset-global (pix_base + y * W + x)
+  int W = A.W, H = A.H, tiles_x = A.tiles_x, tile = blockIdx.x;
+  long long pb = 0;
+  if (A.views) {
+    int v = 0;
+    while (v + 1 < A.n_views && A.view_tile_base[v + 1] <= tile) ++v;
+    const SlmView vw = A.views[v];
+    W = vw.W;
+    H = vw.H;
+    tiles_x = (W + SLM_TILE - 1) / SLM_TILE;
+    tile -= A.view_tile_base[v];
+    pb = vw.pix_base;
+  }
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int lx = threadIdx.x % SLM_TILE, ly = threadIdx.x / SLM_TILE;
   const int px = tx * SLM_TILE + lx, py = ty * SLM_TILE + ly;
-  const bool inside = px < A.W && py < A.H;
-  const int pix = py * A.W + px;
-  const uint2 rng = A.tile_range[tile];
+  const bool inside = px < W && py < H;
+  const long long pix = pb + (long long)py * W + px;
+  const uint2 rng = A.tile_range[blockIdx.x];
   const double dxp = (double)px + 0.5, dyp = (double)py + 0.5;
   const double amin = A.cfg.alpha_min, tstop = A.cfg.t_stop, aclamp = A.cfg.alpha_clamp;
   const int lane = threadIdx.x & 31;
@@ -426,7 +438,7 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
     tot0 = A.rgb[(size_t)pix * 3 + 0];
     tot1 = A.rgb[(size_t)pix * 3 + 1];
     tot2 = A.rgb[(size_t)pix * 3 + 2];
-    if (A.trav_gid) e = A.pix_off[A.pix_base + pix];
+    if (A.trav_gid) e = A.pix_off[A.pix_base + pix];  // single-view export only (pb = 0)
   }
 
   for (unsigned base = rng.x; base < rng.y; base += RB) {
@@ -688,16 +700,19 @@ int slm_tile_ranges(const unsigned long long* keys, long long n, int rank_bits, 
   return slm_cuda_status();
 }
 
+static int raster_grid(const RasterArgs* a) {
+  if (a->views) return a->n_tiles;
+  return a->tiles_x * ((a->H + SLM_TILE - 1) / SLM_TILE);
+}
+
 int slm_raster_count(const RasterArgs* a, cudaStream_t stream) {
-  int tiles_y = (a->H + SLM_TILE - 1) / SLM_TILE;
-  k_raster<false><<<a->tiles_x * tiles_y, RB, 0, stream>>>(*a);
+  k_raster<false><<<raster_grid(a), RB, 0, stream>>>(*a);
   return slm_cuda_status();
 }
 
 int slm_raster_fill(const RasterArgs* a, cudaStream_t stream) {
   if (!a->inst_mask) return SLM_ERR_ARG;  // FILL replays the COUNT pass's keep masks
-  int tiles_y = (a->H + SLM_TILE - 1) / SLM_TILE;
-  k_raster<true><<<a->tiles_x * tiles_y, RB, 0, stream>>>(*a);
+  k_raster<true><<<raster_grid(a), RB, 0, stream>>>(*a);
   return slm_cuda_status();
 }
 

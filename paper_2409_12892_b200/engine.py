@@ -388,28 +388,33 @@ class CacheSet:
         inst_mask = torch.zeros(max(ni, 1) * MASK_WORDS, dtype=torch.int32, device=dev)
         T.tick("project_sort_bin")
 
-        # ---- COUNT pass + residuals, per view -----------------------------------
+        # ---- COUNT pass (all views, one launch) + residuals per view -----------
+        self.rgb_all = torch.empty(self.N * 3, dtype=torch.float64, device=dev)
+        self.t_final_all = torch.empty(self.N, dtype=torch.float64, device=dev)
+
+        def batched_args():
+            a = _lib.SlmRasterArgs()
+            a.tile_range, a.inst_gid, a.splats = ptr(ranges), ptr(inst_gid), ptr(splats_all)
+            a.cfg = cfg_s
+            a.views, a.view_tile_base, a.n_views, a.n_tiles = ptr(self.views_dev), ptr(self.view_tile_base_dev), V, nt
+            a.rgb, a.inst_mask = ptr(self.rgb_all), ptr(inst_mask)
+            return a
+        a = batched_args()
+        a.px_count, a.t_final = ptr(self.px_count), ptr(self.t_final_all)
+        call("slm_raster_count", _lib.byref(a), stream_ptr())
+        T.tick("raster_count")
         for v, cam in enumerate(self.cameras):
             fr = ViewFrame(cam, self.pix_bases[v])
             hw = cam.num_pixels
-            fr.rgb = torch.empty(hw * 3, dtype=torch.float64, device=dev)
-            fr.t_final = torch.empty(hw, dtype=torch.float64, device=dev)
-            a = _lib.SlmRasterArgs()
-            a.tile_range = off(ranges, 2 * tbases[v])
-            a.inst_gid, a.splats = ptr(inst_gid), ptr(splats_all)
-            a.W, a.H, a.tiles_x = cam.width, cam.height, fr.tiles_x
-            a.pix_base, a.cfg = fr.pix_base, cfg_s
-            a.px_count = off(self.px_count, fr.pix_base)
-            a.rgb, a.t_final, a.inst_mask = ptr(fr.rgb), ptr(fr.t_final), ptr(inst_mask)
-            call("slm_raster_count", _lib.byref(a), stream_ptr())
-            T.tick("raster_count")
+            fr.rgb = self.rgb_all[fr.pix_base * 3:(fr.pix_base + hw) * 3]
+            fr.t_final = self.t_final_all[fr.pix_base:fr.pix_base + hw]
             if have_res:
                 ex = {} if residual_exports else None
                 energy_parts.append(residual_pass(fr, gts[v], loss, self.gradr, self.cgrad, ex))
                 if residual_exports:
                     self.residual_exports.append(ex)
-                T.tick("residuals")
             self.frames.append(fr)
+        T.tick("residuals")
         e = int(err.item())
         if e & 1:
             raise ValueError("scene contains non-finite parameters")
@@ -510,18 +515,11 @@ class CacheSet:
         self.rec4 = torch.zeros((E + 16) * 4, dtype=f32, device=dev)
         self.rec_d2 = torch.zeros(E + 16, dtype=f32, device=dev)
         self.rec_pix = torch.zeros(E + 16, dtype=torch.uint8, device=dev)
-        for v, fr in enumerate(self.frames):
-            cam = fr.cam
-            a = _lib.SlmRasterArgs()
-            a.tile_range = off(ranges, 2 * tbases[v])
-            a.inst_gid, a.splats = ptr(inst_gid), ptr(splats_all)
-            a.W, a.H, a.tiles_x = cam.width, cam.height, fr.tiles_x
-            a.pix_base, a.cfg = fr.pix_base, cfg_s
-            a.rgb, a.inst_mask, a.inst_start = ptr(fr.rgb), ptr(inst_mask), ptr(inst_start)
-            a.rec4, a.rec_d2 = ptr(self.rec4), ptr(self.rec_d2)
-            a.rec_pix = ptr(self.rec_pix)
-            call("slm_raster_fill", _lib.byref(a), stream_ptr())
-            T.tick("raster_fill")
+        a = batched_args()
+        a.inst_start = ptr(inst_start)
+        a.rec4, a.rec_d2, a.rec_pix = ptr(self.rec4), ptr(self.rec_d2), ptr(self.rec_pix)
+        call("slm_raster_fill", _lib.byref(a), stream_ptr())
+        T.tick("raster_fill")
         del inst_mask, inst_start, inst_gid, ranges, splats_all
         # product scratch
         self.u = torch.empty(self.N * 4, dtype=f32, device=dev)
