@@ -255,7 +255,7 @@ int slm_tile_runs(const slm_u2* ranges, int n_tiles, const int* used, const int*
                   int* tile_nruns, uint32_t* run_tile, const int* view_tile_base, int n_views, cudaStream_t s);
 int slm_pair_runs(const uint32_t* sorted_gid, const unsigned long long* inst_off, long long G,
                   const uint32_t* post_of_pre, const int* used, const int* run_of, long long ibase, const int* pidx,
-                  const int* pair_run_off, int* pair_runs, long long n, int batched, cudaStream_t s);
+                  const int* pair_run_off, int* pair_runs, long long n, int batched, int* run_slot, cudaStream_t s);
 /* subset-batched projection and binning (all V views of a cache subset per
  * launch): element v * G + g, sorted value (v << 24) | g, global tiles
  * view_tile_base[v] + ty * tiles_x + tx */

@@ -103,7 +103,7 @@ _SIGS = {
     "slm_inst_count": (c_i, [c_vp, c_vp, c_ll, c_vp, c_vp, c_vp, c_vp]),
     "slm_runs_emit": (c_i, [c_vp, c_vp, c_vp, c_vp, c_vp, c_ll, c_ll, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "slm_tile_runs": (c_i, [c_vp, c_i, c_vp, c_vp, c_ll, c_i, c_vp, c_vp, c_vp, c_i, c_vp]),
-    "slm_pair_runs": (c_i, [c_vp, c_vp, c_ll, c_vp, c_vp, c_vp, c_ll, c_vp, c_vp, c_vp, c_ll, c_i, c_vp]),
+    "slm_pair_runs": (c_i, [c_vp, c_vp, c_ll, c_vp, c_vp, c_vp, c_ll, c_vp, c_vp, c_vp, c_ll, c_i, c_vp, c_vp]),
     "slm_preprocess_views": (c_i, [c_vp, c_ll, c_i, c_vp, c_i, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "slm_tile_count_v": (c_i, [c_vp, c_ll, c_ll, c_vp, c_vp, c_vp, c_vp]),
     "slm_tile_emit_v": (c_i, [c_vp, c_vp, c_ll, c_ll, c_vp, c_vp, c_vp, c_i, c_vp, c_vp, c_vp, c_vp]),

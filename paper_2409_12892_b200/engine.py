@@ -494,16 +494,13 @@ class CacheSet:
         self.pair_run_off = torch.empty_like(pair_nruns)
         scan_i32(pair_nruns, self.pair_run_off)
         self.pair_runs = _empty(R, torch.int32, dev)
+        # run_slot: each run's position in pair_runs (J^T kernels write run
+        # partials there so the backward reads a gaussian's runs contiguously)
+        self.run_slot = torch.empty(max(R, 1), dtype=torch.int32, device=dev)
         call("slm_pair_runs", ptr(sv), ptr(inst_off), G, ptr(post_of_pre), ptr(inst_used), ptr(run_of), 0, ptr(pidx),
-             ptr(self.pair_run_off), ptr(self.pair_runs), VG, 1, stream_ptr())
+             ptr(self.pair_run_off), ptr(self.pair_runs), VG, 1, ptr(self.run_slot), stream_ptr())
         del sv, inst_off, post_of_pre
         del pidx, pair_nruns, tile_nruns, inst_used, run_of, ent_of
-        # slot of each run in pair_runs: J^T kernels write run partials there so
-        # the per-gaussian backward reads its pairs' runs contiguously
-        self.run_slot = torch.empty(max(R, 1), dtype=torch.int32, device=dev)
-        if R:
-            self.run_slot.index_copy_(0, self.pair_runs[:R].long(),
-                                       torch.arange(R, dtype=torch.int32, device=dev))
         T.tick("runs_pairs")
 
         # ---- FILL phase: run-ordered records ------------------------------------
