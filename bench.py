@@ -209,6 +209,7 @@ def run_ours(args, cfg):
     d2h = scene.param_count * 4
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    out_host = torch.empty(scene.param_count, dtype=torch.float32).pin_memory()
     from paper_2409_12892_b200.scene import GaussianScene
     barrier()
     e0.record(stream)
@@ -218,7 +219,7 @@ def run_ours(args, cfg):
         gd = [g.to(dev, non_blocking=True) for g in gts_host]
         sc = GaussianScene(xs, scene.sh_degree, scene.background)
         r = lm_direction(sc, cams, gd, sched, lam, iters, None, loss, rank, world)
-        out = r.delta.to("cpu", non_blocking=True)
+        out = out_host.copy_(r.delta, non_blocking=True)
         del sc, gd, xs
     e1.record(stream)
     barrier()
