@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(32 * PK_WARPS) k_gauss_backward_packed(SlmBack
   // attribute-major output with the scale / lambda / dot epilogue
   auto flush = [&](long long g, float c0, float c1) {
     float* o = A.gm + (size_t)g * P;
-    o[lane] = c0;
+    if (lane < P) o[lane] = c0;  // P < 32 below SH degree 2
     if (lane + 32 < P) o[lane + 32] = c1;
   };
   for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n_warps; w += (gridDim.x * blockDim.x) >> 5) {

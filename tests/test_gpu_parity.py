@@ -284,3 +284,28 @@ def test_dense_indexing_and_products(dense):
     out = torch.empty(p.size, dtype=torch.float32, device="cuda")
     cs.jtwj(torch.from_numpy(p).float().cuda(), out)
     assert rel(out.cpu().numpy(), O.jtwj(p, dense["osc"], [gv])) < FTOL
+
+
+@pytest.mark.parametrize("degree", [0, 1, 2])
+def test_products_all_sh_degrees(degree):
+    """b, M and J^T W J p at every SH degree (P = 14 .. 38 < 64 exercises the
+    partial-row paths of the per-gaussian backward)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    truth, init, cams, gts = problem(seed=4, G=40, n_views=2, W=24, H=20, degree=degree)
+    osc = oscene(init)
+    gv, b = [], 0
+    for c, gt in zip(cams, gts):
+        oc = ocam(c)
+        rs = O.rasterize(osc, oc)
+        bb, v = O.build_cache(osc, oc, O.residuals(rs["image"], gt), rast=rs)
+        gv.append(O.gaussian_order(v))
+        b = b + bb
+    scene = init.to_device()
+    cs = CacheSet(scene, cams, [torch.from_numpy(g).cuda() for g in gts])
+    assert rel(cs.rhs().cpu().numpy(), b) < FTOL
+    assert rel(cs.diag().cpu().numpy(), sum(O.diag_jtj(osc, v) for v in gv)) < FTOL
+    p = np.random.default_rng(degree).standard_normal(scene.param_count)
+    out = torch.empty(p.size, dtype=torch.float32, device="cuda")
+    cs.jtwj(torch.from_numpy(p).float().cuda(), out)
+    assert rel(out.cpu().numpy(), O.jtwj(p, osc, gv)) < FTOL
