@@ -368,6 +368,7 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
             a.z += fmaf(d2, da, r.y * c2m);
             acc[pl] = a;
           }
+          __syncwarp();  // the next run may update the same pixels from other lanes
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);

@@ -309,3 +309,29 @@ def test_products_all_sh_degrees(degree):
     out = torch.empty(p.size, dtype=torch.float32, device="cuda")
     cs.jtwj(torch.from_numpy(p).float().cuda(), out)
     assert rel(out.cpu().numpy(), O.jtwj(p, osc, gv)) < FTOL
+
+
+def test_determinism_at_scale():
+    """Bitwise run-to-run determinism of b, M and J^T W J p on a C2-sized subset
+    (100k Gaussians, 8 views @ 256^2): the streaming kernel's shared-memory ring
+    is reused many times per CTA here (the small problems above never wrap it)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2409_12892_b200 import synthetic as S
+    from paper_2409_12892_b200.rasterizer import render
+    truth = S.make_synthetic_scene(0, 100_000, 3)
+    init = S.perturb(truth, 1, 0.1)
+    cams = S.make_camera_ring(8, 256, 256)
+    ts = truth.to_device()
+    gts = [render(ts, c, traversals=False).image.float().contiguous() for c in cams]
+    scene = init.to_device()
+    p = torch.randn(scene.param_count, device="cuda", generator=torch.Generator("cuda").manual_seed(7))
+    outs = []
+    for _ in range(2):
+        cs = CacheSet(scene, cams, gts)
+        g = torch.empty_like(p)
+        cs.jtwj(p, g, 1e-4, cs.diag())
+        outs.append((cs.rhs().clone(), cs.diag().clone(), g))
+        del cs
+    for a, b in zip(outs[0], outs[1]):
+        assert torch.equal(a, b)
