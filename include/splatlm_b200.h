@@ -175,6 +175,7 @@ typedef struct {
   const float* p;           /* direction, p[a * sa + g * sg] (either layout) */
   long long sa, sg;
   void* pm;                 /* [P*12] out: m = dy/dx p per pair (3 float4) */
+  const float* gtab;        /* per-gaussian chain constants (slm_gauss_tab) or NULL */
 } SlmFwdArgs;
 
 /* per-gaussian backward chain */
@@ -193,6 +194,7 @@ typedef struct {
   const int* pair_gid;
   long long n_pairs;
   float* gm;                /* packed form: [G*P] gaussian-major scratch */
+  const float* gtab;        /* per-gaussian chain constants (slm_gauss_tab) or NULL */
   float scale;
   const float* p;           /* optional: fp64 partials of p.(out + lam * max(M,1e-12) * p) */
   const float* Mdiag;
@@ -313,7 +315,12 @@ int slm_chunk_perm(const int* chunk_run, long long n_chunks, const long long* ru
 /* diag_jtj (jacobian.py:486-512), first half: per-pair coefficient tables,
  * then 14 sums per run (a->gradr = grad_r_sq, a->ptab = tables) */
 int slm_pair_tables(const float* xs, long long G, int sh_degree, const int* pair_gid, const uint32_t* pair_vm,
-                    const SlmCamera* cams, int n_pairs, float* tab, cudaStream_t s);
+                    const SlmCamera* cams, int n_pairs, float* tab, const float* gtab, cudaStream_t s);
+/* view-independent part of the per-gaussian chain (rotation, scales, the
+ * quaternion-normalisation derivatives, sigma'), slm_gauss_tab_floats() per
+ * gaussian; once per cache (ref: jacobian.py:159-190, 213-240) */
+int slm_gauss_tab(const float* xs, long long G, float* gtab, cudaStream_t s);
+int slm_gauss_tab_floats(void);
 int slm_diag_runs(const SlmTileArgs* a, cudaStream_t s);
 /* the same 14 sums per run on the streaming kernel, written in pair-run-slot
  * order (a->ptab from slm_pair_tables) */

@@ -68,12 +68,12 @@ class SlmTileArgs(C.Structure):
 
 class SlmFwdArgs(C.Structure):
     _fields_ = [("xs", c_vp), ("G", c_ll), ("pair_gid", c_vp), ("pair_vm", c_vp), ("cams", c_vp), ("n_pairs", c_i),
-                ("p", c_vp), ("sa", c_ll), ("sg", c_ll), ("pm", c_vp)]
+                ("p", c_vp), ("sa", c_ll), ("sg", c_ll), ("pm", c_vp), ("gtab", c_vp)]
 
 
 class SlmBackArgs(C.Structure):
     _fields_ = [("xs", c_vp), ("G", c_ll), ("gpo", c_vp), ("pair_vm", c_vp), ("cams", c_vp), ("pacc", c_vp),
-                ("pair_run_off", c_vp), ("warp_g0", c_vp), ("pair_gid", c_vp), ("n_pairs", c_ll), ("gm", c_vp),
+                ("pair_run_off", c_vp), ("warp_g0", c_vp), ("pair_gid", c_vp), ("n_pairs", c_ll), ("gm", c_vp), ("gtab", c_vp),
                 ("scale", c_f),
                 ("p", c_vp), ("Mdiag", c_vp), ("lam", c_d), ("lam_out", c_i), ("out", c_vp), ("dot_part", c_vp)]
 
@@ -127,7 +127,9 @@ _SIGS = {
     "slm_run_static": (c_i, [c_vp, c_ll, c_vp, c_vp, c_vp]),
     "slm_chunk_perm": (c_i, [c_vp, c_ll, c_vp, c_vp, c_vp]),
     "slm_tile_chunks": (c_i, [c_vp, c_i, c_vp, c_vp, c_vp, c_vp, c_i, c_vp]),
-    "slm_pair_tables": (c_i, [c_vp, c_ll, c_i, c_vp, c_vp, c_vp, c_i, c_vp, c_vp]),
+    "slm_pair_tables": (c_i, [c_vp, c_ll, c_i, c_vp, c_vp, c_vp, c_i, c_vp, c_vp, c_vp]),
+    "slm_gauss_tab": (c_i, [c_vp, c_ll, c_vp, c_vp]),
+    "slm_gauss_tab_floats": (c_i, []),
     "slm_diag_runs": (c_i, [c_vp, c_vp]),
     "slm_diag_stream": (c_i, [c_vp, c_vp]),
     "slm_pair_forward": (c_i, [c_vp, c_i, c_vp]),

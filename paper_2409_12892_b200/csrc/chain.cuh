@@ -18,13 +18,95 @@ struct Tab {
   float mask[3];
 };
 
+// Gaussian-only part of the chain (independent of the view): rotation Rg of
+// the normalised quaternion, s^2 = exp(2 log s), the projected rotation
+// derivatives Mq_l = (dR/dq_hat_l - q_hat_l sum_k q_hat_k dR/dq_hat_k) / |q|
+// (the (I - q_hat q_hat^T) / |q| normalisation chain) and sigma'(logit).
+// Precomputed once per cache (k_gauss_tab, GTAB floats per gaussian) so the
+// per-(gaussian, view) chain only does the camera-dependent part.
+#define GTAB 52  // Rg 9, s2 3, Mq 36, dopa 1, pad
+template <typename Rt>
+__device__ __forceinline__ void gauss_static(const float* __restrict__ xs, long long G, long long g, Rt (&Rg)[9],
+                                             Rt (&s2)[3], Rt (&Mq)[4][9], Rt& dopa) {
+  const Rt q0 = xs[3 * G + g], q1 = xs[4 * G + g], q2 = xs[5 * G + g], q3 = xs[6 * G + g];
+  const Rt qn = sqrt(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
+  const Rt iq = Rt(1) / qn;
+  const Rt w = q0 * iq, a = q1 * iq, b = q2 * iq, c = q3 * iq;
+  const Rt R0[9] = {Rt(1) - Rt(2) * (b * b + c * c), Rt(2) * (a * b - w * c), Rt(2) * (a * c + w * b),
+                    Rt(2) * (a * b + w * c), Rt(1) - Rt(2) * (a * a + c * c), Rt(2) * (b * c - w * a),
+                    Rt(2) * (a * c - w * b), Rt(2) * (b * c + w * a), Rt(1) - Rt(2) * (a * a + b * b)};
+#pragma unroll
+  for (int i = 0; i < 9; ++i) Rg[i] = R0[i];
+  s2[0] = exp(Rt(2) * (Rt)xs[7 * G + g]);
+  s2[1] = exp(Rt(2) * (Rt)xs[8 * G + g]);
+  s2[2] = exp(Rt(2) * (Rt)xs[9 * G + g]);
+  // dR/dq_hat_k (3x3 each), row-major
+  const Rt dRh[4][9] = {
+      {Rt(0), -Rt(2) * c, Rt(2) * b, Rt(2) * c, Rt(0), -Rt(2) * a, -Rt(2) * b, Rt(2) * a, Rt(0)},
+      {Rt(0), Rt(2) * b, Rt(2) * c, Rt(2) * b, -Rt(4) * a, -Rt(2) * w, Rt(2) * c, Rt(2) * w, -Rt(4) * a},
+      {-Rt(4) * b, Rt(2) * a, Rt(2) * w, Rt(2) * a, Rt(0), Rt(2) * c, -Rt(2) * w, Rt(2) * c, -Rt(4) * b},
+      {-Rt(4) * c, -Rt(2) * w, Rt(2) * a, Rt(2) * w, -Rt(4) * c, Rt(2) * b, Rt(2) * a, Rt(2) * b, Rt(0)}};
+  const Rt qh[4] = {w, a, b, c};
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    const Rt S = qh[0] * dRh[0][i] + qh[1] * dRh[1][i] + qh[2] * dRh[2][i] + qh[3] * dRh[3][i];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) Mq[l][i] = (dRh[l][i] - qh[l] * S) * iq;
+  }
+  const Rt o = Rt(1) / (Rt(1) + exp(-(Rt)xs[10 * G + g]));
+  dopa = o * (Rt(1) - o);
+}
+
+static __global__ void __launch_bounds__(256) k_gauss_tab(const float* __restrict__ xs, long long G,
+                                                          float* __restrict__ gtab) {
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < G; g += (long long)gridDim.x * blockDim.x) {
+    float Rg[9], s2[3], Mq[4][9], dopa;
+    gauss_static<float>(xs, G, g, Rg, s2, Mq, dopa);
+    float o[GTAB];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) o[i] = Rg[i];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) o[9 + i] = s2[i];
+#pragma unroll
+    for (int l = 0; l < 4; ++l)
+#pragma unroll
+      for (int i = 0; i < 9; ++i) o[12 + l * 9 + i] = Mq[l][i];
+    o[48] = dopa;
+    o[49] = o[50] = o[51] = 0.f;
+    float4* dst = reinterpret_cast<float4*>(gtab + (size_t)g * GTAB);
+#pragma unroll
+    for (int k = 0; k < GTAB / 4; ++k) dst[k] = make_float4(o[4 * k], o[4 * k + 1], o[4 * k + 2], o[4 * k + 3]);
+  }
+}
+
 template <int K, typename Rt = SLM_CHAIN_T>
 __device__ __forceinline__ void pair_tab(const float* __restrict__ xs, long long G, long long g, const SlmCamera& cam,
-                                         uint32_t clampbits, Tab<K>& T) {
+                                         uint32_t clampbits, Tab<K>& T, const float* __restrict__ gtab = nullptr) {
   const Rt p0 = xs[g], p1 = xs[G + g], p2 = xs[2 * G + g];
-  Rt q[4] = {xs[3 * G + g], xs[4 * G + g], xs[5 * G + g], xs[6 * G + g]};
-  const Rt l0 = xs[7 * G + g], l1 = xs[8 * G + g], l2 = xs[9 * G + g];
-  const Rt logit = xs[10 * G + g];
+  Rt Rg[9], s2[3], Mq[4][9], dopa;
+  if (gtab) {
+    const float4* gr = reinterpret_cast<const float4*>(gtab + (size_t)g * GTAB);
+    float t[GTAB];
+#pragma unroll
+    for (int k = 0; k < GTAB / 4; ++k) {
+      const float4 v = __ldg(gr + k);
+      t[4 * k] = v.x;
+      t[4 * k + 1] = v.y;
+      t[4 * k + 2] = v.z;
+      t[4 * k + 3] = v.w;
+    }
+#pragma unroll
+    for (int i = 0; i < 9; ++i) Rg[i] = t[i];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) s2[i] = t[9 + i];
+#pragma unroll
+    for (int l = 0; l < 4; ++l)
+#pragma unroll
+      for (int i = 0; i < 9; ++i) Mq[l][i] = t[12 + l * 9 + i];
+    dopa = t[48];
+  } else {
+    gauss_static<Rt>(xs, G, g, Rg, s2, Mq, dopa);
+  }
   Rt R[9];
 #pragma unroll
   for (int i = 0; i < 9; ++i) R[i] = (Rt)cam.R[i];
@@ -42,14 +124,6 @@ __device__ __forceinline__ void pair_tab(const float* __restrict__ xs, long long
     T.dmu[0][j] = U[0][j];
     T.dmu[1][j] = U[1][j];
   }
-  // rotation of the gaussian
-  const Rt qn = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
-  const Rt iq = Rt(1) / qn;
-  const Rt w = q[0] * iq, a = q[1] * iq, b = q[2] * iq, c = q[3] * iq;
-  Rt Rg[9] = {Rt(1) - Rt(2) * (b * b + c * c), Rt(2) * (a * b - w * c), Rt(2) * (a * c + w * b),
-                 Rt(2) * (a * b + w * c), Rt(1) - Rt(2) * (a * a + c * c), Rt(2) * (b * c - w * a),
-                 Rt(2) * (a * c - w * b), Rt(2) * (b * c + w * a), Rt(1) - Rt(2) * (a * a + b * b)};
-  const Rt s2[3] = {exp(Rt(2) * l0), exp(Rt(2) * l1), exp(Rt(2) * l2)};
   // M = R Rg (camera-frame axes), Sc = M diag(s2) M^T
   Rt Mm[9];
 #pragma unroll
@@ -82,7 +156,7 @@ __device__ __forceinline__ void pair_tab(const float* __restrict__ xs, long long
   for (int p = 0; p < 3; ++p)
 #pragma unroll
     for (int j = 0; j < 3; ++j) T.dcov[p][j] = dX[0][p] * R[j] + dX[1][p] * R[3 + j] + dX[2][p] * R[6 + j];
-  // quaternion: dcov_l = V_l W^T + W V_l^T, V_l = U dR/dq_l, W = U Rg diag(s2)
+  // quaternion: dcov_l = V_l W^T + W V_l^T, V_l = U Mq_l, W = U Rg diag(s2)
   Rt UR[2][3], Wm[2][3];
 #pragma unroll
   for (int r = 0; r < 2; ++r)
@@ -91,33 +165,13 @@ __device__ __forceinline__ void pair_tab(const float* __restrict__ xs, long long
       UR[r][j] = U[r][0] * Rg[j] + U[r][1] * Rg[3 + j] + U[r][2] * Rg[6 + j];
       Wm[r][j] = UR[r][j] * s2[j];
     }
-  // dR/dq_hat_k (3x3 each), row-major
-  const Rt dRh[4][9] = {
-      {Rt(0), -Rt(2) * c, Rt(2) * b, Rt(2) * c, Rt(0), -Rt(2) * a, -Rt(2) * b, Rt(2) * a, Rt(0)},
-      {Rt(0), Rt(2) * b, Rt(2) * c, Rt(2) * b, -Rt(4) * a, -Rt(2) * w, Rt(2) * c, Rt(2) * w, -Rt(4) * a},
-      {-Rt(4) * b, Rt(2) * a, Rt(2) * w, Rt(2) * a, Rt(0), Rt(2) * c, -Rt(2) * w, Rt(2) * c, -Rt(4) * b},
-      {-Rt(4) * c, -Rt(2) * w, Rt(2) * a, Rt(2) * w, -Rt(4) * c, Rt(2) * b, Rt(2) * a, Rt(2) * b, Rt(0)}};
-  Rt Vh[4][2][3];
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
-#pragma unroll
-      for (int j = 0; j < 3; ++j)
-        Vh[k][r][j] = U[r][0] * dRh[k][j] + U[r][1] * dRh[k][3 + j] + U[r][2] * dRh[k][6 + j];
-  const Rt qh[4] = {w, a, b, c};
 #pragma unroll
   for (int l = 0; l < 4; ++l) {
     Rt V[2][3];
 #pragma unroll
     for (int r = 0; r < 2; ++r)
 #pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        Rt s = Rt(0);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) s += ((k == l ? Rt(1) : Rt(0)) - qh[k] * qh[l]) * Vh[k][r][j];
-        V[r][j] = s * iq;
-      }
+      for (int j = 0; j < 3; ++j) V[r][j] = U[r][0] * Mq[l][j] + U[r][1] * Mq[l][3 + j] + U[r][2] * Mq[l][6 + j];
     const Rt v0w0 = V[0][0] * Wm[0][0] + V[0][1] * Wm[0][1] + V[0][2] * Wm[0][2];
     const Rt v0w1 = V[0][0] * Wm[1][0] + V[0][1] * Wm[1][1] + V[0][2] * Wm[1][2];
     const Rt v1w0 = V[1][0] * Wm[0][0] + V[1][1] * Wm[0][1] + V[1][2] * Wm[0][2];
@@ -152,8 +206,7 @@ __device__ __forceinline__ void pair_tab(const float* __restrict__ xs, long long
     T.dcol[ch][1] = T.mask[ch] * (dcdd[ch][1] - d1 * dd) * ivn;
     T.dcol[ch][2] = T.mask[ch] * (dcdd[ch][2] - d2 * dd) * ivn;
   }
-  const Rt o = Rt(1) / (Rt(1) + exp(-logit));
-  T.dopa = o * (Rt(1) - o);
+  T.dopa = dopa;
 }
 
 // Forward chain of applyJ (ref: jacobian.py:434-443): thread per pair (pairs
@@ -169,7 +222,7 @@ __global__ void __launch_bounds__(128) k_pair_m(SlmFwdArgs A) {
     const long long sa = A.sa, sg = A.sg;
     const float* __restrict__ p = A.p;
     Tab<K> T;
-    pair_tab<K>(A.xs, A.G, g, A.cams[vm & 0xffffu], vm >> 16, T);
+    pair_tab<K>(A.xs, A.G, g, A.cams[vm & 0xffffu], vm >> 16, T, A.gtab);
     float pg[11];
 #pragma unroll
     for (int a = 0; a < 11; ++a) pg[a] = p[a * sa + g * sg];

@@ -47,11 +47,11 @@ __global__ void __launch_bounds__(128) k_pair_tables(const float* __restrict__ x
                                                      const int* __restrict__ pair_gid,
                                                      const uint32_t* __restrict__ pair_vm,
                                                      const SlmCamera* __restrict__ cams, int n_pairs,
-                                                     float* __restrict__ tab) {
+                                                     float* __restrict__ tab, const float* __restrict__ gtab) {
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_pairs; q += gridDim.x * blockDim.x) {
     const uint32_t vm = pair_vm[q];
     Tab<K> T;
-    pair_tab<K>(xs, G, pair_gid[q], cams[vm & 0xffffu], vm >> 16, T);
+    pair_tab<K>(xs, G, pair_gid[q], cams[vm & 0xffffu], vm >> 16, T, gtab);
     float o[DIAG_TAB];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(128, 3) k_gauss_backward(SlmBackArgs A) {
         pair_partials<D, 0, 9>(A, q, a);
         const uint32_t vm = A.pair_vm[q];
         Tab<K> T;
-        pair_tab<K>(A.xs, G, g, A.cams[vm & 0xffffu], vm >> 16, T);
+        pair_tab<K>(A.xs, G, g, A.cams[vm & 0xffffu], vm >> 16, T, A.gtab);
 #pragma unroll
         for (int j = 0; j < 3; ++j)
           og[j] += T.dmu[0][j] * a[0] + T.dmu[1][j] * a[1] + T.dcol[0][j] * a[6] + T.dcol[1][j] * a[7] +
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(32 * PK_WARPS) k_gauss_backward_packed(SlmBack
         const uint32_t vm = A.pair_vm[q];
         if (MODE == 0) {
           Tab<K> T;
-          pair_tab<K>(A.xs, G, g, A.cams[vm & 0xffffu], vm >> 16, T);
+          pair_tab<K>(A.xs, G, g, A.cams[vm & 0xffffu], vm >> 16, T, A.gtab);
 #pragma unroll
           for (int j = 0; j < 3; ++j)
             row[j] = T.dmu[0][j] * a[0] + T.dmu[1][j] * a[1] + T.dcol[0][j] * a[6] + T.dcol[1][j] * a[7] +
@@ -469,15 +469,23 @@ int slm_tile_args_size() { return (int)sizeof(SlmTileArgs); }
 int slm_back_args_size() { return (int)sizeof(SlmBackArgs); }
 int slm_diag_tab_floats() { return DIAG_TAB; }
 
+int slm_gauss_tab(const float* xs, long long G, float* gtab, cudaStream_t st) {
+  if (G <= 0) return SLM_OK;
+  k_gauss_tab<<<slm_blocks(G, 256, 1LL << 30), 256, 0, st>>>(xs, G, gtab);
+  return slm_cuda_status();
+}
+
+int slm_gauss_tab_floats(void) { return GTAB; }
+
 int slm_pair_tables(const float* xs, long long G, int sh_degree, const int* pair_gid, const uint32_t* pair_vm,
-                    const SlmCamera* cams, int n_pairs, float* tab, cudaStream_t st) {
+                    const SlmCamera* cams, int n_pairs, float* tab, const float* gtab, cudaStream_t st) {
   if (n_pairs <= 0) return SLM_OK;
   unsigned b = slm_blocks(n_pairs, 128, 1LL << 30);
   switch (sh_degree) {
-    case 0: k_pair_tables<1><<<b, 128, 0, st>>>(xs, G, pair_gid, pair_vm, cams, n_pairs, tab); break;
-    case 1: k_pair_tables<4><<<b, 128, 0, st>>>(xs, G, pair_gid, pair_vm, cams, n_pairs, tab); break;
-    case 2: k_pair_tables<9><<<b, 128, 0, st>>>(xs, G, pair_gid, pair_vm, cams, n_pairs, tab); break;
-    case 3: k_pair_tables<16><<<b, 128, 0, st>>>(xs, G, pair_gid, pair_vm, cams, n_pairs, tab); break;
+    case 0: k_pair_tables<1><<<b, 128, 0, st>>>(xs, G, pair_gid, pair_vm, cams, n_pairs, tab, gtab); break;
+    case 1: k_pair_tables<4><<<b, 128, 0, st>>>(xs, G, pair_gid, pair_vm, cams, n_pairs, tab, gtab); break;
+    case 2: k_pair_tables<9><<<b, 128, 0, st>>>(xs, G, pair_gid, pair_vm, cams, n_pairs, tab, gtab); break;
+    case 3: k_pair_tables<16><<<b, 128, 0, st>>>(xs, G, pair_gid, pair_vm, cams, n_pairs, tab, gtab); break;
     default: return SLM_ERR_ARG;
   }
   return slm_cuda_status();

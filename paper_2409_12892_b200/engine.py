@@ -528,6 +528,9 @@ class CacheSet:
         self.gm = torch.empty(G * self.P, dtype=torch.float32, device=dev)
         call("slm_warp_bounds", ptr(self.gpo), G, Pn, ptr(self.warp_g0), stream_ptr())
         self.pm = _empty(Pn * 12, f32, dev)
+        # view-independent chain constants per gaussian (scene fixed for the cache)
+        self.gtab = torch.empty(G * _lib.load().slm_gauss_tab_floats(), dtype=f32, device=dev)
+        call("slm_gauss_tab", ptr(scene.x32()), G, ptr(self.gtab), stream_ptr())
         call("slm_run_static", _lib.byref(self._tile_args()), R, ptr(self.run_slot), ptr(self.run_static),
              stream_ptr())
         self._b = None
@@ -549,7 +552,7 @@ class CacheSet:
             self.n_pairs
         a.p = ptr(p)
         a.sa, a.sg = (1, P) if gaussian_major else (G, 1)
-        a.pm = ptr(self.pm)
+        a.pm, a.gtab = ptr(self.pm), ptr(self.gtab)
         call("slm_pair_forward", _lib.byref(a), self.scene.sh_degree, stream_ptr())
 
     def _tile_args(self, with_m: bool = False) -> _lib.SlmTileArgs:
@@ -581,6 +584,7 @@ class CacheSet:
             a.pacc, a.pair_run_off = ptr(self.pacc), None
         a.xs, a.G = ptr(self.scene.x32()), self.G
         a.gpo, a.pair_vm, a.cams = ptr(self.gpo), ptr(self.pair_vm), ptr(self.cams_dev)
+        a.gtab = ptr(self.gtab)
         if self.packed_backward:
             a.warp_g0, a.pair_gid, a.n_pairs = ptr(self.warp_g0), ptr(self.pair_gid), self.n_pairs
             a.gm = ptr(self.gm)
@@ -643,7 +647,7 @@ class CacheSet:
             sums = _empty(self.R * _lib.DIAG_D, torch.float32, self.device)
             ptab = _empty(self.n_pairs * _lib.load().slm_diag_tab_floats(), torch.float32, self.device)
             call("slm_pair_tables", ptr(self.scene.x32()), self.G, self.scene.sh_degree, ptr(self.pair_gid),
-                 ptr(self.pair_vm), ptr(self.cams_dev), self.n_pairs, ptr(ptab), stream_ptr())
+                 ptr(self.pair_vm), ptr(self.cams_dev), self.n_pairs, ptr(ptab), ptr(self.gtab), stream_ptr())
             ra = self._tile_args()
             ra.ptab, ra.gradr, ra.out = ptr(ptab), ptr(self.gradr), ptr(sums)
             call("slm_diag_stream", _lib.byref(ra), stream_ptr())
