@@ -323,6 +323,15 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
     const bool inside = px < vw.W && py < vw.H;
     const long long gp = vw.pix_base + (long long)py * vw.W + px;
     const int c0 = A.tile_chunk_off[t], c1 = A.tile_chunk_off[t + 1];
+    // per-pixel weight / input loaded up front so its latency hides behind the J pass
+    float4 wt = make_float4(1.f, 1.f, 1.f, 0.f);
+    if (MODE & MODE_J) {
+      if (inside && A.gradr) wt = A.gradr[gp];
+    } else if (MODE & MODE_DIAG) {
+      wt = inside ? A.gradr[gp] : make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      wt = inside ? A.u[gp] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
 
     if (MODE & MODE_J) {
       for (int i = lane; i < 256; i += 32) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -384,15 +393,13 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
       }
       float4 uw = make_float4(0.f, 0.f, 0.f, 0.f);
       if (inside) {
-        const float4 wt = A.gradr ? A.gradr[gp] : make_float4(1.f, 1.f, 1.f, 0.f);
         uw = make_float4(u0 * wt.x, u1 * wt.y, u2 * wt.z, 0.f);
         if (MODE & MODE_WRITEU) A.u_out[gp] = uw;
       }
       s_u[p] = uw;
     } else {
-      // J^T: u per pixel; diag: grad_r_sq per pixel
-      const slm_f4* src = (MODE & MODE_DIAG) ? A.gradr : A.u;
-      s_u[p] = inside ? src[gp] : make_float4(0.f, 0.f, 0.f, 0.f);
+      // J^T: u per pixel; diag: grad_r_sq per pixel (loaded above)
+      s_u[p] = wt;
     }
 
     if (MODE & MODE_DIAG) {
