@@ -493,13 +493,33 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
       nrel += __popc(bal);
     }
     __syncwarp();
-    for (int ki = 0; ki < nrel; ++ki) {
-      const int k = s_list[warp][ki];
+    for (int ki = 0; ki < nrel;) {
+      int k;
+      unsigned mk = 0u;  // FILL: the keep mask of this lane's instance in the wave
+      if (FILL) {
+        // a wave = consecutive relevant instances whose keep masks over the
+        // warp's pixels are pairwise disjoint: each lane keeps at most one of
+        // them, so one fp64 evaluation per lane covers the whole wave and the
+        // per-pixel depth order is preserved
+        unsigned occ = 0u;
+        k = -1;
+        for (int nw = 0; ki < nrel && nw < 8; ++nw, ++ki) {
+          const int kk = s_list[warp][ki];
+          const unsigned mw = s_mask[kk * RW + warp];
+          if (mw & occ) break;
+          occ |= mw;
+          if ((mw >> lane) & 1u) {
+            k = kk;
+            mk = mw;
+          }
+        }
+      } else {
+        k = s_list[warp][ki++];
+      }
       bool keep = false;
       double a = 0.0;
-      const int4 bx = s_box[k];
-      bool inb = !done && (!FILL || ((s_mask[k * RW + warp] >> lane) & 1u)) && px >= bx.x && px <= bx.y &&
-                 py >= bx.z && py <= bx.w;
+      const int4 bx = k >= 0 ? s_box[k] : make_int4(1, 0, 1, 0);
+      bool inb = !done && k >= 0 && px >= bx.x && px <= bx.y && py >= bx.z && py <= bx.w;
       if (inb) {
         // -(1/2) d^T conic d in the reference's evaluation order
         double dx = __dsub_rn(dxp, s_mx[k]);
@@ -510,7 +530,7 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
         a = a < aclamp ? a : aclamp;
         keep = (a >= amin) && (a > 0.0) && (T >= tstop);
       }
-      const unsigned m = FILL ? s_mask[k * RW + warp] : __ballot_sync(0xffffffffu, keep);
+      const unsigned m = FILL ? mk : __ballot_sync(0xffffffffu, keep);
       if (!FILL && lane == 0) s_mask[k * RW + warp] = m;
       if (keep) {
         const double wgt = __dmul_rn(a, T);
