@@ -526,7 +526,8 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
         double dy = __dsub_rn(dyp, s_my[k]);
         double q = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(s_ca[k], dx), dx), __dmul_rn(s_cc[k], __dmul_rn(dy, dy))),
                              __dmul_rn(__dmul_rn(__dmul_rn(2.0, s_cb[k]), dy), dx));
-        a = __dmul_rn(s_o[k], exp(__dmul_rn(-0.5, q)));
+        const double ex = __dmul_rn(-0.5, q);
+        a = ex >= -40.0 ? __dmul_rn(s_o[k], slm_exp_neg(ex)) : 0.0;  // exp(-40) * o << alpha_min
         a = a < aclamp ? a : aclamp;
         keep = (a >= amin) && (a > 0.0) && (T >= tstop);
       }
