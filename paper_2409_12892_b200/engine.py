@@ -509,9 +509,11 @@ class CacheSet:
         # {alpha_eff, alpha*T, dc/dalpha_r, dc/dalpha_g}, dc/dalpha_b, tile-local
         # pixel; +16 slots so the 16-byte-granular TMA chunk copies of the
         # product kernels stay in bounds
-        self.rec4 = torch.zeros((E + 16) * 4, dtype=f32, device=dev)
-        self.rec_d2 = torch.zeros(E + 16, dtype=f32, device=dev)
-        self.rec_pix = torch.zeros(E + 16, dtype=torch.uint8, device=dev)
+        # every entry is written by the FILL pass; the +16 tail slots are only
+        # over-read by the 16-byte-granular copies and never used
+        self.rec4 = torch.empty((E + 16) * 4, dtype=f32, device=dev)
+        self.rec_d2 = torch.empty(E + 16, dtype=f32, device=dev)
+        self.rec_pix = torch.empty(E + 16, dtype=torch.uint8, device=dev)
         a = batched_args()
         a.inst_start = ptr(inst_start)
         a.rec4, a.rec_d2, a.rec_pix = ptr(self.rec4), ptr(self.rec_d2), ptr(self.rec_pix)
