@@ -42,6 +42,8 @@ CONFIGS = {
     "c1": dict(G=2000, views=8, W=64, H=64, subsets=1, iters=10, gen="reference", degree=3),
     "c2": dict(G=100_000, views=32, W=256, H=256, subsets=4, iters=8, gen="reference", degree=3),
     "c3": dict(G=1_000_000, views=200, W=1024, H=1024, subsets=8, iters=8, gen="footprint", degree=3),
+    # BASELINE.json configs[3] (Mip-NeRF360 scale; quoted for 8 GPUs, one subset per GPU)
+    "c4": dict(G=3_000_000, views=200, W=1552, H=1032, subsets=8, iters=8, gen="footprint", degree=3),
 }
 
 
