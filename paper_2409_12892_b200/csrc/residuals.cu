@@ -3,7 +3,8 @@
 // color_grad = sum_terms r * dr/dc (ref: residuals.py:249-296, center-pixel
 // SSIM gradient ref: residuals.py:143-159, reflect padding ref: 58-91).
 //
-// fp64 throughout; two separable passes over five statistics x 3 channels.
+// fp64 throughout; separable 2-D window over five statistics x 3 channels,
+// fused into one tiled kernel (no global scratch).
 #include "slm_common.cuh"
 
 #define SSIM_WIN_MAX 31
@@ -21,88 +22,109 @@ __device__ __forceinline__ double gt_at(const ResidArgs& A, size_t i) {
   return A.gt_f32 ? (double)((const float*)A.gt)[i] : ((const double*)A.gt)[i];
 }
 
-// horizontal pass: tmp[p*15 + s*3 + c] for statistics s = x, y, xx, yy, xy
-__global__ void k_ssim_h(ResidArgs A) {
-  long long n = (long long)A.W * A.H;
-  int half = A.win / 2;
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
-    int y = (int)(p / A.W), x = (int)(p % A.W);
-    double acc[15];
-#pragma unroll
-    for (int s = 0; s < 15; ++s) acc[s] = 0.0;
-    for (int j = 0; j < A.win; ++j) {
-      int xx = reflect_idx(x + j - half, A.W);
-      size_t q = ((size_t)y * A.W + xx) * 3;
-      double w = A.taps[j];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        double a = A.img[q + c], b = gt_at(A, q + c);
-        acc[0 + c] += w * a;
-        acc[3 + c] += w * b;
-        acc[6 + c] += w * (a * a);
-        acc[9 + c] += w * (b * b);
-        acc[12 + c] += w * (a * b);
-      }
-    }
-#pragma unroll
-    for (int s = 0; s < 15; ++s) A.tmp[(size_t)p * 15 + s] = acc[s];
-  }
-}
+// One kernel, 16x16 output pixels per CTA (grid-stride over tiles).  Per
+// tile the (16 + win - 1)^2 reflect-padded window of the rendered and the
+// ground-truth image (3 channels) is staged in shared memory; per channel the
+// horizontal pass writes five statistics per (window row, output column) to
+// shared memory and each thread finishes its pixel's vertical pass.  Taps are summed in
+// ascending order in both passes (the order of the reference's separable
+// correlate1d, residuals.py:58-91).
+#define RT 16
 
-__global__ void k_ssim_v(ResidArgs A) {
-  __shared__ double sm[32];
-  long long n = (long long)A.W * A.H;
-  int half = A.win / 2;
+__global__ void __launch_bounds__(256) k_residuals(ResidArgs A) {
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  __shared__ double taps[SSIM_WIN_MAX];
+  const int half = A.win / 2, IW = RT + 2 * half;
+  double* s_a = sm;
+  double* s_b = s_a + 3 * IW * IW;
+  double* s_h = s_b + 3 * IW * IW;
+  const bool ssim = A.mode == 0 && A.lambda2 > 0.0;
+  if (threadIdx.x < A.win) taps[threadIdx.x] = A.taps[threadIdx.x];
+  const int tx = threadIdx.x & (RT - 1), ty = threadIdx.x / RT;
+  const int ntx = (A.W + RT - 1) / RT, nty = (A.H + RT - 1) / RT;
   double e_acc = 0.0;
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
-    int y = (int)(p / A.W), x = (int)(p % A.W);
-    double st[15];
+  for (int t = blockIdx.x; t < ntx * nty; t += gridDim.x) {
+    const int x0 = (t % ntx) * RT, y0 = (t / ntx) * RT;
+    const int x = x0 + tx, y = y0 + ty;
+    const bool inside = x < A.W && y < A.H;
+    const size_t p = inside ? (size_t)y * A.W + x : 0;
+    const double cw = inside ? A.cw_y[y] * A.cw_x[x] : 0.0;
+    float gr[3], cg[3];
+    if (ssim) {
+      __syncthreads();  // previous tile done with the buffers
+      for (int i = threadIdx.x; i < IW * IW; i += blockDim.x) {
+        const int iy = i / IW, ix = i - iy * IW;
+        const int gy = reflect_idx(y0 + iy - half, A.H), gx = reflect_idx(x0 + ix - half, A.W);
+        const size_t q = ((size_t)gy * A.W + gx) * 3;
 #pragma unroll
-    for (int s = 0; s < 15; ++s) st[s] = 0.0;
-    if (A.mode == 0 && A.lambda2 > 0.0) {
-      for (int j = 0; j < A.win; ++j) {
-        int yy = reflect_idx(y + j - half, A.H);
-        const double* t = A.tmp + ((size_t)yy * A.W + x) * 15;
-        double w = A.taps[j];
-#pragma unroll
-        for (int s = 0; s < 15; ++s) st[s] += w * t[s];
+        for (int c = 0; c < 3; ++c) {
+          s_a[c * IW * IW + i] = A.img[q + c];
+          s_b[c * IW * IW + i] = gt_at(A, q + c);
+        }
       }
     }
-    double cw = A.cw_y[y] * A.cw_x[x];
-    float gr[3], cg[3];
-#pragma unroll
+#pragma unroll 1
     for (int c = 0; c < 3; ++c) {
-      size_t i = (size_t)p * 3 + c;
-      double im = A.img[i], g = gt_at(A, i);
-      double e = im - g;
+      double st[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+      if (ssim) {
+        __syncthreads();  // window staged / previous channel's s_h consumed
+        for (int i = threadIdx.x; i < IW * RT; i += blockDim.x) {
+          const int iy = i / RT, ix = i - iy * RT;
+          const double* ra = s_a + c * IW * IW + iy * IW + ix;
+          const double* rb = s_b + c * IW * IW + iy * IW + ix;
+          double h0 = 0.0, h1 = 0.0, h2 = 0.0, h3 = 0.0, h4 = 0.0;
+          for (int j = 0; j < A.win; ++j) {
+            const double w = taps[j], a = ra[j], b = rb[j];
+            h0 += w * a;
+            h1 += w * b;
+            h2 += w * (a * a);
+            h3 += w * (b * b);
+            h4 += w * (a * b);
+          }
+          double* o = s_h + (size_t)i * 5;
+          o[0] = h0; o[1] = h1; o[2] = h2; o[3] = h3; o[4] = h4;
+        }
+        __syncthreads();
+        for (int j = 0; j < A.win; ++j) {
+          const double w = taps[j];
+          const double* hh = s_h + ((ty + j) * RT + tx) * 5;
+#pragma unroll
+          for (int k = 0; k < 5; ++k) st[k] += w * hh[k];
+        }
+      }
+      if (!inside) continue;
+      const size_t i = p * 3 + c;
+      const double im = A.img[i], g = gt_at(A, i);
+      const double e = im - g;
       double grad, cgrad, rabs, rssim = 0.0, drabs, drssim = 0.0;
       if (A.mode == 1) {
         grad = 1.0; cgrad = e; rabs = e; drabs = 1.0;
         e_acc += e * e;
       } else {
-        double ae = fabs(e);
+        const double ae = fabs(e);
         rabs = sqrt(A.lambda1 * ae);
         double w1 = 0.0;
         drabs = 0.0;
         if (A.lambda1 > 0.0) {
-          double ge = ae > A.eps_den ? ae : A.eps_den;
-          double sg = e > 0.0 ? 1.0 : (e < 0.0 ? -1.0 : 0.0);
+          const double ge = ae > A.eps_den ? ae : A.eps_den;
+          const double sg = e > 0.0 ? 1.0 : (e < 0.0 ? -1.0 : 0.0);
           drabs = A.lambda1 * sg / (2.0 * sqrt(A.lambda1 * ge));
           w1 = A.lambda1 / (4.0 * ge);
         }
         double w2 = 0.0;
-        if (A.lambda2 > 0.0) {
-          double mx = st[0 + c], my = st[3 + c];
-          double sxx = st[6 + c] - mx * mx, syy = st[9 + c] - my * my, sxy = st[12 + c] - mx * my;
-          double a1 = 2.0 * mx * my + A.ssim_c1, a2 = 2.0 * sxy + A.ssim_c2;
-          double b1 = mx * mx + my * my + A.ssim_c1, b2 = sxx + syy + A.ssim_c2;
-          double score = (a1 * a2) / (b1 * b2);
-          double dsc = (2.0 * cw / (b1 * b2)) * (my * a2 + a1 * (g - my)) -
-                       score * 2.0 * cw * (mx / b1 + (im - mx) / b2);
+        if (ssim) {
+          const double mx = st[0], my = st[1];
+          const double sxx = st[2] - mx * mx, syy = st[3] - my * my, sxy = st[4] - mx * my;
+          const double a1 = 2.0 * mx * my + A.ssim_c1, a2 = 2.0 * sxy + A.ssim_c2;
+          const double b1 = mx * mx + my * my + A.ssim_c1, b2 = sxx + syy + A.ssim_c2;
+          const double score = (a1 * a2) / (b1 * b2);
+          const double dsc = (2.0 * cw / (b1 * b2)) * (my * a2 + a1 * (g - my)) -
+                             score * 2.0 * cw * (mx / b1 + (im - mx) / b2);
           double om = 1.0 - score;
           om = om > 0.0 ? om : 0.0;
           rssim = sqrt(A.lambda2 * om);
-          double go = om > A.eps_den ? om : A.eps_den;
+          const double go = om > A.eps_den ? om : A.eps_den;
           drssim = -A.lambda2 * dsc / (2.0 * sqrt(A.lambda2 * go));
           w2 = A.lambda2 * dsc * dsc / (4.0 * go);
         }
@@ -117,10 +139,12 @@ __global__ void k_ssim_v(ResidArgs A) {
         if (A.o_rssim) { A.o_rssim[i] = rssim; A.o_drssim[i] = drssim; }
       }
     }
-    A.gradr[p] = make_float4(gr[0], gr[1], gr[2], 0.f);
-    A.cgrad[p] = make_float4(cg[0], cg[1], cg[2], 0.f);
+    if (inside) {
+      A.gradr[p] = make_float4(gr[0], gr[1], gr[2], 0.f);
+      A.cgrad[p] = make_float4(cg[0], cg[1], cg[2], 0.f);
+    }
   }
-  double tot = block_sum_d(e_acc, sm);
+  const double tot = block_sum_d(e_acc, red);
   if (threadIdx.x == 0) A.energy_part[blockIdx.x] = tot;
 }
 
@@ -131,10 +155,15 @@ int slm_resid_args_size() { return (int)sizeof(ResidArgs); }
 // Runs both passes; energy_part must hold `blocks` doubles where blocks is
 // returned through *n_blocks (caller sums them on device or host).
 int slm_residuals(const ResidArgs* a, int blocks, cudaStream_t stream) {
-  if (a->win > SSIM_WIN_MAX || a->win % 2 != 1) return SLM_ERR_ARG;
-  long long n = (long long)a->W * a->H;
-  if (a->mode == 0 && a->lambda2 > 0.0) k_ssim_h<<<slm_blocks(n, 256), 256, 0, stream>>>(*a);
-  k_ssim_v<<<blocks, 256, 0, stream>>>(*a);
+  if (a->win > SSIM_WIN_MAX || a->win % 2 != 1 || blocks <= 0) return SLM_ERR_ARG;
+  const int IW = RT + 2 * (a->win / 2);
+  const size_t smem = (a->mode == 0 && a->lambda2 > 0.0) ? ((size_t)6 * IW * IW + (size_t)IW * RT * 5) * 8 : 0;
+  static size_t smem_set = 0;  // opt-in above the 48 KB default (static + dynamic)
+  if (smem > smem_set) {
+    cudaFuncSetAttribute(k_residuals, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    smem_set = smem;
+  }
+  k_residuals<<<blocks, 256, smem, stream>>>(*a);
   return slm_cuda_status();
 }
 

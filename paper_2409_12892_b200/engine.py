@@ -103,7 +103,6 @@ def ssim_host_tables(H, W, window, sigma):
 
 
 _SSIM_CACHE: dict = {}
-_SCRATCH: dict = {}
 
 
 def _ssim_tables(H, W, window, sigma, dev):
@@ -114,16 +113,6 @@ def _ssim_tables(H, W, window, sigma, dev):
         taps, cwy, cwx = ssim_host_tables(H, W, window, sigma)
         t = tuple(torch.from_numpy(a).to(dev) for a in (taps, cwy, cwx))
         _SSIM_CACHE[key] = t
-    return t
-
-
-def _scratch(n, dev):
-    """Reusable fp64 scratch of the residual kernels (stream-ordered reuse)."""
-    key = str(dev)
-    t = _SCRATCH.get(key)
-    if t is None or t.numel() < n:
-        t = torch.empty(max(int(n), 1), dtype=torch.float64, device=dev)
-        _SCRATCH[key] = t
     return t
 
 
@@ -252,8 +241,6 @@ def residual_pass(frame: ViewFrame, gt: torch.Tensor, loss: LossConfig, gradr: t
     dev = gt.device
     gt = gt.contiguous()
     taps_t, cwy_t, cwx_t = _ssim_tables(H, W, loss.window, loss.sigma, dev)
-    need_ssim = loss.mode == "l1ssim" and loss.lambda2 > 0
-    tmp = _scratch(H * W * 15 if need_ssim else 1, dev)
     blocks = int(min(max((H * W + 255) // 256, 1), 148 * 8))
     part = torch.empty(blocks, dtype=torch.float64, device=dev)
     a = _lib.SlmResidArgs()
@@ -265,7 +252,7 @@ def residual_pass(frame: ViewFrame, gt: torch.Tensor, loss: LossConfig, gradr: t
     a.ssim_c1, a.ssim_c2 = 0.01 ** 2, 0.03 ** 2
     a.mode = 0 if loss.mode == "l1ssim" else 1
     a.win = int(loss.window)
-    a.taps, a.cw_y, a.cw_x, a.tmp = ptr(taps_t), ptr(cwy_t), ptr(cwx_t), ptr(tmp)
+    a.taps, a.cw_y, a.cw_x, a.tmp = ptr(taps_t), ptr(cwy_t), ptr(cwx_t), None
     a.gradr = off(gradr, frame.pix_base * 4)
     a.cgrad = off(cgrad, frame.pix_base * 4)
     a.energy_part = ptr(part)
@@ -276,7 +263,7 @@ def residual_pass(frame: ViewFrame, gt: torch.Tensor, loss: LossConfig, gradr: t
         a.o_rabs, a.o_drabs = ptr(exports["rabs"]), ptr(exports["drabs"])
         a.o_rssim, a.o_drssim = ptr(exports["rssim"]), ptr(exports["drssim"])
     call("slm_residuals", _lib.byref(a), blocks, stream_ptr())
-    keep = (taps_t, cwy_t, cwx_t, tmp)  # noqa: F841 -- alive until the kernels are queued
+    keep = (taps_t, cwy_t, cwx_t)  # noqa: F841 -- alive until the kernels are queued
     return part
 
 
