@@ -44,6 +44,8 @@ CONFIGS = {
     "c3": dict(G=1_000_000, views=200, W=1024, H=1024, subsets=8, iters=8, gen="footprint", degree=3),
     # BASELINE.json configs[3] (Mip-NeRF360 scale; quoted for 8 GPUs, one subset per GPU)
     "c4": dict(G=3_000_000, views=200, W=1552, H=1032, subsets=8, iters=8, gen="footprint", degree=3),
+    # BASELINE.json configs[4] (ScanNet++ scale; 16 subsets, 2 per GPU on 8 GPUs)
+    "c5": dict(G=2_000_000, views=400, W=1616, H=1080, subsets=16, iters=8, gen="footprint", degree=3),
 }
 
 
