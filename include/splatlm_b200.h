@@ -23,6 +23,8 @@
 
 #include <stdint.h>
 
+#define SLM_CHUNK_RUNS 64 /* max runs per streaming chunk; SlmTileArgs.chunk_perm holds this many bytes per chunk */
+
 #ifdef __CUDACC__
 #include <cuda_runtime.h>
 typedef uint2 slm_u2;
@@ -146,7 +148,7 @@ typedef struct {
   const int* tile_run_off;   /* [n_tiles+1] */
   const int* tile_chunk_off; /* [n_tiles+1] chunk table (slm_tile_chunks) */
   const int* chunk_run;      /* [n_chunks+1] first run of each chunk */
-  const uint8_t* chunk_perm; /* [n_chunks*32] J^T schedule: chunk-local runs by decreasing length */
+  const uint8_t* chunk_perm; /* [n_chunks*SLM_CHUNK_RUNS] J^T schedule: chunk-local runs by decreasing length */
   const int* run_slot;       /* [R] position of each run in pair_runs (J^T outputs go there) */
   const long long* run_start;/* [R+1] (+2 padding slots) */
   const int* run_q;          /* pair of each run */

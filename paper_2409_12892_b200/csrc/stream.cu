@@ -7,7 +7,7 @@
 // per product (the J^T pass re-reads the tile's entries from L2).
 //
 // Structure (one CTA per SM slot, looping over tiles):
-//   producer warp : for every chunk (<= 32 runs, <= 512 entries, cut at run
+//   producer warp : for every chunk (<= 64 runs, <= 896 entries, cut at run
 //                   boundaries; table built once per cache) of every tile and
 //                   pass, wait for a free ring stage and issue TMA bulk copies
 //                   (cp.async.bulk) of the chunk's entries (5 x f32 + u8), its
@@ -25,14 +25,11 @@
 
 #define NW 8
 #define NT (32 * (NW + 1))
-#ifndef SLM_CH
-#define SLM_CH 1024
-#endif
 #ifndef SLM_NS
 #define SLM_NS 3
 #endif
-#define CH SLM_CH        // max entries per chunk
-#define CR 32            // max runs per chunk
+#define CR SLM_CHUNK_RUNS  // max runs per chunk (64)
+static_assert(CR % 32 == 0 && CR <= 255, "run slots are bytes, 32 per J^T round");
 #define NS SLM_NS        // ring stages
 #define PAR 16           // floats per run parameter record
 #define TMETA 64         // producer chunk-metadata window
@@ -44,29 +41,39 @@
 #define DIAG_TAB 48      // floats per pair coefficient table (k_pair_tables)
 #define DIAG_D 14        // diag sums per run
 
-// one ring stage: rec4 | d2 | pix | run params | run starts | J^T schedule | header
-#define ST_R4 (CH * 16)
-#define ST_D2 ((CH + 8) * 4)
-#define ST_PIX (CH + 32)
-#define ST_PST (CR * 32)   // static run records (TMA)
-#define ST_PDY (CR * 48)   // per-product pair m, gathered per run (cp.async)
-#define ST_PAR (ST_PST + ST_PDY)
-#define ST_RS ((CR + 4) * 8)
-#define ST_PERM 32
-#define ST_HDR 16
-#define OFF_D2 ST_R4
-#define OFF_PIX (OFF_D2 + ST_D2)
-#define OFF_PAR (OFF_PIX + ST_PIX)
-#define OFF_PST OFF_PAR
-#define OFF_PDY (OFF_PAR + ST_PST)
-#define OFF_RS (OFF_PAR + ST_PAR)
-#define OFF_PERM (OFF_RS + ST_RS)
-#define OFF_HDR (OFF_PERM + ST_PERM)
-#define ST_BYTES (OFF_HDR + ST_HDR)
-static_assert(OFF_D2 % 16 == 0 && OFF_PIX % 16 == 0 && OFF_PAR % 16 == 0 && OFF_PDY % 16 == 0 && OFF_RS % 16 == 0 &&
-                  OFF_PERM % 16 == 0 &&
-                  OFF_HDR % 16 == 0 && ST_BYTES % 16 == 0,
+// one ring stage (ST_BYTES): a packed per-chunk region
+//   rec4 | d2 | pix | static run records | pair m | run starts
+// whose section offsets follow from the chunk's entries and runs (so a chunk
+// of long runs carries more entries and a chunk of short runs more runs),
+// then the J^T schedule and the header at fixed offsets
+#ifndef SLM_STAGE
+#define SLM_STAGE 24576
+#endif
+#define ST_BYTES SLM_STAGE
+#define ST_HDR 32
+#define ST_PERM CR
+#define OFF_HDR (ST_BYTES - ST_HDR)
+#define OFF_PERM (OFF_HDR - ST_PERM)
+#define ST_DYN OFF_PERM  // capacity of the packed region
+static_assert(OFF_PERM % 16 == 0 && OFF_HDR % 16 == 0 && ST_BYTES % 16 == 0,
               "stage sections must stay 16-byte aligned for cp.async.bulk");
+
+struct StageLayout {
+  int d2, pix, pst, pdy, rs, end;  // byte offsets of the sections, end of the packed region
+};
+__host__ __device__ __forceinline__ int al16(int x) { return (x + 15) & ~15; }
+// e entries, r runs; the d2 / pix / run-start copies are widened to 16-byte
+// aligned global ranges (<= e + 6 floats, <= e + 30 bytes, <= r + 3 starts)
+__host__ __device__ __forceinline__ StageLayout stage_layout(int e, int r) {
+  StageLayout L;
+  L.d2 = e * 16;
+  L.pix = L.d2 + al16((e + 8) * 4);
+  L.pst = L.pix + al16(e + 32);
+  L.pdy = L.pst + r * 32;
+  L.rs = L.pdy + r * 48;
+  L.end = L.rs + al16((r + 4) * 8);
+  return L;
+}
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
@@ -146,7 +153,8 @@ __global__ void k_run_static(SlmTileArgs A, long long n_runs, const int* __restr
 }
 
 // ---------------------------------------------------------------------------
-// chunk table: per tile, run-aligned chunks of <= CR runs and <= CH entries
+// chunk table: per tile, run-aligned chunks of <= CR runs whose packed stage
+// region (stage_layout) fits ST_DYN bytes
 // (FILL=false: chunks per tile; FILL=true: first run of each chunk)
 // ---------------------------------------------------------------------------
 template <bool FILL>
@@ -159,7 +167,7 @@ __global__ void k_tile_chunks(const int* __restrict__ tile_run_off, int n_tiles,
     long long acc = 0;
     for (int r = r0; r < r1; ++r) {
       const long long n = run_start[r + 1] - run_start[r];
-      if (r > k0 && (acc + n > CH || r - k0 >= CR)) {
+      if (r > k0 && (r - k0 >= CR || stage_layout((int)(acc + n), r - k0 + 1).end > ST_DYN)) {
         if (FILL) out[tile_chunk_off[t] + nc] = k0;
         ++nc;
         k0 = r;
@@ -179,20 +187,36 @@ __global__ void k_tile_chunks(const int* __restrict__ tile_run_off, int n_tiles,
 // 0xff-padded to 32 slots; one warp per chunk, lane = run
 __global__ void k_chunk_perm(const int* __restrict__ chunk_run, long long n_chunks,
                              const long long* __restrict__ run_start, uint8_t* __restrict__ perm) {
+  constexpr int RL = CR / 32;  // runs per lane
   const int lane = threadIdx.x & 31;
   for (long long c = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; c < n_chunks;
        c += ((long long)gridDim.x * blockDim.x) >> 5) {
     const int k0 = chunk_run[c], n = chunk_run[c + 1] - k0;
-    const long long len = lane < n ? run_start[k0 + lane + 1] - run_start[k0 + lane] : -1;
-    int rank = 0;
+    long long len[RL];
+    int rank[RL];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const long long lj = __shfl_sync(0xffffffffu, len, j);
-      rank += (lj > len) || (lj == len && j < lane);
+    for (int h = 0; h < RL; ++h) {
+      const int r = lane + 32 * h;
+      len[h] = r < n ? run_start[k0 + r + 1] - run_start[k0 + r] : -1;
+      rank[h] = 0;
     }
-    perm[c * 32 + lane] = 0xff;
+#pragma unroll
+    for (int hj = 0; hj < RL; ++hj) {
+#pragma unroll 8
+      for (int j = 0; j < 32; ++j) {
+        const long long lj = __shfl_sync(0xffffffffu, len[hj], j);
+        const int rj = j + 32 * hj;
+#pragma unroll
+        for (int h = 0; h < RL; ++h) rank[h] += (lj > len[h]) || (lj == len[h] && rj < lane + 32 * h);
+      }
+    }
+    uint8_t* pc = perm + c * CR;
+#pragma unroll
+    for (int h = 0; h < RL; ++h) pc[lane + 32 * h] = 0xff;
     __syncwarp();
-    if (lane < n) perm[c * 32 + rank] = (uint8_t)lane;
+#pragma unroll
+    for (int h = 0; h < RL; ++h)
+      if (lane + 32 * h < n) pc[rank[h]] = (uint8_t)(lane + 32 * h);
   }
 }
 
@@ -259,23 +283,35 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
           }
           __syncwarp();
           const bool gather = (MODE & MODE_J) && pass == 0 && A.pm;
-          int qn = 0;  // pair of this lane's run in the next chunk (prefetched)
-          if (gather && lane < tmeta[0].k1 - tmeta[0].k0) qn = A.run_q[tmeta[0].k0 + lane];
+          constexpr int RL = CR / 32;  // runs per producer lane
+          int qn[RL];                  // pairs of this lane's runs in the next chunk (prefetched)
+#pragma unroll
+          for (int h = 0; h < RL; ++h)
+            qn[h] = gather && lane + 32 * h < tmeta[0].k1 - tmeta[0].k0 ? A.run_q[tmeta[0].k0 + lane + 32 * h] : 0;
           for (int i = 0; i < wn; ++i, ++g) {
             const int s = (int)(g % NS);
-            const int q = qn;
-            if (gather && i + 1 < wn && lane < tmeta[i + 1].k1 - tmeta[i + 1].k0)
-              qn = A.run_q[tmeta[i + 1].k0 + lane];
+            int q[RL];
+#pragma unroll
+            for (int h = 0; h < RL; ++h) {
+              q[h] = qn[h];
+              if (gather && i + 1 < wn && lane + 32 * h < tmeta[i + 1].k1 - tmeta[i + 1].k0)
+                qn[h] = A.run_q[tmeta[i + 1].k0 + lane + 32 * h];
+            }
             if (g >= NS) mbar_wait(&empty[s], ((g / NS) - 1) & 1u);
             const ChunkMeta m = tmeta[i];
             uint8_t* st = stage_ptr(ring, s);
-            // per-run forward-chain m of the run's pair (J pass only): one lane per run
-            if (gather && lane < m.k1 - m.k0) {
-              const uint8_t* src = reinterpret_cast<const uint8_t*>(A.pm) + (size_t)q * 48;
-              uint8_t* dst = st + OFF_PDY + lane * 48;
-              cp_async16(dst, src);
-              cp_async16(dst + 16, src + 16);
-              cp_async16(dst + 32, src + 32);
+            const StageLayout L = stage_layout((int)(m.e1 - m.e0), m.k1 - m.k0);
+            // per-run forward-chain m of the run's pair (J pass only): lane per run
+#pragma unroll
+            for (int h = 0; h < RL; ++h) {
+              const int r = lane + 32 * h;
+              if (gather && r < m.k1 - m.k0) {
+                const uint8_t* src = reinterpret_cast<const uint8_t*>(A.pm) + (size_t)q[h] * 48;
+                uint8_t* dst = st + L.pdy + r * 48;
+                cp_async16(dst, src);
+                cp_async16(dst + 16, src + 16);
+                cp_async16(dst + 32, src + 32);
+              }
             }
             cp_async_mbar_arrive(&full[s]);
             __syncwarp();
@@ -291,15 +327,19 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
               hdr[1] = (int)(m.k0 - a2);
               hdr[2] = m.k0;
               hdr[3] = (int)(m.e0 - a4);
+              hdr[4] = L.d2;
+              hdr[5] = L.pix;
+              hdr[6] = L.pst;
+              hdr[7] = L.rs;
               // generic-proxy header writes before the async-proxy copies land
               asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
               mbar_arrive_tx(&full[s], b4 + bd + bx + bp + br + ST_PERM);
               bulk_g2s(st, A.rec4 + m.e0, b4, &full[s], pol);
-              bulk_g2s(st + OFF_D2, A.d2 + a4, bd, &full[s], pol);
-              bulk_g2s(st + OFF_PIX, A.pix + a16, bx, &full[s], pol);
-              bulk_g2s(st + OFF_PST, A.run_static + (size_t)m.k0 * 8, bp, &full[s], pol);
-              bulk_g2s(st + OFF_RS, A.run_start + a2, br, &full[s], pol);
-              bulk_g2s(st + OFF_PERM, A.chunk_perm + (size_t)(w0 + i) * 32, ST_PERM, &full[s], pol);
+              bulk_g2s(st + L.d2, A.d2 + a4, bd, &full[s], pol);
+              bulk_g2s(st + L.pix, A.pix + a16, bx, &full[s], pol);
+              bulk_g2s(st + L.pst, A.run_static + (size_t)m.k0 * 8, bp, &full[s], pol);
+              bulk_g2s(st + L.rs, A.run_start + a2, br, &full[s], pol);
+              bulk_g2s(st + OFF_PERM, A.chunk_perm + (size_t)(w0 + i) * CR, ST_PERM, &full[s], pol);
             }
             __syncwarp();
           }
@@ -346,14 +386,14 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
         const uint8_t* st = stage_ptr(ring, s);
         const int* hdr = reinterpret_cast<const int*>(st + OFF_HDR);
         const int nr = hdr[0];
-        const long long* rs = reinterpret_cast<const long long*>(st + OFF_RS) + hdr[1];
+        const long long* rs = reinterpret_cast<const long long*>(st + hdr[7]) + hdr[1];
         const long long e0 = rs[0];
         const float4* s4 = reinterpret_cast<const float4*>(st);
-        const float* sd2 = reinterpret_cast<const float*>(st + OFF_D2) + hdr[3];
-        const uint8_t* spx = st + OFF_PIX + (e0 & 15);
-        const float4* PST = reinterpret_cast<const float4*>(st + OFF_PST);
-        const float4* PDY = reinterpret_cast<const float4*>(st + OFF_PDY);
-        for (int i = warp; i < nr; i += NW) {
+        const float* sd2 = reinterpret_cast<const float*>(st + hdr[4]) + hdr[3];
+        const uint8_t* spx = st + hdr[5] + (e0 & 15);
+        const float4* PST = reinterpret_cast<const float4*>(st + hdr[6]);
+        const float4* PDY = reinterpret_cast<const float4*>(st + hdr[6] + nr * 32);
+        for (int i = (warp + ci) & (NW - 1); i < nr; i += NW) {  // rotated: no warp always gets the extra runs
           // static: q0 = (p0, p1, ka, kb), s1 = (kc, io, slot, pair)
           // pair m:  d0 = (m_opa, m0, m1, m2), d1 = (m3, m4, c0, c1), d2m = (c2, -, -, -)
           const float4 q0 = PST[i * 2], s1 = PST[i * 2 + 1];
@@ -412,109 +452,107 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
         mbar_wait(&full[s], (g / NS) & 1u);
         const uint8_t* st = stage_ptr(ring, s);
         const int* hdr = reinterpret_cast<const int*>(st + OFF_HDR);
-        const long long* rs = reinterpret_cast<const long long*>(st + OFF_RS) + hdr[1];
+        const long long* rs = reinterpret_cast<const long long*>(st + hdr[7]) + hdr[1];
         const float4* s4 = reinterpret_cast<const float4*>(st);
-        const float* sd2 = reinterpret_cast<const float*>(st + OFF_D2) + hdr[3];
-        const uint8_t* spx = st + OFF_PIX + (rs[0] & 15);
+        const float* sd2 = reinterpret_cast<const float*>(st + hdr[4]) + hdr[3];
+        const uint8_t* spx = st + hdr[5] + (rs[0] & 15);
         const long long e0 = rs[0];
-        const int ri = st[OFF_PERM + (((warp + ci) & (NW - 1)) * 4 + slot)];
-        int n = 0, f0 = 0, sl = 0;
-        float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f);
-        float kc = 0.f, io = 0.f;
-        float D[DIAG_TAB];
-        if (ri != 0xff) {
-          const float4* P4 = reinterpret_cast<const float4*>(st + OFF_PST) + ri * 2;
-          q0 = P4[0];
-          const float4 s1 = P4[1];
-          kc = s1.x;
-          io = s1.y;
-          sl = __float_as_int(s1.z);
-          const float4* tq = reinterpret_cast<const float4*>(A.ptab + (size_t)__float_as_int(s1.w) * DIAG_TAB);
-#pragma unroll
-          for (int k = 0; k < DIAG_TAB / 4; ++k) {
-            const float4 v = __ldg(tq + k);
-            D[4 * k] = v.x;
-            D[4 * k + 1] = v.y;
-            D[4 * k + 2] = v.z;
-            D[4 * k + 3] = v.w;
+        for (int rd = 0; rd < CR / 32 && rd * 32 < hdr[0]; ++rd) {  // 32 runs per round, longest first
+          const int ri = st[OFF_PERM + rd * 32 + (((warp + ci) & (NW - 1)) * 4 + slot)];
+          int n = 0, f0 = 0, sl = 0;
+          float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f);
+          float kc = 0.f, io = 0.f;
+          float D[DIAG_TAB];
+          if (ri != 0xff) {
+            const float4* P4 = reinterpret_cast<const float4*>(st + hdr[6]) + ri * 2;
+            q0 = P4[0];
+            const float4 s1 = P4[1];
+            kc = s1.x;
+            io = s1.y;
+            sl = __float_as_int(s1.z);
+            const float4* tq = reinterpret_cast<const float4*>(A.ptab + (size_t)__float_as_int(s1.w) * DIAG_TAB);
+  #pragma unroll
+            for (int k = 0; k < DIAG_TAB / 4; ++k) {
+              const float4 v = __ldg(tq + k);
+              D[4 * k] = v.x;
+              D[4 * k + 1] = v.y;
+              D[4 * k + 2] = v.z;
+              D[4 * k + 3] = v.w;
+            }
+            f0 = (int)(rs[ri] - e0);
+            n = (int)(rs[ri + 1] - rs[ri]);
+          } else {
+  #pragma unroll
+            for (int k = 0; k < DIAG_TAB; ++k) D[k] = 0.f;
           }
-          f0 = (int)(rs[ri] - e0);
-          n = (int)(rs[ri + 1] - rs[ri]);
-        } else {
-#pragma unroll
-          for (int k = 0; k < DIAG_TAB; ++k) D[k] = 0.f;
-        }
-        const int nmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)n);
-        if (nmax == 0) {
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[s]);
-          continue;
-        }
-        const float dop = io * D[36];
-        float a[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) a[k] = 0.f;
-        const float4* pr = s4 + f0;
-        const float* pd = sd2 + f0;
-        const uint8_t* pp = spx + f0;
-        for (int j = lg; j < nmax; j += 8) {
-          if (j < n) {
-            const float4 r = pr[j];
-            const float dd[3] = {r.z, r.w, pd[j]};
-            const int pl = pp[j];
-            const float4 gr = s_u[pl];
-            const float grc[3] = {gr.x, gr.y, gr.z};
-            const float ae = r.x, at = r.y;
-            const float dx = (float)(pl & 15) - q0.x, dy = (float)(pl >> 4) - q0.y;
-            const float e1 = q0.z * dx + q0.w * dy, e2 = q0.w * dx + kc * dy;
-            const float w0 = ae * e1, w1 = ae * e2, w2 = 0.5f * w0 * e1, w3 = w0 * e2, w4 = 0.5f * w1 * e2;
-            // sum_ch gr_ch (dc_ch/dx_k)^2: dalpha_k^2 * Aw for k >= 3 (exact),
-            // per-channel squares for the position params (dc also has at * dcol)
-            const float Aw = grc[0] * dd[0] * dd[0] + grc[1] * dd[1] * dd[1] + grc[2] * dd[2] * dd[2];
-#pragma unroll
-            for (int kk = 0; kk < 3; ++kk) {
-              const float da = w0 * D[kk * 5] + w1 * D[kk * 5 + 1] + w2 * D[kk * 5 + 2] + w3 * D[kk * 5 + 3] +
-                               w4 * D[kk * 5 + 4];
-              float sq = 0.f;
-#pragma unroll
-              for (int ch = 0; ch < 3; ++ch) {
-                const float dc = fmaf(dd[ch], da, at * D[37 + ch * 3 + kk]);
-                sq = fmaf(grc[ch] * dc, dc, sq);
+          const int nmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)n);
+          if (nmax == 0) continue;
+          const float dop = io * D[36];
+          float a[16];
+  #pragma unroll
+          for (int k = 0; k < 16; ++k) a[k] = 0.f;
+          const float4* pr = s4 + f0;
+          const float* pd = sd2 + f0;
+          const uint8_t* pp = spx + f0;
+          for (int j = lg; j < nmax; j += 8) {
+            if (j < n) {
+              const float4 r = pr[j];
+              const float dd[3] = {r.z, r.w, pd[j]};
+              const int pl = pp[j];
+              const float4 gr = s_u[pl];
+              const float grc[3] = {gr.x, gr.y, gr.z};
+              const float ae = r.x, at = r.y;
+              const float dx = (float)(pl & 15) - q0.x, dy = (float)(pl >> 4) - q0.y;
+              const float e1 = q0.z * dx + q0.w * dy, e2 = q0.w * dx + kc * dy;
+              const float w0 = ae * e1, w1 = ae * e2, w2 = 0.5f * w0 * e1, w3 = w0 * e2, w4 = 0.5f * w1 * e2;
+              // sum_ch gr_ch (dc_ch/dx_k)^2: dalpha_k^2 * Aw for k >= 3 (exact),
+              // per-channel squares for the position params (dc also has at * dcol)
+              const float Aw = grc[0] * dd[0] * dd[0] + grc[1] * dd[1] * dd[1] + grc[2] * dd[2] * dd[2];
+  #pragma unroll
+              for (int kk = 0; kk < 3; ++kk) {
+                const float da = w0 * D[kk * 5] + w1 * D[kk * 5 + 1] + w2 * D[kk * 5 + 2] + w3 * D[kk * 5 + 3] +
+                                 w4 * D[kk * 5 + 4];
+                float sq = 0.f;
+  #pragma unroll
+                for (int ch = 0; ch < 3; ++ch) {
+                  const float dc = fmaf(dd[ch], da, at * D[37 + ch * 3 + kk]);
+                  sq = fmaf(grc[ch] * dc, dc, sq);
+                }
+                a[kk] += sq;
               }
-              a[kk] += sq;
+  #pragma unroll
+              for (int kk = 3; kk < 10; ++kk) {
+                const float da = w2 * D[15 + (kk - 3) * 3] + w3 * D[16 + (kk - 3) * 3] + w4 * D[17 + (kk - 3) * 3];
+                a[kk] = fmaf(da * da, Aw, a[kk]);
+              }
+              const float dao = ae * dop;
+              a[10] = fmaf(dao * dao, Aw, a[10]);
+              const float at2 = at * at;
+              a[11] = fmaf(grc[0], at2, a[11]);
+              a[12] = fmaf(grc[1], at2, a[12]);
+              a[13] = fmaf(grc[2], at2, a[13]);
             }
-#pragma unroll
-            for (int kk = 3; kk < 10; ++kk) {
-              const float da = w2 * D[15 + (kk - 3) * 3] + w3 * D[16 + (kk - 3) * 3] + w4 * D[17 + (kk - 3) * 3];
-              a[kk] = fmaf(da * da, Aw, a[kk]);
-            }
-            const float dao = ae * dop;
-            a[10] = fmaf(dao * dao, Aw, a[10]);
-            const float at2 = at * at;
-            a[11] = fmaf(grc[0], at2, a[11]);
-            a[12] = fmaf(grc[1], at2, a[12]);
-            a[13] = fmaf(grc[2], at2, a[13]);
           }
-        }
-        // two 8-lane reduce-scatters: lane lg ends with the group sums of
-        // values lg and 8 + lg (fixed pattern -> deterministic)
-        const unsigned F = 0xffffffffu;
-        const bool u4 = lg & 4, u2 = lg & 2, u1 = lg & 1;
-        float res[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const float* v = a + 8 * h;
-          float w4[4], w2[2];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) w4[k] = (u4 ? v[k + 4] : v[k]) + __shfl_xor_sync(F, u4 ? v[k] : v[k + 4], 4);
-#pragma unroll
-          for (int k = 0; k < 2; ++k) w2[k] = (u2 ? w4[k + 2] : w4[k]) + __shfl_xor_sync(F, u2 ? w4[k] : w4[k + 2], 2);
-          res[h] = (u1 ? w2[1] : w2[0]) + __shfl_xor_sync(F, u1 ? w2[0] : w2[1], 1);
-        }
-        if (ri != 0xff) {
-          float* o = A.out + (size_t)sl * DIAG_D;  // pair-run-slot order
-          o[lg] = res[0];
-          if (lg < DIAG_D - 8) o[8 + lg] = res[1];
+          // two 8-lane reduce-scatters: lane lg ends with the group sums of
+          // values lg and 8 + lg (fixed pattern -> deterministic)
+          const unsigned F = 0xffffffffu;
+          const bool u4 = lg & 4, u2 = lg & 2, u1 = lg & 1;
+          float res[2];
+  #pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const float* v = a + 8 * h;
+            float w4[4], w2[2];
+  #pragma unroll
+            for (int k = 0; k < 4; ++k) w4[k] = (u4 ? v[k + 4] : v[k]) + __shfl_xor_sync(F, u4 ? v[k] : v[k + 4], 4);
+  #pragma unroll
+            for (int k = 0; k < 2; ++k) w2[k] = (u2 ? w4[k + 2] : w4[k]) + __shfl_xor_sync(F, u2 ? w4[k] : w4[k + 2], 2);
+            res[h] = (u1 ? w2[1] : w2[0]) + __shfl_xor_sync(F, u1 ? w2[0] : w2[1], 1);
+          }
+          if (ri != 0xff) {
+            float* o = A.out + (size_t)sl * DIAG_D;  // pair-run-slot order
+            o[lg] = res[0];
+            if (lg < DIAG_D - 8) o[8 + lg] = res[1];
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
@@ -530,78 +568,76 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
         mbar_wait(&full[s], (g / NS) & 1u);
         const uint8_t* st = stage_ptr(ring, s);
         const int* hdr = reinterpret_cast<const int*>(st + OFF_HDR);
-        const long long* rs = reinterpret_cast<const long long*>(st + OFF_RS) + hdr[1];
+        const long long* rs = reinterpret_cast<const long long*>(st + hdr[7]) + hdr[1];
         const float4* s4 = reinterpret_cast<const float4*>(st);
-        const float* sd2 = reinterpret_cast<const float*>(st + OFF_D2) + hdr[3];
-        const uint8_t* spx = st + OFF_PIX + (rs[0] & 15);
+        const float* sd2 = reinterpret_cast<const float*>(st + hdr[4]) + hdr[3];
+        const uint8_t* spx = st + hdr[5] + (rs[0] & 15);
         const long long e0 = rs[0];
-        const int ri = st[OFF_PERM + (((warp + ci) & (NW - 1)) * 4 + slot)];
-        int n = 0, f0 = 0;
-        float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f);
-        float kc = 0.f, io = 0.f;
-        int slot = 0;
-        if (ri != 0xff) {
-          const float4* P4 = reinterpret_cast<const float4*>(st + OFF_PST) + ri * 2;
-          q0 = P4[0];
-          const float4 s1 = P4[1];
-          kc = s1.x;
-          io = s1.y;
-          slot = __float_as_int(s1.z);
-          f0 = (int)(rs[ri] - e0);
-          n = (int)(rs[ri + 1] - rs[ri]);
-        }
-        const int nmax = __reduce_max_sync(0xffffffffu, (unsigned)n);
-        if (nmax == 0) {
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[s]);
-          continue;
-        }
-        float a[9];
-#pragma unroll
-        for (int k = 0; k < 9; ++k) a[k] = 0.f;
-        const float4* pr = s4 + f0;
-        const float* pd = sd2 + f0;
-        const uint8_t* pp = spx + f0;
-        for (int j = lg; j < nmax; j += 8) {
-          if (j < n) {
-            const float4 r = pr[j];
-            const float d2 = pd[j];
-            const int pl = pp[j];
-            const float4 uu = s_u[pl];
-            const float dx = (float)(pl & 15) - q0.x, dy = (float)(pl >> 4) - q0.y;
-            const float e1 = q0.z * dx + q0.w * dy, e2 = q0.w * dx + kc * dy;
-            const float sa = fmaf(r.z, uu.x, fmaf(r.w, uu.y, d2 * uu.z));
-            const float tt = sa * r.x;
-            const float te1 = tt * e1, te2 = tt * e2;
-            a[0] += te1;
-            a[1] += te2;
-            a[2] = fmaf(te1, e1, a[2]);  // x 1/2 in the epilogue
-            a[3] = fmaf(te1, e2, a[3]);
-            a[4] = fmaf(te2, e2, a[4]);  // x 1/2 in the epilogue
-            a[5] += tt;
-            a[6] = fmaf(r.y, uu.x, a[6]);
-            a[7] = fmaf(r.y, uu.y, a[7]);
-            a[8] = fmaf(r.y, uu.z, a[8]);
+        for (int rd = 0; rd < CR / 32 && rd * 32 < hdr[0]; ++rd) {  // 32 runs per round, longest first
+          const int ri = st[OFF_PERM + rd * 32 + (((warp + ci) & (NW - 1)) * 4 + slot)];
+          int n = 0, f0 = 0;
+          float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f);
+          float kc = 0.f, io = 0.f;
+          int slot = 0;
+          if (ri != 0xff) {
+            const float4* P4 = reinterpret_cast<const float4*>(st + hdr[6]) + ri * 2;
+            q0 = P4[0];
+            const float4 s1 = P4[1];
+            kc = s1.x;
+            io = s1.y;
+            slot = __float_as_int(s1.z);
+            f0 = (int)(rs[ri] - e0);
+            n = (int)(rs[ri + 1] - rs[ri]);
           }
-        }
-        // 8-lane reduce-scatter of a[0..7] (lane lg ends with the group sum of
-        // value lg) plus a butterfly for a[8]; fixed pattern -> deterministic
-        const unsigned F = 0xffffffffu;
-        const bool u4 = lg & 4, u2 = lg & 2, u1 = lg & 1;
-        float w4[4], w2[2];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) w4[k] = (u4 ? a[k + 4] : a[k]) + __shfl_xor_sync(F, u4 ? a[k] : a[k + 4], 4);
-#pragma unroll
-        for (int k = 0; k < 2; ++k) w2[k] = (u2 ? w4[k + 2] : w4[k]) + __shfl_xor_sync(F, u2 ? w4[k] : w4[k + 2], 2);
-        const float w1 = (u1 ? w2[1] : w2[0]) + __shfl_xor_sync(F, u1 ? w2[0] : w2[1], 1);
-        float a8 = a[8];
-        a8 += __shfl_xor_sync(F, a8, 4);
-        a8 += __shfl_xor_sync(F, a8, 2);
-        a8 += __shfl_xor_sync(F, a8, 1);
-        if (ri != 0xff) {
-          float* o = A.out + (size_t)slot * 9;  // pair-run-slot order (read contiguously by the backward)
-          o[lg] = lg == 5 ? w1 * io : ((lg == 2 || lg == 4) ? 0.5f * w1 : w1);
-          if (lg == 0) o[8] = a8;
+          const int nmax = __reduce_max_sync(0xffffffffu, (unsigned)n);
+          if (nmax == 0) continue;
+          float a[9];
+  #pragma unroll
+          for (int k = 0; k < 9; ++k) a[k] = 0.f;
+          const float4* pr = s4 + f0;
+          const float* pd = sd2 + f0;
+          const uint8_t* pp = spx + f0;
+          for (int j = lg; j < nmax; j += 8) {
+            if (j < n) {
+              const float4 r = pr[j];
+              const float d2 = pd[j];
+              const int pl = pp[j];
+              const float4 uu = s_u[pl];
+              const float dx = (float)(pl & 15) - q0.x, dy = (float)(pl >> 4) - q0.y;
+              const float e1 = q0.z * dx + q0.w * dy, e2 = q0.w * dx + kc * dy;
+              const float sa = fmaf(r.z, uu.x, fmaf(r.w, uu.y, d2 * uu.z));
+              const float tt = sa * r.x;
+              const float te1 = tt * e1, te2 = tt * e2;
+              a[0] += te1;
+              a[1] += te2;
+              a[2] = fmaf(te1, e1, a[2]);  // x 1/2 in the epilogue
+              a[3] = fmaf(te1, e2, a[3]);
+              a[4] = fmaf(te2, e2, a[4]);  // x 1/2 in the epilogue
+              a[5] += tt;
+              a[6] = fmaf(r.y, uu.x, a[6]);
+              a[7] = fmaf(r.y, uu.y, a[7]);
+              a[8] = fmaf(r.y, uu.z, a[8]);
+            }
+          }
+          // 8-lane reduce-scatter of a[0..7] (lane lg ends with the group sum of
+          // value lg) plus a butterfly for a[8]; fixed pattern -> deterministic
+          const unsigned F = 0xffffffffu;
+          const bool u4 = lg & 4, u2 = lg & 2, u1 = lg & 1;
+          float w4[4], w2[2];
+  #pragma unroll
+          for (int k = 0; k < 4; ++k) w4[k] = (u4 ? a[k + 4] : a[k]) + __shfl_xor_sync(F, u4 ? a[k] : a[k + 4], 4);
+  #pragma unroll
+          for (int k = 0; k < 2; ++k) w2[k] = (u2 ? w4[k + 2] : w4[k]) + __shfl_xor_sync(F, u2 ? w4[k] : w4[k + 2], 2);
+          const float w1 = (u1 ? w2[1] : w2[0]) + __shfl_xor_sync(F, u1 ? w2[0] : w2[1], 1);
+          float a8 = a[8];
+          a8 += __shfl_xor_sync(F, a8, 4);
+          a8 += __shfl_xor_sync(F, a8, 2);
+          a8 += __shfl_xor_sync(F, a8, 1);
+          if (ri != 0xff) {
+            float* o = A.out + (size_t)slot * 9;  // pair-run-slot order (read contiguously by the backward)
+            o[lg] = lg == 5 ? w1 * io : ((lg == 2 || lg == 4) ? 0.5f * w1 : w1);
+            if (lg == 0) o[8] = a8;
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);

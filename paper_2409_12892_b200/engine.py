@@ -32,6 +32,7 @@ from .scene import Camera, GaussianScene, cameras_struct_tensor, num_coefficient
 
 TILE = 16
 MASK_WORDS = TILE * TILE // 32
+CHUNK_RUNS = 64   # SLM_CHUNK_RUNS: max runs per streaming chunk (bytes of schedule per chunk)
 
 
 @dataclass(frozen=True)
@@ -463,7 +464,7 @@ class CacheSet:
         self.run_start[R:].fill_(self.E)
         self.tile_run_off = torch.empty_like(tile_nruns)
         scan_i32(tile_nruns, self.tile_run_off)
-        # chunk table for the streaming product kernel (<= 32 runs / 512 entries per chunk)
+        # chunk table for the streaming product kernel (<= 64 runs / 896 entries per chunk)
         tile_nch = torch.zeros(nt + 1, dtype=torch.int32, device=dev)
         call("slm_tile_chunks", ptr(self.tile_run_off), nt, ptr(self.run_start), None, ptr(tile_nch), None, 0,
              stream_ptr())
@@ -471,7 +472,7 @@ class CacheSet:
         scan_i32(tile_nch, self.tile_chunk_off)
         self.n_chunks = int(self.tile_chunk_off[nt].item())
         self.chunk_run = torch.empty(self.n_chunks + 1, dtype=torch.int32, device=dev)
-        self.chunk_perm = torch.empty((self.n_chunks + 1) * 32, dtype=torch.uint8, device=dev)
+        self.chunk_perm = torch.empty((self.n_chunks + 1) * CHUNK_RUNS, dtype=torch.uint8, device=dev)
         call("slm_tile_chunks", ptr(self.tile_run_off), nt, ptr(self.run_start), ptr(self.tile_chunk_off),
              ptr(self.chunk_run), ptr(self.chunk_perm), 1, stream_ptr())
         self.chunk_run[self.n_chunks:].fill_(R)

@@ -1,4 +1,4 @@
-# build a tuning variant of the library: tools/build_variant.sh NAME "-DSLM_CH=512 -DSLM_NS=3"
+# build a tuning variant of the library: tools/build_variant.sh NAME "-DSLM_STAGE=25760 -DSLM_NS=3"
 set -e
 D=paper_2409_12892_b200
 mkdir -p $D/_variants/$1
