@@ -254,7 +254,8 @@ int slm_inst_count(const uint32_t* mask, const uint32_t* inst_gid, long long n, 
                    int* pair_cnt, cudaStream_t s);
 int slm_runs_emit(const uint32_t* mask, const uint32_t* inst_gid, const int* used, const int* run_of,
                   const long long* ent_of, long long ibase, long long n, const int* pidx, long long* run_start,
-                  int* run_q, uint32_t* run_mask, int* pair_nruns, long long* inst_start, cudaStream_t s);
+                  int* run_q, uint32_t* run_mask /* optional */, int* pair_nruns, long long* inst_start,
+                  cudaStream_t s);
 int slm_tile_runs(const slm_u2* ranges, int n_tiles, const int* used, const int* run_of, long long ibase, int view,
                   int* tile_nruns, uint32_t* run_tile, const int* view_tile_base, int n_views, cudaStream_t s);
 int slm_pair_runs(const uint32_t* sorted_gid, const unsigned long long* inst_off, long long G,
@@ -290,6 +291,8 @@ long long slm_sort_pairs_u32_workspace(long long n);
 int slm_sort_pairs_u32(void* ws, long long wsb, const uint32_t* kin, uint32_t* kout, const uint32_t* vin,
                        uint32_t* vout, long long n, int begin_bit, int end_bit, cudaStream_t s);
 int slm_iota_u32(uint32_t* out, long long n, cudaStream_t s);
+/* inv[perm[k]] = k for a permutation of [0, n) (run -> pair-run slot) */
+int slm_invert_perm(const int* perm, long long n, int* inv, cudaStream_t s);
 int slm_px_prepare(const uint32_t* cnt, long long n, long long* cnt64, int* nonempty, cudaStream_t s);
 int slm_pairs_prepare(const int* cnt, int V, long long G, long long* cntV, int* flagV, int* flagT, cudaStream_t s);
 int slm_pairs_emit(const int* cnt, int V, long long G, const int* pair_of, const long long* vscan, const int* tscan,

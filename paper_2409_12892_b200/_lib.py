@@ -117,6 +117,7 @@ _SIGS = {
     "slm_sort_pairs_u32_workspace": (c_ll, [c_ll]),
     "slm_sort_pairs_u32": (c_i, [c_vp, c_ll, c_vp, c_vp, c_vp, c_vp, c_ll, c_i, c_i, c_vp]),
     "slm_iota_u32": (c_i, [c_vp, c_ll, c_vp]),
+    "slm_invert_perm": (c_i, [c_vp, c_ll, c_vp, c_vp]),
     "slm_px_prepare": (c_i, [c_vp, c_ll, c_vp, c_vp, c_vp]),
     "slm_pairs_prepare": (c_i, [c_vp, c_i, c_ll, c_vp, c_vp, c_vp, c_vp]),
     "slm_pairs_emit": (c_i, [c_vp, c_i, c_ll, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,

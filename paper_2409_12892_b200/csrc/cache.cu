@@ -119,6 +119,12 @@ __global__ void k_pairs_emit(const int* __restrict__ cnt, int V, long long G, co
   }
 }
 
+// inverse of a permutation of [0, n): inv[perm[k]] = k
+__global__ void k_invert_perm(const int* __restrict__ perm, long long n, int* __restrict__ inv) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+    inv[perm[k]] = (int)k;
+}
+
 __global__ void k_iota_u32(uint32_t* out, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     out[i] = (uint32_t)i;
@@ -141,6 +147,12 @@ int slm_pairs_emit(const int* cnt, int V, long long G, const int* pair_of, const
                    int* pidx, int* gpo, int n_pairs, long long n_entries, cudaStream_t s) {
   k_pairs_emit<<<slm_blocks((long long)V * G, 256), 256, 0, s>>>(cnt, V, G, pair_of, vscan, tscan, splats, pair_off,
                                                                   pair_gid, pair_vm, geo, pidx, gpo, n_pairs, n_entries);
+  return slm_cuda_status();
+}
+
+int slm_invert_perm(const int* perm, long long n, int* inv, cudaStream_t s) {
+  if (n <= 0) return SLM_OK;
+  k_invert_perm<<<slm_blocks(n, 256), 256, 0, s>>>(perm, n, inv);
   return slm_cuda_status();
 }
 

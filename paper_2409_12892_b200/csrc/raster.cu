@@ -312,8 +312,10 @@ __global__ void k_runs_emit(const uint32_t* __restrict__ mask, const uint32_t* _
     const int q = pidx[inst_gid[j]];
     run_start[r] = ent_of[jg];
     run_q[r] = q;
+    if (run_mask) {  // optional per-run keep mask (not needed by the product path)
 #pragma unroll
-    for (int w = 0; w < 8; ++w) run_mask[(size_t)r * 8 + w] = mask[(size_t)j * 8 + w];
+      for (int w = 0; w < 8; ++w) run_mask[(size_t)r * 8 + w] = mask[(size_t)j * 8 + w];
+    }
     atomicAdd(&pair_nruns[q], 1);
   }
 }

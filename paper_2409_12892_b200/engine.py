@@ -451,13 +451,12 @@ class CacheSet:
         R = self.R
         self.run_start = torch.zeros(R + 3, dtype=torch.int64, device=dev)  # +2: 16 B-granular TMA copies
         self.run_q = _empty(R, torch.int32, dev)
-        self.run_mask = _empty(R * MASK_WORDS, torch.int32, dev)
         self.run_tile = _empty(R, torch.int32, dev)
         pair_nruns = torch.zeros(Pn + 1, dtype=torch.int32, device=dev)
         tile_nruns = torch.zeros(nt + 1, dtype=torch.int32, device=dev)
         inst_start = _empty(ni, torch.int64, dev)
         call("slm_runs_emit", ptr(inst_mask), ptr(inst_gid), ptr(inst_used), ptr(run_of), ptr(ent_of), 0, ni,
-             ptr(pidx), ptr(self.run_start), ptr(self.run_q), ptr(self.run_mask), ptr(pair_nruns), ptr(inst_start),
+             ptr(pidx), ptr(self.run_start), ptr(self.run_q), None, ptr(pair_nruns), ptr(inst_start),
              stream_ptr())
         call("slm_tile_runs", ptr(ranges), nt, ptr(inst_used), ptr(run_of), 0, 0, ptr(tile_nruns), ptr(self.run_tile),
              ptr(self.view_tile_base_dev), V, stream_ptr())
@@ -481,12 +480,23 @@ class CacheSet:
         del tile_nch
         self.pair_run_off = torch.empty_like(pair_nruns)
         scan_i32(pair_nruns, self.pair_run_off)
+        # pair -> runs CSR: a stable radix sort of the runs by pair.  Runs are
+        # in (global tile, depth) order, so each pair's runs come out in tile
+        # row-major order -- the (tile row, tile column) order of the
+        # reference's bbox walk (rasterizer.py:283-287).  run_slot: each run's
+        # position in pair_runs (the J^T kernels write run partials there so
+        # the backward reads a gaussian's runs contiguously)
         self.pair_runs = _empty(R, torch.int32, dev)
-        # run_slot: each run's position in pair_runs (J^T kernels write run
-        # partials there so the backward reads a gaussian's runs contiguously)
         self.run_slot = torch.empty(max(R, 1), dtype=torch.int32, device=dev)
-        call("slm_pair_runs", ptr(sv), ptr(inst_off), G, ptr(post_of_pre), ptr(inst_used), ptr(run_of), 0, ptr(pidx),
-             ptr(self.pair_run_off), ptr(self.pair_runs), VG, 1, ptr(self.run_slot), stream_ptr())
+        if R > 0:
+            rid = _empty(R, torch.int32, dev)
+            call("slm_iota_u32", ptr(rid), R, stream_ptr())
+            qk = _empty(R, torch.int32, dev)
+            ws = _empty(_lib.load().slm_sort_pairs_u32_workspace(R), torch.uint8, dev)
+            call("slm_sort_pairs_u32", ptr(ws), ws.numel(), ptr(self.run_q), ptr(qk), ptr(rid), ptr(self.pair_runs),
+                 R, 0, _bits(Pn), stream_ptr())
+            del ws, qk, rid
+            call("slm_invert_perm", ptr(self.pair_runs), R, ptr(self.run_slot), stream_ptr())
         del sv, inst_off, post_of_pre
         del pidx, pair_nruns, tile_nruns, inst_used, run_of, ent_of
         T.tick("runs_pairs")
