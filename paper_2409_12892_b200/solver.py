@@ -173,6 +173,65 @@ class Combiner:
         return out
 
 
+class _GtPrefetch:
+    """Host -> device copies of the next subset's ground-truth images on a side
+    stream into one of two persistent device buffers (double buffering: a
+    buffer is refilled only after the compute stream has consumed it, i.e.
+    after the build of the subset two steps back).  Device-resident images
+    pass through untouched."""
+
+    def __init__(self, gts, device, shards):
+        self.gts, self.device = gts, device
+        self.host = any(not g.is_cuda for g in gts)
+        self.pending = None
+        if self.host:
+            need = max((sum(self._nbytes(gts[i]) for i in views) for _, views in shards), default=0)
+            self.buf = [torch.empty(max(need, 1), dtype=torch.uint8, device=device) for _ in range(2)]
+            self.free = [None, None]
+            self.stream = torch.cuda.Stream(device)
+
+    @staticmethod
+    def _nbytes(g):
+        return 0 if g.is_cuda else (g.numel() * g.element_size() + 255) // 256 * 256
+
+    def start(self, k, views):
+        if not self.host:
+            self.pending = ([self.gts[i] for i in views], None, None)
+            return
+        b = k % 2
+        out, off = [], 0
+        with torch.cuda.stream(self.stream):
+            if self.free[b] is not None:
+                self.stream.wait_event(self.free[b])
+            for i in views:
+                g = self.gts[i]
+                if g.is_cuda:
+                    out.append(g)
+                    continue
+                nb = g.numel() * g.element_size()
+                dst = self.buf[b][off:off + nb].view(g.dtype).view(g.shape)
+                dst.copy_(g, non_blocking=True)
+                out.append(dst)
+                off += self._nbytes(g)
+            ev = torch.cuda.Event()
+            ev.record(self.stream)
+        self.pending = (out, ev, b)
+
+    def take(self):
+        out, ev, b = self.pending
+        self.pending = None
+        if ev is not None:
+            torch.cuda.current_stream(self.device).wait_event(ev)
+        return out, b
+
+    def release(self, b):
+        """The compute stream is done with buffer b once the queued work so far ran."""
+        if b is not None:
+            e = torch.cuda.Event()
+            e.record(torch.cuda.current_stream(self.device))
+            self.free[b] = e
+
+
 @dataclass
 class StepReport:
     delta: torch.Tensor
@@ -187,15 +246,27 @@ def lm_direction(scene, cameras, gts, schedule: BatchSchedule = BatchSchedule(),
                  n_iters: int = 8, config=None, loss: LossConfig = LossConfig(), rank: int = 0,
                  world_size: int = 1, product_timer=None, keep_caches: bool = False) -> StepReport:
     """One LM update direction: per subset cache build, b, M, PCG, Eq. 7
-    combine; subsets are sharded round-robin over ranks."""
+    combine; subsets are sharded round-robin over ranks.
+
+    Ground-truth images may live in (pinned) host memory: each subset's images
+    are then copied on a side stream while the previous subset is solved."""
     n = scene.param_count
     comb = Combiner(n, scene.device)
     ws = PCGWorkspace(n, scene.device)
     energy = 0.0
     entries, pcg_stats = [], []
     caches = []
-    for j, views in schedule.shard(len(cameras), rank, world_size):
-        cs = CacheSet(scene, [cameras[i] for i in views], [gts[i] for i in views], config, loss)
+    shards = list(schedule.shard(len(cameras), rank, world_size))
+    fetch = _GtPrefetch(gts, scene.device, shards)
+    if shards:
+        fetch.start(0, shards[0][1])
+    for k, (j, views) in enumerate(shards):
+        gts_sub, buf = fetch.take()
+        if k + 1 < len(shards):
+            fetch.start(k + 1, shards[k + 1][1])
+        cs = CacheSet(scene, [cameras[i] for i in views], gts_sub, config, loss)
+        fetch.release(buf)  # the images are only read by the build's residual pass
+        del gts_sub
         energy += sum(cs.energies)
         entries.append(cs.E)
         b = cs.rhs()

@@ -240,6 +240,15 @@ def test_lm_direction_batched(posed):
     assert rel(rep.delta.cpu().numpy(), ref) < PCG_TOL
 
 
+def test_lm_direction_host_images(posed):
+    """Ground truth in pinned host memory (copied per subset on a side stream
+    while the previous subset is solved) gives the same bits as device images."""
+    dev = lm_direction(posed["scene"], posed["cams"], posed["gts_d"], BatchSchedule(2), 1e-4, 8)
+    host = [g.cpu().pin_memory() for g in posed["gts_d"]]
+    hst = lm_direction(posed["scene"], posed["cams"], host, BatchSchedule(2), 1e-4, 8)
+    assert torch.equal(dev.delta, hst.delta)
+
+
 def test_determinism(prob):
     outs = []
     for _ in range(2):

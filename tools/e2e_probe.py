@@ -48,3 +48,22 @@ r = lm_direction(sc, cams, gd, sched, 1e-4, 8, None, LossConfig())
 b = ev()
 torch.cuda.synchronize()
 print("host inputs ms", a.elapsed_time(b), "wall", time.perf_counter() - t0)
+for rep in range(3):
+    a = ev()
+    xs = x_host.to(dev, non_blocking=True)
+    sc = GaussianScene(xs, scene.sh_degree, scene.background)
+    r = lm_direction(sc, cams, g_host, sched, 1e-4, 8, None, LossConfig())
+    b = ev()
+    torch.cuda.synchronize()
+    print("host images streamed per subset ms", a.elapsed_time(b))
+    a = ev()
+    xs = x_host.to(dev, non_blocking=True)
+    gd = [g.to(dev, non_blocking=True) for g in g_host]
+    sc = GaussianScene(xs, scene.sh_degree, scene.background)
+    r = lm_direction(sc, cams, gd, sched, 1e-4, 8, None, LossConfig())
+    b = ev()
+    torch.cuda.synchronize()
+    print("host inputs copied up front ms", a.elapsed_time(b))
+    a = ev(); lm_direction(scene, cams, gts, sched, 1e-4, 8, None, LossConfig()); b = ev()
+    torch.cuda.synchronize()
+    print("device inputs ms", a.elapsed_time(b))
