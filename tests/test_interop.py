@@ -51,3 +51,29 @@ def test_cache_dump_matches_oracle(tmp_path):
     assert np.array_equal(d["pixel_ids"], v.pixel) and np.array_equal(d["gaussian_ids"], v.gid)
     assert rel(d["alphas"], v.alpha) < 1e-7 and rel(d["transmittances"], v.T) < 1e-6
     assert rel(d["dc_dalpha"], v.dcda) < 1e-6 and rel(d["dc_dcs"], v.dcdc) < 1e-7
+
+
+def test_pfm_roundtrip(tmp_path):
+    from paper_2409_12892_b200 import imageio as IO
+    img = np.random.default_rng(0).standard_normal((5, 7, 3)).astype(np.float32)
+    IO.write_pfm(tmp_path / "a.pfm", torch.from_numpy(img))
+    back = IO.read_pfm(tmp_path / "a.pfm")
+    assert back.dtype == np.float64 and np.array_equal(back, img.astype(np.float64))
+    with pytest.raises(ValueError):
+        IO.write_pfm(tmp_path / "b.pfm", img[..., :2])
+
+
+@pytest.mark.reference
+def test_pfm_png_match_reference(ref_modules, tmp_path):
+    import sys
+    from paper_2409_12892_b200 import imageio as IO
+    sys.path.insert(0, "/root/reference/pkg/src")
+    from splatlm import imageio as RI
+    img = np.random.default_rng(1).uniform(-0.2, 1.2, (6, 9, 3))
+    IO.write_pfm(tmp_path / "o.pfm", img)
+    RI.write_pfm(tmp_path / "r.pfm", img)
+    assert (tmp_path / "o.pfm").read_bytes() == (tmp_path / "r.pfm").read_bytes()
+    assert np.array_equal(IO.read_pfm(tmp_path / "r.pfm"), RI.read_pfm(tmp_path / "o.pfm"))
+    IO.write_png(tmp_path / "o.png", img)
+    RI.write_png(tmp_path / "r.png", img)
+    assert np.array_equal(IO.read_png(tmp_path / "o.png"), RI.read_png(tmp_path / "r.png"))
