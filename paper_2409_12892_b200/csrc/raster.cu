@@ -495,7 +495,52 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
       nrel += __popc(bal);
     }
     __syncwarp();
-    for (int ki = 0; ki < nrel;) {
+    if (!FILL) {
+      // COUNT, lane queues: per block of 32 relevant instances each lane
+      // collects the ones whose bbox holds its pixel (a 32-bit word) and
+      // walks its own set bits in order, so a step evaluates one (instance,
+      // pixel) pair on every busy lane instead of idling the lanes outside
+      // the bbox; per-pixel depth order is kept.  Keep masks are assembled
+      // with shared-memory atomicOr (order-independent).
+      for (int ki = lane; ki < nrel; ki += 32) s_mask[s_list[warp][ki] * RW + warp] = 0u;
+      __syncwarp();
+      for (int b0 = 0; b0 < nrel; b0 += 32) {
+        const int nbk = min(32, nrel - b0);
+        unsigned wq = 0u;
+        if (!done) {
+          for (int i = 0; i < nbk; ++i) {
+            const int4 bx = s_box[s_list[warp][b0 + i]];
+            wq |= (unsigned)(px >= bx.x && px <= bx.y && py >= bx.z && py <= bx.w) << i;
+          }
+        }
+        while (__any_sync(0xffffffffu, wq != 0u)) {
+          if (wq == 0u) continue;
+          const int k = s_list[warp][b0 + __ffs(wq) - 1];
+          wq &= wq - 1u;
+          const double dx = __dsub_rn(dxp, s_mx[k]);
+          const double dy = __dsub_rn(dyp, s_my[k]);
+          const double q = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(s_ca[k], dx), dx), __dmul_rn(s_cc[k], __dmul_rn(dy, dy))),
+                                     __dmul_rn(__dmul_rn(__dmul_rn(2.0, s_cb[k]), dy), dx));
+          const double ex = __dmul_rn(-0.5, q);
+          double a = ex >= -40.0 ? __dmul_rn(s_o[k], slm_exp_neg(ex)) : 0.0;
+          a = a < aclamp ? a : aclamp;
+          if ((a >= amin) && (a > 0.0)) {  // T >= t_stop holds while the lane is not done
+            atomicOr(&s_mask[k * RW + warp], 1u << lane);
+            const double wgt = __dmul_rn(a, T);
+            C0 = __dadd_rn(C0, __dmul_rn(wgt, s_c0[k]));
+            C1 = __dadd_rn(C1, __dmul_rn(wgt, s_c1[k]));
+            C2 = __dadd_rn(C2, __dmul_rn(wgt, s_c2[k]));
+            T = __dmul_rn(T, 1.0 - a);
+            ++cnt;
+            if (T < tstop) {
+              done = true;
+              wq = 0u;
+            }
+          }
+        }
+      }
+    }
+    for (int ki = 0; FILL && ki < nrel;) {
       int k;
       unsigned mk = 0u;  // FILL: the keep mask of this lane's instance in the wave
       if (FILL) {
