@@ -540,60 +540,39 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
         }
       }
     }
-    for (int ki = 0; FILL && ki < nrel;) {
-      int k;
-      unsigned mk = 0u;  // FILL: the keep mask of this lane's instance in the wave
-      if (FILL) {
-        // a wave = consecutive relevant instances whose keep masks over the
-        // warp's pixels are pairwise disjoint: each lane keeps at most one of
-        // them, so one fp64 evaluation per lane covers the whole wave and the
-        // per-pixel depth order is preserved
-        unsigned occ = 0u;
-        k = -1;
-        for (int nw = 0; ki < nrel && nw < 8; ++nw, ++ki) {
-          const int kk = s_list[warp][ki];
-          const unsigned mw = s_mask[kk * RW + warp];
-          if (mw & occ) break;
-          occ |= mw;
-          if ((mw >> lane) & 1u) {
-            k = kk;
-            mk = mw;
+    if (FILL) {
+      // FILL, lane queues over the COUNT keep masks: per block of 32 relevant
+      // instances each lane walks the ones that kept its pixel, in depth
+      // order, and writes their records (every step is a cache entry)
+      for (int b0 = 0; b0 < nrel; b0 += 32) {
+        const int nbk = min(32, nrel - b0);
+        unsigned wq = 0u;
+        for (int i = 0; i < nbk; ++i) wq |= ((s_mask[s_list[warp][b0 + i] * RW + warp] >> lane) & 1u) << i;
+        while (__any_sync(0xffffffffu, wq != 0u)) {
+          if (wq == 0u) continue;
+          const int k = s_list[warp][b0 + __ffs(wq) - 1];
+          wq &= wq - 1u;
+          const double dx = __dsub_rn(dxp, s_mx[k]);
+          const double dy = __dsub_rn(dyp, s_my[k]);
+          const double q = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(s_ca[k], dx), dx), __dmul_rn(s_cc[k], __dmul_rn(dy, dy))),
+                                     __dmul_rn(__dmul_rn(__dmul_rn(2.0, s_cb[k]), dy), dx));
+          const double ex = __dmul_rn(-0.5, q);
+          double a = ex >= -40.0 ? __dmul_rn(s_o[k], slm_exp_neg(ex)) : 0.0;
+          a = a < aclamp ? a : aclamp;
+          const double wgt = __dmul_rn(a, T);
+          C0 = __dadd_rn(C0, __dmul_rn(wgt, s_c0[k]));
+          C1 = __dadd_rn(C1, __dmul_rn(wgt, s_c1[k]));
+          C2 = __dadd_rn(C2, __dmul_rn(wgt, s_c2[k]));
+          if (A.rec4) {
+            const unsigned m = s_mask[k * RW + warp];
+            const double iom = 1.0 / (1.0 - a);  // stored values are fp32: one fp64 reciprocal suffices
+            const long long dest = s_start[k] + s_pre[k * RW + warp] + __popc(m & lanes_below);
+            A.rec4[dest] = make_float4(a < aclamp ? (float)a : 0.0f, (float)wgt,
+                                       (float)(s_c0[k] * T - (tot0 - C0) * iom),
+                                       (float)(s_c1[k] * T - (tot1 - C1) * iom));
+            A.rec_d2[dest] = (float)(s_c2[k] * T - (tot2 - C2) * iom);
+            A.rec_pix[dest] = (uint8_t)threadIdx.x;
           }
-        }
-      } else {
-        k = s_list[warp][ki++];
-      }
-      bool keep = false;
-      double a = 0.0;
-      const int4 bx = k >= 0 ? s_box[k] : make_int4(1, 0, 1, 0);
-      bool inb = !done && k >= 0 && px >= bx.x && px <= bx.y && py >= bx.z && py <= bx.w;
-      if (inb) {
-        // -(1/2) d^T conic d in the reference's evaluation order
-        double dx = __dsub_rn(dxp, s_mx[k]);
-        double dy = __dsub_rn(dyp, s_my[k]);
-        double q = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(s_ca[k], dx), dx), __dmul_rn(s_cc[k], __dmul_rn(dy, dy))),
-                             __dmul_rn(__dmul_rn(__dmul_rn(2.0, s_cb[k]), dy), dx));
-        const double ex = __dmul_rn(-0.5, q);
-        a = ex >= -40.0 ? __dmul_rn(s_o[k], slm_exp_neg(ex)) : 0.0;  // exp(-40) * o << alpha_min
-        a = a < aclamp ? a : aclamp;
-        keep = (a >= amin) && (a > 0.0) && (T >= tstop);
-      }
-      const unsigned m = FILL ? mk : __ballot_sync(0xffffffffu, keep);
-      if (!FILL && lane == 0) s_mask[k * RW + warp] = m;
-      if (keep) {
-        const double wgt = __dmul_rn(a, T);
-        C0 = __dadd_rn(C0, __dmul_rn(wgt, s_c0[k]));
-        C1 = __dadd_rn(C1, __dmul_rn(wgt, s_c1[k]));
-        C2 = __dadd_rn(C2, __dmul_rn(wgt, s_c2[k]));
-        if (FILL && A.rec4) {
-          const double iom = 1.0 / (1.0 - a);  // stored values are fp32: one fp64 reciprocal suffices
-          const long long dest = s_start[k] + s_pre[k * RW + warp] + __popc(m & lanes_below);
-          A.rec4[dest] = make_float4(a < aclamp ? (float)a : 0.0f, (float)wgt,
-                                     (float)(s_c0[k] * T - (tot0 - C0) * iom), (float)(s_c1[k] * T - (tot1 - C1) * iom));
-          A.rec_d2[dest] = (float)(s_c2[k] * T - (tot2 - C2) * iom);
-          A.rec_pix[dest] = (uint8_t)threadIdx.x;
-        }
-        if (FILL) {
           if (A.trav_gid) {
             const long long le = e - A.view_entry_base;
             A.trav_gid[le] = s_gid[k];
@@ -601,11 +580,10 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
             A.trav_T[le] = T;
           }
           ++e;
+          T = __dmul_rn(T, 1.0 - a);
         }
-        T = __dmul_rn(T, 1.0 - a);
-        ++cnt;
-        if (T < tstop) done = true;  // no later splat can pass T >= t_stop
       }
+      done = done || T < tstop;
     }
     __syncthreads();
     if (!FILL && A.inst_mask) {
