@@ -164,6 +164,9 @@ typedef struct {
   const slm_f4* u;           /* applyJT input, per pixel */
   slm_f4* u_out;             /* applyJ output, per pixel */
   float* out;                /* applyJT [R*9] / diag [R*14] run partials */
+  int* tile_counter;         /* streaming kernels: 1 int of device scratch for
+                                dynamic tile scheduling (reset by the launch);
+                                NULL: static round-robin tiles */
 } SlmTileArgs;
 
 /* per-pair forward chain (applyJ) */

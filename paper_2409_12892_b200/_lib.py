@@ -63,7 +63,7 @@ class SlmTileArgs(C.Structure):
                 ("run_start", c_vp), ("run_q", c_vp), ("run_tile", c_vp), ("run_static", c_vp), ("pm", c_vp),
                 ("geo", c_vp), ("ptab", c_vp),
                 ("rec4", c_vp), ("d2", c_vp), ("pix", c_vp),
-                ("gradr", c_vp), ("u", c_vp), ("u_out", c_vp), ("out", c_vp)]
+                ("gradr", c_vp), ("u", c_vp), ("u_out", c_vp), ("out", c_vp), ("tile_counter", c_vp)]
 
 
 class SlmFwdArgs(C.Structure):

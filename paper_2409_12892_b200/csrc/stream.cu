@@ -33,6 +33,7 @@ static_assert(CR % 32 == 0 && CR <= 255, "run slots are bytes, 32 per J^T round"
 #define NS SLM_NS        // ring stages
 #define PAR 16           // floats per run parameter record
 #define TMETA 64         // producer chunk-metadata window
+#define TQ 4             // tile queue depth (producer -> consumers)
 
 #define MODE_J 1
 #define MODE_WRITEU 2
@@ -240,6 +241,11 @@ template <int MODE>
 __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t full[NS], empty[NS];
+  // tile queue: the producer claims tiles from a global counter (dynamic
+  // load balance over tiles of very different sizes; results do not depend
+  // on which CTA runs a tile) and hands them to the consumers in order
+  __shared__ uint64_t tq_full[TQ], tq_empty[TQ];
+  __shared__ int tq[TQ];
   unsigned char* sp = smem;
   float4* s_u = reinterpret_cast<float4*>(sp);
   sp += 256 * 16;
@@ -255,6 +261,10 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
       mbar_init(&full[s], 1 + 32);  // producer lane 0 (expect_tx) + 32 cp.async arrivals
       mbar_init(&empty[s], NW);
     }
+    for (int s = 0; s < TQ; ++s) {
+      mbar_init(&tq_full[s], 1);
+      mbar_init(&tq_empty[s], NW);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -264,7 +274,17 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
     // ------------------------------ producer ------------------------------
     const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
     unsigned g = 0;
-    for (int t = blockIdx.x; t < A.n_tiles; t += gridDim.x) {
+    for (unsigned tk = 0;; ++tk) {
+      int t = 0;
+      if (lane == 0) {
+        t = A.tile_counter ? atomicAdd(A.tile_counter, 1) : (int)(blockIdx.x + tk * gridDim.x);
+        const unsigned qs = tk % TQ;
+        if (tk >= TQ) mbar_wait(&tq_empty[qs], ((tk / TQ) - 1) & 1u);
+        tq[qs] = t < A.n_tiles ? t : -1;
+        mbar_arrive(&tq_full[qs]);
+      }
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t >= A.n_tiles) break;
       const int c0 = A.tile_chunk_off[t], c1 = A.tile_chunk_off[t + 1];
       for (int pass = 0; pass < n_pass; ++pass) {
         // the cache of a tile is read twice in the fused mode: keep it in L2
@@ -354,7 +374,13 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
   float4* acc = s_acc + warp * 256;
   const int p = threadIdx.x;
   const int slot = lane >> 3, lg = lane & 7;  // J^T: 4 groups of 8 lanes per warp
-  for (int t = blockIdx.x; t < A.n_tiles; t += gridDim.x) {
+  for (unsigned tk = 0;; ++tk) {
+    const unsigned qs = tk % TQ;
+    mbar_wait(&tq_full[qs], (tk / TQ) & 1u);
+    const int t = tq[qs];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&tq_empty[qs]);
+    if (t < 0) break;
     const int v = view_of_tile(A.view_tile_base, A.n_views, t);
     const SlmView vw = A.views[v];
     const int tiles_x = (vw.W + SLM_TILE - 1) / SLM_TILE;
@@ -662,6 +688,7 @@ static int launch_stream(const SlmTileArgs* a, cudaStream_t st) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stream<MODE>, NT, bytes);
   if (per_sm < 1) per_sm = 1;
   const int grid = (int)std::min<long long>((long long)a->n_tiles, (long long)sms * per_sm);
+  if (a->tile_counter) cudaMemsetAsync(a->tile_counter, 0, sizeof(int), st);
   k_stream<MODE><<<grid, NT, bytes, st>>>(*a);
   return slm_cuda_status();
 }

@@ -488,6 +488,7 @@ class CacheSet:
         # the backward reads a gaussian's runs contiguously)
         self.pair_runs = _empty(R, torch.int32, dev)
         self.run_slot = torch.empty(max(R, 1), dtype=torch.int32, device=dev)
+        self.tile_counter = torch.zeros(1, dtype=torch.int32, device=dev)  # dynamic tile scheduling scratch
         if R > 0:
             rid = _empty(R, torch.int32, dev)
             call("slm_iota_u32", ptr(rid), R, stream_ptr())
@@ -568,6 +569,7 @@ class CacheSet:
         a.geo = ptr(self.pair_geo)
         a.rec4, a.d2 = ptr(self.rec4), ptr(self.rec_d2)
         a.pix = ptr(self.rec_pix)
+        a.tile_counter = ptr(self.tile_counter)
         return a
 
     def _backward(self, run_acc, d, out, mode, scale=1.0, p=None, M=None, lam=0.0, dot_part=None, lam_out=True,
