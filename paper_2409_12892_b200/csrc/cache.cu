@@ -86,32 +86,65 @@ __global__ void k_pairs_prepare(const int* __restrict__ cnt /*[V][G]*/, int V, l
   }
 }
 
-__global__ void k_pairs_emit(const int* __restrict__ cnt, int V, long long G, const int* __restrict__ pair_of,
-                             const long long* __restrict__ vscan, const int* __restrict__ tscan,
-                             const SlmSplat* __restrict__ splats /*[V][G]*/, long long* __restrict__ pair_off,
-                             int* __restrict__ pair_gid, uint32_t* __restrict__ pair_vm,
-                             SlmPairGeo* __restrict__ geo, int* __restrict__ pidx, int* __restrict__ gpo /*[G+1]*/,
-                             int n_pairs, long long n_entries) {
-  long long n = (long long)V * G;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const long long v = i / G, g = i % G;
-    if (v == 0) gpo[g] = tscan[g * V];
-    const int c = cnt[i];
-    if (c <= 0) {
-      pidx[i] = -1;
-      continue;
+// Tiled transpose: a block owns PE_SLOTS / V gaussians x all V views.  The
+// view-major inputs (counts, entry scan) are read coalesced and staged in
+// shared memory, the pair outputs are written in (gid, view) order (their q
+// indices are consecutive) and pidx goes back out view-major -- instead of
+// scattering every pair record from a view-major sweep.
+#define PE_SLOTS 1024
+__global__ void __launch_bounds__(256) k_pairs_emit(const int* __restrict__ cnt, int V, long long G,
+                                                    const int* __restrict__ pair_of,
+                                                    const long long* __restrict__ vscan, const int* __restrict__ tscan,
+                                                    const SlmSplat* __restrict__ splats /*[V][G]*/,
+                                                    long long* __restrict__ pair_off, int* __restrict__ pair_gid,
+                                                    uint32_t* __restrict__ pair_vm, SlmPairGeo* __restrict__ geo,
+                                                    int* __restrict__ pidx, int* __restrict__ gpo /*[G+1]*/,
+                                                    int n_pairs, long long n_entries) {
+  __shared__ int s_c[PE_SLOTS], s_q[PE_SLOTS];
+  __shared__ long long s_vs[PE_SLOTS];
+  (void)pair_of;
+  const int GB = PE_SLOTS / V;  // gaussians per block (V <= 255 -> >= 4)
+  const int ns = GB * V;
+  for (long long g0 = (long long)blockIdx.x * GB; g0 < G; g0 += (long long)gridDim.x * GB) {
+    const int gb = (int)min((long long)GB, G - g0);
+    // 1: view-major reads (consecutive threads = consecutive gaussians of a view)
+    for (int k = threadIdx.x; k < ns; k += blockDim.x) {
+      const int v = k / GB, gl = k - v * GB;
+      if (gl < gb) {
+        const long long i = (long long)v * G + g0 + gl;
+        const int c = cnt[i];
+        s_c[gl * V + v] = c;
+        s_vs[gl * V + v] = c > 0 ? vscan[i] : 0;
+      }
     }
-    const int q = tscan[g * V + v];  // (gid, view) numbering
-    pair_off[q] = vscan[i];
-    pair_gid[q] = (int)g;
-    const SlmSplat s = splats[i];
-    pair_vm[q] = (uint32_t)v | (((s.flags >> 1) & 7u) << 16);
-    SlmPairGeo pg;
-    pg.mx = s.mx; pg.my = s.my;
-    pg.ka = (float)s.ca; pg.kb = (float)s.cb; pg.kc = (float)s.cc;
-    pg.inv_o = (float)(1.0 / s.o);
-    geo[q] = pg;
-    pidx[i] = q;
+    __syncthreads();
+    // 2: (gid, view) order: q = tscan is consecutive over the pairs
+    for (int k = threadIdx.x; k < gb * V; k += blockDim.x) {
+      const int gl = k / V, v = k - gl * V;
+      const long long g = g0 + gl;
+      const int q = tscan[g * V + v];
+      if (v == 0) gpo[g] = q;
+      const int c = s_c[k];
+      s_q[k] = c > 0 ? q : -1;
+      if (c > 0) {
+        const SlmSplat sp = splats[(long long)v * G + g];
+        pair_off[q] = s_vs[k];
+        pair_gid[q] = (int)g;
+        pair_vm[q] = (uint32_t)v | (((sp.flags >> 1) & 7u) << 16);
+        SlmPairGeo pg;
+        pg.mx = sp.mx; pg.my = sp.my;
+        pg.ka = (float)sp.ca; pg.kb = (float)sp.cb; pg.kc = (float)sp.cc;
+        pg.inv_o = (float)(1.0 / sp.o);
+        geo[q] = pg;
+      }
+    }
+    __syncthreads();
+    // 3: pidx back in view-major order
+    for (int k = threadIdx.x; k < ns; k += blockDim.x) {
+      const int v = k / GB, gl = k - v * GB;
+      if (gl < gb) pidx[(long long)v * G + g0 + gl] = s_q[gl * V + v];
+    }
+    __syncthreads();
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     gpo[G] = n_pairs;
@@ -145,7 +178,9 @@ int slm_pairs_prepare(const int* cnt, int V, long long G, long long* cntV, int* 
 int slm_pairs_emit(const int* cnt, int V, long long G, const int* pair_of, const long long* vscan, const int* tscan,
                    const SlmSplat* splats, long long* pair_off, int* pair_gid, uint32_t* pair_vm, SlmPairGeo* geo,
                    int* pidx, int* gpo, int n_pairs, long long n_entries, cudaStream_t s) {
-  k_pairs_emit<<<slm_blocks((long long)V * G, 256), 256, 0, s>>>(cnt, V, G, pair_of, vscan, tscan, splats, pair_off,
+  if (V <= 0 || V > 255) return SLM_ERR_ARG;
+  const long long GB = PE_SLOTS / V;
+  k_pairs_emit<<<slm_blocks((G + GB - 1) / GB, 1, 1LL << 30), 256, 0, s>>>(cnt, V, G, pair_of, vscan, tscan, splats, pair_off,
                                                                   pair_gid, pair_vm, geo, pidx, gpo, n_pairs, n_entries);
   return slm_cuda_status();
 }
