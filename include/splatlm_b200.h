@@ -251,8 +251,9 @@ int slm_tile_ranges(const unsigned long long* keys, long long n, int rank_bits, 
  * (build_cache, jacobian.py:383-409) and/or the Traversals arrays */
 int slm_raster_count(const SlmRasterArgs* a, cudaStream_t s);
 int slm_raster_fill(const SlmRasterArgs* a, cudaStream_t s);
-/* runs: per-instance counts (+ per-(view,gaussian) counts), the run table,
- * runs per tile and the pair -> runs CSR (filled in a fixed order) */
+/* runs: per-instance counts (+ per-(view,gaussian) counts), the run table and
+ * runs per tile (the pair -> runs CSR is a stable slm_sort_pairs_u32 of the
+ * runs by pair + slm_invert_perm) */
 int slm_inst_count(const uint32_t* mask, const uint32_t* inst_gid, long long n, long long* cnt, int* used,
                    int* pair_cnt, cudaStream_t s);
 int slm_runs_emit(const uint32_t* mask, const uint32_t* inst_gid, const int* used, const int* run_of,
@@ -261,9 +262,6 @@ int slm_runs_emit(const uint32_t* mask, const uint32_t* inst_gid, const int* use
                   cudaStream_t s);
 int slm_tile_runs(const slm_u2* ranges, int n_tiles, const int* used, const int* run_of, long long ibase, int view,
                   int* tile_nruns, uint32_t* run_tile, const int* view_tile_base, int n_views, cudaStream_t s);
-int slm_pair_runs(const uint32_t* sorted_gid, const unsigned long long* inst_off, long long G,
-                  const uint32_t* post_of_pre, const int* used, const int* run_of, long long ibase, const int* pidx,
-                  const int* pair_run_off, int* pair_runs, long long n, int batched, int* run_slot, cudaStream_t s);
 /* subset-batched projection and binning (all V views of a cache subset per
  * launch): element v * G + g, sorted value (v << 24) | g, global tiles
  * view_tile_base[v] + ty * tiles_x + tx */
@@ -296,7 +294,6 @@ int slm_sort_pairs_u32(void* ws, long long wsb, const uint32_t* kin, uint32_t* k
 int slm_iota_u32(uint32_t* out, long long n, cudaStream_t s);
 /* inv[perm[k]] = k for a permutation of [0, n) (run -> pair-run slot) */
 int slm_invert_perm(const int* perm, long long n, int* inv, cudaStream_t s);
-int slm_px_prepare(const uint32_t* cnt, long long n, long long* cnt64, int* nonempty, cudaStream_t s);
 int slm_pairs_prepare(const int* cnt, int V, long long G, long long* cntV, int* flagV, int* flagT, cudaStream_t s);
 int slm_pairs_emit(const int* cnt, int V, long long G, const int* pair_of, const long long* vscan, const int* tscan,
                    const SlmSplat* splats, long long* pair_off, int* pair_gid, uint32_t* pair_vm, SlmPairGeo* geo,
@@ -320,8 +317,8 @@ int slm_tile_chunks(const int* tile_run_off, int n_tiles, const long long* run_s
                     int* out, uint8_t* chunk_perm, int fill, cudaStream_t s);
 int slm_chunk_perm(const int* chunk_run, long long n_chunks, const long long* run_start, uint8_t* chunk_perm,
                    cudaStream_t s);
-/* diag_jtj (jacobian.py:486-512), first half: per-pair coefficient tables,
- * then 14 sums per run (a->gradr = grad_r_sq, a->ptab = tables) */
+/* diag_jtj (jacobian.py:486-512), first half: per-pair coefficient tables
+ * (then slm_diag_stream) */
 int slm_pair_tables(const float* xs, long long G, int sh_degree, const int* pair_gid, const uint32_t* pair_vm,
                     const SlmCamera* cams, int n_pairs, float* tab, const float* gtab, cudaStream_t s);
 /* view-independent part of the per-gaussian chain (rotation, scales, the
@@ -329,9 +326,8 @@ int slm_pair_tables(const float* xs, long long G, int sh_degree, const int* pair
  * gaussian; once per cache (ref: jacobian.py:159-190, 213-240) */
 int slm_gauss_tab(const float* xs, long long G, float* gtab, cudaStream_t s);
 int slm_gauss_tab_floats(void);
-int slm_diag_runs(const SlmTileArgs* a, cudaStream_t s);
-/* the same 14 sums per run on the streaming kernel, written in pair-run-slot
- * order (a->ptab from slm_pair_tables) */
+/* 14 diag sums per run on the streaming kernel, written in pair-run-slot
+ * order (a->gradr = grad_r_sq, a->ptab from slm_pair_tables) */
 int slm_diag_stream(const SlmTileArgs* a, cudaStream_t s);
 /* forward chain m = dy/dx p per pair (jacobian.py:434-443), 48 B per pair */
 int slm_pair_forward(const SlmFwdArgs* a, int sh_degree, cudaStream_t s);
@@ -363,7 +359,6 @@ int slm_transpose_f32(const float* in, float* out, long long rows, long long col
 int slm_transpose_f64(const double* in, double* out, long long rows, long long cols, cudaStream_t s);
 int slm_f64_to_f32(const double* in, float* out, long long n, cudaStream_t s);
 int slm_axpy_scene(const double* x, const float* d, double gamma, double* out, long long n, cudaStream_t s);
-int slm_sum_parts(const double* part, int n, double* out, cudaStream_t s);
 
 #ifdef __cplusplus
 }

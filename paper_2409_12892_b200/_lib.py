@@ -103,7 +103,6 @@ _SIGS = {
     "slm_inst_count": (c_i, [c_vp, c_vp, c_ll, c_vp, c_vp, c_vp, c_vp]),
     "slm_runs_emit": (c_i, [c_vp, c_vp, c_vp, c_vp, c_vp, c_ll, c_ll, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "slm_tile_runs": (c_i, [c_vp, c_i, c_vp, c_vp, c_ll, c_i, c_vp, c_vp, c_vp, c_i, c_vp]),
-    "slm_pair_runs": (c_i, [c_vp, c_vp, c_ll, c_vp, c_vp, c_vp, c_ll, c_vp, c_vp, c_vp, c_ll, c_i, c_vp, c_vp]),
     "slm_preprocess_views": (c_i, [c_vp, c_ll, c_i, c_vp, c_i, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "slm_tile_count_v": (c_i, [c_vp, c_ll, c_ll, c_vp, c_vp, c_vp, c_vp]),
     "slm_tile_emit_v": (c_i, [c_vp, c_vp, c_ll, c_ll, c_vp, c_vp, c_vp, c_i, c_vp, c_vp, c_vp, c_vp]),
@@ -118,7 +117,6 @@ _SIGS = {
     "slm_sort_pairs_u32": (c_i, [c_vp, c_ll, c_vp, c_vp, c_vp, c_vp, c_ll, c_i, c_i, c_vp]),
     "slm_iota_u32": (c_i, [c_vp, c_ll, c_vp]),
     "slm_invert_perm": (c_i, [c_vp, c_ll, c_vp, c_vp]),
-    "slm_px_prepare": (c_i, [c_vp, c_ll, c_vp, c_vp, c_vp]),
     "slm_pairs_prepare": (c_i, [c_vp, c_i, c_ll, c_vp, c_vp, c_vp, c_vp]),
     "slm_pairs_emit": (c_i, [c_vp, c_i, c_ll, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                              c_i, c_ll, c_vp]),
@@ -131,7 +129,6 @@ _SIGS = {
     "slm_pair_tables": (c_i, [c_vp, c_ll, c_i, c_vp, c_vp, c_vp, c_i, c_vp, c_vp, c_vp]),
     "slm_gauss_tab": (c_i, [c_vp, c_ll, c_vp, c_vp]),
     "slm_gauss_tab_floats": (c_i, []),
-    "slm_diag_runs": (c_i, [c_vp, c_vp]),
     "slm_diag_stream": (c_i, [c_vp, c_vp]),
     "slm_pair_forward": (c_i, [c_vp, c_i, c_vp]),
     "slm_pair_sum": (c_i, [c_vp, c_vp, c_i, c_vp, c_i, c_vp, c_vp]),
@@ -149,7 +146,6 @@ _SIGS = {
     "slm_transpose_f64": (c_i, [c_vp, c_vp, c_ll, c_ll, c_vp]),
     "slm_f64_to_f32": (c_i, [c_vp, c_vp, c_ll, c_vp]),
     "slm_axpy_scene": (c_i, [c_vp, c_vp, c_d, c_vp, c_ll, c_vp]),
-    "slm_sum_parts": (c_i, [c_vp, c_i, c_vp, c_vp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -58,15 +58,6 @@ int slm_sort_pairs_u32(void* ws, long long wsb, const uint32_t* kin, uint32_t* k
 // ---------------------------------------------------------------------------
 // pixel segments
 // ---------------------------------------------------------------------------
-__global__ void k_px_prepare(const uint32_t* __restrict__ cnt, long long n, long long* __restrict__ cnt64,
-                             int* __restrict__ nonempty) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    uint32_t c = cnt[i];
-    cnt64[i] = c;
-    nonempty[i] = c > 0;
-  }
-}
-
 // ---------------------------------------------------------------------------
 // pairs: (gaussian, view) with >= 1 entry, numbered in (gid, view) order:
 // the pairs of one gaussian are contiguous (gpo CSR), so the per-pair chain
@@ -164,11 +155,6 @@ __global__ void k_iota_u32(uint32_t* out, long long n) {
 }
 
 extern "C" {
-
-int slm_px_prepare(const uint32_t* cnt, long long n, long long* cnt64, int* nonempty, cudaStream_t s) {
-  k_px_prepare<<<slm_blocks(n, 256), 256, 0, s>>>(cnt, n, cnt64, nonempty);
-  return slm_cuda_status();
-}
 
 int slm_pairs_prepare(const int* cnt, int V, long long G, long long* cntV, int* flagV, int* flagT, cudaStream_t s) {
   k_pairs_prepare<<<slm_blocks((long long)V * G, 256), 256, 0, s>>>(cnt, V, G, cntV, flagV, flagT);

@@ -80,107 +80,6 @@ __global__ void __launch_bounds__(128) k_pair_tables(const float* __restrict__ x
   }
 }
 
-__global__ void __launch_bounds__(256) k_diag_tile(SlmTileArgs A) {
-  __shared__ long long s_start[TBD + 1];
-  __shared__ int s_q[TBD];
-  __shared__ float s_geo[TBD * 6];
-  __shared__ float4 s_g[256];
-  __shared__ float s_tab[NW][DIAG_TAB];
-  const int t = blockIdx.x;
-  const int v = view_of_tile(A.view_tile_base, A.n_views, t);
-  const SlmView vw = A.views[v];
-  const int tiles_x = (vw.W + SLM_TILE - 1) / SLM_TILE;
-  const int lt = t - A.view_tile_base[v];
-  const int tx = lt % tiles_x, ty = lt / tiles_x;
-  const int r0 = A.tile_run_off[t], r1 = A.tile_run_off[t + 1];
-  const double ox = (double)(tx * SLM_TILE) + 0.5, oy = (double)(ty * SLM_TILE) + 0.5;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (r1 == r0) return;
-  {
-    const int p = threadIdx.x;
-    const int px = tx * SLM_TILE + (p & 15), py = ty * SLM_TILE + (p >> 4);
-    s_g[p] = (px < vw.W && py < vw.H) ? A.gradr[vw.pix_base + (long long)py * vw.W + px]
-                                      : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  for (int rb = r0; rb < r1; rb += TBD) {
-    const int nb = min(TBD, r1 - rb);
-    __syncthreads();
-    const int i = threadIdx.x;
-    if (i < nb) {
-      s_start[i] = A.run_start[rb + i];
-      const int q = A.run_q[rb + i];
-      s_q[i] = q;
-      const SlmPairGeo g = A.geo[q];
-      float* P = s_geo + i * 6;
-      P[0] = (float)(g.mx - ox);
-      P[1] = (float)(g.my - oy);
-      P[2] = g.ka; P[3] = g.kb; P[4] = g.kc; P[5] = g.inv_o;
-    }
-    if (i == 0) s_start[nb] = A.run_start[rb + nb];
-    __syncthreads();
-    for (int k = warp; k < nb; k += NW) {
-      const float* tq = A.ptab + (size_t)s_q[k] * DIAG_TAB;
-      __syncwarp();
-      for (int j = lane; j < DIAG_TAB; j += 32) s_tab[warp][j] = tq[j];
-      __syncwarp();
-      const float* D = s_tab[warp];
-      const long long st = s_start[k];
-      const int n = (int)(s_start[k + 1] - st);
-      const float* P = s_geo + k * 6;
-      const float p0 = P[0], p1 = P[1], ka = P[2], kb = P[3], kc = P[4], io = P[5];
-      float a[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) a[j] = 0.f;
-      for (int j = lane; j < n; j += 32) {
-        const long long e = st + j;
-        const float4 r4 = A.rec4[e];
-        const float ae = r4.x, at = r4.y;
-        const float dd[3] = {r4.z, r4.w, A.d2[e]};
-        const int pl = A.pix[e];
-        const float4 gr = s_g[pl];
-        const float grc[3] = {gr.x, gr.y, gr.z};
-        const float dx = (float)(pl & 15) - p0, dy = (float)(pl >> 4) - p1;
-        const float e1 = ka * dx + kb * dy;
-        const float e2 = kb * dx + kc * dy;
-        const float w0 = ae * e1, w1 = ae * e2, w2 = 0.5f * ae * e1 * e1, w3 = ae * e1 * e2;
-        const float w4 = 0.5f * ae * e2 * e2;
-        // sum_ch grad_r_sq_ch * (dc_ch/dx_k)^2 with dc_ch/dx_k = d_ch * dalpha_k (+ at * dcol_ch,k
-        // for the 3 position params): for k >= 3 it is dalpha_k^2 * Aw, Aw = sum_ch gr_ch d_ch^2
-        // (exact, no cancellation); the position params keep the per-channel squares
-        const float Aw = grc[0] * dd[0] * dd[0] + grc[1] * dd[1] * dd[1] + grc[2] * dd[2] * dd[2];
-#pragma unroll
-        for (int kk = 0; kk < 3; ++kk) {
-          const float da = w0 * D[kk * 5] + w1 * D[kk * 5 + 1] + w2 * D[kk * 5 + 2] + w3 * D[kk * 5 + 3] +
-                           w4 * D[kk * 5 + 4];
-          float sq = 0.f;
-#pragma unroll
-          for (int ch = 0; ch < 3; ++ch) {
-            const float dc = fmaf(dd[ch], da, at * D[37 + ch * 3 + kk]);
-            sq = fmaf(grc[ch] * dc, dc, sq);
-          }
-          a[kk] += sq;
-        }
-#pragma unroll
-        for (int kk = 3; kk < 10; ++kk) {
-          const float da = w2 * D[15 + (kk - 3) * 3] + w3 * D[16 + (kk - 3) * 3] + w4 * D[17 + (kk - 3) * 3];
-          a[kk] = fmaf(da * da, Aw, a[kk]);
-        }
-        {
-          const float da = ae * io * D[36];
-          a[10] = fmaf(da * da, Aw, a[10]);
-        }
-        const float at2 = at * at;
-        a[11] += grc[0] * at2;
-        a[12] += grc[1] * at2;
-        a[13] += grc[2] * at2;
-      }
-      const float s = warp_reduce_scatter16(a, lane);
-      const int slot = rs16_slot(lane);
-      if (!(lane & 1) && slot < DIAG_RUN_D) A.out[(size_t)(rb + k) * DIAG_RUN_D + slot] = s;
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
 // per-pair sums of the run partials (fixed run order -> deterministic):
 // pacc[q] = sum over the pair's runs of acc[run] (D = 9 J^T partials or 14
@@ -488,12 +387,6 @@ int slm_pair_tables(const float* xs, long long G, int sh_degree, const int* pair
     case 3: k_pair_tables<16><<<b, 128, 0, st>>>(xs, G, pair_gid, pair_vm, cams, n_pairs, tab, gtab); break;
     default: return SLM_ERR_ARG;
   }
-  return slm_cuda_status();
-}
-
-int slm_diag_runs(const SlmTileArgs* a, cudaStream_t st) {
-  if (a->n_tiles <= 0) return SLM_OK;
-  k_diag_tile<<<a->n_tiles, 256, 0, st>>>(*a);
   return slm_cuda_status();
 }
 

@@ -168,12 +168,6 @@ __global__ void k_axpy_scene(const double* __restrict__ x, const float* __restri
     out[i] = x[i] + gamma * (double)d[i];
 }
 
-__global__ void k_sum_parts(const double* __restrict__ part, int n, double* __restrict__ out) {
-  __shared__ double sm[32];
-  double t = sum_parts(part, n, sm);
-  if (threadIdx.x == 0) *out = t;
-}
-
 extern "C" {
 
 int slm_vec_blocks() { return VEC_BLOCKS; }
@@ -233,11 +227,6 @@ int slm_f64_to_f32(const double* in, float* out, long long n, cudaStream_t s) {
 
 int slm_axpy_scene(const double* x, const float* d, double gamma, double* out, long long n, cudaStream_t s) {
   k_axpy_scene<<<VEC_BLOCKS, VEC_THREADS, 0, s>>>(x, d, gamma, out, n);
-  return slm_cuda_status();
-}
-
-int slm_sum_parts(const double* part, int n, double* out, cudaStream_t s) {
-  k_sum_parts<<<1, 1024, 0, s>>>(part, n, out);
   return slm_cuda_status();
 }
 

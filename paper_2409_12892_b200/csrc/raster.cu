@@ -346,31 +346,6 @@ __global__ void k_tile_runs(const slm_u2* __restrict__ ranges, int n_tiles, cons
   }
 }
 
-// pair -> runs CSR, filled in a fixed order: per splat, its instances in
-// (tile row, tile column) order (pre-sort order), views handled one per call
-__global__ void k_pair_runs(const uint32_t* __restrict__ sorted_gid, const unsigned long long* __restrict__ inst_off,
-                            long long G, const uint32_t* __restrict__ post_of_pre, const int* __restrict__ used,
-                            const int* __restrict__ run_of, long long ibase, const int* __restrict__ pidx,
-                            const int* __restrict__ pair_run_off, int* __restrict__ pair_runs, long long n,
-                            int batched, int* __restrict__ run_slot) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    unsigned long long beg = inst_off[i], end = inst_off[i + 1];
-    if (beg == end) continue;
-    const uint32_t e = sorted_gid[i];
-    const int q = batched ? pidx[(long long)(e >> 24) * G + (e & 0xffffffu)] : pidx[e];
-    if (q < 0) continue;
-    int k = pair_run_off[q];
-    for (unsigned long long pre = beg; pre < end; ++pre) {
-      const long long jg = ibase + post_of_pre[pre];
-      if (used[jg]) {
-        const int r = run_of[jg];
-        if (run_slot) run_slot[r] = k;
-        pair_runs[k++] = r;
-      }
-    }
-  }
-}
-
 __global__ void k_tile_ranges(const unsigned long long* __restrict__ keys, long long n, int rank_bits,
                               uint2* __restrict__ ranges) {
   long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -732,15 +707,6 @@ int slm_tile_runs(const slm_u2* ranges, int n_tiles, const int* used, const int*
   k_tile_runs<<<slm_blocks((long long)n_tiles * 32, 256), 256, 0, stream>>>(ranges, n_tiles, used, run_of, ibase, view,
                                                                              tile_nruns, run_tile, view_tile_base,
                                                                              n_views);
-  return slm_cuda_status();
-}
-
-int slm_pair_runs(const uint32_t* sorted_gid, const unsigned long long* inst_off, long long G,
-                  const uint32_t* post_of_pre, const int* used, const int* run_of, long long ibase, const int* pidx,
-                  const int* pair_run_off, int* pair_runs, long long n, int batched, int* run_slot,
-                  cudaStream_t stream) {
-  k_pair_runs<<<slm_blocks(n, 128), 128, 0, stream>>>(sorted_gid, inst_off, G, post_of_pre, used, run_of, ibase, pidx,
-                                                       pair_run_off, pair_runs, n, batched, run_slot);
   return slm_cuda_status();
 }
 
