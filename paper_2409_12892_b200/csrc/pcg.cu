@@ -16,6 +16,9 @@
 #define ST_BETA 6
 #define ST_FLAGS 7   // bit0 non-SPD (p^T g <= 0), bit1 converged
 #define ST_ITERS 8
+#define ST_STOP 9    // sticky: the solve has ended (b = 0, converged or non-SPD); the
+                     // iteration kernels become no-ops, so the host can queue
+                     // iterations ahead without a per-iteration sync
 
 #define VEC_BLOCKS 1184  // 148 SMs x 8, fixed -> deterministic partial shapes
 #define VEC_THREADS 256
@@ -26,6 +29,7 @@ __device__ __forceinline__ float mfloor(float m) { return fmaxf(m, 1e-12f); }
 // the search direction by the product, x += alpha p and r -= alpha A p)
 __global__ void k_pcg_pupdate(float* __restrict__ p, const double* __restrict__ r, const float* __restrict__ M,
                               const double* __restrict__ st, long long n) {
+  if (st[ST_STOP] != 0.0) return;
   const double beta = st[ST_BETA];
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     p[i] = (float)(r[i] / (double)mfloor(M[i]) + beta * (double)p[i]);
@@ -59,6 +63,7 @@ __global__ void k_pcg_update(int mode, double* __restrict__ x, double* __restric
                              double lam, double* __restrict__ st, const double* __restrict__ dot_part, int n_dot,
                              double* __restrict__ part /*[3][VEC_BLOCKS]*/, long long n) {
   __shared__ double sm[32];
+  if (mode == 1 && st[ST_STOP] != 0.0) return;
   double alpha = 0.0;
   if (mode == 1) {
     double pg = sum_parts(dot_part, n_dot, sm);
@@ -101,6 +106,7 @@ __global__ void k_pcg_update(int mode, double* __restrict__ x, double* __restric
 // single block: beta = rz_new / rz, exit flags
 __global__ void k_pcg_finalize(int mode, double* __restrict__ st, const double* __restrict__ part, int nb) {
   __shared__ double sm[32];
+  if (mode == 1 && st[ST_STOP] != 0.0) return;
   double rz = sum_parts(part, nb, sm);
   double rr = sum_parts(part + VEC_BLOCKS, nb, sm);
   double bb = mode == 0 ? sum_parts(part + 2 * VEC_BLOCKS, nb, sm) : 0.0;
@@ -110,6 +116,7 @@ __global__ void k_pcg_finalize(int mode, double* __restrict__ st, const double* 
       st[ST_BB] = bb;
       st[ST_BETA] = 0.0;
       st[ST_ITERS] = 0.0;
+      st[ST_STOP] = bb > 0.0 ? 0.0 : 1.0;  // b = 0: x = x0
     } else {
       double pg = st[ST_PG];
       if (!(pg > 0.0)) flags = 1.0;
@@ -120,6 +127,7 @@ __global__ void k_pcg_finalize(int mode, double* __restrict__ st, const double* 
     st[ST_RZ] = rz;
     st[ST_RR] = rr;
     st[ST_FLAGS] = flags;
+    if (flags != 0.0) st[ST_STOP] = 1.0;
   }
 }
 

@@ -24,7 +24,7 @@ from .engine import CacheSet, LossConfig
 from .errors import NonSPDError
 from .scene import Layout, ParamVector
 
-ST_RZ, ST_PG, ST_BB, ST_RR, ST_ALPHA, ST_BETA, ST_FLAGS, ST_ITERS = 0, 2, 3, 4, 5, 6, 7, 8
+ST_RZ, ST_PG, ST_BB, ST_RR, ST_ALPHA, ST_BETA, ST_FLAGS, ST_ITERS, ST_STOP = 0, 2, 3, 4, 5, 6, 7, 8, 9
 
 
 @dataclass(frozen=True)
@@ -52,6 +52,17 @@ def allreduce_sum_(buf: torch.Tensor, group=None) -> torch.Tensor:
     return buf
 
 
+_STOP_HOST = []
+
+
+def _pinned_stop() -> torch.Tensor:
+    """Process-wide pinned 2-slot buffer (a pinned allocation per solve would
+    cost a synchronising cudaHostAlloc)."""
+    if not _STOP_HOST:
+        _STOP_HOST.append(torch.zeros(2, dtype=torch.float64).pin_memory())
+    return _STOP_HOST[0]
+
+
 @dataclass
 class PCGWorkspace:
     """x, r (fp64), p, g (fp32) vectors + device scalar block (SPEC PCGWorkspace)."""
@@ -72,6 +83,9 @@ class PCGWorkspace:
         self.g = torch.empty(self.n, dtype=f, device=self.device)
         self.st = torch.zeros(16, dtype=torch.float64, device=self.device)
         self.part = torch.zeros(3 * _lib.load().slm_vec_blocks(), dtype=torch.float64, device=self.device)
+        # pinned copies of the stop flag, one per in-flight iteration
+        self.stop_host = _pinned_stop()
+        self.stop_ev = [torch.cuda.Event(), torch.cuda.Event()]
 
 
 def pcg_run(cache: CacheSet, b: torch.Tensor, M: torch.Tensor, lam: float, max_iters: int,
@@ -91,28 +105,34 @@ def pcg_run(cache: CacheSet, b: torch.Tensor, M: torch.Tensor, lam: float, max_i
     call("slm_pcg_update", 0, ptr(ws.x), ptr(ws.r), ptr(ws.p), ptr(ws.g), ptr(b), ptr(M), float(lam),
          ptr(ws.st), ptr(dot_part), nb, ptr(ws.part), n, s)
     call("slm_pcg_finalize", 0, ptr(ws.st), ptr(ws.part), s)
-    products = 1
-    bb = float(ws.st[ST_BB].item())
-    iters = 0
-    if bb > 0.0:
-        for _ in range(max_iters):
-            call("slm_pcg_pupdate", ptr(ws.p), ptr(ws.r), ptr(M), ptr(ws.st), n, s)
-            _product(cache, ws.p, ws.g, lam, M, dot_part, timer)
-            products += 1
-            call("slm_pcg_update", 1, ptr(ws.x), ptr(ws.r), ptr(ws.p), ptr(ws.g), ptr(b), ptr(M), float(lam),
-                 ptr(ws.st), ptr(dot_part), nb, ptr(ws.part), n, s)
-            call("slm_pcg_finalize", 1, ptr(ws.st), ptr(ws.part), s)
-            iters += 1
-            flags = int(ws.st[ST_FLAGS].item())
-            if flags & 1:
-                raise NonSPDError(f"p^T g = {float(ws.st[ST_PG].item())} <= 0 at PCG iteration {iters}")
-            if flags & 2:
+    # Iterations are queued one ahead of the host's exit check: the device
+    # keeps a sticky stop flag (b = 0, converged, non-SPD) that turns the
+    # iteration kernels into no-ops, and the host reads iteration i-1's flag
+    # (async copy + event) only after iteration i is queued -- no per-
+    # iteration drain of the GPU; at most one extra product runs on exit.
+    for it in range(max_iters + 1):
+        if it > 0:
+            ws.stop_ev[(it - 1) % 2].synchronize()
+            if ws.stop_host[(it - 1) % 2] != 0.0:
                 break
+        if it == max_iters:
+            break
+        call("slm_pcg_pupdate", ptr(ws.p), ptr(ws.r), ptr(M), ptr(ws.st), n, s)
+        _product(cache, ws.p, ws.g, lam, M, dot_part, timer)
+        call("slm_pcg_update", 1, ptr(ws.x), ptr(ws.r), ptr(ws.p), ptr(ws.g), ptr(b), ptr(M), float(lam),
+             ptr(ws.st), ptr(dot_part), nb, ptr(ws.part), n, s)
+        call("slm_pcg_finalize", 1, ptr(ws.st), ptr(ws.part), s)
+        ws.stop_host[it % 2].copy_(ws.st[ST_STOP], non_blocking=True)
+        ws.stop_ev[it % 2].record()
+    st_h = ws.st.cpu()
+    iters = int(st_h[ST_ITERS])
+    if int(st_h[ST_FLAGS]) & 1:
+        raise NonSPDError(f"p^T g = {float(st_h[ST_PG])} <= 0 at PCG iteration {iters}")
     if stats is not None:
-        stats["products"] = products
+        stats["products"] = 1 + iters
         stats["iterations"] = iters
-        stats["rr"] = float(ws.st[ST_RR].item())
-        stats["bb"] = bb
+        stats["rr"] = float(st_h[ST_RR])
+        stats["bb"] = float(st_h[ST_BB])
     return ws.x
 
 
