@@ -403,12 +403,15 @@ class CacheSet:
                     self.residual_exports.append(ex)
             self.frames.append(fr)
         T.tick("residuals")
-        e = int(err.item())
+        # one host sync for the error flags and the per-view energies
+        sums = [err.to(torch.float64).reshape(1)] + [p.sum().reshape(1) for p in energy_parts]
+        host = torch.cat(sums).cpu().tolist()
+        e = int(host[0])
         if e & 1:
             raise ValueError("scene contains non-finite parameters")
         if e & 2:
             raise ValueError("quaternion with (near-)zero norm")
-        self.energies = [float(p.sum().item()) for p in energy_parts] if have_res else None
+        self.energies = host[1:] if have_res else None
 
         # ---- instances -> runs ---------------------------------------------
         inst_cnt = torch.zeros(ni + 1, dtype=torch.int64, device=dev)
