@@ -215,10 +215,11 @@ def run_ours(args, cfg):
     e1 = torch.cuda.Event(enable_timing=True)
     out_host = torch.empty(scene.param_count, dtype=torch.float32).pin_memory()
     from paper_2409_12892_b200.scene import GaussianScene
-    barrier()
-    e0.record(stream)
     n_e2e = max(1, min(args.steps, 3))
-    for _ in range(n_e2e):
+    for it in range(1 + n_e2e):  # one untimed warm-up call (first use of the pinned buffers)
+        if it == 1:
+            barrier()
+            e0.record(stream)
         xs = x_host.to(dev, non_blocking=True)
         sc = GaussianScene(xs, scene.sh_degree, scene.background)
         # the images stay in pinned host memory: lm_direction copies each

@@ -12,7 +12,7 @@ from paper_2409_12892_b200.engine import LossConfig  # noqa: E402
 from paper_2409_12892_b200.scene import GaussianScene  # noqa: E402
 from paper_2409_12892_b200.solver import BatchSchedule, lm_direction  # noqa: E402
 
-cfg = bench.CONFIGS["c3"]
+cfg = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c3"]
 dev = torch.device("cuda", 0)
 init, cams, gts = bench.make_workload(cfg, dev)
 scene = init.to_device(dev)
