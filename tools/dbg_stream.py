@@ -30,3 +30,10 @@ out = torch.empty_like(p)
 cs.jtwj(p, out)
 torch.cuda.synchronize()
 print("jtwj ok", flush=True)
+M = cs.diag()
+torch.cuda.synchronize()
+print("diag ok", flush=True)
+from paper_2409_12892_b200.solver import pcg_run  # noqa: E402
+x = pcg_run(cs, b, M, 1e-4, 3)
+torch.cuda.synchronize()
+print("pcg ok", flush=True)
