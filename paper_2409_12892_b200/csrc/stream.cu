@@ -48,7 +48,7 @@ static_assert(CR % 32 == 0 && CR <= 255, "run slots are bytes, 32 per J^T round"
 // of long runs carries more entries and a chunk of short runs more runs),
 // then the J^T schedule and the header at fixed offsets
 #ifndef SLM_STAGE
-#define SLM_STAGE 24576
+#define SLM_STAGE 25680  // the largest stage that keeps 2 CTAs / SM (static_assert below)
 #endif
 #define ST_BYTES SLM_STAGE
 #define ST_HDR 32
@@ -229,6 +229,11 @@ __device__ __forceinline__ uint8_t* stage_ptr(uint8_t* ring, int s) { return rin
 __host__ __device__ constexpr size_t stream_smem_bytes(int mode) {
   return 256 * 16 + ((mode & MODE_J) ? (size_t)NW * 256 * 16 : 0) + (size_t)NS * ST_BYTES + TMETA * 24;
 }
+
+// 2 CTAs / SM: 228 KB of shared memory per SM, 1 KB reserved per CTA, and a
+// few hundred bytes of static barriers / tile queue per CTA
+static_assert(stream_smem_bytes(MODE_J | MODE_JT) + 256 <= 228 * 1024 / 2 - 1024,
+              "the fused streaming kernel must keep 2 CTAs per SM");
 
 struct ChunkMeta {
   int k0, k1;
