@@ -226,14 +226,20 @@ __global__ void k_chunk_perm(const int* __restrict__ chunk_run, long long n_chun
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint8_t* stage_ptr(uint8_t* ring, int s) { return ring + (size_t)s * ST_BYTES; }
 
+// ring depth: the J modes spend 32 KB on per-warp pixel accumulators; the
+// J^T-only and diag modes use that room for one more stage
+__host__ __device__ constexpr int ns_of(int mode) { return (mode & MODE_J) ? NS : NS + 1; }
+
 __host__ __device__ constexpr size_t stream_smem_bytes(int mode) {
-  return 256 * 16 + ((mode & MODE_J) ? (size_t)NW * 256 * 16 : 0) + (size_t)NS * ST_BYTES + TMETA * 24;
+  return 256 * 16 + ((mode & MODE_J) ? (size_t)NW * 256 * 16 : 0) + (size_t)ns_of(mode) * ST_BYTES + TMETA * 24;
 }
 
 // 2 CTAs / SM: 228 KB of shared memory per SM, 1 KB reserved per CTA, and a
 // few hundred bytes of static barriers / tile queue per CTA
-static_assert(stream_smem_bytes(MODE_J | MODE_JT) + 256 <= 228 * 1024 / 2 - 1024,
-              "the fused streaming kernel must keep 2 CTAs per SM");
+static_assert(stream_smem_bytes(MODE_J | MODE_JT) + 256 <= 228 * 1024 / 2 - 1024 &&
+                  stream_smem_bytes(MODE_JT) + 256 <= 228 * 1024 / 2 - 1024 &&
+                  stream_smem_bytes(MODE_DIAG) + 256 <= 228 * 1024 / 2 - 1024,
+              "the streaming kernels must keep 2 CTAs per SM");
 
 struct ChunkMeta {
   int k0, k1;
@@ -245,7 +251,8 @@ struct ChunkMeta {
 template <int MODE>
 __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ uint64_t full[NS], empty[NS];
+  constexpr int NSM = ns_of(MODE);
+  __shared__ uint64_t full[NSM], empty[NSM];
   // tile queue: the producer claims tiles from a global counter (dynamic
   // load balance over tiles of very different sizes; results do not depend
   // on which CTA runs a tile) and hands them to the consumers in order
@@ -257,12 +264,12 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
   float4* s_acc = reinterpret_cast<float4*>(sp);
   sp += (MODE & MODE_J) ? (size_t)NW * 256 * 16 : 0;
   uint8_t* ring = sp;
-  sp += (size_t)NS * ST_BYTES;
+  sp += (size_t)NSM * ST_BYTES;
   ChunkMeta* tmeta = reinterpret_cast<ChunkMeta*>(sp);
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NS; ++s) {
+    for (int s = 0; s < NSM; ++s) {
       mbar_init(&full[s], 1 + 32);  // producer lane 0 (expect_tx) + 32 cp.async arrivals
       mbar_init(&empty[s], NW);
     }
@@ -314,7 +321,7 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
           for (int h = 0; h < RL; ++h)
             qn[h] = gather && lane + 32 * h < tmeta[0].k1 - tmeta[0].k0 ? A.run_q[tmeta[0].k0 + lane + 32 * h] : 0;
           for (int i = 0; i < wn; ++i, ++g) {
-            const int s = (int)(g % NS);
+            const int s = (int)(g % NSM);
             int q[RL];
 #pragma unroll
             for (int h = 0; h < RL; ++h) {
@@ -322,7 +329,7 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
               if (gather && i + 1 < wn && lane + 32 * h < tmeta[i + 1].k1 - tmeta[i + 1].k0)
                 qn[h] = A.run_q[tmeta[i + 1].k0 + lane + 32 * h];
             }
-            if (g >= NS) mbar_wait(&empty[s], ((g / NS) - 1) & 1u);
+            if (g >= NSM) mbar_wait(&empty[s], ((g / NSM) - 1) & 1u);
             const ChunkMeta m = tmeta[i];
             uint8_t* st = stage_ptr(ring, s);
             const StageLayout L = stage_layout((int)(m.e1 - m.e0), m.k1 - m.k0);
@@ -412,8 +419,8 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
       // runs are taken in a fixed order -> deterministic).  Measured faster
       // than flat 32-entry windows with __match_any conflict resolution.
       for (int ci = c0; ci < c1; ++ci, ++g) {
-        const int s = (int)(g % NS);
-        mbar_wait(&full[s], (g / NS) & 1u);
+        const int s = (int)(g % NSM);
+        mbar_wait(&full[s], (g / NSM) & 1u);
         const uint8_t* st = stage_ptr(ring, s);
         const int* hdr = reinterpret_cast<const int*>(st + OFF_HDR);
         const int nr = hdr[0];
@@ -479,8 +486,8 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
       // groups / schedule as J^T; each group holds its pair's 48-float chain
       // table in registers (run record P[5] = pair index, from L2)
       for (int ci = c0; ci < c1; ++ci, ++g) {
-        const int s = (int)(g % NS);
-        mbar_wait(&full[s], (g / NS) & 1u);
+        const int s = (int)(g % NSM);
+        mbar_wait(&full[s], (g / NSM) & 1u);
         const uint8_t* st = stage_ptr(ring, s);
         const int* hdr = reinterpret_cast<const int*>(st + OFF_HDR);
         const long long* rs = reinterpret_cast<const long long*>(st + hdr[7]) + hdr[1];
@@ -595,8 +602,8 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
       // pass J^T: 4 runs per warp (8 lanes each) from the chunk's
       // length-sorted schedule; the warp's slot block rotates with the chunk
       for (int ci = c0; ci < c1; ++ci, ++g) {
-        const int s = (int)(g % NS);
-        mbar_wait(&full[s], (g / NS) & 1u);
+        const int s = (int)(g % NSM);
+        mbar_wait(&full[s], (g / NSM) & 1u);
         const uint8_t* st = stage_ptr(ring, s);
         const int* hdr = reinterpret_cast<const int*>(st + OFF_HDR);
         const long long* rs = reinterpret_cast<const long long*>(st + hdr[7]) + hdr[1];
