@@ -370,6 +370,20 @@ __global__ void k_tile_ranges(const unsigned long long* __restrict__ keys, long 
 // ---------------------------------------------------------------------------
 typedef SlmRasterArgs RasterArgs;
 
+// 32x32 bit-matrix transpose across a warp: lane i holds row i on entry and
+// column i on exit (bit j of lane i's result = bit i of lane j's input);
+// five butterfly rounds swapping the off-diagonal blocks
+__device__ __forceinline__ unsigned transpose32(unsigned x, int lane) {
+  const unsigned lo[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int r = 0; r < 5; ++r) {
+    const int j = 16 >> r;
+    const unsigned y = __shfl_xor_sync(0xffffffffu, x, j);
+    x = (lane & j) ? ((x & ~lo[r]) | ((y >> j) & lo[r])) : ((x & lo[r]) | ((y & lo[r]) << j));
+  }
+  return x;
+}
+
 #define RB 256
 #define RW (RB / 32)
 template <bool FILL>
@@ -481,13 +495,21 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
       __syncwarp();
       for (int b0 = 0; b0 < nrel; b0 += 32) {
         const int nbk = min(32, nrel - b0);
-        unsigned wq = 0u;
-        if (!done) {
-          for (int i = 0; i < nbk; ++i) {
-            const int4 bx = s_box[s_list[warp][b0 + i]];
-            wq |= (unsigned)(px >= bx.x && px <= bx.y && py >= bx.z && py <= bx.w) << i;
+        // lane i: the warp-pixel mask of instance b0 + i (its bbox clipped to
+        // the warp's two rows), then a 32x32 bit transpose gives every lane
+        // its word (bit i: instance b0 + i may touch the lane's pixel)
+        unsigned m = 0u;
+        if (lane < nbk) {
+          const int4 bx = s_box[s_list[warp][b0 + lane]];
+          const int cx0 = max(bx.x - tx * SLM_TILE, 0), cx1 = min(bx.y - tx * SLM_TILE, SLM_TILE - 1);
+          if (cx0 <= cx1) {
+            const unsigned rm = (2u << cx1) - (1u << cx0);
+            if (bx.z <= row0 && row0 <= bx.w) m |= rm;
+            if (bx.z <= row0 + 1 && row0 + 1 <= bx.w) m |= rm << 16;
           }
         }
+        unsigned wq = transpose32(m, lane);
+        if (done) wq = 0u;
         while (__any_sync(0xffffffffu, wq != 0u)) {
           if (wq == 0u) continue;
           const int k = s_list[warp][b0 + __ffs(wq) - 1];
@@ -521,8 +543,7 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
       // order, and writes their records (every step is a cache entry)
       for (int b0 = 0; b0 < nrel; b0 += 32) {
         const int nbk = min(32, nrel - b0);
-        unsigned wq = 0u;
-        for (int i = 0; i < nbk; ++i) wq |= ((s_mask[s_list[warp][b0 + i] * RW + warp] >> lane) & 1u) << i;
+        unsigned wq = transpose32(lane < nbk ? s_mask[s_list[warp][b0 + lane] * RW + warp] : 0u, lane);
         while (__any_sync(0xffffffffu, wq != 0u)) {
           if (wq == 0u) continue;
           const int k = s_list[warp][b0 + __ffs(wq) - 1];
