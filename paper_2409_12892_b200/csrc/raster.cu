@@ -489,10 +489,8 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
       // collects the ones whose bbox holds its pixel (a 32-bit word) and
       // walks its own set bits in order, so a step evaluates one (instance,
       // pixel) pair on every busy lane instead of idling the lanes outside
-      // the bbox; per-pixel depth order is kept.  Keep masks are assembled
-      // with shared-memory atomicOr (order-independent).
-      for (int ki = lane; ki < nrel; ki += 32) s_mask[s_list[warp][ki] * RW + warp] = 0u;
-      __syncwarp();
+      // the bbox; per-pixel depth order is kept.  The keep masks come back
+      // through the inverse transpose of the lanes' kept-bit words.
       for (int b0 = 0; b0 < nrel; b0 += 32) {
         const int nbk = min(32, nrel - b0);
         // lane i: the warp-pixel mask of instance b0 + i (its bbox clipped to
@@ -510,9 +508,11 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
         }
         unsigned wq = transpose32(m, lane);
         if (done) wq = 0u;
+        unsigned kw = 0u;  // bit i: this lane's pixel keeps instance b0 + i
         while (__any_sync(0xffffffffu, wq != 0u)) {
           if (wq == 0u) continue;
-          const int k = s_list[warp][b0 + __ffs(wq) - 1];
+          const int i = __ffs(wq) - 1;
+          const int k = s_list[warp][b0 + i];
           wq &= wq - 1u;
           const double dx = __dsub_rn(dxp, s_mx[k]);
           const double dy = __dsub_rn(dyp, s_my[k]);
@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
           double a = ex >= -40.0 ? __dmul_rn(s_o[k], slm_exp_neg(ex)) : 0.0;
           a = a < aclamp ? a : aclamp;
           if ((a >= amin) && (a > 0.0)) {  // T >= t_stop holds while the lane is not done
-            atomicOr(&s_mask[k * RW + warp], 1u << lane);
+            kw |= 1u << i;
             const double wgt = __dmul_rn(a, T);
             C0 = __dadd_rn(C0, __dmul_rn(wgt, s_c0[k]));
             C1 = __dadd_rn(C1, __dmul_rn(wgt, s_c1[k]));
@@ -535,6 +535,9 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
             }
           }
         }
+        // the transpose back gives lane i instance b0 + i's keep mask
+        const unsigned km = transpose32(kw, lane);
+        if (lane < nbk) s_mask[s_list[warp][b0 + lane] * RW + warp] = km;
       }
     }
     if (FILL) {
