@@ -27,15 +27,19 @@ LAMBDA_MIN, LAMBDA_MAX = 1e-4, 1e4   # SPEC:473 bounds used by trust_region_upda
 
 
 def view_energy(scene: GaussianScene, camera, gt: torch.Tensor, config=None, loss: LossConfig = LossConfig(),
-                cfg_s=None) -> torch.Tensor:
+                cfg_s=None, err: torch.Tensor | None = None) -> torch.Tensor:
     """E = sum r^2 of one view as a device fp64 scalar (render COUNT pass +
-    residual kernel, no cache)."""
+    residual kernel, no cache).  `gt` may live on the host (it is copied to
+    the scene's device); the projection's error flags (non-finite
+    parameters, zero quaternion) are OR-ed into `err` when given."""
     from .rasterizer import DEFAULT_CONFIG
     dev = scene.device
+    gt = gt.to(dev, non_blocking=True)
     config = config if config is not None else DEFAULT_CONFIG
     cfg_s = cfg_s if cfg_s is not None else rast_cfg_struct(config, scene.background)
     fr = ViewFrame(camera, 0)
-    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    if err is None:
+        err = torch.zeros(1, dtype=torch.int32, device=dev)
     project_and_bin(scene, fr, cfg_s, err)
     hw = camera.num_pixels
     fr.rgb = torch.empty(hw * 3, dtype=torch.float64, device=dev)
@@ -51,21 +55,34 @@ def view_energy(scene: GaussianScene, camera, gt: torch.Tensor, config=None, los
 
 
 def energy(scene: GaussianScene, cameras, gts, config=None, loss: LossConfig = LossConfig(), rank: int = 0,
-           world_size: int = 1) -> float:
+           world_size: int = 1, nonfinite: str = "raise") -> float:
     """sum over views of ||F||^2 (ref: residuals.py:241-246 per view); with
     world_size > 1 the views are sharded round-robin and the partial energies
-    summed with one scalar all_reduce."""
+    summed with one scalar all_reduce (the error flags travel in the same
+    buffer, one sync).
+
+    A scene with non-finite parameters or a zero quaternion raises ValueError
+    like the reference's render (ref rasterizer.py:81-82, 124-125), or gives
+    +inf with nonfinite="inf" (line-search candidates)."""
     from .rasterizer import DEFAULT_CONFIG
     from .solver import allreduce_sum_
     config = config if config is not None else DEFAULT_CONFIG
     cfg_s = rast_cfg_struct(config, scene.background)
-    tot = torch.zeros(1, dtype=torch.float64, device=scene.device)
+    err = torch.zeros(1, dtype=torch.int32, device=scene.device)
+    tot = torch.zeros(2, dtype=torch.float64, device=scene.device)
     for i, (c, g) in enumerate(zip(cameras, gts)):
         if i % world_size == rank:
-            tot = tot + view_energy(scene, c, g, config, loss, cfg_s)
+            tot[0] += view_energy(scene, c, g, config, loss, cfg_s, err)
+    tot[1] = err[0].to(torch.float64)
     if world_size > 1:
         allreduce_sum_(tot)
-    return float(tot.item())
+    e, flags = tot.tolist()
+    if flags != 0:
+        if nonfinite == "inf":
+            return float("inf")
+        raise ValueError("scene contains non-finite parameters" if int(flags) & 1
+                         else "quaternion with (near-)zero norm")
+    return e
 
 
 def offset_scene(scene: GaussianScene, delta: torch.Tensor, gamma: float) -> GaussianScene:
@@ -85,7 +102,7 @@ def line_search(scene: GaussianScene, delta: torch.Tensor, cameras, gts, depth: 
     best_g = 0.0
     best_e = energy(scene, cameras, gts, config, loss, rank, world_size) if e0 is None else float(e0)
     for gma in sorted(2.0 ** -i for i in range(depth + 1)):
-        e = energy(offset_scene(scene, delta, gma), cameras, gts, config, loss, rank, world_size)
+        e = energy(offset_scene(scene, delta, gma), cameras, gts, config, loss, rank, world_size, nonfinite="inf")
         if e < best_e:
             best_g, best_e = gma, e
     return best_g, best_e
@@ -126,6 +143,7 @@ class LMStepReport:
     energy_before: float
     energy_after: float
     delta: torch.Tensor
+    direction: object = None     # solver.StepReport of the batched direction (PCG stats, entries)
 
 
 def lm_step(scene: GaussianScene, cameras, gts, schedule: BatchSchedule = BatchSchedule(), lam: float = 1e-4,
@@ -161,4 +179,4 @@ def lm_step(scene: GaussianScene, cameras, gts, schedule: BatchSchedule = BatchS
         rho = float(t.item())
     accept, lam_new = trust_region_update(lam, rho)
     new_scene = offset_scene(scene, delta, gamma) if accept else scene
-    return LMStepReport(new_scene, lam_new, accept, gamma, rho, e_old, e_new, delta)
+    return LMStepReport(new_scene, lam_new, accept, gamma, rho, e_old, e_new, delta, rep)
