@@ -419,6 +419,11 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
   const uint2 rng = A.tile_range[blockIdx.x];
   const double dxp = (double)px + 0.5, dyp = (double)py + 0.5;
   const double amin = A.cfg.alpha_min, tstop = A.cfg.t_stop, aclamp = A.cfg.alpha_clamp;
+  // o * exp(-40) < 4.3e-18: below any alpha_min > 1e-17 the tail can never be
+  // kept and is mapped to alpha = 0; with alpha_min = 0 (RenderConfig.smooth,
+  // ref rasterizer.py:42-45, 292-296) every alpha > 0 counts, so the tail is
+  // evaluated with the full-range exp down to its underflow
+  const bool tail = !(amin > 1e-17);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const unsigned lanes_below = (1u << lane) - 1u;
@@ -519,7 +524,7 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
           const double q = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(s_ca[k], dx), dx), __dmul_rn(s_cc[k], __dmul_rn(dy, dy))),
                                      __dmul_rn(__dmul_rn(__dmul_rn(2.0, s_cb[k]), dy), dx));
           const double ex = __dmul_rn(-0.5, q);
-          double a = ex >= -40.0 ? __dmul_rn(s_o[k], slm_exp_neg(ex)) : 0.0;
+          double a = ex >= -40.0 ? __dmul_rn(s_o[k], slm_exp_neg(ex)) : (tail ? __dmul_rn(s_o[k], exp(ex)) : 0.0);
           a = a < aclamp ? a : aclamp;
           if ((a >= amin) && (a > 0.0)) {  // T >= t_stop holds while the lane is not done
             kw |= 1u << i;
@@ -556,7 +561,7 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
           const double q = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(s_ca[k], dx), dx), __dmul_rn(s_cc[k], __dmul_rn(dy, dy))),
                                      __dmul_rn(__dmul_rn(__dmul_rn(2.0, s_cb[k]), dy), dx));
           const double ex = __dmul_rn(-0.5, q);
-          double a = ex >= -40.0 ? __dmul_rn(s_o[k], slm_exp_neg(ex)) : 0.0;
+          double a = ex >= -40.0 ? __dmul_rn(s_o[k], slm_exp_neg(ex)) : (tail ? __dmul_rn(s_o[k], exp(ex)) : 0.0);
           a = a < aclamp ? a : aclamp;
           const double wgt = __dmul_rn(a, T);
           C0 = __dadd_rn(C0, __dmul_rn(wgt, s_c0[k]));

@@ -689,16 +689,23 @@ template <int MODE>
 static int launch_stream(const SlmTileArgs* a, cudaStream_t st) {
   if (a->n_tiles <= 0) return SLM_OK;
   const size_t bytes = stream_smem_bytes(MODE);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_stream<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    configured = true;
-  }
-  int dev = 0, sms = 148, per_sm = 1;
+  // the dynamic shared-memory opt-in and the occupancy are per device: a
+  // process may drive several GPUs (one stream each)
+  constexpr int kMaxDev = 64;
+  static int s_per_sm[kMaxDev] = {0};   // 0: not configured on that device yet
+  static int s_sms[kMaxDev] = {0};
+  int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stream<MODE>, NT, bytes);
-  if (per_sm < 1) per_sm = 1;
+  if (dev < 0 || dev >= kMaxDev) return SLM_ERR_ARG;
+  if (s_per_sm[dev] == 0) {
+    cudaFuncSetAttribute(k_stream<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    int sms = 148, per_sm = 1;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stream<MODE>, NT, bytes);
+    s_sms[dev] = sms;
+    s_per_sm[dev] = per_sm < 1 ? 1 : per_sm;
+  }
+  const int sms = s_sms[dev], per_sm = s_per_sm[dev];
   const int grid = (int)std::min<long long>((long long)a->n_tiles, (long long)sms * per_sm);
   if (a->tile_counter) cudaMemsetAsync(a->tile_counter, 0, sizeof(int), st);
   k_stream<MODE><<<grid, NT, bytes, st>>>(*a);

@@ -308,6 +308,11 @@ class CacheSet:
         self.views_dev = _lib.struct_tensor(views, dev)
         cfg_s = rast_cfg_struct(self.config, scene.background)
         self.cfg_s = cfg_s
+        self._b = None
+        self._M = None
+        if G == 0:
+            self._init_empty(gts, weights, loss, residual_exports)
+            return
         err = torch.zeros(1, dtype=torch.int32, device=dev)
         T = timer if timer is not None else _NoTimer()
         T.tick("start")
@@ -537,8 +542,37 @@ class CacheSet:
         call("slm_gauss_tab", ptr(scene.x32()), G, ptr(self.gtab), stream_ptr())
         call("slm_run_static", _lib.byref(self._tile_args()), R, ptr(self.run_slot), ptr(self.run_static),
              stream_ptr())
-        self._b = None
-        self._M = None
+
+    def _init_empty(self, gts, weights, loss, residual_exports):
+        """G = 0: background images, no entries; b and M are
+        empty and every product is the zero map."""
+        dev, N = self.device, self.N
+        self.E = self.R = self.n_pairs = self.n_chunks = self.n_inst_total = 0
+        bg = torch.tensor(self.scene.background, dtype=torch.float64, device=dev)
+        self.rgb_all = bg.repeat(N)
+        self.t_final_all = torch.ones(N, dtype=torch.float64, device=dev)
+        have_w = gts is not None or weights is not None
+        self.gradr = torch.zeros(N * 4, dtype=torch.float32, device=dev) if have_w else None
+        self.cgrad = torch.zeros(N * 4, dtype=torch.float32, device=dev) if have_w else None
+        self.u = torch.zeros(N * 4, dtype=torch.float32, device=dev)
+        self.frames, parts = [], []
+        self.residual_exports = [] if residual_exports else None
+        for v, cam in enumerate(self.cameras):
+            fr = ViewFrame(cam, self.pix_bases[v])
+            hw = cam.num_pixels
+            fr.rgb = self.rgb_all[fr.pix_base * 3:(fr.pix_base + hw) * 3]
+            fr.t_final = self.t_final_all[fr.pix_base:fr.pix_base + hw]
+            if weights is not None:
+                g4, c4 = weights[v]
+                self.gradr[fr.pix_base * 4:fr.pix_base * 4 + g4.numel()].copy_(g4)
+                self.cgrad[fr.pix_base * 4:fr.pix_base * 4 + c4.numel()].copy_(c4)
+            elif gts is not None:
+                ex = {} if residual_exports else None
+                parts.append(residual_pass(fr, gts[v].to(dev), loss, self.gradr, self.cgrad, ex))
+                if residual_exports:
+                    self.residual_exports.append(ex)
+            self.frames.append(fr)
+        self.energies = [float(p.sum().item()) for p in parts] if gts is not None else None
 
     # ------------------------------------------------------------------
     @property
@@ -550,6 +584,8 @@ class CacheSet:
         """Forward chain m = dy/dx p per pair into self.pm (48 B per pair); the
         J / fused product kernels gather it per run."""
         G, P = self.G, self.P
+        if G == 0:
+            return
         a = _lib.SlmFwdArgs()
         a.xs, a.G = ptr(self.scene.x32()), G
         a.pair_gid, a.pair_vm, a.cams, a.n_pairs = ptr(self.pair_gid), ptr(self.pair_vm), ptr(self.cams_dev), \
@@ -602,6 +638,8 @@ class CacheSet:
         """u (or u_hat) into self.u from the run records written by pair_forward."""
         if weighted and self.gradr is None:
             raise ValueError("cache was built without residual weights")
+        if self.G == 0:
+            return self.u.zero_()
         a = self._tile_args(with_m=True)
         a.gradr = ptr(self.gradr) if weighted else None
         a.u_out = ptr(self.u)
@@ -610,6 +648,8 @@ class CacheSet:
 
     def apply_jt_raw(self, u: torch.Tensor, out: torch.Tensor, scale: float = 1.0, p=None, M=None, lam=0.0,
                      dot_part=None):
+        if self.G == 0:
+            return out
         ra = self._tile_args()
         ra.u, ra.out = ptr(u), ptr(self.run_acc)
         call("slm_apply_jt_runs", _lib.byref(ra), stream_ptr())
@@ -626,6 +666,10 @@ class CacheSet:
         sums, per-gaussian backward chain."""
         if self.gradr is None:
             raise ValueError("cache was built without residual weights")
+        if self.G == 0:
+            if dot_part is not None:
+                dot_part.zero_()
+            return out
         self.pair_forward(p)
         a = self._tile_args(with_m=True)
         a.gradr, a.out = ptr(self.gradr), ptr(self.run_acc)
@@ -650,6 +694,9 @@ class CacheSet:
             if self.gradr is None:
                 raise ValueError("cache was built without residual weights")
             sums = _empty(self.R * _lib.DIAG_D, torch.float32, self.device)
+            if self.G == 0:
+                self._M = torch.empty(0, dtype=torch.float32, device=self.device)
+                return self._M
             ptab = _empty(self.n_pairs * _lib.load().slm_diag_tab_floats(), torch.float32, self.device)
             call("slm_pair_tables", ptr(self.scene.x32()), self.G, self.scene.sh_degree, ptr(self.pair_gid),
                  ptr(self.pair_vm), ptr(self.cams_dev), self.n_pairs, ptr(ptab), ptr(self.gtab), stream_ptr())
@@ -673,6 +720,12 @@ class CacheSet:
         (ref: jacobian.py:401-409) and its gaussian-sorted permutation
         (ref: jacobian.py:93-105), reconstructed from the run order."""
         cam = self.cameras[v]
+        if self.G == 0:
+            e, f = np.zeros(0, np.int64), np.zeros(0)
+            return dict(pixel_ids=e, gaussian_ids=e, alphas=f, alpha_eff=f, transmittances=f,
+                        dc_dalpha=np.zeros((0, 3)), dc_dcs=f, offsets=np.zeros(cam.num_pixels + 1, np.int64),
+                        g_pixel_ids=e, g_gaussian_ids=e, g_offsets=np.zeros(1, np.int64), g_source_index=e,
+                        g_dc_dalpha=np.zeros((0, 3)), g_alpha_eff=f, g_dc_dcs=f)
         t0, t1 = self.view_tile_base[v], self.view_tile_base[v + 1]
         tro = self.tile_run_off.cpu().numpy()
         r0, r1 = int(tro[t0]), int(tro[t1])

@@ -38,10 +38,14 @@ def view_energy(scene: GaussianScene, camera, gt: torch.Tensor, config=None, los
     config = config if config is not None else DEFAULT_CONFIG
     cfg_s = cfg_s if cfg_s is not None else rast_cfg_struct(config, scene.background)
     fr = ViewFrame(camera, 0)
+    hw = camera.num_pixels
+    if scene.num_gaussians == 0:      # the background image
+        fr.rgb = torch.tensor(scene.background, dtype=torch.float64, device=dev).repeat(hw)
+        g4 = torch.empty(hw * 4, dtype=torch.float32, device=dev)
+        return residual_pass(fr, gt, loss, g4, torch.empty_like(g4)).sum()
     if err is None:
         err = torch.zeros(1, dtype=torch.int32, device=dev)
     project_and_bin(scene, fr, cfg_s, err)
-    hw = camera.num_pixels
     fr.rgb = torch.empty(hw * 3, dtype=torch.float64, device=dev)
     fr.t_final = torch.empty(hw, dtype=torch.float64, device=dev)
     cnt = torch.zeros(hw + 1, dtype=torch.int32, device=dev)

@@ -61,6 +61,8 @@ class ProjectedSplats:
 
 
 def project_scene(scene: GaussianScene, camera: Camera, config: RenderConfig = DEFAULT_CONFIG) -> ProjectedSplats:
+    if scene.num_gaussians == 0:
+        return ProjectedSplats.from_bytes(torch.empty(0, dtype=torch.uint8, device=scene.device), 0)
     fr = ViewFrame(camera, 0)
     err = torch.zeros(1, dtype=torch.int32, device=scene.device)
     project_and_bin(scene, fr, rast_cfg_struct(config, scene.background), err, depth_only=True)
@@ -105,6 +107,8 @@ def render(scene: GaussianScene, camera: Camera, config: RenderConfig = DEFAULT_
     """ref: rasterizer.py:319-358."""
     dev = scene.device
     G = scene.num_gaussians
+    if G == 0:
+        return _render_empty(scene, camera, traversals)
     cfg_s = rast_cfg_struct(config, scene.background)
     fr = ViewFrame(camera, 0)
     err = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -138,4 +142,22 @@ def render(scene: GaussianScene, camera: Camera, config: RenderConfig = DEFAULT_
     pix = torch.repeat_interleave(torch.arange(hw, device=dev), (off[1:] - off[:-1]))
     tr = Traversals(pixel_ids=pix, gaussian_ids=tg[:E], alphas=ta[:E], transmittances=tt[:E], offsets=off,
                     t_final=fr.t_final, splat_colors=splats.color, width=camera.width, height=camera.height)
+    return RenderResult(image, tr, splats)
+
+
+def _render_empty(scene: GaussianScene, camera: Camera, traversals: bool) -> RenderResult:
+    """an empty scene renders the background with empty traversals."""
+    dev = scene.device
+    hw = camera.num_pixels
+    bg = torch.tensor(scene.background, dtype=torch.float64, device=dev)
+    image = bg.expand(camera.height, camera.width, 3).contiguous()
+    splats = project_scene(scene, camera)
+    if not traversals:
+        return RenderResult(image, None, splats)
+    e64 = torch.empty(0, dtype=torch.int64, device=dev)
+    ef = torch.empty(0, dtype=torch.float64, device=dev)
+    tr = Traversals(pixel_ids=e64, gaussian_ids=e64.clone(), alphas=ef, transmittances=ef.clone(),
+                    offsets=torch.zeros(hw + 1, dtype=torch.int64, device=dev),
+                    t_final=torch.ones(hw, dtype=torch.float64, device=dev), splat_colors=splats.color,
+                    width=camera.width, height=camera.height)
     return RenderResult(image, tr, splats)

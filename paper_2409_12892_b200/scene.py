@@ -106,8 +106,8 @@ class GaussianScene:
 
     def __init__(self, x: torch.Tensor, sh_degree: int, background=(0.0, 0.0, 0.0)):
         P = params_per_gaussian(sh_degree)
-        if x.dim() != 1 or x.numel() % P != 0 or x.numel() == 0:
-            raise ValueError(f"parameter vector length {x.numel()} is not a positive multiple of {P}")
+        if x.dim() != 1 or x.numel() % P != 0:
+            raise ValueError(f"parameter vector length {x.numel()} is not a multiple of {P}")
         self.x = x if x.dtype == torch.float64 else x.double()
         self.sh_degree = int(sh_degree)
         self.background = np.asarray(background, dtype=np.float64).reshape(3)

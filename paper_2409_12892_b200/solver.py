@@ -94,6 +94,10 @@ def pcg_run(cache: CacheSet, b: torch.Tensor, M: torch.Tensor, lam: float, max_i
 
     Raises NonSPDError when p^T g <= 0."""
     n = b.numel()
+    if n == 0:                        # empty scene: nothing to solve
+        if stats is not None:
+            stats.update(products=0, iterations=0, rr=0.0, bb=0.0)
+        return torch.zeros(0, dtype=torch.float64, device=b.device)
     ws = ws or PCGWorkspace(n, b.device)
     nb = _lib.load().slm_backward_blocks(cache.G)
     dot_part = torch.zeros(nb, dtype=torch.float64, device=b.device)
@@ -107,16 +111,11 @@ def pcg_run(cache: CacheSet, b: torch.Tensor, M: torch.Tensor, lam: float, max_i
     call("slm_pcg_finalize", 0, ptr(ws.st), ptr(ws.part), s)
     # Iterations are queued one ahead of the host's exit check: the device
     # keeps a sticky stop flag (b = 0, converged, non-SPD) that turns the
-    # iteration kernels into no-ops, and the host reads iteration i-1's flag
-    # (async copy + event) only after iteration i is queued -- no per-
-    # iteration drain of the GPU; at most one extra product runs on exit.
-    for it in range(max_iters + 1):
-        if it > 0:
-            ws.stop_ev[(it - 1) % 2].synchronize()
-            if ws.stop_host[(it - 1) % 2] != 0.0:
-                break
-        if it == max_iters:
-            break
+    # vector kernels into no-ops, and the host reads iteration i-1's flag
+    # (async copy + event) only after iteration i is queued, so the GPU never
+    # drains between iterations; on an early exit the one product queued
+    # ahead runs but its result is discarded by the gated update.
+    for it in range(max_iters):
         call("slm_pcg_pupdate", ptr(ws.p), ptr(ws.r), ptr(M), ptr(ws.st), n, s)
         _product(cache, ws.p, ws.g, lam, M, dot_part, timer)
         call("slm_pcg_update", 1, ptr(ws.x), ptr(ws.r), ptr(ws.p), ptr(ws.g), ptr(b), ptr(M), float(lam),
@@ -124,12 +123,18 @@ def pcg_run(cache: CacheSet, b: torch.Tensor, M: torch.Tensor, lam: float, max_i
         call("slm_pcg_finalize", 1, ptr(ws.st), ptr(ws.part), s)
         ws.stop_host[it % 2].copy_(ws.st[ST_STOP], non_blocking=True)
         ws.stop_ev[it % 2].record()
+        if it > 0:
+            ws.stop_ev[(it - 1) % 2].synchronize()
+            if ws.stop_host[(it - 1) % 2] != 0.0:
+                break
     st_h = ws.st.cpu()
     iters = int(st_h[ST_ITERS])
     if int(st_h[ST_FLAGS]) & 1:
         raise NonSPDError(f"p^T g = {float(st_h[ST_PG])} <= 0 at PCG iteration {iters}")
     if stats is not None:
-        stats["products"] = 1 + iters
+        # b = 0: x = x0 = 0 and the reference makes no product; the
+        # product of the zero x0 is still launched here but its result is unused
+        stats["products"] = 1 + iters if float(st_h[ST_BB]) > 0.0 else 0
         stats["iterations"] = iters
         stats["rr"] = float(st_h[ST_RR])
         stats["bb"] = float(st_h[ST_BB])
@@ -159,12 +164,15 @@ def pcg_solve(scene, cache, b: ParamVector, M_diag: ParamVector, lambda_reg: flo
 
 class Combiner:
     """Eq. 7 accumulator in fp64: num += M * Delta, den += M; finalize
-    num / max(den, 1e-12) to the fp32 direction."""
+    num / max(den, 1e-12) to the fp32 direction.  The buffer is packed
+    [num (n); den (n); energy; accepted batches] so that one all_reduce
+    combines everything a rank contributes to the LM step."""
 
     def __init__(self, n: int, device):
-        self.buf = torch.zeros(2 * n, dtype=torch.float64, device=device)
+        self.buf = torch.zeros(2 * n + 2, dtype=torch.float64, device=device)
         self.n = n
         self.accepted = 0
+        self.energy = 0.0
 
     @property
     def num(self):
@@ -172,20 +180,25 @@ class Combiner:
 
     @property
     def den(self):
-        return self.buf[self.n:]
+        return self.buf[self.n:2 * self.n]
 
     def add(self, delta: torch.Tensor, M: torch.Tensor):
         call("slm_combine_acc", ptr(self.num), ptr(self.den), ptr(delta), ptr(M), self.n, stream_ptr())
         self.accepted += 1
 
-    def allreduce(self, group=None):
-        """ONE packed all_reduce of [num; den] plus the accepted-batch count."""
+    def allreduce(self, group=None, world_size: int | None = None):
+        """ONE packed all_reduce of [num; den; energy; accepted] when the
+        subsets are sharded over several ranks (world_size > 1)."""
         import torch.distributed as dist
-        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-            allreduce_sum_(self.buf, group)
-            acc = torch.tensor([self.accepted], dtype=torch.int64, device=self.buf.device)
-            allreduce_sum_(acc, group)
-            self.accepted = int(acc.item())
+        if not (dist.is_available() and dist.is_initialized()):
+            return
+        w = dist.get_world_size(group) if world_size is None else world_size
+        if w <= 1:
+            return
+        self.buf[2 * self.n:].copy_(torch.tensor([self.energy, float(self.accepted)], dtype=torch.float64))
+        allreduce_sum_(self.buf, group)
+        e, a = self.buf[2 * self.n:].tolist()
+        self.energy, self.accepted = e, int(round(a))
 
     def finalize(self) -> torch.Tensor:
         out = torch.empty(self.n, dtype=torch.float32, device=self.buf.device)
@@ -273,7 +286,6 @@ def lm_direction(scene, cameras, gts, schedule: BatchSchedule = BatchSchedule(),
     n = scene.param_count
     comb = Combiner(n, scene.device)
     ws = PCGWorkspace(n, scene.device)
-    energy = 0.0
     entries, pcg_stats = [], []
     caches = []
     shards = list(schedule.shard(len(cameras), rank, world_size))
@@ -287,7 +299,7 @@ def lm_direction(scene, cameras, gts, schedule: BatchSchedule = BatchSchedule(),
         cs = CacheSet(scene, [cameras[i] for i in views], gts_sub, config, loss)
         fetch.release(buf)  # the images are only read by the build's residual pass
         del gts_sub
-        energy += sum(cs.energies)
+        comb.energy += sum(cs.energies)
         entries.append(cs.E)
         b = cs.rhs()
         M = cs.diag()
@@ -303,10 +315,11 @@ def lm_direction(scene, cameras, gts, schedule: BatchSchedule = BatchSchedule(),
             cs.view_ids = list(views)
             caches.append(cs)
         del cs
-    comb.allreduce()
+    comb.allreduce(world_size=world_size)
     if comb.accepted == 0:
         raise NonSPDError("all batches rejected by PCG failure")
-    rep = StepReport(comb.finalize(), energy, comb.accepted, entries, pcg_stats, [])
+    # energy: the global sum over all subsets' views (every rank gets it)
+    rep = StepReport(comb.finalize(), comb.energy, comb.accepted, entries, pcg_stats, [])
     rep.caches = caches
     return rep
 
