@@ -163,7 +163,9 @@ typedef struct {
   const slm_f4* gradr;       /* applyJ: weighting (NULL: unweighted u_hat); diag: grad_r_sq */
   const slm_f4* u;           /* applyJT input, per pixel */
   slm_f4* u_out;             /* applyJ output, per pixel */
-  float* out;                /* applyJT [R*9] / diag [R*14] run partials */
+  float* out;                /* applyJT [R*8] run partials 0-7 (32-byte records) /
+                                diag [R*14] run sums, pair-run-slot order */
+  float* out1;               /* applyJT [R] run partial 8, pair-run-slot order */
   int* tile_counter;         /* streaming kernels: 1 int of device scratch for
                                 dynamic tile scheduling (reset by the launch);
                                 NULL: static round-robin tiles */
@@ -180,7 +182,7 @@ typedef struct {
   const float* p;           /* direction, p[a * sa + g * sg] (either layout) */
   long long sa, sg;
   void* pm;                 /* [P*12] out: m = dy/dx p per pair (3 float4) */
-  const float* gtab;        /* per-gaussian chain constants (slm_gauss_tab) or NULL */
+  const float* gtab;        /* per-gaussian chain rows (slm_gauss_tab) */
 } SlmFwdArgs;
 
 /* per-gaussian backward chain */
@@ -190,16 +192,16 @@ typedef struct {
   const int* gpo;           /* [G+1] gaussian -> pairs (pairs are (gid, view)-numbered) */
   const uint32_t* pair_vm;  /* view | clamp bits << 16 */
   const SlmCamera* cams;
-  const float* pacc;        /* pair_run_off == NULL: per-pair sums (slm_pair_sum);
-                               else per-run partials in pair-run-slot order (the
-                               J^T kernels write run r to its slot in pair_runs) */
-  const int* pair_run_off;  /* [P+1] pair -> run slots, or NULL */
-  const int* warp_g0;       /* packed form: first gaussian of each 32-pair window
-                               (slm_warp_bounds), or NULL for thread-per-gaussian */
+  const float* pacc;        /* per-run partials in pair-run-slot order (the J^T /
+                               diag kernels write run r to its slot in pair_runs):
+                               mode 0 [R*8] partials 0-7, mode 1 [R*14] sums */
+  const float* pacc1;       /* mode 0: [R] partial 8 per run slot */
+  const int* pair_run_off;  /* [P+1] pair -> run slots */
+  const int* warp_g0;       /* first gaussian of each 32-pair window (slm_warp_bounds) */
   const int* pair_gid;
   long long n_pairs;
-  float* gm;                /* packed form: [G*P] gaussian-major scratch */
-  const float* gtab;        /* per-gaussian chain constants (slm_gauss_tab) or NULL */
+  float* gm;                /* [G*P] gaussian-major scratch */
+  const float* gtab;        /* per-gaussian chain rows (slm_gauss_tab) */
   float scale;
   const float* p;           /* optional: fp64 partials of p.(out + lam * max(M,1e-12) * p) */
   const float* Mdiag;
@@ -321,29 +323,31 @@ int slm_chunk_perm(const int* chunk_run, long long n_chunks, const long long* ru
  * (then slm_diag_stream) */
 int slm_pair_tables(const float* xs, long long G, int sh_degree, const int* pair_gid, const uint32_t* pair_vm,
                     const SlmCamera* cams, int n_pairs, float* tab, const float* gtab, cudaStream_t s);
-/* view-independent part of the per-gaussian chain (rotation, scales, the
- * quaternion-normalisation derivatives, sigma'), slm_gauss_tab_floats() per
- * gaussian; once per cache (ref: jacobian.py:159-190, 213-240) */
-int slm_gauss_tab(const float* xs, long long G, float* gtab, cudaStream_t s);
-int slm_gauss_tab_floats(void);
+/* per-gaussian chain rows, slm_gauss_tab_floats(sh_degree) floats each (16-byte
+ * aligned): the view-independent part of the chain (rotation, scales, the
+ * quaternion-normalisation derivatives, sigma'), the position and the SH
+ * coefficients; once per cache (ref: jacobian.py:159-190, 213-240) */
+int slm_gauss_tab(const float* xs, long long G, int sh_degree, float* gtab, cudaStream_t s);
+int slm_gauss_tab_floats(int sh_degree);
 /* 14 diag sums per run on the streaming kernel, written in pair-run-slot
  * order (a->gradr = grad_r_sq, a->ptab from slm_pair_tables) */
 int slm_diag_stream(const SlmTileArgs* a, cudaStream_t s);
 /* forward chain m = dy/dx p per pair (jacobian.py:434-443), 48 B per pair */
 int slm_pair_forward(const SlmFwdArgs* a, int sh_degree, cudaStream_t s);
-/* per-pair sums of run partials (d = 9 J^T partials or 14 diag sums) */
-int slm_pair_sum(const int* pair_run_off, const int* pair_runs, int n_pairs, const float* run_acc, int d,
-                 float* pacc, cudaStream_t s);
 /* backward chain per gaussian, attribute-major out (jacobian.py:314-353):
- * mode 0 from J^T pair sums, mode 1 from diag pair sums */
+ * mode 0 from the J^T run partials, mode 1 from the diag run sums */
 int slm_backward_blocks(long long G);
 int slm_warp_bounds(const int* gpo, long long G, int n_pairs, int* warp_g0, cudaStream_t s);
 int slm_pair_backward(const SlmBackArgs* a, int mode, int sh_degree, cudaStream_t s);
 
 /* ---- PCG (Alg. 1; SPEC pcg_solve 391-399) ------------------ */
 int slm_vec_blocks(void);
-int slm_pcg_pinit(float* p, const float* b, const float* M, long long n, cudaStream_t s);
-int slm_pcg_pupdate(float* p, const double* r, const float* M, const double* st, long long n, cudaStream_t s);
+/* p (attribute-major, G*P) and, when p_gm != NULL, its padded gaussian-major
+ * copy p_gm[g * pg + a] (pg = slm_gm_stride(P), pad 0) for the forward chain */
+int slm_gm_stride(int P);
+int slm_pcg_pinit(float* p, float* p_gm, const float* b, const float* M, long long G, int P, cudaStream_t s);
+int slm_pcg_pupdate(float* p, float* p_gm, const double* r, const float* M, const double* st, long long G, int P,
+                    cudaStream_t s);
 int slm_pcg_update(int mode, double* x, double* r, const float* p, const float* g, const float* b, const float* M,
                    double lam, double* st, const double* dot_part, int n_dot, double* part, long long n,
                    cudaStream_t s);

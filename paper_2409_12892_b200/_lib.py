@@ -63,7 +63,7 @@ class SlmTileArgs(C.Structure):
                 ("run_start", c_vp), ("run_q", c_vp), ("run_tile", c_vp), ("run_static", c_vp), ("pm", c_vp),
                 ("geo", c_vp), ("ptab", c_vp),
                 ("rec4", c_vp), ("d2", c_vp), ("pix", c_vp),
-                ("gradr", c_vp), ("u", c_vp), ("u_out", c_vp), ("out", c_vp), ("tile_counter", c_vp)]
+                ("gradr", c_vp), ("u", c_vp), ("u_out", c_vp), ("out", c_vp), ("out1", c_vp), ("tile_counter", c_vp)]
 
 
 class SlmFwdArgs(C.Structure):
@@ -72,7 +72,7 @@ class SlmFwdArgs(C.Structure):
 
 
 class SlmBackArgs(C.Structure):
-    _fields_ = [("xs", c_vp), ("G", c_ll), ("gpo", c_vp), ("pair_vm", c_vp), ("cams", c_vp), ("pacc", c_vp),
+    _fields_ = [("xs", c_vp), ("G", c_ll), ("gpo", c_vp), ("pair_vm", c_vp), ("cams", c_vp), ("pacc", c_vp), ("pacc1", c_vp),
                 ("pair_run_off", c_vp), ("warp_g0", c_vp), ("pair_gid", c_vp), ("n_pairs", c_ll), ("gm", c_vp), ("gtab", c_vp),
                 ("scale", c_f),
                 ("p", c_vp), ("Mdiag", c_vp), ("lam", c_d), ("lam_out", c_i), ("out", c_vp), ("dot_part", c_vp)]
@@ -81,7 +81,7 @@ class SlmBackArgs(C.Structure):
 SPLAT_BYTES = 96
 PAIR_GEO_BYTES = 32
 PAIR_M_BYTES = 48
-JT_D = 9
+JT_D = 9          # J^T partials per run: 8 (32-byte records) + 1 (separate array)
 DIAG_D = 14
 
 # name -> (restype, argtypes)
@@ -127,17 +127,17 @@ _SIGS = {
     "slm_chunk_perm": (c_i, [c_vp, c_ll, c_vp, c_vp, c_vp]),
     "slm_tile_chunks": (c_i, [c_vp, c_i, c_vp, c_vp, c_vp, c_vp, c_i, c_vp]),
     "slm_pair_tables": (c_i, [c_vp, c_ll, c_i, c_vp, c_vp, c_vp, c_i, c_vp, c_vp, c_vp]),
-    "slm_gauss_tab": (c_i, [c_vp, c_ll, c_vp, c_vp]),
-    "slm_gauss_tab_floats": (c_i, []),
+    "slm_gauss_tab": (c_i, [c_vp, c_ll, c_i, c_vp, c_vp]),
+    "slm_gauss_tab_floats": (c_i, [c_i]),
     "slm_diag_stream": (c_i, [c_vp, c_vp]),
     "slm_pair_forward": (c_i, [c_vp, c_i, c_vp]),
-    "slm_pair_sum": (c_i, [c_vp, c_vp, c_i, c_vp, c_i, c_vp, c_vp]),
     "slm_backward_blocks": (c_i, [c_ll]),
     "slm_warp_bounds": (c_i, [c_vp, c_ll, c_i, c_vp, c_vp]),
     "slm_pair_backward": (c_i, [c_vp, c_i, c_i, c_vp]),
     "slm_vec_blocks": (c_i, []),
-    "slm_pcg_pinit": (c_i, [c_vp, c_vp, c_vp, c_ll, c_vp]),
-    "slm_pcg_pupdate": (c_i, [c_vp, c_vp, c_vp, c_vp, c_ll, c_vp]),
+    "slm_gm_stride": (c_i, [c_i]),
+    "slm_pcg_pinit": (c_i, [c_vp, c_vp, c_vp, c_vp, c_ll, c_i, c_vp]),
+    "slm_pcg_pupdate": (c_i, [c_vp, c_vp, c_vp, c_vp, c_vp, c_ll, c_i, c_vp]),
     "slm_pcg_update": (c_i, [c_i, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_d, c_vp, c_vp, c_i, c_vp, c_ll, c_vp]),
     "slm_pcg_finalize": (c_i, [c_i, c_vp, c_vp, c_vp]),
     "slm_combine_acc": (c_i, [c_vp, c_vp, c_vp, c_vp, c_ll, c_vp]),

@@ -3,6 +3,14 @@
 #pragma once
 #include "slm_common.cuh"
 
+// minimum resident blocks per SM of the per-pair chain kernels (register cap)
+#ifndef SLM_PM_MINB
+#define SLM_PM_MINB 4
+#endif
+#ifndef SLM_BW_MINB
+#define SLM_BW_MINB 4
+#endif
+
 // arithmetic type of the per-pair chain (outputs are stored as float)
 #ifndef SLM_CHAIN_T
 #define SLM_CHAIN_T float
@@ -22,9 +30,14 @@ struct Tab {
 // the normalised quaternion, s^2 = exp(2 log s), the projected rotation
 // derivatives Mq_l = (dR/dq_hat_l - q_hat_l sum_k q_hat_k dR/dq_hat_k) / |q|
 // (the (I - q_hat q_hat^T) / |q| normalisation chain) and sigma'(logit).
-// Precomputed once per cache (k_gauss_tab, GTAB floats per gaussian) so the
-// per-(gaussian, view) chain only does the camera-dependent part.
-#define GTAB 52  // Rg 9, s2 3, Mq 36, dopa 1, pad
+// Precomputed once per cache (k_gauss_tab) together with the position and the
+// SH coefficients, so the per-(gaussian, view) chain reads one contiguous,
+// 16-byte aligned row per gaussian (gtab_floats(K) floats):
+//   [Rg 9 | s2 3 | Mq 36 | dopa | pos 3 | SH coefficients 3K (channel-major), pad]
+#define GT_DOPA 48
+#define GT_POS 49
+#define GT_SH 52
+__host__ __device__ constexpr int gtab_floats(int K) { return GT_SH + ((3 * K + 3) & ~3); }
 template <typename Rt>
 __device__ __forceinline__ void gauss_static(const float* __restrict__ xs, long long G, long long g, Rt (&Rg)[9],
                                              Rt (&s2)[3], Rt (&Mq)[4][9], Rt& dopa) {
@@ -57,12 +70,14 @@ __device__ __forceinline__ void gauss_static(const float* __restrict__ xs, long 
   dopa = o * (Rt(1) - o);
 }
 
+template <int K>
 static __global__ void __launch_bounds__(256) k_gauss_tab(const float* __restrict__ xs, long long G,
                                                           float* __restrict__ gtab) {
+  constexpr int GT = gtab_floats(K);
   for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < G; g += (long long)gridDim.x * blockDim.x) {
     float Rg[9], s2[3], Mq[4][9], dopa;
     gauss_static<float>(xs, G, g, Rg, s2, Mq, dopa);
-    float o[GTAB];
+    float o[GT];
 #pragma unroll
     for (int i = 0; i < 9; ++i) o[i] = Rg[i];
 #pragma unroll
@@ -71,42 +86,53 @@ static __global__ void __launch_bounds__(256) k_gauss_tab(const float* __restric
     for (int l = 0; l < 4; ++l)
 #pragma unroll
       for (int i = 0; i < 9; ++i) o[12 + l * 9 + i] = Mq[l][i];
-    o[48] = dopa;
-    o[49] = o[50] = o[51] = 0.f;
-    float4* dst = reinterpret_cast<float4*>(gtab + (size_t)g * GTAB);
+    o[GT_DOPA] = dopa;
 #pragma unroll
-    for (int k = 0; k < GTAB / 4; ++k) dst[k] = make_float4(o[4 * k], o[4 * k + 1], o[4 * k + 2], o[4 * k + 3]);
+    for (int i = 0; i < 3; ++i) o[GT_POS + i] = xs[i * G + g];
+#pragma unroll
+    for (int i = GT_SH; i < GT; ++i) o[i] = i - GT_SH < 3 * K ? xs[(long long)(11 + i - GT_SH) * G + g] : 0.f;
+    float4* dst = reinterpret_cast<float4*>(gtab + (size_t)g * GT);
+#pragma unroll
+    for (int k = 0; k < GT / 4; ++k) dst[k] = make_float4(o[4 * k], o[4 * k + 1], o[4 * k + 2], o[4 * k + 3]);
+  }
+}
+
+// 16-byte read-only load that the compiler keeps in program order relative to
+// the other ordered loads: the chain kernels load each part of the gaussian's
+// row right before its use, which bounds the live registers (and so keeps
+// occupancy up in these latency-bound kernels)
+__device__ __forceinline__ float4 ldg4_ordered(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+}
+template <int N>
+__device__ __forceinline__ void ldg_row(const float* __restrict__ src, float* dst) {
+#pragma unroll
+  for (int k = 0; k < N / 4; ++k) {
+    const float4 v = ldg4_ordered(reinterpret_cast<const float4*>(src) + k);
+    dst[4 * k] = v.x;
+    dst[4 * k + 1] = v.y;
+    dst[4 * k + 2] = v.z;
+    dst[4 * k + 3] = v.w;
   }
 }
 
 template <int K, typename Rt = SLM_CHAIN_T>
 __device__ __forceinline__ void pair_tab(const float* __restrict__ xs, long long G, long long g, const SlmCamera& cam,
-                                         uint32_t clampbits, Tab<K>& T, const float* __restrict__ gtab = nullptr) {
-  const Rt p0 = xs[g], p1 = xs[G + g], p2 = xs[2 * G + g];
-  Rt Rg[9], s2[3], Mq[4][9], dopa;
-  if (gtab) {
-    const float4* gr = reinterpret_cast<const float4*>(gtab + (size_t)g * GTAB);
-    float t[GTAB];
+                                         uint32_t clampbits, Tab<K>& T, const float* __restrict__ gtab) {
+  constexpr int GT = gtab_floats(K);
+  const float* grow = gtab + (size_t)g * GT;
+  float t[GT];
+  ldg_row<12>(grow, t);                 // Rg, s2
+  ldg_row<4>(grow + GT_DOPA, t + GT_DOPA);  // dopa, position
+  Rt Rg[9], s2[3], Mq[4][9];
 #pragma unroll
-    for (int k = 0; k < GTAB / 4; ++k) {
-      const float4 v = __ldg(gr + k);
-      t[4 * k] = v.x;
-      t[4 * k + 1] = v.y;
-      t[4 * k + 2] = v.z;
-      t[4 * k + 3] = v.w;
-    }
+  for (int i = 0; i < 9; ++i) Rg[i] = t[i];
 #pragma unroll
-    for (int i = 0; i < 9; ++i) Rg[i] = t[i];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) s2[i] = t[9 + i];
-#pragma unroll
-    for (int l = 0; l < 4; ++l)
-#pragma unroll
-      for (int i = 0; i < 9; ++i) Mq[l][i] = t[12 + l * 9 + i];
-    dopa = t[48];
-  } else {
-    gauss_static<Rt>(xs, G, g, Rg, s2, Mq, dopa);
-  }
+  for (int i = 0; i < 3; ++i) s2[i] = t[9 + i];
+  const Rt dopa = t[GT_DOPA];
+  const Rt p0 = t[GT_POS], p1 = t[GT_POS + 1], p2 = t[GT_POS + 2];
   Rt R[9];
 #pragma unroll
   for (int i = 0; i < 9; ++i) R[i] = (Rt)cam.R[i];
@@ -165,6 +191,11 @@ __device__ __forceinline__ void pair_tab(const float* __restrict__ xs, long long
       UR[r][j] = U[r][0] * Rg[j] + U[r][1] * Rg[3 + j] + U[r][2] * Rg[6 + j];
       Wm[r][j] = UR[r][j] * s2[j];
     }
+  ldg_row<36>(grow + 12, t + 12);        // Mq
+#pragma unroll
+  for (int l = 0; l < 4; ++l)
+#pragma unroll
+    for (int i = 0; i < 9; ++i) Mq[l][i] = t[12 + l * 9 + i];
 #pragma unroll
   for (int l = 0; l < 4; ++l) {
     Rt V[2][3];
@@ -188,6 +219,7 @@ __device__ __forceinline__ void pair_tab(const float* __restrict__ xs, long long
     T.dcov[2][7 + i] = Rt(2) * s2[i] * UR[1][i] * UR[1][i];
   }
   // colour
+  ldg_row<GT - GT_SH>(grow + GT_SH, t + GT_SH);  // SH coefficients
   const Rt v0 = p0 - (Rt)cam.C[0], v1 = p1 - (Rt)cam.C[1], v2 = p2 - (Rt)cam.C[2];
   const Rt vn = sqrt(v0 * v0 + v1 * v1 + v2 * v2), ivn = Rt(1) / vn;
   const Rt d0 = v0 * ivn, d1 = v1 * ivn, d2 = v2 * ivn;
@@ -196,7 +228,7 @@ __device__ __forceinline__ void pair_tab(const float* __restrict__ xs, long long
 #pragma unroll
   for (int k = 0; k < K; ++k) T.Y[k] = (float)Yr[k];
   Rt dcdd[3][3];
-  auto coef = [&](int ch, int k) { return (Rt)xs[(long long)(11 + ch * K + k) * G + g]; };
+  auto coef = [&](int ch, int k) { return (Rt)t[GT_SH + ch * K + k]; };
   sh_grad_dot<Rt, K>(d0, d1, d2, coef, dcdd);
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) {
@@ -213,39 +245,48 @@ __device__ __forceinline__ void pair_tab(const float* __restrict__ xs, long long
 // are (gid, view)-numbered, so neighbouring threads share the gaussian's
 // parameters), m = dy/dx p packed as 3 float4 (48 B).  The product kernel's
 // producer warp gathers it per run (cp.async) next to the static run records.
+// p is read either attribute-major / unpadded gaussian-major (p[a sa + g sg])
+// or, when sa = 1 and sg is a multiple of 4 >= P (the padded gaussian-major
+// copy the PCG kernels write), as 16-byte row loads.
 template <int K>
-__global__ void __launch_bounds__(128) k_pair_m(SlmFwdArgs A) {
+__global__ void __launch_bounds__(128, SLM_PM_MINB) k_pair_m(SlmFwdArgs A) {
+  constexpr int P = 11 + 3 * K, P4 = (P + 3) / 4;
   float4* __restrict__ pm = reinterpret_cast<float4*>(A.pm);
+  const long long sa = A.sa, sg = A.sg;
+  const float* __restrict__ p = A.p;
+  const bool rows = sa == 1 && (sg & 3) == 0 && sg >= 4 * P4 && ((uintptr_t)p & 15) == 0;
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < A.n_pairs; q += gridDim.x * blockDim.x) {
     const long long g = A.pair_gid[q];
     const uint32_t vm = A.pair_vm[q];
-    const long long sa = A.sa, sg = A.sg;
-    const float* __restrict__ p = A.p;
     Tab<K> T;
     pair_tab<K>(A.xs, A.G, g, A.cams[vm & 0xffffu], vm >> 16, T, A.gtab);
-    float pg[11];
+    float pv[4 * P4];
+    if (rows) {
+      ldg_row<4 * P4>(p + g * sg, pv);
+    } else {
 #pragma unroll
-    for (int a = 0; a < 11; ++a) pg[a] = p[a * sa + g * sg];
+      for (int a = 0; a < P; ++a) pv[a] = p[a * sa + g * sg];
+    }
     float mmu0 = 0.f, mmu1 = 0.f, mc[3] = {0.f, 0.f, 0.f}, mcol[3];
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-      mmu0 += T.dmu[0][j] * pg[j];
-      mmu1 += T.dmu[1][j] * pg[j];
+      mmu0 += T.dmu[0][j] * pv[j];
+      mmu1 += T.dmu[1][j] * pv[j];
     }
 #pragma unroll
     for (int k = 0; k < 3; ++k)
 #pragma unroll
-      for (int j = 0; j < 10; ++j) mc[k] += T.dcov[k][j] * pg[j];
+      for (int j = 0; j < 10; ++j) mc[k] += T.dcov[k][j] * pv[j];
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
       float s = 0.f;
 #pragma unroll
-      for (int k = 0; k < K; ++k) s += T.Y[k] * p[(11 + ch * K + k) * sa + g * sg];
-      mcol[ch] = T.dcol[ch][0] * pg[0] + T.dcol[ch][1] * pg[1] + T.dcol[ch][2] * pg[2] + T.mask[ch] * s;
+      for (int k = 0; k < K; ++k) s += T.Y[k] * pv[11 + ch * K + k];
+      mcol[ch] = T.dcol[ch][0] * pv[0] + T.dcol[ch][1] * pv[1] + T.dcol[ch][2] * pv[2] + T.mask[ch] * s;
     }
     // record layout slots 5..13: inv_o * m_opa (scaled in k_run_records), m_mu0, m_mu1,
     // m_cov0/2, m_cov1, m_cov2/2, m_col0..2
-    pm[(size_t)q * 3 + 0] = make_float4(T.dopa * pg[10], mmu0, mmu1, 0.5f * mc[0]);
+    pm[(size_t)q * 3 + 0] = make_float4(T.dopa * pv[10], mmu0, mmu1, 0.5f * mc[0]);
     pm[(size_t)q * 3 + 1] = make_float4(mc[1], 0.5f * mc[2], mcol[0], mcol[1]);
     pm[(size_t)q * 3 + 2] = make_float4(mcol[2], 0.f, 0.f, 0.f);
   }

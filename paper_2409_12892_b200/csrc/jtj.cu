@@ -3,35 +3,8 @@
 // in stream.cu.
 #include "chain.cuh"
 
-#define NW 8          // warps per CTA (diag)
 #define DIAG_TAB 48   // floats per pair coefficient table (diag)
 #define DIAG_RUN_D 14
-#define TBD 256
-
-__device__ __forceinline__ int view_of_tile(const int* __restrict__ vtb, int n_views, int t) {
-  int v = 0;
-  while (v + 1 < n_views && vtb[v + 1] <= t) ++v;
-  return v;
-}
-
-__device__ __forceinline__ int rs16_slot(int lane) {
-  return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
-}
-// reduce-scatter of 16 per-lane values in 16 shuffles; lanes 2i, 2i+1 end
-// with the warp sum of value rs16_slot(lane); fixed pattern -> deterministic
-__device__ __forceinline__ float warp_reduce_scatter16(const float (&v)[16], int lane) {
-  const unsigned F = 0xffffffffu;
-  float w8[8], w4[4], w2[2];
-  const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4, u2 = lane & 2;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) w8[j] = (u16 ? v[j + 8] : v[j]) + __shfl_xor_sync(F, u16 ? v[j] : v[j + 8], 16);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) w4[j] = (u8 ? w8[j + 4] : w8[j]) + __shfl_xor_sync(F, u8 ? w8[j] : w8[j + 4], 8);
-#pragma unroll
-  for (int j = 0; j < 2; ++j) w2[j] = (u4 ? w4[j + 2] : w4[j]) + __shfl_xor_sync(F, u4 ? w4[j] : w4[j + 2], 4);
-  float w1 = (u2 ? w2[1] : w2[0]) + __shfl_xor_sync(F, u2 ? w2[0] : w2[1], 2);
-  return w1 + __shfl_xor_sync(F, w1, 1);
-}
 
 // ---------------------------------------------------------------------------
 // diag(J^T W J): per run, 11 geometry sums of grad_r_sq * (dc/dx_k)^2 and the
@@ -81,151 +54,17 @@ __global__ void __launch_bounds__(128) k_pair_tables(const float* __restrict__ x
 }
 
 // ---------------------------------------------------------------------------
-// per-pair sums of the run partials (fixed run order -> deterministic):
-// pacc[q] = sum over the pair's runs of acc[run] (D = 9 J^T partials or 14
-// diag sums); pairs are (gid, view)-numbered, so the backward chain below
-// reads them contiguously
-// ---------------------------------------------------------------------------
-template <int D>
-__global__ void k_pair_sum(const int* __restrict__ pair_run_off, const int* __restrict__ pair_runs, int n_pairs,
-                           const float* __restrict__ acc, float* __restrict__ pacc) {
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_pairs; q += gridDim.x * blockDim.x) {
-    float a[D];
-#pragma unroll
-    for (int j = 0; j < D; ++j) a[j] = 0.f;
-    for (int rr = pair_run_off[q]; rr < pair_run_off[q + 1]; ++rr) {
-      const float* src = acc + (size_t)pair_runs[rr] * D;
-#pragma unroll
-      for (int j = 0; j < D; ++j) a[j] += src[j];
-    }
-#pragma unroll
-    for (int j = 0; j < D; ++j) pacc[(size_t)q * D + j] = a[j];
-  }
-}
-
-// ---------------------------------------------------------------------------
-// per-gaussian backward chain (ref: jacobian.py:314-353 / 506-510):
-//   MODE 0: out = scale * sum_pairs tab^T pacc   (J^T partials)
-//   MODE 1: out = sum_pairs pacc, SH block via basis^2   (diag sums)
-// optional fp64 partials of p.(out + lam * max(M, 1e-12) * p) (PCG), and
-// out += lam * max(M, 1e-12) * p when lam_out
-// ---------------------------------------------------------------------------
-// sum of one pair's run partials (slot order) or its precomputed pair sum
-template <int D, int J0, int J1>
-__device__ __forceinline__ void pair_partials(const SlmBackArgs& A, int q, float (&a)[J1 - J0]) {
-#pragma unroll
-  for (int j = 0; j < J1 - J0; ++j) a[j] = 0.f;
-  if (A.pair_run_off) {
-    for (int rr = A.pair_run_off[q]; rr < A.pair_run_off[q + 1]; ++rr) {
-#pragma unroll
-      for (int j = 0; j < J1 - J0; ++j) a[j] += A.pacc[(size_t)rr * D + J0 + j];
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < J1 - J0; ++j) a[j] = A.pacc[(size_t)q * D + J0 + j];
-  }
-}
-
-// Two sweeps over the gaussian's pairs keep the live state small (geometry
-// accumulators + chain, then the 3 x K SH accumulators + basis) so the kernel
-// runs at 4 blocks / SM without spills.
-template <int K, int MODE>
-__global__ void __launch_bounds__(128, 3) k_gauss_backward(SlmBackArgs A) {
-  __shared__ double sm[32];
-  constexpr int D = MODE == 0 ? 9 : DIAG_RUN_D;
-  const long long G = A.G;
-  double dot = 0.0;
-  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < G; g += (long long)gridDim.x * blockDim.x) {
-    const int k0 = A.gpo[g], k1 = A.gpo[g + 1];
-    // ---- sweep 1: the 11 geometry parameters
-    float og[11];
-#pragma unroll
-    for (int j = 0; j < 11; ++j) og[j] = 0.f;
-    for (int q = k0; q < k1; ++q) {  // this gaussian's pairs, in view order
-      if (MODE == 0) {
-        float a[9];
-        pair_partials<D, 0, 9>(A, q, a);
-        const uint32_t vm = A.pair_vm[q];
-        Tab<K> T;
-        pair_tab<K>(A.xs, G, g, A.cams[vm & 0xffffu], vm >> 16, T, A.gtab);
-#pragma unroll
-        for (int j = 0; j < 3; ++j)
-          og[j] += T.dmu[0][j] * a[0] + T.dmu[1][j] * a[1] + T.dcol[0][j] * a[6] + T.dcol[1][j] * a[7] +
-                   T.dcol[2][j] * a[8];
-#pragma unroll
-        for (int j = 0; j < 10; ++j) og[j] += T.dcov[0][j] * a[2] + T.dcov[1][j] * a[3] + T.dcov[2][j] * a[4];
-        og[10] += T.dopa * a[5];
-      } else {
-        float a[11];
-        pair_partials<D, 0, 11>(A, q, a);
-#pragma unroll
-        for (int j = 0; j < 11; ++j) og[j] += a[j];
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 11; ++j) {
-      float v = A.scale * og[j];
-      const long long i = (long long)j * G + g;
-      if (A.p) {
-        const double pv = (double)A.p[i];
-        const double lt = A.Mdiag ? A.lam * (double)fmaxf(A.Mdiag[i], 1e-12f) * pv : 0.0;
-        dot += pv * ((double)v + lt);
-        if (A.lam_out) v = (float)((double)v + lt);
-      }
-      A.out[i] = v;
-    }
-    // ---- sweep 2: the SH block, (colour partial * clamp mask) x basis (MODE 0)
-    // or (colour sum * clamp mask) x basis^2 (MODE 1)
-    float osh[3][K];
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch)
-#pragma unroll
-      for (int k = 0; k < K; ++k) osh[ch][k] = 0.f;
-    const float px = A.xs[g], py = A.xs[G + g], pz = A.xs[2 * G + g];
-    for (int q = k0; q < k1; ++q) {
-      float c[3];
-      if (MODE == 0) pair_partials<D, 6, 9>(A, q, c);
-      else pair_partials<D, 11, 14>(A, q, c);
-      const uint32_t vm = A.pair_vm[q];
-      const SlmCamera& cam = A.cams[vm & 0xffffu];
-      const float v0 = px - (float)cam.C[0], v1 = py - (float)cam.C[1], v2 = pz - (float)cam.C[2];
-      const float ivn = 1.f / sqrtf(v0 * v0 + v1 * v1 + v2 * v2);
-      float Y[K];
-      sh_basis<float, K>(v0 * ivn, v1 * ivn, v2 * ivn, Y);
-#pragma unroll
-      for (int ch = 0; ch < 3; ++ch) {
-        const float s = ((vm >> (16 + ch)) & 1u) ? 0.f : c[ch];
-#pragma unroll
-        for (int k = 0; k < K; ++k) osh[ch][k] += MODE == 0 ? s * Y[k] : s * Y[k] * Y[k];
-      }
-    }
-#pragma unroll
-    for (int a = 11; a < 11 + 3 * K; ++a) {
-      float v = A.scale * osh[(a - 11) / K][(a - 11) % K];
-      const long long i = (long long)a * G + g;
-      if (A.p) {
-        const double pv = (double)A.p[i];
-        const double lt = A.Mdiag ? A.lam * (double)fmaxf(A.Mdiag[i], 1e-12f) * pv : 0.0;
-        dot += pv * ((double)v + lt);
-        if (A.lam_out) v = (float)((double)v + lt);
-      }
-      A.out[i] = v;
-    }
-  }
-  if (A.dot_part) {
-    double t = block_sum_d(dot, sm);
-    if (threadIdx.x == 0) A.dot_part[blockIdx.x] = t;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Packed per-gaussian backward: warp w owns the gaussians whose first pair
-// falls in pairs [32w, 32w + 32) (warp_g0 from k_warp_bounds), lane = pair.
-// Each lane sums its pair's run partials (contiguous slots), applies its
-// view's 9 -> 59 chain and writes the row to a per-warp shared tile; the lanes
-// then walk the rows in pair order summing columns j = lane, lane + 32 per
-// gaussian (fixed order -> deterministic).  Loads are coalesced across lanes
-// and there is no per-thread serial loop over a gaussian's pairs.
+// Per-gaussian backward chain (ref: jacobian.py:314-353 / 506-510), packed:
+// warp w owns the gaussians whose first pair falls in pairs [32w, 32w + 32)
+// (warp_g0 from k_warp_bounds), lane = pair.  Each lane sums its pair's run
+// partials (contiguous slots, 16-byte loads), applies its view's 9 -> P chain
+// and writes the row to a per-warp shared tile; the lanes then sum the rows
+// of each gaussian column-wise (j = lane, lane + 32), the gaussians' row
+// segments found with one ballot (rows are in (gid, view) order), in fixed
+// row order (deterministic), and write gaussian-major scratch rows that
+// k_gm_to_am transposes.
+//   MODE 0 (J^T): run partials 0-7 as 32-byte records (pacc) + partial 8 (pacc1)
+//   MODE 1 (diag): 14 sums per run (pacc); SH block via basis^2
 // ---------------------------------------------------------------------------
 __global__ void k_warp_bounds(const int* __restrict__ gpo, long long G, int n_warps, int* __restrict__ warp_g0) {
   for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g <= G; g += (long long)gridDim.x * blockDim.x) {
@@ -237,17 +76,18 @@ __global__ void k_warp_bounds(const int* __restrict__ gpo, long long G, int n_wa
 
 #define PK_WARPS 4
 template <int K, int MODE>
-__global__ void __launch_bounds__(32 * PK_WARPS) k_gauss_backward_packed(SlmBackArgs A, const int* __restrict__ warp_g0,
+__global__ void __launch_bounds__(32 * PK_WARPS, SLM_BW_MINB) k_gauss_backward_packed(SlmBackArgs A, const int* __restrict__ warp_g0,
                                                                        int n_warps) {
   constexpr int P = 11 + 3 * K;
-  constexpr int PP = P | 1;  // odd row stride: conflict-free row writes and column reads
-  constexpr int D = MODE == 0 ? 9 : DIAG_RUN_D;
+  constexpr int PP = P > 32 ? 65 : 33;  // odd row stride, every lane's column pair inside the row
   __shared__ float s_v[PK_WARPS][32 * PP];
-  __shared__ int s_g[PK_WARPS][32];
+  const unsigned F = 0xffffffffu;
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const long long G = A.G;
   // gaussian-major scratch row (contiguous, coalesced); k_gm_to_am writes the
-  // attribute-major output with the scale / lambda / dot epilogue
+  // attribute-major output with the scale / lambda / dot epilogue (fusing that
+  // epilogue here -- per-lane attribute-strided p / M / out accesses -- was
+  // measured 1.5x slower)
   auto flush = [&](long long g, float c0, float c1) {
     float* o = A.gm + (size_t)g * P;
     if (lane < P) o[lane] = c0;  // P < 32 below SH degree 2
@@ -261,16 +101,25 @@ __global__ void __launch_bounds__(32 * PK_WARPS) k_gauss_backward_packed(SlmBack
     float c0 = 0.f, c1 = 0.f;
     for (int base = q0; base < q1; base += 32) {
       const int q = base + lane;
+      int myg = 0x7fffffff;
       if (q < q1) {
-        const long long g = A.pair_gid[q];
-        s_g[wl][lane] = (int)g;
+        myg = A.pair_gid[q];
         float* row = s_v[wl] + lane * PP;
-        float a[D];
-        pair_partials<D, 0, D>(A, q, a);
         const uint32_t vm = A.pair_vm[q];
+        const int r0 = A.pair_run_off[q], r1 = A.pair_run_off[q + 1];
         if (MODE == 0) {
+          float a[9];
+#pragma unroll
+          for (int j = 0; j < 9; ++j) a[j] = 0.f;
+          const float4* p4 = reinterpret_cast<const float4*>(A.pacc);
+          for (int rr = r0; rr < r1; ++rr) {
+            const float4 u = __ldg(p4 + 2 * (size_t)rr), v = __ldg(p4 + 2 * (size_t)rr + 1);
+            a[0] += u.x; a[1] += u.y; a[2] += u.z; a[3] += u.w;
+            a[4] += v.x; a[5] += v.y; a[6] += v.z; a[7] += v.w;
+            a[8] += __ldg(A.pacc1 + rr);
+          }
           Tab<K> T;
-          pair_tab<K>(A.xs, G, g, A.cams[vm & 0xffffu], vm >> 16, T, A.gtab);
+          pair_tab<K>(A.xs, G, myg, A.cams[vm & 0xffffu], vm >> 16, T, A.gtab);
 #pragma unroll
           for (int j = 0; j < 3; ++j)
             row[j] = T.dmu[0][j] * a[0] + T.dmu[1][j] * a[1] + T.dcol[0][j] * a[6] + T.dcol[1][j] * a[7] +
@@ -285,11 +134,18 @@ __global__ void __launch_bounds__(32 * PK_WARPS) k_gauss_backward_packed(SlmBack
             for (int k = 0; k < K; ++k) row[11 + ch * K + k] = sc * T.Y[k];
           }
         } else {
+          float a[DIAG_RUN_D];
+#pragma unroll
+          for (int j = 0; j < DIAG_RUN_D; ++j) a[j] = 0.f;
+          for (int rr = r0; rr < r1; ++rr) {
+#pragma unroll
+            for (int j = 0; j < DIAG_RUN_D; ++j) a[j] += __ldg(A.pacc + (size_t)rr * DIAG_RUN_D + j);
+          }
 #pragma unroll
           for (int j = 0; j < 11; ++j) row[j] = a[j];
           const SlmCamera& cam = A.cams[vm & 0xffffu];
-          const float v0 = A.xs[g] - (float)cam.C[0], v1 = A.xs[G + g] - (float)cam.C[1];
-          const float v2 = A.xs[2 * G + g] - (float)cam.C[2];
+          const float* gt = A.gtab + (size_t)myg * gtab_floats(K) + GT_POS;
+          const float v0 = gt[0] - (float)cam.C[0], v1 = gt[1] - (float)cam.C[1], v2 = gt[2] - (float)cam.C[2];
           const float ivn = 1.f / sqrtf(v0 * v0 + v1 * v1 + v2 * v2);
           float Y[K];
           sh_basis<float, K>(v0 * ivn, v1 * ivn, v2 * ivn, Y);
@@ -302,17 +158,33 @@ __global__ void __launch_bounds__(32 * PK_WARPS) k_gauss_backward_packed(SlmBack
         }
       }
       __syncwarp();
+      // row segments of the window's gaussians (rows are gid-sorted)
       const int nr = min(32, q1 - base);
-      for (int i = 0; i < nr; ++i) {  // rows in pair order
-        const int gi = s_g[wl][i];
+      const int prev = __shfl_up_sync(F, myg, 1);
+      unsigned starts = __ballot_sync(F, lane < nr && (lane == 0 || myg != prev));
+      while (starts) {
+        const int i0 = __ffs(starts) - 1;
+        starts &= starts - 1;
+        const int i1 = starts ? __ffs(starts) - 1 : nr;
+        const int gi = __shfl_sync(F, myg, i0);
         while (cur < gi) {  // finish cur (and any pair-less gaussians before gi)
           flush(cur, c0, c1);
           c0 = c1 = 0.f;
           ++cur;
         }
-        const float* r = s_v[wl] + i * PP;
-        c0 += r[lane];
-        if (lane + 32 < P) c1 += r[lane + 32];
+        const float* r = s_v[wl] + i0 * PP + lane;
+        int i = i0;
+        for (; i + 4 <= i1; i += 4, r += 4 * PP) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            c0 += r[k * PP];
+            if (P > 32) c1 += r[k * PP + 32];
+          }
+        }
+        for (; i < i1; ++i, r += PP) {
+          c0 += r[0];
+          if (P > 32) c1 += r[32];
+        }
       }
       __syncwarp();
     }
@@ -368,13 +240,22 @@ int slm_tile_args_size() { return (int)sizeof(SlmTileArgs); }
 int slm_back_args_size() { return (int)sizeof(SlmBackArgs); }
 int slm_diag_tab_floats() { return DIAG_TAB; }
 
-int slm_gauss_tab(const float* xs, long long G, float* gtab, cudaStream_t st) {
+int slm_gauss_tab(const float* xs, long long G, int sh_degree, float* gtab, cudaStream_t st) {
   if (G <= 0) return SLM_OK;
-  k_gauss_tab<<<slm_blocks(G, 256, 1LL << 30), 256, 0, st>>>(xs, G, gtab);
+  const unsigned b = slm_blocks(G, 256, 1LL << 30);
+  switch (sh_degree) {
+    case 0: k_gauss_tab<1><<<b, 256, 0, st>>>(xs, G, gtab); break;
+    case 1: k_gauss_tab<4><<<b, 256, 0, st>>>(xs, G, gtab); break;
+    case 2: k_gauss_tab<9><<<b, 256, 0, st>>>(xs, G, gtab); break;
+    case 3: k_gauss_tab<16><<<b, 256, 0, st>>>(xs, G, gtab); break;
+    default: return SLM_ERR_ARG;
+  }
   return slm_cuda_status();
 }
 
-int slm_gauss_tab_floats(void) { return GTAB; }
+int slm_gauss_tab_floats(int sh_degree) {
+  return sh_degree < 0 || sh_degree > 3 ? -1 : gtab_floats((sh_degree + 1) * (sh_degree + 1));
+}
 
 int slm_pair_tables(const float* xs, long long G, int sh_degree, const int* pair_gid, const uint32_t* pair_vm,
                     const SlmCamera* cams, int n_pairs, float* tab, const float* gtab, cudaStream_t st) {
@@ -394,7 +275,7 @@ int slm_fwd_args_size() { return (int)sizeof(SlmFwdArgs); }
 
 int slm_pair_forward(const SlmFwdArgs* a, int sh_degree, cudaStream_t st) {
   if (a->n_pairs <= 0) return SLM_OK;
-  if (!a->pm) return SLM_ERR_ARG;
+  if (!a->pm || !a->gtab) return SLM_ERR_ARG;
   unsigned b = slm_blocks(a->n_pairs, 128, 1LL << 30);
   switch (sh_degree) {
     case 0: k_pair_m<1><<<b, 128, 0, st>>>(*a); break;
@@ -403,16 +284,6 @@ int slm_pair_forward(const SlmFwdArgs* a, int sh_degree, cudaStream_t st) {
     case 3: k_pair_m<16><<<b, 128, 0, st>>>(*a); break;
     default: return SLM_ERR_ARG;
   }
-  return slm_cuda_status();
-}
-
-int slm_pair_sum(const int* pair_run_off, const int* pair_runs, int n_pairs, const float* run_acc, int d,
-                 float* pacc, cudaStream_t st) {
-  if (n_pairs <= 0) return SLM_OK;
-  unsigned b = slm_blocks(n_pairs, 256, 1LL << 30);
-  if (d == 9) k_pair_sum<9><<<b, 256, 0, st>>>(pair_run_off, pair_runs, n_pairs, run_acc, pacc);
-  else if (d == DIAG_RUN_D) k_pair_sum<DIAG_RUN_D><<<b, 256, 0, st>>>(pair_run_off, pair_runs, n_pairs, run_acc, pacc);
-  else return SLM_ERR_ARG;
   return slm_cuda_status();
 }
 
@@ -425,38 +296,23 @@ int slm_warp_bounds(const int* gpo, long long G, int n_pairs, int* warp_g0, cuda
 }
 
 int slm_pair_backward(const SlmBackArgs* a, int mode, int sh_degree, cudaStream_t st) {
-  unsigned b = (unsigned)slm_backward_blocks(a->G);
-  if (a->warp_g0) {  // packed: warp per 32-pair window of gaussians
-    const int nw = (int)((a->n_pairs >> 5) + 1);
+  if (!a->warp_g0 || !a->pair_run_off || !a->gtab || (mode == 0 && !a->pacc1)) return SLM_ERR_ARG;
+  const unsigned b = (unsigned)slm_backward_blocks(a->G);
+  const int nw = (int)((a->n_pairs >> 5) + 1);
 #define SLM_PK(KK)                                                                         \
   if (mode == 0)                                                                           \
     k_gauss_backward_packed<KK, 0><<<b, 32 * PK_WARPS, 0, st>>>(*a, a->warp_g0, nw);       \
   else                                                                                     \
     k_gauss_backward_packed<KK, 1><<<b, 32 * PK_WARPS, 0, st>>>(*a, a->warp_g0, nw);       \
   k_gm_to_am<11 + 3 * KK><<<b, 256, 0, st>>>(*a);
-    switch (sh_degree) {
-      case 0: SLM_PK(1) break;
-      case 1: SLM_PK(4) break;
-      case 2: SLM_PK(9) break;
-      case 3: SLM_PK(16) break;
-      default: return SLM_ERR_ARG;
-    }
-#undef SLM_PK
-    return slm_cuda_status();
-  }
-#define SLM_BW(KK)                                  \
-  if (mode == 0)                                    \
-    k_gauss_backward<KK, 0><<<b, 128, 0, st>>>(*a); \
-  else                                              \
-    k_gauss_backward<KK, 1><<<b, 128, 0, st>>>(*a);
   switch (sh_degree) {
-    case 0: SLM_BW(1) break;
-    case 1: SLM_BW(4) break;
-    case 2: SLM_BW(9) break;
-    case 3: SLM_BW(16) break;
+    case 0: SLM_PK(1) break;
+    case 1: SLM_PK(4) break;
+    case 2: SLM_PK(9) break;
+    case 3: SLM_PK(16) break;
     default: return SLM_ERR_ARG;
   }
-#undef SLM_BW
+#undef SLM_PK
   return slm_cuda_status();
 }
 

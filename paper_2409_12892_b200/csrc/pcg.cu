@@ -7,6 +7,8 @@
 // deterministic and needs one 8-byte host read per iteration (exit test).
 #include "slm_common.cuh"
 
+#include <algorithm>
+
 // state layout (double[16])
 #define ST_RZ 0
 #define ST_PG 2
@@ -25,21 +27,42 @@
 
 __device__ __forceinline__ float mfloor(float m) { return fmaxf(m, 1e-12f); }
 
-// p = r / Mf + beta * p  (r fp64; p is stored fp32 and used consistently as
-// the search direction by the product, x += alpha p and r -= alpha A p)
-__global__ void k_pcg_pupdate(float* __restrict__ p, const double* __restrict__ r, const float* __restrict__ M,
-                              const double* __restrict__ st, long long n) {
-  if (st[ST_STOP] != 0.0) return;
-  const double beta = st[ST_BETA];
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    p[i] = (float)(r[i] / (double)mfloor(M[i]) + beta * (double)p[i]);
-}
+// padded gaussian-major stride of the forward chain's copy of p (16-byte rows)
+__host__ __device__ constexpr int gm_stride(int P) { return (P + 3) & ~3; }
 
-// p = x0 = b / Mf  (Alg. 1 line 4)
-__global__ void k_pcg_pinit(float* __restrict__ p, const float* __restrict__ b, const float* __restrict__ M,
-                            long long n) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    p[i] = (float)((double)b[i] / (double)mfloor(M[i]));
+// p = r / Mf + beta * p  (INIT: p = x0 = b / Mf, Alg. 1 line 4), r fp64; p is
+// stored fp32 and used consistently as the search direction by the product,
+// x += alpha p and r -= alpha A p.  Tiles of 32 gaussians: attribute-major
+// reads / writes coalesced over gaussians, and (p_gm != NULL) the tile is
+// transposed in shared memory to the padded gaussian-major rows the forward
+// chain loads with 16-byte loads.
+template <bool INIT>
+__global__ void __launch_bounds__(256) k_pcg_p(float* __restrict__ p, float* __restrict__ p_gm,
+                                               const double* __restrict__ r, const float* __restrict__ b,
+                                               const float* __restrict__ M, const double* __restrict__ st,
+                                               long long G, int P) {
+  if (!INIT && st[ST_STOP] != 0.0) return;
+  extern __shared__ float tile[];  // [32][PG + 1]
+  const double beta = INIT ? 0.0 : st[ST_BETA];
+  const int PG = gm_stride(P), TS = PG + 1;
+  for (long long g0 = (long long)blockIdx.x * 32; g0 < G; g0 += (long long)gridDim.x * 32) {
+    const int ng = (int)min((long long)32, G - g0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < 32 * PG; i += blockDim.x) {
+      const int a = i >> 5, gl = i & 31;
+      float v = 0.f;
+      if (a < P && gl < ng) {
+        const long long idx = (long long)a * G + g0 + gl;
+        v = INIT ? (float)((double)b[idx] / (double)mfloor(M[idx]))
+                 : (float)(r[idx] / (double)mfloor(M[idx]) + beta * (double)p[idx]);
+        p[idx] = v;
+      }
+      tile[gl * TS + a] = v;
+    }
+    if (!p_gm) continue;
+    __syncthreads();
+    for (int i = threadIdx.x; i < ng * PG; i += blockDim.x) p_gm[g0 * PG + i] = tile[(i / PG) * TS + i % PG];
+  }
 }
 
 // sum of a block-partials array in a fixed order (every block gets the same bits)
@@ -180,13 +203,22 @@ extern "C" {
 
 int slm_vec_blocks() { return VEC_BLOCKS; }
 
-int slm_pcg_pinit(float* p, const float* b, const float* M, long long n, cudaStream_t s) {
-  k_pcg_pinit<<<VEC_BLOCKS, VEC_THREADS, 0, s>>>(p, b, M, n);
+int slm_gm_stride(int P) { return gm_stride(P); }
+
+static unsigned p_blocks(long long G) { return (unsigned)std::min<long long>((G + 31) / 32, 148LL * 8); }
+
+int slm_pcg_pinit(float* p, float* p_gm, const float* b, const float* M, long long G, int P, cudaStream_t s) {
+  if (G <= 0) return SLM_OK;
+  const size_t sm = (size_t)32 * (gm_stride(P) + 1) * sizeof(float);
+  k_pcg_p<true><<<p_blocks(G), 256, sm, s>>>(p, p_gm, nullptr, b, M, nullptr, G, P);
   return slm_cuda_status();
 }
 
-int slm_pcg_pupdate(float* p, const double* r, const float* M, const double* st, long long n, cudaStream_t s) {
-  k_pcg_pupdate<<<VEC_BLOCKS, VEC_THREADS, 0, s>>>(p, r, M, st, n);
+int slm_pcg_pupdate(float* p, float* p_gm, const double* r, const float* M, const double* st, long long G, int P,
+                    cudaStream_t s) {
+  if (G <= 0) return SLM_OK;
+  const size_t sm = (size_t)32 * (gm_stride(P) + 1) * sizeof(float);
+  k_pcg_p<false><<<p_blocks(G), 256, sm, s>>>(p, p_gm, r, nullptr, M, st, G, P);
   return slm_cuda_status();
 }
 

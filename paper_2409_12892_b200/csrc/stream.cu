@@ -20,7 +20,7 @@
 //                   reduction and pass J^T.
 //   pass J  : per-warp shared pixel accumulators (a run never repeats a pixel),
 //             summed in fixed warp order -> deterministic, no atomics.
-//   pass J^T: 9 partials per run, 16-shuffle reduce-scatter, one store per run.
+//   pass J^T: 9 partials per run, 8-lane reduce-scatter, one 32-byte store per run.
 #include "chain.cuh"
 
 #define NW 8
@@ -31,6 +31,10 @@
 #define CR SLM_CHUNK_RUNS  // max runs per chunk (64)
 static_assert(CR % 32 == 0 && CR <= 255, "run slots are bytes, 32 per J^T round");
 #define NS SLM_NS        // ring stages
+#ifndef SLM_JT_UNROLL
+#define SLM_JT_UNROLL 2
+#endif
+constexpr int kJtUnroll = SLM_JT_UNROLL;  // J^T entry-loop unroll (tuning)
 #define PAR 16           // floats per run parameter record
 #define TMETA 64         // producer chunk-metadata window
 #define TQ 4             // tile queue depth (producer -> consumers)
@@ -130,9 +134,12 @@ __device__ __forceinline__ int view_of_tile(const int* __restrict__ vtb, int n_v
 
 // ---------------------------------------------------------------------------
 // static run records (once per cache; the scene is fixed during a solve):
-//   (p0, p1, ka, kb) splat centre relative to the tile's pixel-centre origin
-//   and conic, (kc, inv_o, slot, pair) -- slot = the run's position in
-//   pair_runs (J^T / diag outputs go there), pair = its (gid, view) pair.
+//   (c1, c2, ka, kb), (kb, kc, inv_o, slot): the conic (ka, kb, kc) and
+//   e = conic (px - mu) at the tile's first pixel centre, so that at tile-local
+//   pixel (x, y) e1 = ka x + kb y + c1, e2 = kb x + kc y + c2 (two FFMA2 per
+//   entry; c1, c2 formed in fp64); slot = the run's position in pair_runs
+//   (J^T / diag outputs go there).  The two float4 halves load as the
+//   register pairs (c1, c2), (ka, kb), (kb, kc) the packed FMAs use.
 // The per-product forward chain m of the run's pair is gathered per chunk by
 // the producer warp (cp.async from the per-pair m of slm_pair_forward).
 // ---------------------------------------------------------------------------
@@ -147,10 +154,36 @@ __global__ void k_run_static(SlmTileArgs A, long long n_runs, const int* __restr
     const double ox = (double)((lt % tiles_x) * SLM_TILE) + 0.5, oy = (double)((lt / tiles_x) * SLM_TILE) + 0.5;
     const int q = A.run_q[r];
     const SlmPairGeo g = A.geo[q];
+    const double dx = ox - g.mx, dy = oy - g.my;
+    const double c1 = (double)g.ka * dx + (double)g.kb * dy, c2 = (double)g.kb * dx + (double)g.kc * dy;
     float4* o = reinterpret_cast<float4*>(out + r * 8);
-    o[0] = make_float4((float)(g.mx - ox), (float)(g.my - oy), g.ka, g.kb);
-    o[1] = make_float4(g.kc, g.inv_o, __int_as_float(run_slot[r]), __int_as_float(q));
+    o[0] = make_float4((float)c1, (float)c2, g.ka, g.kb);
+    o[1] = make_float4(g.kb, g.kc, g.inv_o, __int_as_float(run_slot[r]));
   }
+}
+
+// e = (e1, e2) = conic (px - mu) at tile-local pixel pl of a run: two packed
+// FMAs on the run's (ka, kb), (kb, kc), (c1, c2) (RunE, formed once per run)
+// (packed 64-bit operands, so the pairs stay in fixed register pairs)
+struct RunE {
+  uint64_t kab, kbc, c;
+};
+__device__ __forceinline__ uint64_t pack2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ RunE run_e_of(const float4& q0, const float4& s1) {
+  return RunE{pack2(q0.z, q0.w), pack2(s1.x, s1.y), pack2(q0.x, q0.y)};
+}
+__device__ __forceinline__ float2 run_e(const RunE& k, int pl) {
+  const float x = (float)(pl & 15), y = (float)(pl >> 4);
+  uint64_t t, e;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(t) : "l"(k.kbc), "l"(pack2(y, y)), "l"(k.c));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(e) : "l"(k.kab), "l"(pack2(x, x)), "l"(t));
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(e));
+  return r;
 }
 
 // ---------------------------------------------------------------------------
@@ -365,7 +398,12 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
               hdr[7] = L.rs;
               // generic-proxy header writes before the async-proxy copies land
               asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-              mbar_arrive_tx(&full[s], b4 + bd + bx + bp + br + ST_PERM);
+              // diag: the chunk's run -> pair indices (their chain tables) into
+              // the pair-m section, which that mode does not use
+              const long long aq = m.k0 & ~3LL, zq = (m.k1 + 3) & ~3LL;
+              const unsigned bq = (MODE & MODE_DIAG) ? (unsigned)(zq - aq) * 4u : 0u;
+              mbar_arrive_tx(&full[s], b4 + bd + bx + bp + br + ST_PERM + bq);
+              if (MODE & MODE_DIAG) bulk_g2s(st + L.pdy, A.run_q + aq, bq, &full[s], pol);
               bulk_g2s(st, A.rec4 + m.e0, b4, &full[s], pol);
               bulk_g2s(st + L.d2, A.d2 + a4, bd, &full[s], pol);
               bulk_g2s(st + L.pix, A.pix + a16, bx, &full[s], pol);
@@ -432,27 +470,33 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
         const float4* PST = reinterpret_cast<const float4*>(st + hdr[6]);
         const float4* PDY = reinterpret_cast<const float4*>(st + hdr[6] + nr * 32);
         for (int i = (warp + ci) & (NW - 1); i < nr; i += NW) {  // rotated: no warp always gets the extra runs
-          // static: q0 = (p0, p1, ka, kb), s1 = (kc, io, slot, pair)
+          // static: q0 = (c1, c2, ka, kb), s1 = (kb, kc, io, slot)
           // pair m:  d0 = (m_opa, m0, m1, m2), d1 = (m3, m4, c0, c1), d2m = (c2, -, -, -)
           const float4 q0 = PST[i * 2], s1 = PST[i * 2 + 1];
           const float4 d0 = PDY[i * 3], d1 = PDY[i * 3 + 1];
           const float c2m = PDY[i * 3 + 2].x;
-          const float a0 = s1.y * d0.x;
+          const float a0 = s1.z * d0.x;
           const int f0 = (int)(rs[i] - e0), n = (int)(rs[i + 1] - rs[i]);
           const float4* pr = s4 + f0;
           const float* pd = sd2 + f0;
           const uint8_t* pp = spx + f0;
+          const float2 mc01 = make_float2(d1.z, d1.w);
+          const RunE ke = run_e_of(q0, s1);
           for (int j = lane; j < n; j += 32) {
             const float4 r = pr[j];
             const float d2 = pd[j];
             const int pl = pp[j];
-            const float dx = (float)(pl & 15) - q0.x, dy = (float)(pl >> 4) - q0.y;
-            const float e1 = q0.z * dx + q0.w * dy, e2 = q0.w * dx + s1.x * dy;
-            const float da = r.x * (a0 + e1 * (d0.y + e1 * d0.w + e2 * d1.x) + e2 * (d0.z + e2 * d1.y));
+            const float2 e = run_e(ke, pl);
+            // dalpha = alpha_eff (m_o/o + e1 m0 + e2 m1 + e1^2 m2 + e1 e2 m3 + e2^2 m4)
+            const float t1 = fmaf(e.x, d0.w, fmaf(e.y, d1.x, d0.y)), t2 = fmaf(e.y, d1.y, d0.z);
+            const float da = r.x * fmaf(e.x, t1, fmaf(e.y, t2, a0));
             float4 a = acc[pl];
-            a.x += fmaf(r.z, da, r.y * d1.z);
-            a.y += fmaf(r.w, da, r.y * d1.w);
-            a.z += fmaf(d2, da, r.y * c2m);
+            // u_ch += dc/dalpha_ch dalpha + alpha T m_col,ch
+            const float2 axy = __ffma2_rn(make_float2(r.z, r.w), make_float2(da, da),
+                                          __ffma2_rn(make_float2(r.y, r.y), mc01, make_float2(a.x, a.y)));
+            a.x = axy.x;
+            a.y = axy.y;
+            a.z = fmaf(d2, da, fmaf(r.y, c2m, a.z));
             acc[pl] = a;
           }
           __syncwarp();  // the next run may update the same pixels from other lanes
@@ -498,17 +542,19 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
         for (int rd = 0; rd < CR / 32 && rd * 32 < hdr[0]; ++rd) {  // 32 runs per round, longest first
           const int ri = st[OFF_PERM + rd * 32 + (((warp + ci) & (NW - 1)) * 4 + slot)];
           int n = 0, f0 = 0, sl = 0;
-          float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f);
+          float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = q0;
           float kc = 0.f, io = 0.f;
           float D[DIAG_TAB];
           if (ri != 0xff) {
             const float4* P4 = reinterpret_cast<const float4*>(st + hdr[6]) + ri * 2;
             q0 = P4[0];
-            const float4 s1 = P4[1];
-            kc = s1.x;
-            io = s1.y;
-            sl = __float_as_int(s1.z);
-            const float4* tq = reinterpret_cast<const float4*>(A.ptab + (size_t)__float_as_int(s1.w) * DIAG_TAB);
+            s1 = P4[1];
+            kc = s1.y;
+            io = s1.z;
+            sl = __float_as_int(s1.w);
+            // the run's pair (its chain table), staged by the producer
+            const int* sq = reinterpret_cast<const int*>(st + hdr[6] + hdr[0] * 32) + (hdr[2] & 3);
+            const float4* tq = reinterpret_cast<const float4*>(A.ptab + (size_t)sq[ri] * DIAG_TAB);
   #pragma unroll
             for (int k = 0; k < DIAG_TAB / 4; ++k) {
               const float4 v = __ldg(tq + k);
@@ -526,6 +572,7 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
           const int nmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)n);
           if (nmax == 0) continue;
           const float dop = io * D[36];
+          const RunE ke = run_e_of(q0, s1);
           float a[16];
   #pragma unroll
           for (int k = 0; k < 16; ++k) a[k] = 0.f;
@@ -540,8 +587,8 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
               const float4 gr = s_u[pl];
               const float grc[3] = {gr.x, gr.y, gr.z};
               const float ae = r.x, at = r.y;
-              const float dx = (float)(pl & 15) - q0.x, dy = (float)(pl >> 4) - q0.y;
-              const float e1 = q0.z * dx + q0.w * dy, e2 = q0.w * dx + kc * dy;
+              const float2 e = run_e(ke, pl);
+              const float e1 = e.x, e2 = e.y;
               const float w0 = ae * e1, w1 = ae * e2, w2 = 0.5f * w0 * e1, w3 = w0 * e2, w4 = 0.5f * w1 * e2;
               // sum_ch gr_ch (dc_ch/dx_k)^2: dalpha_k^2 * Aw for k >= 3 (exact),
               // per-channel squares for the position params (dc also has at * dcol)
@@ -614,49 +661,51 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
         for (int rd = 0; rd < CR / 32 && rd * 32 < hdr[0]; ++rd) {  // 32 runs per round, longest first
           const int ri = st[OFF_PERM + rd * 32 + (((warp + ci) & (NW - 1)) * 4 + slot)];
           int n = 0, f0 = 0;
-          float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f);
-          float kc = 0.f, io = 0.f;
+          float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = q0;
+          float io = 0.f;
           int slot = 0;
           if (ri != 0xff) {
             const float4* P4 = reinterpret_cast<const float4*>(st + hdr[6]) + ri * 2;
             q0 = P4[0];
-            const float4 s1 = P4[1];
-            kc = s1.x;
-            io = s1.y;
-            slot = __float_as_int(s1.z);
+            s1 = P4[1];
+            io = s1.z;
+            slot = __float_as_int(s1.w);
             f0 = (int)(rs[ri] - e0);
             n = (int)(rs[ri + 1] - rs[ri]);
           }
           const int nmax = __reduce_max_sync(0xffffffffu, (unsigned)n);
           if (nmax == 0) continue;
-          float a[9];
-  #pragma unroll
-          for (int k = 0; k < 9; ++k) a[k] = 0.f;
+          // per-run partials: a01 = sum t (e1, e2), a23 = sum t e1 (e1, e2),
+          // a4 = sum t e2^2, a5 = sum t, a67 / a8 = sum alpha T u (t = s_alpha
+          // alpha_eff).  The group runs to the warp's longest run; lanes past
+          // their run's end read in-stage data and add exact zeros (selects,
+          // so garbage never reaches the sums): no branch in the loop
+          float2 a01 = make_float2(0.f, 0.f), a23 = a01, a67 = a01;
+          float a4 = 0.f, a5 = 0.f, a8 = 0.f;
           const float4* pr = s4 + f0;
           const float* pd = sd2 + f0;
           const uint8_t* pp = spx + f0;
+          const RunE ke = run_e_of(q0, s1);
+#pragma unroll(kJtUnroll)
           for (int j = lg; j < nmax; j += 8) {
-            if (j < n) {
-              const float4 r = pr[j];
-              const float d2 = pd[j];
-              const int pl = pp[j];
-              const float4 uu = s_u[pl];
-              const float dx = (float)(pl & 15) - q0.x, dy = (float)(pl >> 4) - q0.y;
-              const float e1 = q0.z * dx + q0.w * dy, e2 = q0.w * dx + kc * dy;
-              const float sa = fmaf(r.z, uu.x, fmaf(r.w, uu.y, d2 * uu.z));
-              const float tt = sa * r.x;
-              const float te1 = tt * e1, te2 = tt * e2;
-              a[0] += te1;
-              a[1] += te2;
-              a[2] = fmaf(te1, e1, a[2]);  // x 1/2 in the epilogue
-              a[3] = fmaf(te1, e2, a[3]);
-              a[4] = fmaf(te2, e2, a[4]);  // x 1/2 in the epilogue
-              a[5] += tt;
-              a[6] = fmaf(r.y, uu.x, a[6]);
-              a[7] = fmaf(r.y, uu.y, a[7]);
-              a[8] = fmaf(r.y, uu.z, a[8]);
-            }
+            const bool ok = j < n;
+            const float4 r = pr[j];
+            const float d2 = pd[j];
+            const int pl = pp[j];
+            const float4 uu = s_u[pl];
+            const float2 e = run_e(ke, pl);
+            const float sa = fmaf(r.z, uu.x, fmaf(r.w, uu.y, d2 * uu.z));
+            const float tt = ok ? sa * r.x : 0.f;
+            const float ry = ok ? r.y : 0.f;
+            const float2 te = __fmul2_rn(make_float2(tt, tt), e);
+            a01 = __fadd2_rn(a01, te);
+            a23 = __ffma2_rn(make_float2(te.x, te.x), e, a23);  // x 1/2 on a[2] in the epilogue
+            a4 = fmaf(te.y, e.y, a4);                            // x 1/2 in the epilogue
+            a5 += tt;
+            a67 = __ffma2_rn(make_float2(ry, ry), make_float2(uu.x, uu.y), a67);
+            a8 = fmaf(ry, uu.z, a8);
           }
+          const float a[9] = {a01.x, a01.y, a23.x, a23.y, a4, a5, a67.x, a67.y, a8};
           // 8-lane reduce-scatter of a[0..7] (lane lg ends with the group sum of
           // value lg) plus a butterfly for a[8]; fixed pattern -> deterministic
           const unsigned F = 0xffffffffu;
@@ -667,14 +716,14 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
   #pragma unroll
           for (int k = 0; k < 2; ++k) w2[k] = (u2 ? w4[k + 2] : w4[k]) + __shfl_xor_sync(F, u2 ? w4[k] : w4[k + 2], 2);
           const float w1 = (u1 ? w2[1] : w2[0]) + __shfl_xor_sync(F, u1 ? w2[0] : w2[1], 1);
-          float a8 = a[8];
           a8 += __shfl_xor_sync(F, a8, 4);
           a8 += __shfl_xor_sync(F, a8, 2);
           a8 += __shfl_xor_sync(F, a8, 1);
           if (ri != 0xff) {
-            float* o = A.out + (size_t)slot * 9;  // pair-run-slot order (read contiguously by the backward)
-            o[lg] = lg == 5 ? w1 * io : ((lg == 2 || lg == 4) ? 0.5f * w1 : w1);
-            if (lg == 0) o[8] = a8;
+            // pair-run-slot order (read contiguously by the backward): partials
+            // 0-7 as one 32-byte record, partial 8 in A.out1
+            A.out[(size_t)slot * 8 + lg] = lg == 5 ? w1 * io : ((lg == 2 || lg == 4) ? 0.5f * w1 : w1);
+            if (lg == 0) A.out1[slot] = a8;
           }
         }
         __syncwarp();

@@ -527,19 +527,18 @@ class CacheSet:
         call("slm_raster_fill", _lib.byref(a), stream_ptr())
         T.tick("raster_fill")
         del inst_mask, inst_start, inst_gid, ranges, splats_all
-        # product scratch
+        # product scratch: J^T run partials 0-7 (32-byte records) then partial 8
         self.u = torch.empty(self.N * 4, dtype=f32, device=dev)
         self.run_acc = _empty(R * _lib.JT_D, f32, dev)
         self.run_static = _empty(R * 8, f32, dev)
-        self.pacc = _empty(Pn * _lib.DIAG_D, f32, dev)
-        self.packed_backward = True
         self.warp_g0 = torch.empty((Pn >> 5) + 2, dtype=torch.int32, device=dev)
         self.gm = torch.empty(G * self.P, dtype=torch.float32, device=dev)
         call("slm_warp_bounds", ptr(self.gpo), G, Pn, ptr(self.warp_g0), stream_ptr())
         self.pm = _empty(Pn * 12, f32, dev)
-        # view-independent chain constants per gaussian (scene fixed for the cache)
-        self.gtab = torch.empty(G * _lib.load().slm_gauss_tab_floats(), dtype=f32, device=dev)
-        call("slm_gauss_tab", ptr(scene.x32()), G, ptr(self.gtab), stream_ptr())
+        # per-gaussian chain rows: view-independent chain constants, position,
+        # SH coefficients (the scene is fixed for the cache)
+        self.gtab = torch.empty(G * _lib.load().slm_gauss_tab_floats(scene.sh_degree), dtype=f32, device=dev)
+        call("slm_gauss_tab", ptr(scene.x32()), G, scene.sh_degree, ptr(self.gtab), stream_ptr())
         call("slm_run_static", _lib.byref(self._tile_args()), R, ptr(self.run_slot), ptr(self.run_static),
              stream_ptr())
 
@@ -580,9 +579,11 @@ class CacheSet:
         """Bytes of the record stream (budget accounting, ref: jacobian.py:76-80)."""
         return 21 * self.E + 48 * self.R + 36 * self.n_chunks
 
-    def pair_forward(self, p: torch.Tensor, gaussian_major: bool = False):
+    def pair_forward(self, p: torch.Tensor, gaussian_major: bool = False, p_gm: torch.Tensor | None = None):
         """Forward chain m = dy/dx p per pair into self.pm (48 B per pair); the
-        J / fused product kernels gather it per run."""
+        J / fused product kernels gather it per run.  p_gm: the padded
+        gaussian-major copy of p (stride slm_gm_stride(P)) written by the PCG
+        p kernels, read with 16-byte row loads."""
         G, P = self.G, self.P
         if G == 0:
             return
@@ -590,8 +591,11 @@ class CacheSet:
         a.xs, a.G = ptr(self.scene.x32()), G
         a.pair_gid, a.pair_vm, a.cams, a.n_pairs = ptr(self.pair_gid), ptr(self.pair_vm), ptr(self.cams_dev), \
             self.n_pairs
-        a.p = ptr(p)
-        a.sa, a.sg = (1, P) if gaussian_major else (G, 1)
+        if p_gm is not None:
+            a.p, a.sa, a.sg = ptr(p_gm), 1, _lib.load().slm_gm_stride(P)
+        else:
+            a.p = ptr(p)
+            a.sa, a.sg = (1, P) if gaussian_major else (G, 1)
         a.pm, a.gtab = ptr(self.pm), ptr(self.gtab)
         call("slm_pair_forward", _lib.byref(a), self.scene.sh_degree, stream_ptr())
 
@@ -611,24 +615,18 @@ class CacheSet:
         a.tile_counter = ptr(self.tile_counter)
         return a
 
-    def _backward(self, run_acc, d, out, mode, scale=1.0, p=None, M=None, lam=0.0, dot_part=None, lam_out=True,
-                  slot_order=False):
-        """run partials -> per-gaussian chain, attribute-major out.  slot_order:
-        run_acc is already in pair-run-slot order (J^T kernels); otherwise it is
-        run-indexed and first reduced to per-pair sums."""
+    def _backward(self, run_acc, out, mode, scale=1.0, p=None, M=None, lam=0.0, dot_part=None, lam_out=True):
+        """run partials (pair-run-slot order, as the J^T / diag streaming
+        kernels write them) -> per-gaussian chain, attribute-major out."""
         a = _lib.SlmBackArgs()
-        if slot_order:
-            a.pacc, a.pair_run_off = ptr(run_acc), ptr(self.pair_run_off)
-        else:
-            call("slm_pair_sum", ptr(self.pair_run_off), ptr(self.pair_runs), self.n_pairs, ptr(run_acc), d,
-                 ptr(self.pacc), stream_ptr())
-            a.pacc, a.pair_run_off = ptr(self.pacc), None
+        a.pacc, a.pair_run_off = ptr(run_acc), ptr(self.pair_run_off)
+        if mode == 0:
+            a.pacc1 = off(run_acc, 8 * self.R)
         a.xs, a.G = ptr(self.scene.x32()), self.G
         a.gpo, a.pair_vm, a.cams = ptr(self.gpo), ptr(self.pair_vm), ptr(self.cams_dev)
         a.gtab = ptr(self.gtab)
-        if self.packed_backward:
-            a.warp_g0, a.pair_gid, a.n_pairs = ptr(self.warp_g0), ptr(self.pair_gid), self.n_pairs
-            a.gm = ptr(self.gm)
+        a.warp_g0, a.pair_gid, a.n_pairs = ptr(self.warp_g0), ptr(self.pair_gid), self.n_pairs
+        a.gm = ptr(self.gm)
         a.scale, a.p, a.Mdiag, a.lam = float(scale), ptr(p), ptr(M), float(lam)
         a.lam_out = 1 if lam_out else 0
         a.out, a.dot_part = ptr(out), ptr(dot_part)
@@ -651,13 +649,13 @@ class CacheSet:
         if self.G == 0:
             return out
         ra = self._tile_args()
-        ra.u, ra.out = ptr(u), ptr(self.run_acc)
+        ra.u, ra.out, ra.out1 = ptr(u), ptr(self.run_acc), off(self.run_acc, 8 * self.R)
         call("slm_apply_jt_runs", _lib.byref(ra), stream_ptr())
-        self._backward(self.run_acc, _lib.JT_D, out, 0, scale, p, M, lam, dot_part, slot_order=True)
+        self._backward(self.run_acc, out, 0, scale, p, M, lam, dot_part)
         return out
 
     def jtwj(self, p: torch.Tensor, out: torch.Tensor, lam: float = 0.0, M=None, dot_part=None,
-             lam_out: bool = True):
+             lam_out: bool = True, p_gm: torch.Tensor | None = None):
         """out = J^T W J p (+ lam * max(M, 1e-12) * p when lam_out); attribute-major
         fp32.  dot_part receives fp64 block partials of p.(J^T W J p + lam Mf p).
 
@@ -670,12 +668,11 @@ class CacheSet:
             if dot_part is not None:
                 dot_part.zero_()
             return out
-        self.pair_forward(p)
+        self.pair_forward(p, p_gm=p_gm)
         a = self._tile_args(with_m=True)
-        a.gradr, a.out = ptr(self.gradr), ptr(self.run_acc)
+        a.gradr, a.out, a.out1 = ptr(self.gradr), ptr(self.run_acc), off(self.run_acc, 8 * self.R)
         call("slm_jtwj_runs", _lib.byref(a), stream_ptr())
-        self._backward(self.run_acc, _lib.JT_D, out, 0, 1.0, p, M if lam != 0.0 else None, lam, dot_part, lam_out,
-                       slot_order=True)
+        self._backward(self.run_acc, out, 0, 1.0, p, M if lam != 0.0 else None, lam, dot_part, lam_out)
         return out
 
     def rhs(self) -> torch.Tensor:
@@ -704,7 +701,7 @@ class CacheSet:
             ra.ptab, ra.gradr, ra.out = ptr(ptab), ptr(self.gradr), ptr(sums)
             call("slm_diag_stream", _lib.byref(ra), stream_ptr())
             M = torch.empty(self.G * self.P, dtype=torch.float32, device=self.device)
-            self._backward(sums, _lib.DIAG_D, M, 1, slot_order=True)
+            self._backward(sums, M, 1)
             self._M = M
         return self._M
 

@@ -65,9 +65,13 @@ def _pinned_stop() -> torch.Tensor:
 
 @dataclass
 class PCGWorkspace:
-    """x, r (fp64), p, g (fp32) vectors + device scalar block (SPEC PCGWorkspace)."""
+    """x, r (fp64), p, g (fp32) vectors + device scalar block (SPEC PCGWorkspace).
+    With G, P given, also the padded gaussian-major copy p_gm of p that the
+    forward chain of the product reads with 16-byte row loads."""
     n: int
     device: torch.device
+    G: int = 0
+    P: int = 0
     x: torch.Tensor = field(init=False)
     r: torch.Tensor = field(init=False)
     p: torch.Tensor = field(init=False)
@@ -81,6 +85,9 @@ class PCGWorkspace:
         self.r = torch.empty(self.n, dtype=torch.float64, device=self.device)
         self.p = torch.empty(self.n, dtype=f, device=self.device)
         self.g = torch.empty(self.n, dtype=f, device=self.device)
+        self.p_gm = None
+        if self.G > 0 and self.G * self.P == self.n:
+            self.p_gm = torch.empty(self.G * _lib.load().slm_gm_stride(self.P), dtype=f, device=self.device)
         self.st = torch.zeros(16, dtype=torch.float64, device=self.device)
         self.part = torch.zeros(3 * _lib.load().slm_vec_blocks(), dtype=torch.float64, device=self.device)
         # pinned copies of the stop flag, one per in-flight iteration
@@ -98,14 +105,15 @@ def pcg_run(cache: CacheSet, b: torch.Tensor, M: torch.Tensor, lam: float, max_i
         if stats is not None:
             stats.update(products=0, iterations=0, rr=0.0, bb=0.0)
         return torch.zeros(0, dtype=torch.float64, device=b.device)
-    ws = ws or PCGWorkspace(n, b.device)
+    ws = ws or PCGWorkspace(n, b.device, cache.G, cache.P)
+    G, P = (cache.G, cache.P) if cache.G * cache.P == n else (n, 1)
     nb = _lib.load().slm_backward_blocks(cache.G)
     dot_part = torch.zeros(nb, dtype=torch.float64, device=b.device)
     s = stream_ptr()
     ws.st.zero_()
     # p := b / Mf  (= x0, Alg. 1 line 4); g0 = A x0
-    call("slm_pcg_pinit", ptr(ws.p), ptr(b), ptr(M), n, s)
-    _product(cache, ws.p, ws.g, lam, M, dot_part, timer)
+    call("slm_pcg_pinit", ptr(ws.p), ptr(ws.p_gm), ptr(b), ptr(M), G, P, s)
+    _product(cache, ws.p, ws.g, lam, M, dot_part, timer, ws.p_gm)
     call("slm_pcg_update", 0, ptr(ws.x), ptr(ws.r), ptr(ws.p), ptr(ws.g), ptr(b), ptr(M), float(lam),
          ptr(ws.st), ptr(dot_part), nb, ptr(ws.part), n, s)
     call("slm_pcg_finalize", 0, ptr(ws.st), ptr(ws.part), s)
@@ -116,8 +124,8 @@ def pcg_run(cache: CacheSet, b: torch.Tensor, M: torch.Tensor, lam: float, max_i
     # drains between iterations; on an early exit the one product queued
     # ahead runs but its result is discarded by the gated update.
     for it in range(max_iters):
-        call("slm_pcg_pupdate", ptr(ws.p), ptr(ws.r), ptr(M), ptr(ws.st), n, s)
-        _product(cache, ws.p, ws.g, lam, M, dot_part, timer)
+        call("slm_pcg_pupdate", ptr(ws.p), ptr(ws.p_gm), ptr(ws.r), ptr(M), ptr(ws.st), G, P, s)
+        _product(cache, ws.p, ws.g, lam, M, dot_part, timer, ws.p_gm)
         call("slm_pcg_update", 1, ptr(ws.x), ptr(ws.r), ptr(ws.p), ptr(ws.g), ptr(b), ptr(M), float(lam),
              ptr(ws.st), ptr(dot_part), nb, ptr(ws.part), n, s)
         call("slm_pcg_finalize", 1, ptr(ws.st), ptr(ws.part), s)
@@ -141,13 +149,13 @@ def pcg_run(cache: CacheSet, b: torch.Tensor, M: torch.Tensor, lam: float, max_i
     return ws.x
 
 
-def _product(cache, p, g, lam, M, dot_part, timer):
+def _product(cache, p, g, lam, M, dot_part, timer, p_gm=None):
     """g = J^T W J p (fp32); dot_part = fp64 partials of p.(g + lam Mf p)."""
     if timer is None:
-        cache.jtwj(p, g, lam, M, dot_part, lam_out=False)
+        cache.jtwj(p, g, lam, M, dot_part, lam_out=False, p_gm=p_gm)
     else:
         with timer:
-            cache.jtwj(p, g, lam, M, dot_part, lam_out=False)
+            cache.jtwj(p, g, lam, M, dot_part, lam_out=False, p_gm=p_gm)
 
 
 def pcg_solve(scene, cache, b: ParamVector, M_diag: ParamVector, lambda_reg: float, max_iters: int,
@@ -285,7 +293,7 @@ def lm_direction(scene, cameras, gts, schedule: BatchSchedule = BatchSchedule(),
     are then copied on a side stream while the previous subset is solved."""
     n = scene.param_count
     comb = Combiner(n, scene.device)
-    ws = PCGWorkspace(n, scene.device)
+    ws = PCGWorkspace(n, scene.device, scene.num_gaussians, scene.params_per_gaussian)
     entries, pcg_stats = [], []
     caches = []
     shards = list(schedule.shard(len(cameras), rank, world_size))

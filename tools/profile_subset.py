@@ -17,6 +17,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import bench  # noqa: E402
+from paper_2409_12892_b200 import _lib  # noqa: E402
 from paper_2409_12892_b200.engine import CacheSet, PhaseTimer  # noqa: E402
 from paper_2409_12892_b200.solver import BatchSchedule, pcg_run  # noqa: E402
 
@@ -58,6 +59,11 @@ def main():
         phases["diag"] = c.elapsed_time(d)
         p = torch.randn(scene.param_count, device=dev)
         g = torch.empty_like(p)
+        # the padded gaussian-major copy the PCG p kernels hand to the product
+        PG = _lib.load().slm_gm_stride(cs.P)
+        p_gm = torch.zeros(cs.G, PG, device=dev)
+        p_gm[:, :cs.P] = p.view(cs.P, cs.G).t()
+        p_gm = p_gm.reshape(-1)
         k = []
         for _ in range(3):
             e0 = ev()
@@ -76,25 +82,24 @@ def main():
         f = []
         for _ in range(3):
             f0 = ev()
-            cs.jtwj(p, g, 1e-4, M, None)
+            cs.jtwj(p, g, 1e-4, M, None, p_gm=p_gm)
             f1 = ev()
             f.append((f0, f1))
         torch.cuda.synchronize()
         phases["fused_jtwj_product"] = f[-1][0].elapsed_time(f[-1][1])
         # the fused product's launches timed one by one
-        from paper_2409_12892_b200 import _lib
-        from paper_2409_12892_b200._lib import call, ptr, stream_ptr
+        from paper_2409_12892_b200._lib import call, off, ptr, stream_ptr
         dp = torch.zeros(_lib.load().slm_backward_blocks(cs.G), dtype=torch.float64, device=dev)
         ks = []
         for _ in range(3):
             t0 = ev()
-            cs.pair_forward(p)
+            cs.pair_forward(p, p_gm=p_gm)
             t1 = ev()
             a = cs._tile_args(with_m=True)
-            a.gradr, a.out = ptr(cs.gradr), ptr(cs.run_acc)
+            a.gradr, a.out, a.out1 = ptr(cs.gradr), ptr(cs.run_acc), off(cs.run_acc, 8 * cs.R)
             call("slm_jtwj_runs", _lib.byref(a), stream_ptr())
             t2 = ev()
-            cs._backward(cs.run_acc, _lib.JT_D, g, 0, 1.0, p, M, 1e-4, dp, False, slot_order=True)
+            cs._backward(cs.run_acc, g, 0, 1.0, p, M, 1e-4, dp, False)
             t3 = ev()
             ks.append((t0, t1, t2, t3))
         torch.cuda.synchronize()
