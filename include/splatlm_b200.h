@@ -151,6 +151,7 @@ typedef struct {
   const uint8_t* chunk_perm; /* [n_chunks*SLM_CHUNK_RUNS] J^T schedule: chunk-local runs by decreasing length */
   const int* run_slot;       /* [R] position of each run in pair_runs (J^T outputs go there) */
   const long long* run_start;/* [R+1] (+2 padding slots) */
+  const uint32_t* run_fn;    /* [R] chunk-local first entry | length << 16 (slm_chunk_perm) */
   const int* run_q;          /* pair of each run */
   const uint32_t* run_tile;  /* view << 24 | tile */
   const float* run_static;   /* [R*8] static run records (slm_run_static) */
@@ -318,7 +319,7 @@ int slm_run_static(const SlmTileArgs* a, long long n_runs, const int* run_slot, 
 int slm_tile_chunks(const int* tile_run_off, int n_tiles, const long long* run_start, const int* tile_chunk_off,
                     int* out, uint8_t* chunk_perm, int fill, cudaStream_t s);
 int slm_chunk_perm(const int* chunk_run, long long n_chunks, const long long* run_start, uint8_t* chunk_perm,
-                   cudaStream_t s);
+                   uint32_t* run_fn, cudaStream_t s);
 /* diag_jtj (jacobian.py:486-512), first half: per-pair coefficient tables
  * (then slm_diag_stream) */
 int slm_pair_tables(const float* xs, long long G, int sh_degree, const int* pair_gid, const uint32_t* pair_vm,

@@ -60,7 +60,7 @@ class SlmResidArgs(C.Structure):
 class SlmTileArgs(C.Structure):
     _fields_ = [("views", c_vp), ("view_tile_base", c_vp), ("n_views", c_i), ("n_tiles", c_i),
                 ("tile_run_off", c_vp), ("tile_chunk_off", c_vp), ("chunk_run", c_vp), ("chunk_perm", c_vp), ("run_slot", c_vp),
-                ("run_start", c_vp), ("run_q", c_vp), ("run_tile", c_vp), ("run_static", c_vp), ("pm", c_vp),
+                ("run_start", c_vp), ("run_fn", c_vp), ("run_q", c_vp), ("run_tile", c_vp), ("run_static", c_vp), ("pm", c_vp),
                 ("geo", c_vp), ("ptab", c_vp),
                 ("rec4", c_vp), ("d2", c_vp), ("pix", c_vp),
                 ("gradr", c_vp), ("u", c_vp), ("u_out", c_vp), ("out", c_vp), ("out1", c_vp), ("tile_counter", c_vp)]
@@ -124,7 +124,7 @@ _SIGS = {
     "slm_apply_jt_runs": (c_i, [c_vp, c_vp]),
     "slm_jtwj_runs": (c_i, [c_vp, c_vp]),
     "slm_run_static": (c_i, [c_vp, c_ll, c_vp, c_vp, c_vp]),
-    "slm_chunk_perm": (c_i, [c_vp, c_ll, c_vp, c_vp, c_vp]),
+    "slm_chunk_perm": (c_i, [c_vp, c_ll, c_vp, c_vp, c_vp, c_vp]),
     "slm_tile_chunks": (c_i, [c_vp, c_i, c_vp, c_vp, c_vp, c_vp, c_i, c_vp]),
     "slm_pair_tables": (c_i, [c_vp, c_ll, c_i, c_vp, c_vp, c_vp, c_i, c_vp, c_vp, c_vp]),
     "slm_gauss_tab": (c_i, [c_vp, c_ll, c_i, c_vp, c_vp]),

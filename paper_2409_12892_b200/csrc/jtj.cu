@@ -201,27 +201,43 @@ __global__ void __launch_bounds__(32 * PK_WARPS, SLM_BW_MINB) k_gauss_backward_p
 // of p.(v + lam Mf p)
 template <int P>
 __global__ void __launch_bounds__(256) k_gm_to_am(SlmBackArgs A) {
-  __shared__ float t[32][P + 1];
+  constexpr int TS = P | 1;  // odd tile stride: conflict-free column reads
+  __shared__ float t[32 * TS];
   __shared__ double sm[32];
   const long long G = A.G;
   double dot = 0.0;
   for (long long g0 = (long long)blockIdx.x * 32; g0 < G; g0 += (long long)gridDim.x * 32) {
     const int ng = (int)min((long long)32, G - g0);
     __syncthreads();
-    for (int i = threadIdx.x; i < ng * P; i += blockDim.x) t[i / P][i % P] = A.gm[(size_t)g0 * P + i];
+    if (ng == 32) {
+      // full tile: 32 consecutive rows = 8 * P float4 (16-byte aligned: g0 % 32 == 0)
+      const float4* src = reinterpret_cast<const float4*>(A.gm + (size_t)g0 * P);
+      for (int i = threadIdx.x; i < 8 * P; i += blockDim.x) {
+        const float4 v = src[i];
+        const int e = 4 * i;
+        t[(e / P) * TS + e % P] = v.x;
+        t[((e + 1) / P) * TS + (e + 1) % P] = v.y;
+        t[((e + 2) / P) * TS + (e + 2) % P] = v.z;
+        t[((e + 3) / P) * TS + (e + 3) % P] = v.w;
+      }
+    } else {
+      for (int i = threadIdx.x; i < ng * P; i += blockDim.x) t[(i / P) * TS + i % P] = A.gm[(size_t)g0 * P + i];
+    }
     __syncthreads();
+#pragma unroll 4
     for (int i = threadIdx.x; i < 32 * P; i += blockDim.x) {
       const int a = i >> 5, gl = i & 31;
-      if (gl >= ng) continue;
-      float v = A.scale * t[gl][a];
-      const long long idx = (long long)a * G + g0 + gl;
-      if (A.p) {
-        const double pv = (double)A.p[idx];
-        const double lt = A.Mdiag ? A.lam * (double)fmaxf(A.Mdiag[idx], 1e-12f) * pv : 0.0;
-        dot += pv * ((double)v + lt);
-        if (A.lam_out) v = (float)((double)v + lt);
+      if (gl < ng) {
+        float v = A.scale * t[gl * TS + a];
+        const long long idx = (long long)a * G + g0 + gl;
+        if (A.p) {
+          const double pv = (double)A.p[idx];
+          const double lt = A.Mdiag ? A.lam * (double)fmaxf(A.Mdiag[idx], 1e-12f) * pv : 0.0;
+          dot += pv * ((double)v + lt);
+          if (A.lam_out) v = (float)((double)v + lt);
+        }
+        A.out[idx] = v;
       }
-      A.out[idx] = v;
     }
   }
   if (A.dot_part) {

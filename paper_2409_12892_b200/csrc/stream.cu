@@ -64,19 +64,19 @@ static_assert(OFF_PERM % 16 == 0 && OFF_HDR % 16 == 0 && ST_BYTES % 16 == 0,
               "stage sections must stay 16-byte aligned for cp.async.bulk");
 
 struct StageLayout {
-  int d2, pix, pst, pdy, rs, end;  // byte offsets of the sections, end of the packed region
+  int d2, pix, pst, pdy, rf, end;  // byte offsets of the sections, end of the packed region
 };
 __host__ __device__ __forceinline__ int al16(int x) { return (x + 15) & ~15; }
-// e entries, r runs; the d2 / pix / run-start copies are widened to 16-byte
-// aligned global ranges (<= e + 6 floats, <= e + 30 bytes, <= r + 3 starts)
+// e entries, r runs; the d2 / pix / run-word copies are widened to 16-byte
+// aligned global ranges (<= e + 6 floats, <= e + 30 bytes, <= r + 6 words)
 __host__ __device__ __forceinline__ StageLayout stage_layout(int e, int r) {
   StageLayout L;
   L.d2 = e * 16;
   L.pix = L.d2 + al16((e + 8) * 4);
   L.pst = L.pix + al16(e + 32);
   L.pdy = L.pst + r * 32;
-  L.rs = L.pdy + r * 48;
-  L.end = L.rs + al16((r + 4) * 8);
+  L.rf = L.pdy + r * 48;
+  L.end = L.rf + al16((r + 6) * 4);
   return L;
 }
 
@@ -220,7 +220,8 @@ __global__ void k_tile_chunks(const int* __restrict__ tile_run_off, int n_tiles,
 // each chunk's group schedule: its runs by decreasing length (ties by index),
 // 0xff-padded to 32 slots; one warp per chunk, lane = run
 __global__ void k_chunk_perm(const int* __restrict__ chunk_run, long long n_chunks,
-                             const long long* __restrict__ run_start, uint8_t* __restrict__ perm) {
+                             const long long* __restrict__ run_start, uint8_t* __restrict__ perm,
+                             uint32_t* __restrict__ run_fn) {
   constexpr int RL = CR / 32;  // runs per lane
   const int lane = threadIdx.x & 31;
   for (long long c = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; c < n_chunks;
@@ -233,6 +234,8 @@ __global__ void k_chunk_perm(const int* __restrict__ chunk_run, long long n_chun
       const int r = lane + 32 * h;
       len[h] = r < n ? run_start[k0 + r + 1] - run_start[k0 + r] : -1;
       rank[h] = 0;
+      // the run's word: chunk-local first entry | length << 16
+      if (r < n) run_fn[k0 + r] = (uint32_t)(run_start[k0 + r] - run_start[k0]) | ((uint32_t)len[h] << 16);
     }
 #pragma unroll
     for (int hj = 0; hj < RL; ++hj) {
@@ -383,32 +386,31 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
             if (lane == 0) {
               const long long a4 = m.e0 & ~3LL, z4 = (m.e1 + 3) & ~3LL;
               const long long a16 = m.e0 & ~15LL, z16 = (m.e1 + 15) & ~15LL;
-              const long long a2 = m.k0 & ~1LL, z2 = (m.k1 + 2) & ~1LL;
+              const long long aq = m.k0 & ~3LL, zq = (m.k1 + 3) & ~3LL;
               const unsigned b4 = (unsigned)(m.e1 - m.e0) * 16u, bd = (unsigned)(z4 - a4) * 4u;
               const unsigned bx = (unsigned)(z16 - a16), bp = (unsigned)(m.k1 - m.k0) * 32u;
-              const unsigned br = (unsigned)(z2 - a2) * 8u;
+              const unsigned br = (unsigned)(zq - aq) * 4u;
               int* hdr = reinterpret_cast<int*>(st + OFF_HDR);
               hdr[0] = m.k1 - m.k0;
-              hdr[1] = (int)(m.k0 - a2);
+              hdr[1] = (int)(m.k0 - aq);                // first run word / pair index
               hdr[2] = m.k0;
-              hdr[3] = (int)(m.e0 - a4);
-              hdr[4] = L.d2;
-              hdr[5] = L.pix;
+              hdr[3] = 0;
+              hdr[4] = L.d2 + (int)(m.e0 - a4) * 4;     // the chunk's first d2
+              hdr[5] = L.pix + (int)(m.e0 - a16);       // the chunk's first pixel byte
               hdr[6] = L.pst;
-              hdr[7] = L.rs;
+              hdr[7] = L.rf;
               // generic-proxy header writes before the async-proxy copies land
               asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
               // diag: the chunk's run -> pair indices (their chain tables) into
               // the pair-m section, which that mode does not use
-              const long long aq = m.k0 & ~3LL, zq = (m.k1 + 3) & ~3LL;
-              const unsigned bq = (MODE & MODE_DIAG) ? (unsigned)(zq - aq) * 4u : 0u;
+              const unsigned bq = (MODE & MODE_DIAG) ? br : 0u;
               mbar_arrive_tx(&full[s], b4 + bd + bx + bp + br + ST_PERM + bq);
               if (MODE & MODE_DIAG) bulk_g2s(st + L.pdy, A.run_q + aq, bq, &full[s], pol);
               bulk_g2s(st, A.rec4 + m.e0, b4, &full[s], pol);
               bulk_g2s(st + L.d2, A.d2 + a4, bd, &full[s], pol);
               bulk_g2s(st + L.pix, A.pix + a16, bx, &full[s], pol);
               bulk_g2s(st + L.pst, A.run_static + (size_t)m.k0 * 8, bp, &full[s], pol);
-              bulk_g2s(st + L.rs, A.run_start + a2, br, &full[s], pol);
+              bulk_g2s(st + L.rf, A.run_fn + aq, br, &full[s], pol);
               bulk_g2s(st + OFF_PERM, A.chunk_perm + (size_t)(w0 + i) * CR, ST_PERM, &full[s], pol);
             }
             __syncwarp();
@@ -462,11 +464,10 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
         const uint8_t* st = stage_ptr(ring, s);
         const int* hdr = reinterpret_cast<const int*>(st + OFF_HDR);
         const int nr = hdr[0];
-        const long long* rs = reinterpret_cast<const long long*>(st + hdr[7]) + hdr[1];
-        const long long e0 = rs[0];
+        const uint32_t* rf = reinterpret_cast<const uint32_t*>(st + hdr[7]) + hdr[1];
         const float4* s4 = reinterpret_cast<const float4*>(st);
-        const float* sd2 = reinterpret_cast<const float*>(st + hdr[4]) + hdr[3];
-        const uint8_t* spx = st + hdr[5] + (e0 & 15);
+        const float* sd2 = reinterpret_cast<const float*>(st + hdr[4]);
+        const uint8_t* spx = st + hdr[5];
         const float4* PST = reinterpret_cast<const float4*>(st + hdr[6]);
         const float4* PDY = reinterpret_cast<const float4*>(st + hdr[6] + nr * 32);
         for (int i = (warp + ci) & (NW - 1); i < nr; i += NW) {  // rotated: no warp always gets the extra runs
@@ -476,7 +477,8 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
           const float4 d0 = PDY[i * 3], d1 = PDY[i * 3 + 1];
           const float c2m = PDY[i * 3 + 2].x;
           const float a0 = s1.z * d0.x;
-          const int f0 = (int)(rs[i] - e0), n = (int)(rs[i + 1] - rs[i]);
+          const uint32_t fn = rf[i];
+          const int f0 = (int)(fn & 0xffffu), n = (int)(fn >> 16);
           const float4* pr = s4 + f0;
           const float* pd = sd2 + f0;
           const uint8_t* pp = spx + f0;
@@ -534,11 +536,10 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
         mbar_wait(&full[s], (g / NSM) & 1u);
         const uint8_t* st = stage_ptr(ring, s);
         const int* hdr = reinterpret_cast<const int*>(st + OFF_HDR);
-        const long long* rs = reinterpret_cast<const long long*>(st + hdr[7]) + hdr[1];
+        const uint32_t* rf = reinterpret_cast<const uint32_t*>(st + hdr[7]) + hdr[1];
         const float4* s4 = reinterpret_cast<const float4*>(st);
-        const float* sd2 = reinterpret_cast<const float*>(st + hdr[4]) + hdr[3];
-        const uint8_t* spx = st + hdr[5] + (rs[0] & 15);
-        const long long e0 = rs[0];
+        const float* sd2 = reinterpret_cast<const float*>(st + hdr[4]);
+        const uint8_t* spx = st + hdr[5];
         for (int rd = 0; rd < CR / 32 && rd * 32 < hdr[0]; ++rd) {  // 32 runs per round, longest first
           const int ri = st[OFF_PERM + rd * 32 + (((warp + ci) & (NW - 1)) * 4 + slot)];
           int n = 0, f0 = 0, sl = 0;
@@ -553,7 +554,7 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
             io = s1.z;
             sl = __float_as_int(s1.w);
             // the run's pair (its chain table), staged by the producer
-            const int* sq = reinterpret_cast<const int*>(st + hdr[6] + hdr[0] * 32) + (hdr[2] & 3);
+            const int* sq = reinterpret_cast<const int*>(st + hdr[6] + hdr[0] * 32) + hdr[1];
             const float4* tq = reinterpret_cast<const float4*>(A.ptab + (size_t)sq[ri] * DIAG_TAB);
   #pragma unroll
             for (int k = 0; k < DIAG_TAB / 4; ++k) {
@@ -563,8 +564,9 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
               D[4 * k + 2] = v.z;
               D[4 * k + 3] = v.w;
             }
-            f0 = (int)(rs[ri] - e0);
-            n = (int)(rs[ri + 1] - rs[ri]);
+            const uint32_t fn = rf[ri];
+            f0 = (int)(fn & 0xffffu);
+            n = (int)(fn >> 16);
           } else {
   #pragma unroll
             for (int k = 0; k < DIAG_TAB; ++k) D[k] = 0.f;
@@ -653,11 +655,10 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
         mbar_wait(&full[s], (g / NSM) & 1u);
         const uint8_t* st = stage_ptr(ring, s);
         const int* hdr = reinterpret_cast<const int*>(st + OFF_HDR);
-        const long long* rs = reinterpret_cast<const long long*>(st + hdr[7]) + hdr[1];
+        const uint32_t* rf = reinterpret_cast<const uint32_t*>(st + hdr[7]) + hdr[1];
         const float4* s4 = reinterpret_cast<const float4*>(st);
-        const float* sd2 = reinterpret_cast<const float*>(st + hdr[4]) + hdr[3];
-        const uint8_t* spx = st + hdr[5] + (rs[0] & 15);
-        const long long e0 = rs[0];
+        const float* sd2 = reinterpret_cast<const float*>(st + hdr[4]);
+        const uint8_t* spx = st + hdr[5];
         for (int rd = 0; rd < CR / 32 && rd * 32 < hdr[0]; ++rd) {  // 32 runs per round, longest first
           const int ri = st[OFF_PERM + rd * 32 + (((warp + ci) & (NW - 1)) * 4 + slot)];
           int n = 0, f0 = 0;
@@ -670,8 +671,9 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
             s1 = P4[1];
             io = s1.z;
             slot = __float_as_int(s1.w);
-            f0 = (int)(rs[ri] - e0);
-            n = (int)(rs[ri + 1] - rs[ri]);
+            const uint32_t fn = rf[ri];
+            f0 = (int)(fn & 0xffffu);
+            n = (int)(fn >> 16);
           }
           const int nmax = __reduce_max_sync(0xffffffffu, (unsigned)n);
           if (nmax == 0) continue;
@@ -783,10 +785,10 @@ int slm_tile_chunks(const int* tile_run_off, int n_tiles, const long long* run_s
 }
 
 int slm_chunk_perm(const int* chunk_run, long long n_chunks, const long long* run_start, uint8_t* chunk_perm,
-                   cudaStream_t st) {
+                   uint32_t* run_fn, cudaStream_t st) {
   if (n_chunks <= 0) return SLM_OK;
   k_chunk_perm<<<slm_blocks(n_chunks * 32, 256, 1LL << 30), 256, 0, st>>>(chunk_run, n_chunks, run_start,
-                                                                         chunk_perm);
+                                                                         chunk_perm, run_fn);
   return slm_cuda_status();
 }
 

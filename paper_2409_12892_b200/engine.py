@@ -458,7 +458,7 @@ class CacheSet:
         # ---- run table, runs per tile, pair -> runs ----------------------------
         R = self.R
         self.run_start = torch.zeros(R + 3, dtype=torch.int64, device=dev)  # +2: 16 B-granular TMA copies
-        self.run_q = _empty(R, torch.int32, dev)
+        self.run_q = _empty(R + 8, torch.int32, dev)   # +8: 16-byte granular TMA copies (diag)
         self.run_tile = _empty(R, torch.int32, dev)
         pair_nruns = torch.zeros(Pn + 1, dtype=torch.int32, device=dev)
         tile_nruns = torch.zeros(nt + 1, dtype=torch.int32, device=dev)
@@ -483,8 +483,9 @@ class CacheSet:
         call("slm_tile_chunks", ptr(self.tile_run_off), nt, ptr(self.run_start), ptr(self.tile_chunk_off),
              ptr(self.chunk_run), ptr(self.chunk_perm), 1, stream_ptr())
         self.chunk_run[self.n_chunks:].fill_(R)
+        self.run_fn = _empty(R + 8, torch.int32, dev)   # +8: 16-byte granular TMA copies stay in bounds
         call("slm_chunk_perm", ptr(self.chunk_run), self.n_chunks, ptr(self.run_start), ptr(self.chunk_perm),
-             stream_ptr())
+             ptr(self.run_fn), stream_ptr())
         del tile_nch
         self.pair_run_off = torch.empty_like(pair_nruns)
         scan_i32(pair_nruns, self.pair_run_off)
@@ -608,6 +609,7 @@ class CacheSet:
         a.chunk_perm, a.run_slot = ptr(self.chunk_perm), ptr(self.run_slot)
         a.run_start, a.run_q, a.run_tile, a.run_static = ptr(self.run_start), ptr(self.run_q), ptr(self.run_tile), \
             ptr(self.run_static)
+        a.run_fn = ptr(self.run_fn)
         a.pm = ptr(self.pm) if with_m else None
         a.geo = ptr(self.pair_geo)
         a.rec4, a.d2 = ptr(self.rec4), ptr(self.rec_d2)
