@@ -114,11 +114,11 @@ def make_workload(cfg, device, only=None):
     G, V, W, H, deg = cfg["G"], cfg["views"], cfg["W"], cfg["H"], cfg["degree"]
     if cfg["gen"] == "reference":
         truth = S.make_synthetic_scene(0, G, deg)
-        init = S.perturb(truth, 1, 0.1)
+        init = S.perturb(truth, 1, cfg.get("perturb", 0.1))
         cams = S.make_camera_ring(V, W, H)
     else:
         truth = S.make_footprint_scene(0, G, W, H, deg, k_target=32.0)
-        init = S.perturb(truth, 1, 0.02)
+        init = S.perturb(truth, 1, cfg.get("perturb", 0.02))
         cams = S.make_camera_ring(V, W, H)
     tscene = truth.to_device(device)
     gts = []
@@ -231,6 +231,21 @@ def run_ours(args, cfg):
     barrier()
     e2e_ms = e0.elapsed_time(e1) / n_e2e
     _ = out
+    # one untimed full LM iteration (direction + line search + rho + trust
+    # region) on the same inputs: is the benchmarked direction a descent
+    # step, and where does a step's time go (CUDA-event phases)
+    from paper_2409_12892_b200 import lm as L
+    from paper_2409_12892_b200.engine import PhaseTimer
+    pt = PhaseTimer()
+    e_before = L.energy(scene, cams, gts, rank=rank, world_size=world)
+    lr = L.lm_step(scene, cams, gts, sched, lam, iters, rank=rank, world_size=world, phase_timer=pt)
+    e_after = L.energy(lr.scene, cams, gts, rank=rank, world_size=world) if lr.accepted else e_before
+    lm_info = {"energy_before": e_before, "energy_after": e_after, "gamma": lr.gamma, "rho": lr.rho,
+               "accepted": bool(lr.accepted), "lam_new": lr.lam,
+               "observed_fraction": lr.direction.observed_fraction,
+               "energy_views": "all views; line search on the strided 30 % (SPEC:409-417)"}
+    phases = {k: round(v, 2) for k, v in (lr.direction.phases or {}).items()}
+    del lr
     # max over ranks
     vals = torch.tensor([ms, e2e_ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -265,7 +280,9 @@ def run_ours(args, cfg):
                                f"{cfg['iters']} PCG iters, lambda 1e-4",
                    "generator": cfg["gen"], "entries_per_subset": E_sub,
                    "entries_per_pixel": round(E_sub / N_sub, 2) if N_sub else None,
-                   "pcg": rep.pcg[:2], "l2": "inputs larger than L2 (cache >> 126 MB)",
+                   "pcg": rep.pcg[:2], "lm_step": lm_info,
+                   "phases_ms_per_step": phases,
+                   "l2": "inputs larger than L2 (cache >> 126 MB)",
                    "parallelism": f"subsets round-robin over {world} rank(s), one NCCL all_reduce"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,

@@ -152,13 +152,13 @@ class LMStepReport:
 
 def lm_step(scene: GaussianScene, cameras, gts, schedule: BatchSchedule = BatchSchedule(), lam: float = 1e-4,
             n_iters: int = 8, ls_fraction: float = 0.3, config=None, loss: LossConfig = LossConfig(),
-            rank: int = 0, world_size: int = 1) -> LMStepReport:
+            rank: int = 0, world_size: int = 1, phase_timer=None) -> LMStepReport:
     """One LM iteration (SPEC lm_fit body): batched direction (Eq. 7), line
     search on a strided ls_fraction of the views (PAPER 3.2), rho on the first
     batch's frozen caches, trust-region accept / revert."""
     n = len(cameras)
     rep = lm_direction(scene, cameras, gts, schedule, lam, n_iters, config, loss, rank, world_size,
-                       keep_caches=True)
+                       keep_caches=True, phase_timer=phase_timer)
     delta = rep.delta
     step = max(1, int(round(1.0 / ls_fraction))) if ls_fraction > 0 else 1
     ls_views = list(range(0, n, step))

@@ -20,7 +20,7 @@ import torch
 
 from . import _lib
 from ._lib import call, ptr, stream_ptr
-from .engine import CacheSet, LossConfig
+from .engine import CacheSet, LossConfig, _NoTimer
 from .errors import NonSPDError
 from .scene import Layout, ParamVector
 
@@ -281,17 +281,31 @@ class StepReport:
     entries: list
     pcg: list
     product_ms: list
+    observed: torch.Tensor | None = None   # device count of gaussians with sum_i M_i(opacity) > 0
+    n_gaussians: int = 0
+    phases: dict | None = None             # per-phase ms (phase_timer given)
+
+    @property
+    def observed_fraction(self) -> float | None:
+        """Fraction of gaussians observed by the step's subsets (nonzero
+        opacity curvature in the combined den = sum_i M_i; one host read)."""
+        if self.observed is None or self.n_gaussians == 0:
+            return None
+        return float(self.observed.item()) / self.n_gaussians
 
 
 def lm_direction(scene, cameras, gts, schedule: BatchSchedule = BatchSchedule(), lambda_reg: float = 1e-4,
                  n_iters: int = 8, config=None, loss: LossConfig = LossConfig(), rank: int = 0,
-                 world_size: int = 1, product_timer=None, keep_caches: bool = False) -> StepReport:
+                 world_size: int = 1, product_timer=None, keep_caches: bool = False,
+                 phase_timer=None) -> StepReport:
     """One LM update direction: per subset cache build, b, M, PCG, Eq. 7
     combine; subsets are sharded round-robin over ranks.
 
     Ground-truth images may live in (pinned) host memory: each subset's images
     are then copied on a side stream while the previous subset is solved."""
     n = scene.param_count
+    T = phase_timer if phase_timer is not None else _NoTimer()
+    T.tick("start")
     comb = Combiner(n, scene.device)
     ws = PCGWorkspace(n, scene.device, scene.num_gaussians, scene.params_per_gaussian)
     entries, pcg_stats = [], []
@@ -304,30 +318,41 @@ def lm_direction(scene, cameras, gts, schedule: BatchSchedule = BatchSchedule(),
         gts_sub, buf = fetch.take()
         if k + 1 < len(shards):
             fetch.start(k + 1, shards[k + 1][1])
-        cs = CacheSet(scene, [cameras[i] for i in views], gts_sub, config, loss)
+        cs = CacheSet(scene, [cameras[i] for i in views], gts_sub, config, loss, timer=phase_timer)
+        T.tick("cache_tables")
         fetch.release(buf)  # the images are only read by the build's residual pass
         del gts_sub
         comb.energy += sum(cs.energies)
         entries.append(cs.E)
         b = cs.rhs()
+        T.tick("rhs")
         M = cs.diag()
+        T.tick("diag")
         st = {}
         try:
             d = pcg_run(cs, b, M, lambda_reg, n_iters, ws, stats=st, timer=product_timer)
         except NonSPDError:
             pcg_stats.append({"rejected": True})
             continue
+        T.tick("pcg")
         pcg_stats.append(st)
         comb.add(d, M)
+        T.tick("combine")
         if keep_caches and not caches:  # the first accepted batch (rho's frozen caches)
             cs.view_ids = list(views)
             caches.append(cs)
         del cs
     comb.allreduce(world_size=world_size)
+    T.tick("allreduce")
     if comb.accepted == 0:
         raise NonSPDError("all batches rejected by PCG failure")
     # energy: the global sum over all subsets' views (every rank gets it)
-    rep = StepReport(comb.finalize(), comb.energy, comb.accepted, entries, pcg_stats, [])
+    G = scene.num_gaussians
+    rep = StepReport(comb.finalize(), comb.energy, comb.accepted, entries, pcg_stats, [],
+                     (comb.den[10 * G:11 * G] > 0).sum() if G else None, G)
+    T.tick("finalize")
+    if phase_timer is not None:
+        rep.phases = phase_timer.summary()
     rep.caches = caches
     return rep
 

@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -15 > gpurun_out/pytest_gpu.log
-bash tools/gpu_ab.sh c3 > gpurun_out/ab6.log 2>&1
+timeout 1200 python bench.py > gpurun_out/bench_c3.log 2>&1
+bash tools/gpu_ncu_product.sh prod_r02

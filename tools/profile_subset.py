@@ -33,6 +33,8 @@ def main():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--skip-pcg", action="store_true")
+    ap.add_argument("--product-only", action="store_true",
+                    help="build, rhs, diag, then 2 fused products inside an NVTX range 'product' (ncu --nvtx)")
     args = ap.parse_args()
     cfg = dict(bench.CONFIGS[args.config])
     torch.cuda.set_device(0)
@@ -59,6 +61,21 @@ def main():
         phases["diag"] = c.elapsed_time(d)
         p = torch.randn(scene.param_count, device=dev)
         g = torch.empty_like(p)
+        if args.product_only:
+            PG = _lib.load().slm_gm_stride(cs.P)
+            p_gm = torch.zeros(cs.G, PG, device=dev)
+            p_gm[:, :cs.P] = p.view(cs.P, cs.G).t()
+            p_gm = p_gm.reshape(-1)
+            dp = torch.zeros(_lib.load().slm_backward_blocks(cs.G), dtype=torch.float64, device=dev)
+            cs.jtwj(p, g, 1e-4, M, dp, False, p_gm=p_gm)      # warm
+            torch.cuda.synchronize()
+            torch.cuda.nvtx.range_push("product")
+            for _ in range(2):
+                cs.jtwj(p, g, 1e-4, M, dp, False, p_gm=p_gm)
+            torch.cuda.nvtx.range_pop()
+            torch.cuda.synchronize()
+            print(json.dumps(dict(phases, E=cs.E, N=cs.N, R=cs.R, pairs=cs.n_pairs, G=cs.G)))
+            return
         # the padded gaussian-major copy the PCG p kernels hand to the product
         PG = _lib.load().slm_gm_stride(cs.P)
         p_gm = torch.zeros(cs.G, PG, device=dev)
