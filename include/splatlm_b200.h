@@ -302,6 +302,19 @@ int slm_pairs_emit(const int* cnt, int V, long long G, const int* pair_of, const
                    const SlmSplat* splats, long long* pair_off, int* pair_gid, uint32_t* pair_vm, SlmPairGeo* geo,
                    int* pidx, int* gpo, int n_pairs, long long n_entries, cudaStream_t s);
 
+/* reference-order export of one view (parity / interop, not on the solve
+ * path): from the run order, the pixel-sorted index arrays of build_cache
+ * (jacobian.py:401-409) and the gaussian-sorted ones of
+ * sort_cache_by_gaussians (jacobian.py:93-105); pos_pix[e - e_base] = the
+ * pixel-order position of run-order entry e.  px_off: the view's per-pixel
+ * entry offsets [HW+1]; g_off: its per-gaussian offsets [G+1] */
+int slm_export_view(const int* tile_run_off, int t0, int n_tiles, int tiles_x, int W, const long long* run_start,
+                    const int* run_q, const uint32_t* run_tile, const int* pair_gid, const uint32_t* pair_vm,
+                    const int* pair_run_off, const int* pair_runs, int n_pairs, int view, const uint8_t* pix,
+                    const long long* px_off, const long long* g_off, long long e_base, long long* pos_pix,
+                    long long* pixel_ids, long long* gaussian_ids, long long* g_pixel_ids, long long* g_gaussian_ids,
+                    long long* g_source_index, cudaStream_t s);
+
 /* ---- products ----------------------------------------------------------------
  * apply_j (jacobian.py:419-455) fused with weight_residuals (458-464) when
  * a->gradr != NULL; one CTA per tile of the subset */

@@ -120,6 +120,8 @@ _SIGS = {
     "slm_pairs_prepare": (c_i, [c_vp, c_i, c_ll, c_vp, c_vp, c_vp, c_vp]),
     "slm_pairs_emit": (c_i, [c_vp, c_i, c_ll, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                              c_i, c_ll, c_vp]),
+    "slm_export_view": (c_i, [c_vp, c_i, c_i, c_i, c_i, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i, c_i, c_vp,
+                              c_vp, c_vp, c_ll, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "slm_apply_j": (c_i, [c_vp, c_vp]),
     "slm_apply_jt_runs": (c_i, [c_vp, c_vp]),
     "slm_jtwj_runs": (c_i, [c_vp, c_vp]),

@@ -1,14 +1,15 @@
 // Gradient-cache assembly: pixel segments and (gaussian, view) pairs.
 //
-// The gaussian-order record stream itself (sortCacheByGaussians, PAPER:273,
-// 305-306) is written directly by the FILL raster pass (raster.cu): pairs are
-// numbered in (view, gid) order and each pair's block is filled in pixel
-// row-major order, so one view's gaussian-order sequence equals the
-// reference's np.lexsort((pixel_ids, gaussian_ids)) (ref: jacobian.py:93-105)
-// with no sort at all.
+// There is no second (gaussian-order) record stream: the FILL raster pass
+// writes one run-ordered stream whose runs are reachable per tile (J) and per
+// (gaussian, view) pair through the pair -> runs CSR (J^T, backward), and the
+// reference's pixel- and gaussian-sorted orders (ref: jacobian.py:93-121) are
+// exported from it on demand (slm_export_view, parity / interop only).
 #include "slm_common.cuh"
 
 #include <cub/cub.cuh>
+
+#include <algorithm>
 
 // ---------------------------------------------------------------------------
 // scans / sorts (CUB) -- workspace sizes are queried by the host
@@ -154,6 +155,106 @@ __global__ void k_iota_u32(uint32_t* out, long long n) {
     out[i] = (uint32_t)i;
 }
 
+
+// ---------------------------------------------------------------------------
+// Reference-order export of one view (parity / interop only, not on the
+// solve path), computed on the device from the run order:
+//   pixel order    (ref: jacobian.py:401-409; entries pixel-major, blending
+//                   (depth) order within a pixel)
+//   gaussian order (ref: jacobian.py:93-105, np.lexsort((pixel_ids,
+//                   gaussian_ids)): gid-major, pixel id within a gaussian)
+// k_export_pixel: block per tile, a shared counter per tile pixel; runs are
+//   taken in depth order and a run never repeats a pixel, so an entry's rank
+//   at its pixel is the counter value when its run is reached:
+//   pos_pix[e] = px_off[pixel] + rank.
+// k_export_gauss: thread per pair of the view.  The pair's runs are in tile
+//   row-major order (pair_runs CSR) and each run's entries in tile-local
+//   row-major order, so within one tile row of the pair the entries of local
+//   row ly follow run by run in tile-column order; 16 row counters (pass 1)
+//   give each row's first rank and pass 2 hands out consecutive ranks:
+//   pos_g[e] = g_off[gid] + rank by pixel id among the pair's entries.
+// Outputs are the reference's index arrays: pixel_ids / gaussian_ids (pixel
+// order), g_pixel_ids / g_gaussian_ids / source_index (gaussian order).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_export_pixel(const int* __restrict__ tile_run_off, int t0, int n_tiles,
+                                                      int tiles_x, int W, const long long* __restrict__ run_start,
+                                                      const int* __restrict__ run_q, const int* __restrict__ pair_gid,
+                                                      const uint8_t* __restrict__ pix,
+                                                      const long long* __restrict__ px_off, long long e_base,
+                                                      long long* __restrict__ pos_pix, long long* __restrict__ pixel_ids,
+                                                      long long* __restrict__ gaussian_ids) {
+  __shared__ int cnt[256];
+  for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const long long ox = (long long)(t % tiles_x) * SLM_TILE, oy = (long long)(t / tiles_x) * SLM_TILE;
+    const int r0 = tile_run_off[t0 + t], r1 = tile_run_off[t0 + t + 1];
+    for (int r = r0; r < r1; ++r) {
+      const long long s = run_start[r];
+      const int n = (int)(run_start[r + 1] - s);
+      if ((int)threadIdx.x < n) {
+        const int pl = pix[s + threadIdx.x];
+        const long long px = (oy + (pl >> 4)) * W + ox + (pl & 15);
+        const int k = cnt[pl];
+        cnt[pl] = k + 1;
+        const long long pp = px_off[px] + k;
+        pos_pix[s + threadIdx.x - e_base] = pp;
+        pixel_ids[pp] = px;
+        gaussian_ids[pp] = pair_gid[run_q[r]];
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void k_export_gauss(int n_pairs, int view, int tiles_x, int W, const uint32_t* __restrict__ pair_vm,
+                               const int* __restrict__ pair_gid, const int* __restrict__ pair_run_off,
+                               const int* __restrict__ pair_runs, const uint32_t* __restrict__ run_tile,
+                               const long long* __restrict__ run_start, const uint8_t* __restrict__ pix,
+                               const long long* __restrict__ g_off, long long e_base,
+                               const long long* __restrict__ pos_pix, long long* __restrict__ g_pixel_ids,
+                               long long* __restrict__ g_gaussian_ids, long long* __restrict__ g_source_index) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_pairs; q += gridDim.x * blockDim.x) {
+    if ((int)(pair_vm[q] & 0xffffu) != view) continue;
+    const int gid = pair_gid[q];
+    long long rank = g_off[gid];
+    const int a = pair_run_off[q], b = pair_run_off[q + 1];
+    for (int k = a; k < b;) {
+      const int ty = (int)(run_tile[pair_runs[k]] & 0xffffffu) / tiles_x;
+      int k2 = k + 1;
+      while (k2 < b && (int)(run_tile[pair_runs[k2]] & 0xffffffu) / tiles_x == ty) ++k2;
+      long long cur[16];
+      int rc[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) rc[i] = 0;
+      for (int kk = k; kk < k2; ++kk) {  // pass 1: entries per local row of this tile row
+        const int r = pair_runs[kk];
+        for (long long e = run_start[r]; e < run_start[r + 1]; ++e) ++rc[pix[e] >> 4];
+      }
+      long long acc = rank;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        cur[i] = acc;
+        acc += rc[i];
+      }
+      for (int kk = k; kk < k2; ++kk) {  // pass 2: ranks by pixel id
+        const int r = pair_runs[kk];
+        const int lt = (int)(run_tile[r] & 0xffffffu);
+        const long long ox = (long long)(lt % tiles_x) * SLM_TILE, oy = (long long)ty * SLM_TILE;
+        for (long long e = run_start[r]; e < run_start[r + 1]; ++e) {
+          const int pl = pix[e];
+          const long long pos = cur[pl >> 4]++;
+          g_pixel_ids[pos] = (oy + (pl >> 4)) * W + ox + (pl & 15);
+          g_gaussian_ids[pos] = gid;
+          g_source_index[pos] = pos_pix[e - e_base];
+        }
+      }
+      rank = acc;
+      k = k2;
+    }
+  }
+}
+
 extern "C" {
 
 int slm_pairs_prepare(const int* cnt, int V, long long G, long long* cntV, int* flagV, int* flagT, cudaStream_t s) {
@@ -180,6 +281,23 @@ int slm_invert_perm(const int* perm, long long n, int* inv, cudaStream_t s) {
 int slm_iota_u32(uint32_t* out, long long n, cudaStream_t s) {
   if (n <= 0) return SLM_OK;
   k_iota_u32<<<slm_blocks(n, 256), 256, 0, s>>>(out, n);
+  return slm_cuda_status();
+}
+
+int slm_export_view(const int* tile_run_off, int t0, int n_tiles, int tiles_x, int W, const long long* run_start,
+                    const int* run_q, const uint32_t* run_tile, const int* pair_gid, const uint32_t* pair_vm,
+                    const int* pair_run_off, const int* pair_runs, int n_pairs, int view, const uint8_t* pix,
+                    const long long* px_off, const long long* g_off, long long e_base, long long* pos_pix,
+                    long long* pixel_ids, long long* gaussian_ids, long long* g_pixel_ids, long long* g_gaussian_ids,
+                    long long* g_source_index, cudaStream_t s) {
+  if (n_tiles <= 0) return SLM_OK;
+  k_export_pixel<<<(unsigned)std::min(n_tiles, 148 * 16), 256, 0, s>>>(tile_run_off, t0, n_tiles, tiles_x, W, run_start,
+                                                                     run_q, pair_gid, pix, px_off, e_base, pos_pix,
+                                                                     pixel_ids, gaussian_ids);
+  if (n_pairs > 0)
+    k_export_gauss<<<slm_blocks(n_pairs, 128, 1LL << 30), 128, 0, s>>>(
+        n_pairs, view, tiles_x, W, pair_vm, pair_gid, pair_run_off, pair_runs, run_tile, run_start, pix, g_off, e_base,
+        pos_pix, g_pixel_ids, g_gaussian_ids, g_source_index);
   return slm_cuda_status();
 }
 

@@ -717,7 +717,9 @@ class CacheSet:
     def export_view(self, v: int) -> dict:
         """Reference-shaped arrays of view v: the pixel-sorted cache
         (ref: jacobian.py:401-409) and its gaussian-sorted permutation
-        (ref: jacobian.py:93-105), reconstructed from the run order."""
+        (ref: jacobian.py:93-105).  Both orders are computed on the device from
+        the run order (slm_export_view); the record values are then placed
+        with that device-computed permutation."""
         cam = self.cameras[v]
         if self.G == 0:
             e, f = np.zeros(0, np.int64), np.zeros(0)
@@ -725,36 +727,37 @@ class CacheSet:
                         dc_dalpha=np.zeros((0, 3)), dc_dcs=f, offsets=np.zeros(cam.num_pixels + 1, np.int64),
                         g_pixel_ids=e, g_gaussian_ids=e, g_offsets=np.zeros(1, np.int64), g_source_index=e,
                         g_dc_dalpha=np.zeros((0, 3)), g_alpha_eff=f, g_dc_dcs=f)
+        dev, i64 = self.device, torch.int64
         t0, t1 = self.view_tile_base[v], self.view_tile_base[v + 1]
-        tro = self.tile_run_off.cpu().numpy()
-        r0, r1 = int(tro[t0]), int(tro[t1])
-        rs = self.run_start[r0:r1 + 1].cpu().numpy()
-        e0, e1 = int(rs[0]), int(rs[-1])
-        run_q = self.run_q[r0:r1].cpu().numpy()
-        run_tile = self.run_tile[r0:r1].cpu().numpy().view(np.uint32) & 0xFFFFFF
-        pair_gid = self.pair_gid[: self.n_pairs].cpu().numpy()
-        n = np.diff(rs)
-        run_of_e = np.repeat(np.arange(r1 - r0), n)
-        pl = self.rec_pix[e0:e1].cpu().numpy().astype(np.int64)
-        tiles_x = (cam.width + TILE - 1) // TILE
-        tile = run_tile[run_of_e].astype(np.int64)
-        px = (tile % tiles_x) * TILE + (pl & 15)
-        py = (tile // tiles_x) * TILE + (pl >> 4)
-        pixel = py * cam.width + px
-        gid = pair_gid[run_q[run_of_e]].astype(np.int64)
+        r0, r1 = (int(x) for x in self.tile_run_off[[t0, t1]].tolist())
+        e0, e1 = (int(x) for x in self.run_start[[r0, r1]].tolist())
+        Ev, hw, G = e1 - e0, cam.num_pixels, self.G
+        pb = self.pix_bases[v]
+        px_cnt = torch.zeros(hw + 1, dtype=i64, device=dev)
+        px_cnt[:hw] = self.px_count[pb:pb + hw]
+        px_off = torch.empty_like(px_cnt)
+        scan_i64(px_cnt, px_off)
+        g_cnt = torch.zeros(G + 1, dtype=i64, device=dev)
+        g_cnt[:G] = self.pair_cnt[v * G:(v + 1) * G]
+        g_off = torch.empty_like(g_cnt)
+        scan_i64(g_cnt, g_off)
+        out = {k: _empty(Ev, i64, dev) for k in ("pos_pix", "pixel_ids", "gaussian_ids", "g_pixel_ids",
+                                                  "g_gaussian_ids", "g_source_index")}
+        call("slm_export_view", ptr(self.tile_run_off), t0, t1 - t0, (cam.width + TILE - 1) // TILE, cam.width,
+             ptr(self.run_start), ptr(self.run_q), ptr(self.run_tile), ptr(self.pair_gid), ptr(self.pair_vm),
+             ptr(self.pair_run_off), ptr(self.pair_runs), self.n_pairs, v, ptr(self.rec_pix), ptr(px_off),
+             ptr(g_off), e0, ptr(out["pos_pix"]), ptr(out["pixel_ids"]), ptr(out["gaussian_ids"]),
+             ptr(out["g_pixel_ids"]), ptr(out["g_gaussian_ids"]), ptr(out["g_source_index"]), stream_ptr())
+        h = {k: t[:Ev].cpu().numpy() for k, t in out.items()}
+        pos, src = h["pos_pix"], h["g_source_index"]
         r4 = self.rec4[4 * e0:4 * e1].view(-1, 4).cpu().numpy().astype(np.float64)
-        f = [r4[:, 0], r4[:, 1], r4[:, 2], r4[:, 3], self.rec_d2[e0:e1].cpu().numpy().astype(np.float64)]
-        order = np.argsort(pixel, kind="stable")      # runs of one tile are in depth order
-        pixel, gid = pixel[order], gid[order]
-        ae, at = f[0][order], f[1][order]
-        dcda = np.stack([f[2][order], f[3][order], f[4][order]], 1)
+        d2 = self.rec_d2[e0:e1].cpu().numpy().astype(np.float64)
+        ae, at = np.empty(Ev), np.empty(Ev)
+        dcda = np.empty((Ev, 3))
+        ae[pos], at[pos] = r4[:, 0], r4[:, 1]
+        dcda[pos] = np.stack([r4[:, 2], r4[:, 3], d2], 1)
         alpha = np.where(ae == 0.0, self.config.alpha_clamp, ae)
-        offsets = np.zeros(cam.num_pixels + 1, np.int64)
-        offsets[1:] = np.cumsum(np.bincount(pixel, minlength=cam.num_pixels))
-        gperm = np.lexsort((pixel, gid))
-        goff = np.zeros(self.G + 1, np.int64)
-        goff[1:] = np.cumsum(np.bincount(gid, minlength=self.G))
-        return dict(pixel_ids=pixel, gaussian_ids=gid, alphas=alpha, alpha_eff=ae, transmittances=at / alpha,
-                    dc_dalpha=dcda, dc_dcs=at, offsets=offsets,
-                    g_pixel_ids=pixel[gperm], g_gaussian_ids=gid[gperm], g_offsets=goff, g_source_index=gperm,
-                    g_dc_dalpha=dcda[gperm], g_alpha_eff=ae[gperm], g_dc_dcs=at[gperm])
+        return dict(pixel_ids=h["pixel_ids"], gaussian_ids=h["gaussian_ids"], alphas=alpha, alpha_eff=ae,
+                    transmittances=at / alpha, dc_dalpha=dcda, dc_dcs=at, offsets=px_off.cpu().numpy(),
+                    g_pixel_ids=h["g_pixel_ids"], g_gaussian_ids=h["g_gaussian_ids"], g_offsets=g_off.cpu().numpy(),
+                    g_source_index=src, g_dc_dalpha=dcda[src], g_alpha_eff=ae[src], g_dc_dcs=at[src])

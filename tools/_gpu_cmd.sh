@@ -1,2 +1,1 @@
-timeout 1200 python bench.py > gpurun_out/bench_c3.log 2>&1
-bash tools/gpu_ncu_product.sh prod_r02
+timeout 1500 python -m pytest tests -m gpu -x -q --durations=8 2>&1 | tail -25 > gpurun_out/pytest_gpu.log
