@@ -17,8 +17,9 @@ copied back, every step.  `roofline` = the J^T W J p product (pair forward +
 applyJ + applyJT + pair backward) against measured HBM bandwidth, algorithmic
 bytes 48 E + 36 N + 16 M per product.  `--impl reference` times
 the reference's own numpy implementation (pip-installed into baseline/_ref)
-driven through Alg. 1 / Eq. 7 (oracle/ref_driver.py) on the host cores, on a
-bounded sample of the same generator, and projects it to the workload.
+driven through Alg. 1 / Eq. 7 on every host core (one process per core and
+view, oracle/ref_parallel.py), on a bounded sample of the same generator, and
+projects it to the workload.
 """
 
 from __future__ import annotations
@@ -305,10 +306,10 @@ def run_ours(args, cfg):
 # reference package is absent.
 # ---------------------------------------------------------------------------
 
-def cpu_sample(cfg):
+def cpu_sample(cfg, n_views=2):
     """Bounded sample of the same generator at the same pixels-per-Gaussian
-    (hence the same entries-per-pixel): G_s Gaussians, 2 views, resolution
-    scaled so that W*H / G matches the workload."""
+    (hence the same entries-per-pixel): G_s Gaussians, n_views views,
+    resolution scaled so that W*H / G matches the workload."""
     import numpy as np
 
     from paper_2409_12892_b200 import synthetic as S
@@ -319,56 +320,79 @@ def cpu_sample(cfg):
     H = max(16, int(round(cfg["H"] * scale)))
     if cfg["gen"] == "reference":
         truth = S.make_synthetic_scene(0, Gs, cfg["degree"])
-        init = S.perturb(truth, 1, 0.1)
+        init = S.perturb(truth, 1, cfg.get("perturb", 0.1))
     else:
         truth = S.make_footprint_scene(0, Gs, W, H, cfg["degree"], k_target=32.0)
-        init = S.perturb(truth, 1, 0.02)
-    cams = S.make_camera_ring(2, W, H)
+        init = S.perturb(truth, 1, cfg.get("perturb", 0.02))
+    cams = S.make_camera_ring(n_views, W, H)
     return truth, init, cams, (Gs, W, H)
 
 
-def time_cpu_sample(cfg, n_iters):
-    """(seconds, entries, shape, kind, phases) of one LM direction on the sample."""
-    from oracle import ref_driver as RD
-    truth, init, cams, shape = cpu_sample(cfg)
-    R = RD.import_reference()
-    if R is not None:
-        R["parallel"].set_num_threads(1)   # GIL-bound render is slower with more (SURVEY 6)
-        rs, rc = RD.ref_scene(R, truth), [RD.ref_camera(R, c) for c in cams]
-        gts = [R["rasterizer"].render(rs, c).image.rgb for c in rc]
-        si = RD.ref_scene(R, init)
-        ph = {}
+class CpuArm:
+    """The reference's own numpy code (baseline/_ref) driven through Alg. 1 /
+    Eq. 7 on the host: one process per host core (oracle/ref_parallel.py; the
+    reference's render is GIL-bound, so processes, not threads), one view per
+    core of a bounded sample; the oracle port (1 core) only when the reference
+    package is absent.  The sample's inputs are prepared once; `run()` times
+    one LM direction."""
+
+    def __init__(self, cfg):
+        from oracle import ref_driver as RD
+        self.cfg = cfg
+        self.R = RD.import_reference()
+        self.cores = (os.cpu_count() or 1) if self.R is not None else 1
+        truth, init, cams, self.shape = cpu_sample(cfg, max(2, self.cores) if self.R is not None else 2)
+        self.n_views = len(cams)
+        if self.R is not None:
+            self.kind = "reference"
+            self.R["parallel"].set_num_threads(1)
+            rc = [RD.ref_camera(self.R, c) for c in cams]
+            self.gts = [self.R["rasterizer"].render(RD.ref_scene(self.R, truth), c).image.rgb for c in rc]
+            self.scene, self.cams = RD.ref_scene(self.R, init), rc
+        else:
+            import oracle as O
+            self.kind = "port"
+
+            def osc(h):
+                return O.OScene(h.positions, h.rotations, h.log_scales, h.opacity_logits, h.sh_coeffs,
+                                h.sh_degree, h.background)
+            self.cams = [O.OCamera(c.rotation, c.translation, c.fx, c.fy, c.cx, c.cy, c.width, c.height)
+                         for c in cams]
+            self.gts = [O.rasterize(osc(truth), c)["image"] for c in self.cams]
+            self.scene = osc(init)
+
+    def run(self):
+        """(seconds, entries, phases) of one LM direction on the sample."""
+        iters = self.cfg["iters"]
         t0 = time.perf_counter()
-        _, E, _ = RD.lm_direction(R, si, rc, gts, n_batches=1, lam=1e-4, n_iters=n_iters, phases=ph)
-        return time.perf_counter() - t0, E, shape, "reference", ph
-    import oracle as O
+        if self.kind == "reference":
+            from oracle import ref_parallel as RP
+            ph = {}
+            _, E, _ = RP.lm_direction(self.R, self.scene, self.cams, self.gts, n_batches=1, lam=1e-4,
+                                      n_iters=iters, workers=self.cores, phases=ph)
+            return time.perf_counter() - t0, E, ph
+        import oracle as O
+        O.lm_direction(self.scene, self.cams, self.gts, n_batches=1, lam=1e-4, n_iters=iters)
+        dt = time.perf_counter() - t0
+        E = sum(O.rasterize(self.scene, c)["pixel"].size for c in self.cams)
+        return dt, E, {}
 
-    def osc(h):
-        return O.OScene(h.positions, h.rotations, h.log_scales, h.opacity_logits, h.sh_coeffs, h.sh_degree,
-                        h.background)
-    ocams = [O.OCamera(c.rotation, c.translation, c.fx, c.fy, c.cx, c.cy, c.width, c.height) for c in cams]
-    gts = [O.rasterize(osc(truth), c)["image"] for c in ocams]
-    s = osc(init)
-    t0 = time.perf_counter()
-    O.lm_direction(s, ocams, gts, n_batches=1, lam=1e-4, n_iters=n_iters)
-    dt = time.perf_counter() - t0
-    E = sum(O.rasterize(s, c)["pixel"].size for c in ocams)
-    return dt, E, shape, "port", {}
-
-
-def _sample_text(kind, shape, E, dt, iters, ph):
-    who = "reference splatlm (baseline/_ref) + Alg. 1/Eq. 7 driver" if kind == "reference" else "oracle port"
-    phs = ", ".join(f"{k} {v:.2f}s" for k, v in ph.items())
-    return (f"{who}: LM step on {shape[0]} Gaussians, 2 views @ {shape[1]}x{shape[2]}, {E} entries, "
-            f"{iters} PCG iters = {dt:.2f} s ({1e9 * dt / max(E, 1):.0f} ns/entry; {phs})")
+    def text(self, E, dt, ph):
+        who = ("reference splatlm (baseline/_ref) + Alg. 1/Eq. 7 driver, view-parallel over "
+               f"{self.cores} processes" if self.kind == "reference" else "oracle port, 1 core")
+        phs = ", ".join(f"{k} {v:.2f}s" for k, v in ph.items())
+        return (f"{who}: LM step on {self.shape[0]} Gaussians, {self.n_views} views @ {self.shape[1]}x"
+                f"{self.shape[2]}, {E} entries, {self.cfg['iters']} PCG iters = {dt:.2f} s "
+                f"({1e9 * dt / max(E, 1):.0f} ns/entry wall; {phs})")
 
 
 def cpu_baseline(cfg, rep, args):
-    dt, E, shape, kind, ph = time_cpu_sample(cfg, cfg["iters"])
+    arm = CpuArm(cfg)
+    dt, E, ph = arm.run()
     E_full = sum(rep.entries) * 1.0
     proj_ms = dt * 1e3 * (E_full / max(E, 1)) if rep.entries else None
-    return {"value": round(proj_ms, 1) if proj_ms else None, "unit": "ms", "cores": 1, "kind": kind,
-            "sample": _sample_text(kind, shape, E, dt, cfg["iters"], ph)
+    return {"value": round(proj_ms, 1) if proj_ms else None, "unit": "ms", "cores": arm.cores, "kind": arm.kind,
+            "sample": arm.text(E, dt, ph)
             + f"; projected linearly in cache entries to the workload's {int(E_full)} entries/step",
             "cpu": _cpu_name(), "os_cpu_count": os.cpu_count()}
 
@@ -388,14 +412,15 @@ def run_reference(args, cfg):
     if rank != 0:
         return None
     os.environ.setdefault("OMP_NUM_THREADS", "1")
+    arm = CpuArm(cfg)
     times = []
     for i in range(args.warmup + args.steps):
-        dt, E, shape, kind, ph = time_cpu_sample(cfg, cfg["iters"])
+        dt, E, ph = arm.run()
         if i >= args.warmup:
             times.append(dt)
     dt = statistics.median(times)
     # entries of the full workload: K (entries per pixel, from the sample) x pixels
-    k = E / (2 * shape[1] * shape[2])
+    k = E / (arm.n_views * arm.shape[1] * arm.shape[2])
     E_full = k * cfg["views"] * cfg["W"] * cfg["H"]
     ms = dt * 1e3 * E_full / E
     line = {"metric": METRIC, "value": round(ms, 1), "unit": "ms", "n_gpus": 0, "steps": args.steps,
@@ -403,8 +428,8 @@ def run_reference(args, cfg):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": {"workload": f"{args.config.upper()} (same generator), projected from a bounded sample",
                        "entries_per_pixel": round(k, 2)},
-            "cpu_baseline": {"value": round(ms, 1), "unit": "ms", "cores": 1, "kind": kind,
-                             "sample": _sample_text(kind, shape, E, dt, cfg["iters"], ph)
+            "cpu_baseline": {"value": round(ms, 1), "unit": "ms", "cores": arm.cores, "kind": arm.kind,
+                             "sample": arm.text(E, dt, ph)
                              + f"; median of {args.steps}, x{E_full / E:.0f} entries to the workload"},
             "e2e": {"value": round(ms, 1), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
