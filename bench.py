@@ -45,8 +45,10 @@ CONFIGS = {
     "c3": dict(G=1_000_000, views=200, W=1024, H=1024, subsets=8, iters=8, gen="footprint", degree=3),
     # BASELINE.json configs[3] (Mip-NeRF360 scale; quoted for 8 GPUs, one subset per GPU)
     "c4": dict(G=3_000_000, views=200, W=1552, H=1032, subsets=8, iters=8, gen="footprint", degree=3),
-    # BASELINE.json configs[4] (ScanNet++ scale; 16 subsets, 2 per GPU on 8 GPUs)
-    "c5": dict(G=2_000_000, views=400, W=1616, H=1080, subsets=16, iters=8, gen="footprint", degree=3),
+    # BASELINE.json configs[4] (ScanNet++ scale; 16 subsets, 2 per GPU on 8 GPUs), the gradient cache
+    # sized near the 180 GB of one GPU: K ~ 86 entries per pixel
+    "c5": dict(G=2_000_000, views=400, W=1616, H=1080, subsets=16, iters=8, gen="footprint", degree=3,
+               k_target=71.0),
 }
 
 
@@ -118,7 +120,7 @@ def make_workload(cfg, device, only=None):
         init = S.perturb(truth, 1, cfg.get("perturb", 0.1))
         cams = S.make_camera_ring(V, W, H)
     else:
-        truth = S.make_footprint_scene(0, G, W, H, deg, k_target=32.0)
+        truth = S.make_footprint_scene(0, G, W, H, deg, k_target=cfg.get("k_target", 32.0))
         init = S.perturb(truth, 1, cfg.get("perturb", 0.02))
         cams = S.make_camera_ring(V, W, H)
     tscene = truth.to_device(device)
@@ -178,8 +180,12 @@ def run_ours(args, cfg):
             e.record(stream)
             self.ev[-1][1] = e
 
+    offload = None if args.offload in (None, "none", "0") else (args.offload if args.offload == "auto"
+                                                                  else float(args.offload))
+
     def step(timer=None):
-        return lm_direction(scene, cams, gts, sched, lam, iters, None, loss, rank, world, product_timer=timer)
+        return lm_direction(scene, cams, gts, sched, lam, iters, None, loss, rank, world, product_timer=timer,
+                            offload=offload)
 
     def barrier():
         torch.cuda.synchronize()
@@ -282,6 +288,8 @@ def run_ours(args, cfg):
                    "generator": cfg["gen"], "entries_per_subset": E_sub,
                    "entries_per_pixel": round(E_sub / N_sub, 2) if N_sub else None,
                    "pcg": rep.pcg[:2], "lm_step": lm_info,
+                   "offload": {"mode": args.offload, "host_record_bytes_per_step": 21 * sum(rep.offloaded_entries),
+                               "peak_hbm_gb": round(torch.cuda.max_memory_allocated(dev) / 1e9, 1)},
                    "phases_ms_per_step": phases,
                    "l2": "inputs larger than L2 (cache >> 126 MB)",
                    "parallelism": f"subsets round-robin over {world} rank(s), one NCCL all_reduce"},
@@ -322,7 +330,7 @@ def cpu_sample(cfg, n_views=2):
         truth = S.make_synthetic_scene(0, Gs, cfg["degree"])
         init = S.perturb(truth, 1, cfg.get("perturb", 0.1))
     else:
-        truth = S.make_footprint_scene(0, Gs, W, H, cfg["degree"], k_target=32.0)
+        truth = S.make_footprint_scene(0, Gs, W, H, cfg["degree"], k_target=cfg.get("k_target", 32.0))
         init = S.perturb(truth, 1, cfg.get("perturb", 0.02))
     cams = S.make_camera_ring(n_views, W, H)
     return truth, init, cams, (Gs, W, H)
@@ -444,6 +452,9 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--offload", default=None,
+                    help="cache offload to host memory: a fraction of the records, or 'auto' (only what "
+                         "does not fit in HBM); default none")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

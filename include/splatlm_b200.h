@@ -116,6 +116,14 @@ typedef struct {
   const int* view_tile_base;
   int n_views;
   int n_tiles;
+  /* FILL: cache offload ("CPU offloading of cache parts"):
+   * when rec4_h != NULL, entries >= e_split are written to host-pinned,
+   * device-mapped streams indexed from e_hbase (a multiple of 16, <= e_split):
+   * rec4_h[e - e_hbase] etc.; the device streams hold entries [0, e_split) */
+  slm_f4* rec4_h;
+  float* rec_d2_h;
+  uint8_t* rec_pix_h;
+  long long e_split, e_hbase;
 } SlmRasterArgs;
 
 /* residual weights (residuals.py:249-296) */
@@ -170,6 +178,12 @@ typedef struct {
   int* tile_counter;         /* streaming kernels: 1 int of device scratch for
                                 dynamic tile scheduling (reset by the launch);
                                 NULL: static round-robin tiles */
+  /* offloaded record tail (see SlmRasterArgs): chunks starting at an entry
+   * >= e_split (a chunk boundary) are streamed from the host-mapped copies */
+  const slm_f4* rec4_h;
+  const float* d2_h;
+  const uint8_t* pix_h;
+  long long e_split, e_hbase;
 } SlmTileArgs;
 
 /* per-pair forward chain (applyJ) */

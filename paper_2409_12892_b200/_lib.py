@@ -45,7 +45,8 @@ class SlmRasterArgs(C.Structure):
                 ("px_count", c_vp), ("rgb", c_vp), ("t_final", c_vp), ("inst_mask", c_vp),
                 ("inst_start", c_vp), ("rec4", c_vp), ("rec_d2", c_vp), ("rec_pix", c_vp),
                 ("pix_off", c_vp), ("view_entry_base", c_ll), ("trav_gid", c_vp), ("trav_alpha", c_vp),
-                ("trav_T", c_vp), ("views", c_vp), ("view_tile_base", c_vp), ("n_views", c_i), ("n_tiles", c_i)]
+                ("trav_T", c_vp), ("views", c_vp), ("view_tile_base", c_vp), ("n_views", c_i), ("n_tiles", c_i),
+                ("rec4_h", c_vp), ("rec_d2_h", c_vp), ("rec_pix_h", c_vp), ("e_split", c_ll), ("e_hbase", c_ll)]
 
 
 class SlmResidArgs(C.Structure):
@@ -63,7 +64,8 @@ class SlmTileArgs(C.Structure):
                 ("run_start", c_vp), ("run_fn", c_vp), ("run_q", c_vp), ("run_tile", c_vp), ("run_static", c_vp), ("pm", c_vp),
                 ("geo", c_vp), ("ptab", c_vp),
                 ("rec4", c_vp), ("d2", c_vp), ("pix", c_vp),
-                ("gradr", c_vp), ("u", c_vp), ("u_out", c_vp), ("out", c_vp), ("out1", c_vp), ("tile_counter", c_vp)]
+                ("gradr", c_vp), ("u", c_vp), ("u_out", c_vp), ("out", c_vp), ("out1", c_vp), ("tile_counter", c_vp),
+                ("rec4_h", c_vp), ("d2_h", c_vp), ("pix_h", c_vp), ("e_split", c_ll), ("e_hbase", c_ll)]
 
 
 class SlmFwdArgs(C.Structure):

@@ -570,12 +570,21 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
           if (A.rec4) {
             const unsigned m = s_mask[k * RW + warp];
             const double iom = 1.0 / (1.0 - a);  // stored values are fp32: one fp64 reciprocal suffices
-            const long long dest = s_start[k] + s_pre[k * RW + warp] + __popc(m & lanes_below);
-            A.rec4[dest] = make_float4(a < aclamp ? (float)a : 0.0f, (float)wgt,
-                                       (float)(s_c0[k] * T - (tot0 - C0) * iom),
-                                       (float)(s_c1[k] * T - (tot1 - C1) * iom));
-            A.rec_d2[dest] = (float)(s_c2[k] * T - (tot2 - C2) * iom);
-            A.rec_pix[dest] = (uint8_t)threadIdx.x;
+            long long dest = s_start[k] + s_pre[k * RW + warp] + __popc(m & lanes_below);
+            slm_f4* r4 = A.rec4;
+            float* rd2 = A.rec_d2;
+            uint8_t* rpx = A.rec_pix;
+            if (A.rec4_h && dest >= A.e_split) {  // offloaded tail (host-mapped streams)
+              r4 = A.rec4_h;
+              rd2 = A.rec_d2_h;
+              rpx = A.rec_pix_h;
+              dest -= A.e_hbase;
+            }
+            r4[dest] = make_float4(a < aclamp ? (float)a : 0.0f, (float)wgt,
+                                   (float)(s_c0[k] * T - (tot0 - C0) * iom),
+                                   (float)(s_c1[k] * T - (tot1 - C1) * iom));
+            rd2[dest] = (float)(s_c2[k] * T - (tot2 - C2) * iom);
+            rpx[dest] = (uint8_t)threadIdx.x;
           }
           if (A.trav_gid) {
             const long long le = e - A.view_entry_base;

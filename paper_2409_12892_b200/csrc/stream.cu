@@ -406,9 +406,13 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
               const unsigned bq = (MODE & MODE_DIAG) ? br : 0u;
               mbar_arrive_tx(&full[s], b4 + bd + bx + bp + br + ST_PERM + bq);
               if (MODE & MODE_DIAG) bulk_g2s(st + L.pdy, A.run_q + aq, bq, &full[s], pol);
-              bulk_g2s(st, A.rec4 + m.e0, b4, &full[s], pol);
-              bulk_g2s(st + L.d2, A.d2 + a4, bd, &full[s], pol);
-              bulk_g2s(st + L.pix, A.pix + a16, bx, &full[s], pol);
+              // record streams: device, or the host-mapped offloaded tail
+              // (the split is a chunk boundary and e_hbase <= a16 <= a4)
+              const bool off = A.rec4_h && m.e0 >= A.e_split;
+              const long long hb = off ? A.e_hbase : 0;
+              bulk_g2s(st, (off ? A.rec4_h : A.rec4) + (m.e0 - hb), b4, &full[s], pol);
+              bulk_g2s(st + L.d2, (off ? A.d2_h : A.d2) + (a4 - hb), bd, &full[s], pol);
+              bulk_g2s(st + L.pix, (off ? A.pix_h : A.pix) + (a16 - hb), bx, &full[s], pol);
               bulk_g2s(st + L.pst, A.run_static + (size_t)m.k0 * 8, bp, &full[s], pol);
               bulk_g2s(st + L.rf, A.run_fn + aq, br, &full[s], pol);
               bulk_g2s(st + OFF_PERM, A.chunk_perm + (size_t)(w0 + i) * CR, ST_PERM, &full[s], pol);

@@ -280,10 +280,18 @@ class CacheSet:
         loss: LossConfig.
         weights: precomputed per-view (grad_r_sq4, color_grad4) instead of gts.
         timer: optional PhaseTimer.
+        offload: cache offload ("CPU offloading of cache
+            parts"): None / 0 keeps every record in HBM; a fraction f places
+            the last ~f of the record streams (from a chunk boundary) in
+            host-pinned, device-mapped memory that FILL writes and the
+            streaming kernels' TMA reads over the host link; "auto" offloads
+            only what does not fit in the device's free memory next to the
+            product scratch.
     """
 
     def __init__(self, scene: GaussianScene, cameras: list[Camera], gts=None, config=None, loss=LossConfig(),
-                 residual_exports: bool = False, weights=None, timer=None, keep_source_index: bool = False):
+                 residual_exports: bool = False, weights=None, timer=None, keep_source_index: bool = False,
+                 offload=None):
         from .rasterizer import DEFAULT_CONFIG
         self.scene = scene
         self.config = config if config is not None else DEFAULT_CONFIG
@@ -519,12 +527,21 @@ class CacheSet:
         # product kernels stay in bounds
         # every entry is written by the FILL pass; the +16 tail slots are only
         # over-read by the 16-byte-granular copies and never used
-        self.rec4 = torch.empty((E + 16) * 4, dtype=f32, device=dev)
-        self.rec_d2 = torch.empty(E + 16, dtype=f32, device=dev)
-        self.rec_pix = torch.empty(E + 16, dtype=torch.uint8, device=dev)
+        split = self._offload_split(offload)
+        self.e_split, self.e_hbase = split, split & ~15
+        self.rec4 = torch.empty((split + 16) * 4, dtype=f32, device=dev)
+        self.rec_d2 = torch.empty(split + 16, dtype=f32, device=dev)
+        self.rec_pix = torch.empty(split + 16, dtype=torch.uint8, device=dev)
+        self.rec4_h = self.rec_d2_h = self.rec_pix_h = None
+        if split < E:
+            nh = E - self.e_hbase + 16
+            self.rec4_h = torch.empty(nh * 4, dtype=f32, pin_memory=True)
+            self.rec_d2_h = torch.empty(nh, dtype=f32, pin_memory=True)
+            self.rec_pix_h = torch.empty(nh, dtype=torch.uint8, pin_memory=True)
         a = batched_args()
         a.inst_start = ptr(inst_start)
         a.rec4, a.rec_d2, a.rec_pix = ptr(self.rec4), ptr(self.rec_d2), ptr(self.rec_pix)
+        self._offload_args(a, "rec_d2_h", "rec_pix_h")
         call("slm_raster_fill", _lib.byref(a), stream_ptr())
         T.tick("raster_fill")
         del inst_mask, inst_start, inst_gid, ranges, splats_all
@@ -543,11 +560,67 @@ class CacheSet:
         call("slm_run_static", _lib.byref(self._tile_args()), R, ptr(self.run_slot), ptr(self.run_static),
              stream_ptr())
 
+    # ------------------------------------------------------------------
+    # cache offload
+    # ------------------------------------------------------------------
+    @property
+    def offloaded_entries(self) -> int:
+        return self.E - self.e_split if self.rec4_h is not None else 0
+
+    def _offload_split(self, offload) -> int:
+        """First entry of the host-resident tail: a chunk boundary (a chunk's
+        records are streamed from one place), E when nothing is offloaded."""
+        E = self.E
+        if not offload or E == 0 or self.n_chunks == 0:
+            return E
+        if offload == "auto":
+            free, _ = torch.cuda.mem_get_info(self.device)
+            st = torch.cuda.memory_stats(self.device)
+            free += st.get("reserved_bytes.all.current", 0) - st.get("allocated_bytes.all.current", 0)
+            # product / diag / PCG scratch allocated after FILL, plus 2 GB
+            scratch = (16 * self.N + 100 * self.R + 250 * self.n_pairs + 700 * self.G * 1 + (2 << 30))
+            cap = (free - scratch) // 21
+            if E <= cap:
+                return E
+            target = max(0, int(cap))
+        else:
+            f = float(offload)
+            if not 0.0 < f <= 1.0:
+                raise ValueError("offload must be None, 'auto' or a fraction in (0, 1]")
+            target = int(E * (1.0 - f))
+        starts = self.run_start[self.chunk_run[:self.n_chunks].long()]
+        k = int(torch.searchsorted(starts, torch.tensor([target], dtype=starts.dtype, device=starts.device)).item())
+        return int(starts[k].item()) if k < self.n_chunks else E
+
+    def _offload_args(self, a, d2_name: str, pix_name: str):
+        """Fill the offload fields of a raster / tile argument struct."""
+        if self.rec4_h is None:
+            return
+        a.rec4_h = ptr(self.rec4_h)
+        setattr(a, d2_name, ptr(self.rec_d2_h))
+        setattr(a, pix_name, ptr(self.rec_pix_h))
+        a.e_split, a.e_hbase = self.e_split, self.e_hbase
+
+    def _records(self, e0: int, e1: int):
+        """Host copies (rec4 [n, 4], d2 [n], pix [n]) of entries [e0, e1),
+        from the device streams and the offloaded tail."""
+        parts = []
+        s = min(e1, self.e_split)
+        if e0 < s:
+            parts.append((self.rec4[4 * e0:4 * s].view(-1, 4).cpu(), self.rec_d2[e0:s].cpu(), self.rec_pix[e0:s].cpu()))
+        if self.rec4_h is not None and e1 > self.e_split:
+            h0, h1 = max(e0, self.e_split) - self.e_hbase, e1 - self.e_hbase
+            parts.append((self.rec4_h[4 * h0:4 * h1].view(-1, 4), self.rec_d2_h[h0:h1], self.rec_pix_h[h0:h1]))
+        if not parts:
+            return np.zeros((0, 4), np.float32), np.zeros(0, np.float32), np.zeros(0, np.uint8)
+        return tuple(torch.cat([p[i] for p in parts]).numpy() for i in range(3))
+
     def _init_empty(self, gts, weights, loss, residual_exports):
         """G = 0: background images, no entries; b and M are
         empty and every product is the zero map."""
         dev, N = self.device, self.N
         self.E = self.R = self.n_pairs = self.n_chunks = self.n_inst_total = 0
+        self.rec4_h, self.e_split, self.e_hbase = None, 0, 0
         bg = torch.tensor(self.scene.background, dtype=torch.float64, device=dev)
         self.rgb_all = bg.repeat(N)
         self.t_final_all = torch.ones(N, dtype=torch.float64, device=dev)
@@ -579,6 +652,11 @@ class CacheSet:
     def nbytes(self) -> int:
         """Bytes of the record stream (budget accounting, ref: jacobian.py:76-80)."""
         return 21 * self.E + 48 * self.R + 36 * self.n_chunks
+
+    @property
+    def host_nbytes(self) -> int:
+        """Bytes of the offloaded (host-resident) record tail."""
+        return 21 * self.offloaded_entries
 
     def pair_forward(self, p: torch.Tensor, gaussian_major: bool = False, p_gm: torch.Tensor | None = None):
         """Forward chain m = dy/dx p per pair into self.pm (48 B per pair); the
@@ -614,6 +692,7 @@ class CacheSet:
         a.geo = ptr(self.pair_geo)
         a.rec4, a.d2 = ptr(self.rec4), ptr(self.rec_d2)
         a.pix = ptr(self.rec_pix)
+        self._offload_args(a, "d2_h", "pix_h")
         a.tile_counter = ptr(self.tile_counter)
         return a
 
@@ -743,15 +822,17 @@ class CacheSet:
         scan_i64(g_cnt, g_off)
         out = {k: _empty(Ev, i64, dev) for k in ("pos_pix", "pixel_ids", "gaussian_ids", "g_pixel_ids",
                                                   "g_gaussian_ids", "g_source_index")}
+        r4, d2, pxb = self._records(e0, e1)
+        pix_v = torch.from_numpy(np.concatenate([pxb, np.zeros(16, np.uint8)])).to(dev)  # the view's pixel bytes
+        pix_ptr = C.c_void_p(pix_v.data_ptr() - e0)   # the kernel indexes entries globally
         call("slm_export_view", ptr(self.tile_run_off), t0, t1 - t0, (cam.width + TILE - 1) // TILE, cam.width,
              ptr(self.run_start), ptr(self.run_q), ptr(self.run_tile), ptr(self.pair_gid), ptr(self.pair_vm),
-             ptr(self.pair_run_off), ptr(self.pair_runs), self.n_pairs, v, ptr(self.rec_pix), ptr(px_off),
+             ptr(self.pair_run_off), ptr(self.pair_runs), self.n_pairs, v, pix_ptr, ptr(px_off),
              ptr(g_off), e0, ptr(out["pos_pix"]), ptr(out["pixel_ids"]), ptr(out["gaussian_ids"]),
              ptr(out["g_pixel_ids"]), ptr(out["g_gaussian_ids"]), ptr(out["g_source_index"]), stream_ptr())
         h = {k: t[:Ev].cpu().numpy() for k, t in out.items()}
         pos, src = h["pos_pix"], h["g_source_index"]
-        r4 = self.rec4[4 * e0:4 * e1].view(-1, 4).cpu().numpy().astype(np.float64)
-        d2 = self.rec_d2[e0:e1].cpu().numpy().astype(np.float64)
+        r4, d2 = r4.astype(np.float64), d2.astype(np.float64)
         ae, at = np.empty(Ev), np.empty(Ev)
         dcda = np.empty((Ev, 3))
         ae[pos], at[pos] = r4[:, 0], r4[:, 1]

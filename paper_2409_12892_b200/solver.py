@@ -297,7 +297,7 @@ class StepReport:
 def lm_direction(scene, cameras, gts, schedule: BatchSchedule = BatchSchedule(), lambda_reg: float = 1e-4,
                  n_iters: int = 8, config=None, loss: LossConfig = LossConfig(), rank: int = 0,
                  world_size: int = 1, product_timer=None, keep_caches: bool = False,
-                 phase_timer=None) -> StepReport:
+                 phase_timer=None, offload=None) -> StepReport:
     """One LM update direction: per subset cache build, b, M, PCG, Eq. 7
     combine; subsets are sharded round-robin over ranks.
 
@@ -308,7 +308,7 @@ def lm_direction(scene, cameras, gts, schedule: BatchSchedule = BatchSchedule(),
     T.tick("start")
     comb = Combiner(n, scene.device)
     ws = PCGWorkspace(n, scene.device, scene.num_gaussians, scene.params_per_gaussian)
-    entries, pcg_stats = [], []
+    entries, pcg_stats, offloaded = [], [], []
     caches = []
     shards = list(schedule.shard(len(cameras), rank, world_size))
     fetch = _GtPrefetch(gts, scene.device, shards)
@@ -318,7 +318,8 @@ def lm_direction(scene, cameras, gts, schedule: BatchSchedule = BatchSchedule(),
         gts_sub, buf = fetch.take()
         if k + 1 < len(shards):
             fetch.start(k + 1, shards[k + 1][1])
-        cs = CacheSet(scene, [cameras[i] for i in views], gts_sub, config, loss, timer=phase_timer)
+        cs = CacheSet(scene, [cameras[i] for i in views], gts_sub, config, loss, timer=phase_timer, offload=offload)
+        offloaded.append(cs.offloaded_entries)
         T.tick("cache_tables")
         fetch.release(buf)  # the images are only read by the build's residual pass
         del gts_sub
@@ -351,6 +352,7 @@ def lm_direction(scene, cameras, gts, schedule: BatchSchedule = BatchSchedule(),
     rep = StepReport(comb.finalize(), comb.energy, comb.accepted, entries, pcg_stats, [],
                      (comb.den[10 * G:11 * G] > 0).sum() if G else None, G)
     T.tick("finalize")
+    rep.offloaded_entries = offloaded
     if phase_timer is not None:
         rep.phases = phase_timer.summary()
     rep.caches = caches

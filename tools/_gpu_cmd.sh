@@ -1,1 +1,2 @@
-timeout 1500 python -m pytest tests -m gpu -x -q --durations=8 2>&1 | tail -25 > gpurun_out/pytest_gpu.log
+free -g > gpurun_out/host_mem.txt
+timeout 900 python -m pytest tests/test_offload.py -m gpu -x -q 2>&1 | tail -15 > gpurun_out/pytest_offload.log
