@@ -1,2 +1,2 @@
-free -g > gpurun_out/host_mem.txt
-timeout 900 python -m pytest tests/test_offload.py -m gpu -x -q 2>&1 | tail -15 > gpurun_out/pytest_offload.log
+timeout 1200 python bench.py --config c5 --steps 1 --warmup 3 --no-cpu > gpurun_out/bench_c5.log 2>&1
+timeout 1200 python bench.py --config c5 --steps 1 --warmup 3 --no-cpu --offload 0.25 > gpurun_out/bench_c5_off.log 2>&1
