@@ -1,2 +1,1 @@
-timeout 1200 python bench.py --config c5 --steps 1 --warmup 3 --no-cpu > gpurun_out/bench_c5.log 2>&1
-timeout 1200 python bench.py --config c5 --steps 1 --warmup 3 --no-cpu --offload 0.25 > gpurun_out/bench_c5_off.log 2>&1
+PARITY_OUT_C2=gpurun_out/parity_c2.json timeout 1200 python -m pytest tests/test_c2_subset.py -m gpu -q --durations=5 2>&1 | tail -25 > gpurun_out/pytest_c2.log
