@@ -139,7 +139,6 @@ typedef struct {
   const double* taps;
   const double* cw_y;
   const double* cw_x;
-  double* tmp;      /* unused (kept for ABI stability; the SSIM passes stage in shared memory) */
   slm_f4* gradr;
   slm_f4* cgrad;
   double* energy_part;

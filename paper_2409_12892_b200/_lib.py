@@ -52,7 +52,7 @@ class SlmRasterArgs(C.Structure):
 class SlmResidArgs(C.Structure):
     _fields_ = [("img", c_vp), ("gt", c_vp), ("gt_f32", c_i), ("W", c_i), ("H", c_i),
                 ("lambda1", c_d), ("lambda2", c_d), ("eps_den", c_d), ("ssim_c1", c_d), ("ssim_c2", c_d),
-                ("mode", c_i), ("win", c_i), ("taps", c_vp), ("cw_y", c_vp), ("cw_x", c_vp), ("tmp", c_vp),
+                ("mode", c_i), ("win", c_i), ("taps", c_vp), ("cw_y", c_vp), ("cw_x", c_vp),
                 ("gradr", c_vp), ("cgrad", c_vp), ("energy_part", c_vp),
                 ("o_gradr", c_vp), ("o_cgrad", c_vp), ("o_rabs", c_vp), ("o_rssim", c_vp),
                 ("o_drabs", c_vp), ("o_drssim", c_vp)]

@@ -6,21 +6,25 @@
 // tile by tile with u kept in shared memory; the cache is read from HBM once
 // per product (the J^T pass re-reads the tile's entries from L2).
 //
-// Structure (one CTA per SM slot, looping over tiles):
-//   producer warp : for every chunk (<= 64 runs, <= 896 entries, cut at run
-//                   boundaries; table built once per cache) of every tile and
-//                   pass, wait for a free ring stage and issue TMA bulk copies
-//                   (cp.async.bulk) of the chunk's entries (5 x f32 + u8), its
-//                   runs' 64-byte parameter records and run starts; completion
-//                   is signalled on the stage's full mbarrier.
-//   8 consumer warps: wait full, take the chunk's runs round-robin with lanes
-//                   over each run's entries (all reads from shared memory),
-//                   arrive on the stage's empty mbarrier.  A named barrier among
-//                   the consumers only separates pass J, the per-tile u
-//                   reduction and pass J^T.
-//   pass J  : per-warp shared pixel accumulators (a run never repeats a pixel),
-//             summed in fixed warp order -> deterministic, no atomics.
-//   pass J^T: 9 partials per run, 8-lane reduce-scatter, one 32-byte store per run.
+// Structure (2 persistent CTAs per SM, tiles claimed from a global counter):
+//   producer warp : for every chunk (<= 64 runs whose packed image fits one
+//                   25 KB ring stage, cut at run boundaries; table built once
+//                   per cache) of every tile and pass, wait for a free stage
+//                   and issue TMA bulk copies (cp.async.bulk) of the chunk's
+//                   records (float4 + float + u8 = 21 B per entry), its runs'
+//                   32-byte static records and (offset | length) words and the
+//                   J^T schedule, plus cp.async gathers of the runs' 48-byte
+//                   pair forward chain m (J pass); completion is signalled on
+//                   the stage's full mbarrier.
+//   8 consumer warps: wait full, work from shared memory only, arrive on the
+//                   stage's empty mbarrier.  A named barrier among the
+//                   consumers only separates pass J, the per-tile u reduction
+//                   and pass J^T.
+//   pass J  : one run per warp, lanes over its entries, per-warp shared pixel
+//             accumulators (a run never repeats a pixel), summed in fixed warp
+//             order -> deterministic, no atomics.
+//   pass J^T: 8-lane groups on the chunk's length-sorted schedule, 9 partials
+//             per run, 8-lane reduce-scatter, one 32-byte store per run.
 #include "chain.cuh"
 
 #define NW 8

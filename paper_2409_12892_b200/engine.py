@@ -253,7 +253,7 @@ def residual_pass(frame: ViewFrame, gt: torch.Tensor, loss: LossConfig, gradr: t
     a.ssim_c1, a.ssim_c2 = 0.01 ** 2, 0.03 ** 2
     a.mode = 0 if loss.mode == "l1ssim" else 1
     a.win = int(loss.window)
-    a.taps, a.cw_y, a.cw_x, a.tmp = ptr(taps_t), ptr(cwy_t), ptr(cwx_t), None
+    a.taps, a.cw_y, a.cw_x = ptr(taps_t), ptr(cwy_t), ptr(cwx_t)
     a.gradr = off(gradr, frame.pix_base * 4)
     a.cgrad = off(cgrad, frame.pix_base * 4)
     a.energy_part = ptr(part)
@@ -290,8 +290,7 @@ class CacheSet:
     """
 
     def __init__(self, scene: GaussianScene, cameras: list[Camera], gts=None, config=None, loss=LossConfig(),
-                 residual_exports: bool = False, weights=None, timer=None, keep_source_index: bool = False,
-                 offload=None):
+                 residual_exports: bool = False, weights=None, timer=None, offload=None):
         from .rasterizer import DEFAULT_CONFIG
         self.scene = scene
         self.config = config if config is not None else DEFAULT_CONFIG

@@ -68,9 +68,12 @@ class GradientCache:
 
 
 def build_cache(scene: GaussianScene, camera, bundle: ResidualBundle | list, config: RenderConfig = DEFAULT_CONFIG,
-                render_result=None, view_id: int = 0, keep_source_index: bool = True):
+                render_result=None, view_id: int = 0):
     """b = -J^T F and the (pixel-sorted) cache; `camera` may be a list of views
-    with a matching list of bundles (one Eq. 7 batch)."""
+    with a matching list of bundles (one Eq. 7 batch).  `render_result` is
+    accepted for signature compatibility (ref: jacobian.py:360-363) and not
+    needed: the device build re-runs the fp64 rasteriser (COUNT + FILL), which
+    is cheaper than shipping a host Traversals back to the GPU."""
     cams = camera if isinstance(camera, (list, tuple)) else [camera]
     bundles = bundle if isinstance(bundle, (list, tuple)) else [bundle]
     if len(cams) != len(bundles):
@@ -78,8 +81,7 @@ def build_cache(scene: GaussianScene, camera, bundle: ResidualBundle | list, con
     for c, b in zip(cams, bundles):
         if (b.height, b.width) != (c.height, c.width):
             raise ValueError("residual bundle does not match the camera resolution")
-    cs = CacheSet(scene, list(cams), None, config, LossConfig(), keep_source_index=keep_source_index,
-                  weights=[(b.gradr4, b.cgrad4) for b in bundles])
+    cs = CacheSet(scene, list(cams), None, config, LossConfig(), weights=[(b.gradr4, b.cgrad4) for b in bundles])
     b = ParamVector(cs.rhs().clone(), Layout.ATTRIBUTE_MAJOR, scene.num_gaussians, scene.params_per_gaussian)
     return b, GradientCache(cs, CacheOrder.PIXEL_SORTED, view_id)
 
@@ -140,10 +142,7 @@ def dump_cache(cache: GradientCache, path, view: int = 0) -> None:
     ex = cache.export(view)
     gs = cache.order is CacheOrder.GAUSSIAN_SORTED
     if gs:
-        src = ex.get("g_source_index")
-        if src is None:
-            raise ValueError("gaussian-order dump needs a cache built with keep_source_index=True")
-        sel = src
+        sel = ex["g_source_index"]
     else:
         sel = np.arange(ex["pixel_ids"].size)
     n = sel.size

@@ -47,7 +47,7 @@ def oracle_views(prob):
 
 @pytest.fixture(scope="module")
 def cacheset(prob):
-    return CacheSet(prob["scene"], prob["cams"], prob["gts_d"], keep_source_index=True, residual_exports=True)
+    return CacheSet(prob["scene"], prob["cams"], prob["gts_d"], residual_exports=True)
 
 
 def test_sort_x_roundtrip(prob):
