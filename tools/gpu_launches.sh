@@ -1,4 +1,4 @@
-# launch list of one C3 subset (build + rhs + diag + products): per-kernel time and DRAM bytes
+# launch list of one C3 subset (build + rhs + diag + products): per-kernel time, DRAM bytes, instructions; $1 = tag
 mkdir -p gpurun_out/ncu
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum --clock-control none --csv \
-  --log-file gpurun_out/ncu/launches_${1:-cur}.csv python tools/profile_subset.py --config c3 --reps 1 --skip-pcg > /dev/null 2>&1
+  --log-file gpurun_out/ncu/launches_${1:-cur}.csv python tools/profile_subset.py --config c3 --reps 1 --product-only > gpurun_out/ncu/launches_${1:-cur}.log 2>&1
