@@ -11,5 +11,5 @@ timeout 900 python bench.py --config c5 --steps 1 --warmup 3 --no-cpu > gpurun_o
 timeout 900 python bench.py --impl reference --steps 1 --warmup 0 > gpurun_out/bench_ref.log 2>&1
 bash tools/gpu_ncu_product.sh prod_final
 bash tools/gpu_launches.sh final
-bash tools/sanitize.sh > gpurun_out/sanitizer/summary.txt 2>&1
+mkdir -p gpurun_out/sanitizer; bash tools/sanitize.sh > gpurun_out/sanitizer/summary.txt 2>&1
 cat gpurun_out/pytest_gpu.log gpurun_out/smoke.log
