@@ -1,1 +1,1 @@
-bash tools/gpu_launches.sh build_r02
+mkdir -p gpurun_out/sanitizer; bash tools/sanitize.sh > gpurun_out/sanitizer/summary.txt 2>&1
