@@ -164,7 +164,6 @@ typedef struct {
   const float* run_static;   /* [R*8] static run records (slm_run_static) */
   const void* pm;            /* [P*12] per-pair forward chain m (slm_pair_forward); NULL: J^T / diag only */
   const SlmPairGeo* geo;
-  const float* ptab;         /* diag: per-pair coefficient tables (slm_pair_tables) */
   const slm_f4* rec4;
   const float* d2;
   const uint8_t* pix;
@@ -172,8 +171,10 @@ typedef struct {
   const slm_f4* u;           /* applyJT input, per pixel */
   slm_f4* u_out;             /* applyJ output, per pixel */
   float* out;                /* applyJT [R*8] run partials 0-7 (32-byte records) /
-                                diag [R*14] run sums, pair-run-slot order */
+                                diag [R*40] run moments, pair-run-slot order */
   float* out1;               /* applyJT [R] run partial 8, pair-run-slot order */
+  float* rhs8;               /* diag with u = colour gradient: its J^T partials 0-7 [R*8] */
+  float* rhs1;               /* ... and partial 8 [R] */
   int* tile_counter;         /* streaming kernels: 1 int of device scratch for
                                 dynamic tile scheduling (reset by the launch);
                                 NULL: static round-robin tiles */
@@ -208,7 +209,7 @@ typedef struct {
   const SlmCamera* cams;
   const float* pacc;        /* per-run partials in pair-run-slot order (the J^T /
                                diag kernels write run r to its slot in pair_runs):
-                               mode 0 [R*8] partials 0-7, mode 1 [R*14] sums */
+                               mode 0 [R*8] partials 0-7, mode 1 [R*40] moments */
   const float* pacc1;       /* mode 0: [R] partial 8 per run slot */
   const int* pair_run_off;  /* [P+1] pair -> run slots */
   const int* warp_g0;       /* first gaussian of each 32-pair window (slm_warp_bounds) */
@@ -236,7 +237,7 @@ int slm_resid_args_size(void);
 int slm_tile_args_size(void);
 int slm_back_args_size(void);
 int slm_fwd_args_size(void);
-int slm_diag_tab_floats(void);
+int slm_diag_moment_floats(void);
 
 /* ---- projection / rasterisation ------------------------------------------
  * replaces project_scene (rasterizer.py:116-165): fp64 splats of one view,
@@ -346,23 +347,21 @@ int slm_tile_chunks(const int* tile_run_off, int n_tiles, const long long* run_s
                     int* out, uint8_t* chunk_perm, int fill, cudaStream_t s);
 int slm_chunk_perm(const int* chunk_run, long long n_chunks, const long long* run_start, uint8_t* chunk_perm,
                    uint32_t* run_fn, cudaStream_t s);
-/* diag_jtj (jacobian.py:486-512), first half: per-pair coefficient tables
- * (then slm_diag_stream) */
-int slm_pair_tables(const float* xs, long long G, int sh_degree, const int* pair_gid, const uint32_t* pair_vm,
-                    const SlmCamera* cams, int n_pairs, float* tab, const float* gtab, cudaStream_t s);
 /* per-gaussian chain rows, slm_gauss_tab_floats(sh_degree) floats each (16-byte
  * aligned): the view-independent part of the chain (rotation, scales, the
  * quaternion-normalisation derivatives, sigma'), the position and the SH
  * coefficients; once per cache (ref: jacobian.py:159-190, 213-240) */
 int slm_gauss_tab(const float* xs, long long G, int sh_degree, float* gtab, cudaStream_t s);
 int slm_gauss_tab_floats(int sh_degree);
-/* 14 diag sums per run on the streaming kernel, written in pair-run-slot
- * order (a->gradr = grad_r_sq, a->ptab from slm_pair_tables) */
+/* diag_jtj (jacobian.py:486-512), first half: slm_diag_moment_floats() moment
+ * sums per run on the streaming kernel, pair-run-slot order (a->gradr =
+ * grad_r_sq, a->out); with a->u = the colour gradient, the same sweep writes
+ * its J^T partials (the rhs, jacobian.py:411-413) to a->rhs8 / a->rhs1 */
 int slm_diag_stream(const SlmTileArgs* a, cudaStream_t s);
 /* forward chain m = dy/dx p per pair (jacobian.py:434-443), 48 B per pair */
 int slm_pair_forward(const SlmFwdArgs* a, int sh_degree, cudaStream_t s);
 /* backward chain per gaussian, attribute-major out (jacobian.py:314-353):
- * mode 0 from the J^T run partials, mode 1 from the diag run sums */
+ * mode 0 from the J^T run partials, mode 1 from the diag run moments */
 int slm_backward_blocks(long long G);
 int slm_warp_bounds(const int* gpo, long long G, int n_pairs, int* warp_g0, cudaStream_t s);
 int slm_pair_backward(const SlmBackArgs* a, int mode, int sh_degree, cudaStream_t s);

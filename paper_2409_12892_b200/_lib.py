@@ -62,9 +62,9 @@ class SlmTileArgs(C.Structure):
     _fields_ = [("views", c_vp), ("view_tile_base", c_vp), ("n_views", c_i), ("n_tiles", c_i),
                 ("tile_run_off", c_vp), ("tile_chunk_off", c_vp), ("chunk_run", c_vp), ("chunk_perm", c_vp), ("run_slot", c_vp),
                 ("run_start", c_vp), ("run_fn", c_vp), ("run_q", c_vp), ("run_tile", c_vp), ("run_static", c_vp), ("pm", c_vp),
-                ("geo", c_vp), ("ptab", c_vp),
+                ("geo", c_vp),
                 ("rec4", c_vp), ("d2", c_vp), ("pix", c_vp),
-                ("gradr", c_vp), ("u", c_vp), ("u_out", c_vp), ("out", c_vp), ("out1", c_vp), ("tile_counter", c_vp),
+                ("gradr", c_vp), ("u", c_vp), ("u_out", c_vp), ("out", c_vp), ("out1", c_vp), ("rhs8", c_vp), ("rhs1", c_vp), ("tile_counter", c_vp),
                 ("rec4_h", c_vp), ("d2_h", c_vp), ("pix_h", c_vp), ("e_split", c_ll), ("e_hbase", c_ll)]
 
 
@@ -84,7 +84,7 @@ SPLAT_BYTES = 96
 PAIR_GEO_BYTES = 32
 PAIR_M_BYTES = 48
 JT_D = 9          # J^T partials per run: 8 (32-byte records) + 1 (separate array)
-DIAG_D = 14
+DIAG_M = 40       # diag moment floats per run
 
 # name -> (restype, argtypes)
 _SIGS = {
@@ -92,7 +92,7 @@ _SIGS = {
     "slm_pair_geo_size": (c_i, []), "slm_view_size": (c_i, []), "slm_raster_args_size": (c_i, []),
     "slm_resid_args_size": (c_i, []), "slm_tile_args_size": (c_i, []), "slm_back_args_size": (c_i, []),
     "slm_fwd_args_size": (c_i, []),
-    "slm_diag_tab_floats": (c_i, []),
+    "slm_diag_moment_floats": (c_i, []),
     "slm_preprocess": (c_i, [c_vp, c_ll, c_i, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "slm_sort_pairs_u64_workspace": (c_ll, [c_ll]),
     "slm_sort_pairs_u64": (c_i, [c_vp, c_ll, c_vp, c_vp, c_vp, c_vp, c_ll, c_i, c_i, c_vp]),
@@ -130,7 +130,6 @@ _SIGS = {
     "slm_run_static": (c_i, [c_vp, c_ll, c_vp, c_vp, c_vp]),
     "slm_chunk_perm": (c_i, [c_vp, c_ll, c_vp, c_vp, c_vp, c_vp]),
     "slm_tile_chunks": (c_i, [c_vp, c_i, c_vp, c_vp, c_vp, c_vp, c_i, c_vp]),
-    "slm_pair_tables": (c_i, [c_vp, c_ll, c_i, c_vp, c_vp, c_vp, c_i, c_vp, c_vp, c_vp]),
     "slm_gauss_tab": (c_i, [c_vp, c_ll, c_i, c_vp, c_vp]),
     "slm_gauss_tab_floats": (c_i, [c_i]),
     "slm_diag_stream": (c_i, [c_vp, c_vp]),

@@ -10,6 +10,9 @@
 #ifndef SLM_BW_MINB
 #define SLM_BW_MINB 4
 #endif
+#ifndef SLM_BW1_MINB
+#define SLM_BW1_MINB 3   // the diag backward (moments + chain per pair) keeps more registers
+#endif
 
 // arithmetic type of the per-pair chain (outputs are stored as float)
 #ifndef SLM_CHAIN_T

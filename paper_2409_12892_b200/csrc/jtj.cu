@@ -3,55 +3,7 @@
 // in stream.cu.
 #include "chain.cuh"
 
-#define DIAG_TAB 48   // floats per pair coefficient table (diag)
-#define DIAG_RUN_D 14
-
-// ---------------------------------------------------------------------------
-// diag(J^T W J): per run, 11 geometry sums of grad_r_sq * (dc/dx_k)^2 and the
-// three channel sums grad_r_sq * (alpha T)^2 that the SH block needs
-// (ref: jacobian.py:496-508) -- exact squares per entry.  The per-pair
-// coefficient tables come from k_pair_tables (one thread per pair).
-// table layout: [0,15) k=0..2 x (dmu0, dmu1, dcov0, dcov1, dcov2);
-//               [15,36) k=3..9 x (dcov0, dcov1, dcov2); [36] dopa;
-//               [37,46) dcol[ch][j] (position columns)
-// ---------------------------------------------------------------------------
-template <int K>
-__global__ void __launch_bounds__(128) k_pair_tables(const float* __restrict__ xs, long long G,
-                                                     const int* __restrict__ pair_gid,
-                                                     const uint32_t* __restrict__ pair_vm,
-                                                     const SlmCamera* __restrict__ cams, int n_pairs,
-                                                     float* __restrict__ tab, const float* __restrict__ gtab) {
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_pairs; q += gridDim.x * blockDim.x) {
-    const uint32_t vm = pair_vm[q];
-    Tab<K> T;
-    pair_tab<K>(xs, G, pair_gid[q], cams[vm & 0xffffu], vm >> 16, T, gtab);
-    float o[DIAG_TAB];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      o[k * 5 + 0] = T.dmu[0][k];
-      o[k * 5 + 1] = T.dmu[1][k];
-      o[k * 5 + 2] = T.dcov[0][k];
-      o[k * 5 + 3] = T.dcov[1][k];
-      o[k * 5 + 4] = T.dcov[2][k];
-    }
-#pragma unroll
-    for (int k = 3; k < 10; ++k) {
-      o[15 + (k - 3) * 3 + 0] = T.dcov[0][k];
-      o[15 + (k - 3) * 3 + 1] = T.dcov[1][k];
-      o[15 + (k - 3) * 3 + 2] = T.dcov[2][k];
-    }
-    o[36] = T.dopa;
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch)
-#pragma unroll
-      for (int j = 0; j < 3; ++j) o[37 + ch * 3 + j] = T.dcol[ch][j];
-    o[46] = 0.f;
-    o[47] = 0.f;
-    float4* dst = reinterpret_cast<float4*>(tab + (size_t)q * DIAG_TAB);  // 16-byte stores
-#pragma unroll
-    for (int k = 0; k < DIAG_TAB / 4; ++k) dst[k] = make_float4(o[4 * k], o[4 * k + 1], o[4 * k + 2], o[4 * k + 3]);
-  }
-}
+#define DIAG_M 40     // diag moment floats per run (stream.cu diag pass)
 
 // ---------------------------------------------------------------------------
 // Per-gaussian backward chain (ref: jacobian.py:314-353 / 506-510), packed:
@@ -64,7 +16,8 @@ __global__ void __launch_bounds__(128) k_pair_tables(const float* __restrict__ x
 // row order (deterministic), and write gaussian-major scratch rows that
 // k_gm_to_am transposes.
 //   MODE 0 (J^T): run partials 0-7 as 32-byte records (pacc) + partial 8 (pacc1)
-//   MODE 1 (diag): 14 sums per run (pacc); SH block via basis^2
+//   MODE 1 (diag): 40 moment floats per run (pacc), the pair's chain applied
+//                  to them once per pair; SH block via basis^2
 // ---------------------------------------------------------------------------
 __global__ void k_warp_bounds(const int* __restrict__ gpo, long long G, int n_warps, int* __restrict__ warp_g0) {
   for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g <= G; g += (long long)gridDim.x * blockDim.x) {
@@ -76,7 +29,7 @@ __global__ void k_warp_bounds(const int* __restrict__ gpo, long long G, int n_wa
 
 #define PK_WARPS 4
 template <int K, int MODE>
-__global__ void __launch_bounds__(32 * PK_WARPS, SLM_BW_MINB) k_gauss_backward_packed(SlmBackArgs A, const int* __restrict__ warp_g0,
+__global__ void __launch_bounds__(32 * PK_WARPS, MODE == 0 ? SLM_BW_MINB : SLM_BW1_MINB) k_gauss_backward_packed(SlmBackArgs A, const int* __restrict__ warp_g0,
                                                                        int n_warps) {
   constexpr int P = 11 + 3 * K;
   constexpr int PP = P > 32 ? 65 : 33;  // odd row stride, every lane's column pair inside the row
@@ -134,26 +87,69 @@ __global__ void __launch_bounds__(32 * PK_WARPS, SLM_BW_MINB) k_gauss_backward_p
             for (int k = 0; k < K; ++k) row[11 + ch * K + k] = sc * T.Y[k];
           }
         } else {
-          float a[DIAG_RUN_D];
+          // diag from the run moments (stream.cu diag pass): S (5x5 upper
+          // triangle), V_ch (3 x 5), T3_ch, O / o^2; the pair's chain applied
+          // once: M_k = D^T S D + 2 sum_ch c_ch D.V_ch + sum_ch c_ch^2 T3_ch
+          float mo[36];
 #pragma unroll
-          for (int j = 0; j < DIAG_RUN_D; ++j) a[j] = 0.f;
+          for (int j = 0; j < 36; ++j) mo[j] = 0.f;
+          const float4* p4 = reinterpret_cast<const float4*>(A.pacc);
           for (int rr = r0; rr < r1; ++rr) {
 #pragma unroll
-            for (int j = 0; j < DIAG_RUN_D; ++j) a[j] += __ldg(A.pacc + (size_t)rr * DIAG_RUN_D + j);
+            for (int k = 0; k < 9; ++k) {
+              const float4 v = __ldg(p4 + (size_t)rr * (DIAG_M / 4) + k);
+              mo[4 * k] += v.x;
+              mo[4 * k + 1] += v.y;
+              mo[4 * k + 2] += v.z;
+              mo[4 * k + 3] += v.w;
+            }
+          }
+          Tab<K> T;
+          pair_tab<K>(A.xs, G, myg, A.cams[vm & 0xffffu], vm >> 16, T, A.gtab);
+          auto S = [&](int i, int j) {  // upper-triangle index of the symmetric 5x5 S
+            const int a = i < j ? i : j, b = i < j ? j : i;
+            return mo[a * 5 - a * (a - 1) / 2 + (b - a)];
+          };
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const float D[5] = {T.dmu[0][k], T.dmu[1][k], T.dcov[0][k], T.dcov[1][k], T.dcov[2][k]};
+            float q = 0.f;
+#pragma unroll
+            for (int i = 0; i < 5; ++i) {
+              float t = 0.f;
+#pragma unroll
+              for (int j = 0; j < 5; ++j) t = fmaf(S(i, j), D[j], t);
+              q = fmaf(D[i], t, q);
+            }
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+              const float c = T.dcol[ch][k];
+              float dv = 0.f;
+#pragma unroll
+              for (int i = 0; i < 5; ++i) dv = fmaf(D[i], mo[15 + ch * 5 + i], dv);
+              q = fmaf(2.f * c, dv, fmaf(c * c, mo[30 + ch], q));
+            }
+            row[k] = q;
           }
 #pragma unroll
-          for (int j = 0; j < 11; ++j) row[j] = a[j];
-          const SlmCamera& cam = A.cams[vm & 0xffffu];
-          const float* gt = A.gtab + (size_t)myg * gtab_floats(K) + GT_POS;
-          const float v0 = gt[0] - (float)cam.C[0], v1 = gt[1] - (float)cam.C[1], v2 = gt[2] - (float)cam.C[2];
-          const float ivn = 1.f / sqrtf(v0 * v0 + v1 * v1 + v2 * v2);
-          float Y[K];
-          sh_basis<float, K>(v0 * ivn, v1 * ivn, v2 * ivn, Y);
+          for (int k = 3; k < 10; ++k) {
+            const float D[3] = {T.dcov[0][k], T.dcov[1][k], T.dcov[2][k]};
+            float q = 0.f;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+              float t = 0.f;
+#pragma unroll
+              for (int j = 0; j < 3; ++j) t = fmaf(S(2 + i, 2 + j), D[j], t);
+              q = fmaf(D[i], t, q);
+            }
+            row[k] = q;
+          }
+          row[10] = T.dopa * T.dopa * mo[33];
 #pragma unroll
           for (int ch = 0; ch < 3; ++ch) {
-            const float sc = ((vm >> (16 + ch)) & 1u) ? 0.f : a[11 + ch];
+            const float sc = T.mask[ch] * mo[30 + ch];
 #pragma unroll
-            for (int k = 0; k < K; ++k) row[11 + ch * K + k] = sc * Y[k] * Y[k];
+            for (int k = 0; k < K; ++k) row[11 + ch * K + k] = sc * T.Y[k] * T.Y[k];
           }
         }
       }
@@ -254,7 +250,7 @@ extern "C" {
 int slm_view_size() { return (int)sizeof(SlmView); }
 int slm_tile_args_size() { return (int)sizeof(SlmTileArgs); }
 int slm_back_args_size() { return (int)sizeof(SlmBackArgs); }
-int slm_diag_tab_floats() { return DIAG_TAB; }
+int slm_diag_moment_floats() { return DIAG_M; }
 
 int slm_gauss_tab(const float* xs, long long G, int sh_degree, float* gtab, cudaStream_t st) {
   if (G <= 0) return SLM_OK;
@@ -273,19 +269,6 @@ int slm_gauss_tab_floats(int sh_degree) {
   return sh_degree < 0 || sh_degree > 3 ? -1 : gtab_floats((sh_degree + 1) * (sh_degree + 1));
 }
 
-int slm_pair_tables(const float* xs, long long G, int sh_degree, const int* pair_gid, const uint32_t* pair_vm,
-                    const SlmCamera* cams, int n_pairs, float* tab, const float* gtab, cudaStream_t st) {
-  if (n_pairs <= 0) return SLM_OK;
-  unsigned b = slm_blocks(n_pairs, 128, 1LL << 30);
-  switch (sh_degree) {
-    case 0: k_pair_tables<1><<<b, 128, 0, st>>>(xs, G, pair_gid, pair_vm, cams, n_pairs, tab, gtab); break;
-    case 1: k_pair_tables<4><<<b, 128, 0, st>>>(xs, G, pair_gid, pair_vm, cams, n_pairs, tab, gtab); break;
-    case 2: k_pair_tables<9><<<b, 128, 0, st>>>(xs, G, pair_gid, pair_vm, cams, n_pairs, tab, gtab); break;
-    case 3: k_pair_tables<16><<<b, 128, 0, st>>>(xs, G, pair_gid, pair_vm, cams, n_pairs, tab, gtab); break;
-    default: return SLM_ERR_ARG;
-  }
-  return slm_cuda_status();
-}
 
 int slm_fwd_args_size() { return (int)sizeof(SlmFwdArgs); }
 

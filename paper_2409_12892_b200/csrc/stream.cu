@@ -47,8 +47,7 @@ constexpr int kJtUnroll = SLM_JT_UNROLL;  // J^T entry-loop unroll (tuning)
 #define MODE_WRITEU 2
 #define MODE_JT 4
 #define MODE_DIAG 8
-#define DIAG_TAB 48      // floats per pair coefficient table (k_pair_tables)
-#define DIAG_D 14        // diag sums per run
+#define DIAG_M 40        // diag moment floats per run (34 used, see the diag pass)
 
 // one ring stage (ST_BYTES): a packed per-chunk region
 //   rec4 | d2 | pix | static run records | pair m | run starts
@@ -271,7 +270,8 @@ __device__ __forceinline__ uint8_t* stage_ptr(uint8_t* ring, int s) { return rin
 __host__ __device__ constexpr int ns_of(int mode) { return (mode & MODE_J) ? NS : NS + 1; }
 
 __host__ __device__ constexpr size_t stream_smem_bytes(int mode) {
-  return 256 * 16 + ((mode & MODE_J) ? (size_t)NW * 256 * 16 : 0) + (size_t)ns_of(mode) * ST_BYTES + TMETA * 24;
+  return 256 * 16 + ((mode & MODE_J) ? (size_t)NW * 256 * 16 : 0) + ((mode & MODE_DIAG) ? 256 * 16 : 0) +
+         (size_t)ns_of(mode) * ST_BYTES + TMETA * 24;
 }
 
 // 2 CTAs / SM: 228 KB of shared memory per SM, 1 KB reserved per CTA, and a
@@ -303,6 +303,8 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
   sp += 256 * 16;
   float4* s_acc = reinterpret_cast<float4*>(sp);
   sp += (MODE & MODE_J) ? (size_t)NW * 256 * 16 : 0;
+  float4* s_c = reinterpret_cast<float4*>(sp);  // diag: the rhs colour gradient per pixel
+  sp += (MODE & MODE_DIAG) ? 256 * 16 : 0;
   uint8_t* ring = sp;
   sp += (size_t)NSM * ST_BYTES;
   ChunkMeta* tmeta = reinterpret_cast<ChunkMeta*>(sp);
@@ -455,6 +457,7 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
       if (inside && A.gradr) wt = A.gradr[gp];
     } else if (MODE & MODE_DIAG) {
       wt = inside ? A.gradr[gp] : make_float4(0.f, 0.f, 0.f, 0.f);
+      s_c[p] = inside && A.u ? A.u[gp] : make_float4(0.f, 0.f, 0.f, 0.f);
     } else {
       wt = inside ? A.u[gp] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
@@ -536,9 +539,21 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
 
     if (MODE & MODE_DIAG) {
       consumer_sync();
-      // diag(J^T W J) sums per run (ref: jacobian.py:486-512): same 8-lane
-      // groups / schedule as J^T; each group holds its pair's 48-float chain
-      // table in registers (run record P[5] = pair index, from L2)
+      // diag(J^T W J) (ref: jacobian.py:486-512) in moment form, plus the
+      // J^T partials of the colour gradient (b = -J^T color_grad, ref
+      // jacobian.py:411-413) in the same sweep over the cache.  Per entry
+      // with w = alpha_eff (e1, e2, e1^2/2, e1 e2, e2^2/2), Aw = sum_ch
+      // gr_ch dd_ch^2 (dd = dc/dalpha) and g_ch = gr_ch dd_ch alphaT, a run
+      // accumulates
+      //   S = sum Aw w w^T (15), V_ch = sum g_ch w (15), T3_ch = sum gr_ch
+      //   (alphaT)^2 (3), O = sum Aw alpha_eff^2 (1),
+      // so that for a parameter with chain coefficients D (da = w.D) and
+      // colour coefficients c_ch, sum gr_ch (dd_ch da + alphaT c_ch)^2 =
+      // D^T S D + 2 sum_ch c_ch D.V_ch + sum_ch c_ch^2 T3_ch: the backward
+      // applies the pair's chain once per pair instead of once per entry.
+      // Same 8-lane groups / length-sorted schedule as the J^T pass; lanes
+      // past their run's end add exact zeros (selects).
+      const bool rhs = A.u != nullptr;
       for (int ci = c0; ci < c1; ++ci, ++g) {
         const int s = (int)(g % NSM);
         mbar_wait(&full[s], (g / NSM) & 1u);
@@ -552,101 +567,107 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
           const int ri = st[OFF_PERM + rd * 32 + (((warp + ci) & (NW - 1)) * 4 + slot)];
           int n = 0, f0 = 0, sl = 0;
           float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = q0;
-          float kc = 0.f, io = 0.f;
-          float D[DIAG_TAB];
+          float io = 0.f;
           if (ri != 0xff) {
             const float4* P4 = reinterpret_cast<const float4*>(st + hdr[6]) + ri * 2;
             q0 = P4[0];
             s1 = P4[1];
-            kc = s1.y;
             io = s1.z;
             sl = __float_as_int(s1.w);
-            // the run's pair (its chain table), staged by the producer
-            const int* sq = reinterpret_cast<const int*>(st + hdr[6] + hdr[0] * 32) + hdr[1];
-            const float4* tq = reinterpret_cast<const float4*>(A.ptab + (size_t)sq[ri] * DIAG_TAB);
-  #pragma unroll
-            for (int k = 0; k < DIAG_TAB / 4; ++k) {
-              const float4 v = __ldg(tq + k);
-              D[4 * k] = v.x;
-              D[4 * k + 1] = v.y;
-              D[4 * k + 2] = v.z;
-              D[4 * k + 3] = v.w;
-            }
             const uint32_t fn = rf[ri];
             f0 = (int)(fn & 0xffffu);
             n = (int)(fn >> 16);
-          } else {
-  #pragma unroll
-            for (int k = 0; k < DIAG_TAB; ++k) D[k] = 0.f;
           }
           const int nmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)n);
           if (nmax == 0) continue;
-          const float dop = io * D[36];
           const RunE ke = run_e_of(q0, s1);
-          float a[16];
-  #pragma unroll
-          for (int k = 0; k < 16; ++k) a[k] = 0.f;
+          float m[DIAG_M];  // S (15, row-major upper triangle), V (3 x 5), T3 (3), O, pad
+#pragma unroll
+          for (int k = 0; k < DIAG_M; ++k) m[k] = 0.f;
+          float2 a01 = make_float2(0.f, 0.f), a23 = a01, a67 = a01;  // rhs J^T partials
+          float a4 = 0.f, a5 = 0.f, a8 = 0.f;
           const float4* pr = s4 + f0;
           const float* pd = sd2 + f0;
           const uint8_t* pp = spx + f0;
           for (int j = lg; j < nmax; j += 8) {
-            if (j < n) {
-              const float4 r = pr[j];
-              const float dd[3] = {r.z, r.w, pd[j]};
-              const int pl = pp[j];
-              const float4 gr = s_u[pl];
-              const float grc[3] = {gr.x, gr.y, gr.z};
-              const float ae = r.x, at = r.y;
-              const float2 e = run_e(ke, pl);
-              const float e1 = e.x, e2 = e.y;
-              const float w0 = ae * e1, w1 = ae * e2, w2 = 0.5f * w0 * e1, w3 = w0 * e2, w4 = 0.5f * w1 * e2;
-              // sum_ch gr_ch (dc_ch/dx_k)^2: dalpha_k^2 * Aw for k >= 3 (exact),
-              // per-channel squares for the position params (dc also has at * dcol)
-              const float Aw = grc[0] * dd[0] * dd[0] + grc[1] * dd[1] * dd[1] + grc[2] * dd[2] * dd[2];
-  #pragma unroll
-              for (int kk = 0; kk < 3; ++kk) {
-                const float da = w0 * D[kk * 5] + w1 * D[kk * 5 + 1] + w2 * D[kk * 5 + 2] + w3 * D[kk * 5 + 3] +
-                                 w4 * D[kk * 5 + 4];
-                float sq = 0.f;
-  #pragma unroll
-                for (int ch = 0; ch < 3; ++ch) {
-                  const float dc = fmaf(dd[ch], da, at * D[37 + ch * 3 + kk]);
-                  sq = fmaf(grc[ch] * dc, dc, sq);
-                }
-                a[kk] += sq;
-              }
-  #pragma unroll
-              for (int kk = 3; kk < 10; ++kk) {
-                const float da = w2 * D[15 + (kk - 3) * 3] + w3 * D[16 + (kk - 3) * 3] + w4 * D[17 + (kk - 3) * 3];
-                a[kk] = fmaf(da * da, Aw, a[kk]);
-              }
-              const float dao = ae * dop;
-              a[10] = fmaf(dao * dao, Aw, a[10]);
-              const float at2 = at * at;
-              a[11] = fmaf(grc[0], at2, a[11]);
-              a[12] = fmaf(grc[1], at2, a[12]);
-              a[13] = fmaf(grc[2], at2, a[13]);
+            const bool ok = j < n;
+            const float4 r = pr[j];
+            const int pl = pp[j];
+            const float4 gr = s_u[pl];
+            const float ae = ok ? r.x : 0.f, at = ok ? r.y : 0.f;
+            const float dd0 = ok ? r.z : 0.f, dd1 = ok ? r.w : 0.f, dd2 = ok ? pd[j] : 0.f;
+            const float2 e = run_e(ke, pl);
+            const float w0 = ae * e.x, w1 = ae * e.y;
+            const float w[5] = {w0, w1, 0.5f * w0 * e.x, w0 * e.y, 0.5f * w1 * e.y};
+            const float g0 = gr.x * dd0, g1 = gr.y * dd1, g2 = gr.z * dd2;
+            const float Aw = fmaf(g0, dd0, fmaf(g1, dd1, g2 * dd2));
+            float aw[5];
+#pragma unroll
+            for (int i = 0; i < 5; ++i) aw[i] = Aw * w[i];
+            int k = 0;
+#pragma unroll
+            for (int i = 0; i < 5; ++i)
+#pragma unroll
+              for (int jj = i; jj < 5; ++jj, ++k) m[k] = fmaf(aw[i], w[jj], m[k]);
+            const float ga[3] = {g0 * at, g1 * at, g2 * at};
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch)
+#pragma unroll
+              for (int i = 0; i < 5; ++i) m[15 + ch * 5 + i] = fmaf(ga[ch], w[i], m[15 + ch * 5 + i]);
+            const float at2 = at * at;
+            m[30] = fmaf(gr.x, at2, m[30]);
+            m[31] = fmaf(gr.y, at2, m[31]);
+            m[32] = fmaf(gr.z, at2, m[32]);
+            m[33] = fmaf(Aw * ae, ae, m[33]);
+            if (rhs) {  // J^T partials of the colour gradient, as in the J^T pass
+              const float4 uu = s_c[pl];
+              const float sa = fmaf(dd0, uu.x, fmaf(dd1, uu.y, dd2 * uu.z));
+              const float tt = sa * ae;
+              const float2 te = __fmul2_rn(make_float2(tt, tt), e);
+              a01 = __fadd2_rn(a01, te);
+              a23 = __ffma2_rn(make_float2(te.x, te.x), e, a23);
+              a4 = fmaf(te.y, e.y, a4);
+              a5 += tt;
+              a67 = __ffma2_rn(make_float2(at, at), make_float2(uu.x, uu.y), a67);
+              a8 = fmaf(at, uu.z, a8);
             }
           }
-          // two 8-lane reduce-scatters: lane lg ends with the group sums of
-          // values lg and 8 + lg (fixed pattern -> deterministic)
+          // 8-lane reduce-scatter of the 40 moment floats (5 blocks of 8: lane
+          // lg ends with values lg + 8 b); fixed pattern -> deterministic
           const unsigned F = 0xffffffffu;
           const bool u4 = lg & 4, u2 = lg & 2, u1 = lg & 1;
-          float res[2];
-  #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const float* v = a + 8 * h;
+          float res[5];
+#pragma unroll
+          for (int h = 0; h < 5; ++h) {
+            const float* v = m + 8 * h;
             float w4[4], w2[2];
-  #pragma unroll
+#pragma unroll
             for (int k = 0; k < 4; ++k) w4[k] = (u4 ? v[k + 4] : v[k]) + __shfl_xor_sync(F, u4 ? v[k] : v[k + 4], 4);
-  #pragma unroll
+#pragma unroll
             for (int k = 0; k < 2; ++k) w2[k] = (u2 ? w4[k + 2] : w4[k]) + __shfl_xor_sync(F, u2 ? w4[k] : w4[k + 2], 2);
             res[h] = (u1 ? w2[1] : w2[0]) + __shfl_xor_sync(F, u1 ? w2[0] : w2[1], 1);
           }
           if (ri != 0xff) {
-            float* o = A.out + (size_t)sl * DIAG_D;  // pair-run-slot order
-            o[lg] = res[0];
-            if (lg < DIAG_D - 8) o[8 + lg] = res[1];
+            float* o = A.out + (size_t)sl * DIAG_M;  // pair-run-slot order
+            res[4] = lg == 1 ? res[4] * io * io : res[4];  // O (value 33) carries 1/o^2: opacity da = alpha_eff dopa / o
+#pragma unroll
+            for (int h = 0; h < 5; ++h) o[8 * h + lg] = res[h];
+          }
+          if (rhs) {
+            const float a[8] = {a01.x, a01.y, a23.x, a23.y, a4, a5, a67.x, a67.y};
+            float w4[4], w2[2];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) w4[k] = (u4 ? a[k + 4] : a[k]) + __shfl_xor_sync(F, u4 ? a[k] : a[k + 4], 4);
+#pragma unroll
+            for (int k = 0; k < 2; ++k) w2[k] = (u2 ? w4[k + 2] : w4[k]) + __shfl_xor_sync(F, u2 ? w4[k] : w4[k + 2], 2);
+            const float w1 = (u1 ? w2[1] : w2[0]) + __shfl_xor_sync(F, u1 ? w2[0] : w2[1], 1);
+            a8 += __shfl_xor_sync(F, a8, 4);
+            a8 += __shfl_xor_sync(F, a8, 2);
+            a8 += __shfl_xor_sync(F, a8, 1);
+            if (ri != 0xff) {
+              A.rhs8[(size_t)sl * 8 + lg] = lg == 5 ? w1 * io : ((lg == 2 || lg == 4) ? 0.5f * w1 : w1);
+              if (lg == 0) A.rhs1[sl] = a8;
+            }
           }
         }
         __syncwarp();
@@ -803,8 +824,9 @@ int slm_chunk_perm(const int* chunk_run, long long n_chunks, const long long* ru
 // u = J p (a->gradr weights it) written to a->u_out
 int slm_apply_j(const SlmTileArgs* a, cudaStream_t st) { return launch_stream<MODE_J | MODE_WRITEU>(a, st); }
 
-// diag(J^T W J) sums per run (14, pair-run-slot order) from a->gradr and the
-// per-pair tables a->ptab
+// diag(J^T W J) moments per run (40 floats, pair-run-slot order) from
+// a->gradr; with a->u = the colour gradient also its J^T partials (the rhs)
+// into a->rhs8 / a->rhs1, in the same sweep
 int slm_diag_stream(const SlmTileArgs* a, cudaStream_t st) { return launch_stream<MODE_DIAG>(a, st); }
 
 // J^T partials per run from the per-pixel a->u

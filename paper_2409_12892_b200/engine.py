@@ -756,13 +756,17 @@ class CacheSet:
         return out
 
     def rhs(self) -> torch.Tensor:
-        """b = -J^T color_grad, summed over the subset's views (ref: jacobian.py:411-413)."""
+        """b = -J^T color_grad, summed over the subset's views (ref: jacobian.py:411-413).
+        With residual weights it comes from the same cache sweep as diag()."""
         if self._b is None:
             if self.cgrad is None:
                 raise ValueError("cache was built without residuals")
-            b = torch.empty(self.G * self.P, dtype=torch.float32, device=self.device)
-            self.apply_jt_raw(self.cgrad, b, -1.0)
-            self._b = b
+            if self.gradr is not None:
+                self._diag_and_rhs()
+            else:
+                b = torch.empty(self.G * self.P, dtype=torch.float32, device=self.device)
+                self.apply_jt_raw(self.cgrad, b, -1.0)
+                self._b = b
         return self._b
 
     def diag(self) -> torch.Tensor:
@@ -770,20 +774,34 @@ class CacheSet:
         if self._M is None:
             if self.gradr is None:
                 raise ValueError("cache was built without residual weights")
-            sums = _empty(self.R * _lib.DIAG_D, torch.float32, self.device)
-            if self.G == 0:
-                self._M = torch.empty(0, dtype=torch.float32, device=self.device)
-                return self._M
-            ptab = _empty(self.n_pairs * _lib.load().slm_diag_tab_floats(), torch.float32, self.device)
-            call("slm_pair_tables", ptr(self.scene.x32()), self.G, self.scene.sh_degree, ptr(self.pair_gid),
-                 ptr(self.pair_vm), ptr(self.cams_dev), self.n_pairs, ptr(ptab), ptr(self.gtab), stream_ptr())
-            ra = self._tile_args()
-            ra.ptab, ra.gradr, ra.out = ptr(ptab), ptr(self.gradr), ptr(sums)
-            call("slm_diag_stream", _lib.byref(ra), stream_ptr())
-            M = torch.empty(self.G * self.P, dtype=torch.float32, device=self.device)
-            self._backward(sums, M, 1)
-            self._M = M
+            self._diag_and_rhs()
         return self._M
+
+    def _diag_and_rhs(self):
+        """One sweep of the streaming kernel over the cache: the diag moments
+        per run and (with a colour gradient) the rhs J^T partials; then the
+        two per-gaussian backward chains."""
+        dev, n = self.device, self.G * self.P
+        if self.G == 0:
+            self._M = torch.empty(0, dtype=torch.float32, device=dev)
+            if self.cgrad is not None:
+                self._b = torch.empty(0, dtype=torch.float32, device=dev)
+            return
+        moments = _empty(self.R * _lib.DIAG_M, torch.float32, dev)
+        want_b = self.cgrad is not None and self._b is None
+        ra = self._tile_args()
+        ra.gradr, ra.out = ptr(self.gradr), ptr(moments)
+        if want_b:
+            ra.u, ra.rhs8, ra.rhs1 = ptr(self.cgrad), ptr(self.run_acc), off(self.run_acc, 8 * self.R)
+        call("slm_diag_stream", _lib.byref(ra), stream_ptr())
+        if self._M is None:
+            M = torch.empty(n, dtype=torch.float32, device=dev)
+            self._backward(moments, M, 1)
+            self._M = M
+        if want_b:
+            b = torch.empty(n, dtype=torch.float32, device=dev)
+            self._backward(self.run_acc, b, 0, -1.0)
+            self._b = b
 
     # ------------------------------------------------------------------
     # parity exports (test infrastructure; host-side reconstruction)

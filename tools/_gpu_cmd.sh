@@ -1,1 +1,1 @@
-mkdir -p gpurun_out/sanitizer; bash tools/sanitize.sh > gpurun_out/sanitizer/summary.txt 2>&1
+bash tools/gpu_ab.sh c3 bw1m3 bw1m4 > gpurun_out/ab8.log 2>&1
