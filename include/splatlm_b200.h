@@ -256,11 +256,10 @@ int slm_sort_pairs_u64(void* ws, long long ws_bytes, const unsigned long long* k
  * rasterizer.py:253-261, 283-287) */
 int slm_tile_count(const uint32_t* sorted_gid, const unsigned long long* sorted_key, long long G,
                    const SlmSplat* splats, int tiles_x, int tiles_y, unsigned long long* n_inst, cudaStream_t s);
+/* (tile, depth rank) keys of every (tile, splat) instance, the splat as the
+ * value: after the key sort the values are the tile's instance list */
 int slm_tile_emit(const uint32_t* sorted_gid, const unsigned long long* inst_off, long long G, const SlmSplat* splats,
-                  int tiles_x, int tiles_y, int rank_bits, unsigned long long* keys, uint32_t* vals,
-                  uint32_t* inst_g_pre, cudaStream_t s);
-int slm_tile_post(const uint32_t* sorted_pre, const uint32_t* inst_g_pre, long long n, uint32_t* inst_gid,
-                  uint32_t* post_of_pre, cudaStream_t s);
+                  int tiles_x, int tiles_y, int rank_bits, unsigned long long* keys, uint32_t* vals, cudaStream_t s);
 int slm_tile_ranges(const unsigned long long* keys, long long n, int rank_bits, slm_u2* ranges, int n_tiles,
                     cudaStream_t s);
 /* render (rasterizer.py:319-358): COUNT pass = image, T_final, per-pixel
@@ -289,7 +288,7 @@ int slm_tile_count_v(const uint32_t* sv, long long n, long long G, const SlmSpla
                      unsigned long long* n_inst, cudaStream_t s);
 int slm_tile_emit_v(const uint32_t* sv, const unsigned long long* inst_off, long long n, long long G,
                     const SlmSplat* splats, const SlmView* views, const int* view_tile_base, int rank_bits,
-                    unsigned long long* keys, uint32_t* vals, uint32_t* inst_s_pre, cudaStream_t s);
+                    unsigned long long* keys, uint32_t* vals, cudaStream_t s);
 long long slm_sort_keys_u32_workspace(long long n);
 int slm_sort_keys_u32(void* ws, long long ws_bytes, const uint32_t* kin, uint32_t* kout, long long n, int begin_bit,
                       int end_bit, cudaStream_t s);

@@ -182,13 +182,12 @@ __global__ void k_tile_count(const uint32_t* __restrict__ sorted_gid, const unsi
   }
 }
 
-// instances are emitted per splat in (tile row, tile column) order; the sort
-// value is the pre-sort instance index so the per-splat grouping can be
-// recovered after the (tile, depth rank) sort (k_tile_post)
+// instances are emitted per splat in (tile row, tile column) order with the
+// key (tile, depth rank) -- unique per instance -- and the splat as the value,
+// so after the key sort the values are each tile's splats in depth order
 __global__ void k_tile_emit(const uint32_t* __restrict__ sorted_gid, const unsigned long long* __restrict__ inst_off,
                             long long G, const SlmSplat* __restrict__ splats, int tiles_x, int tiles_y,
-                            int rank_bits, unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals,
-                            uint32_t* __restrict__ inst_g_pre) {
+                            int rank_bits, unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   for (; i < G; i += (long long)gridDim.x * blockDim.x) {
     unsigned long long beg = inst_off[i], end = inst_off[i + 1];
@@ -200,8 +199,7 @@ __global__ void k_tile_emit(const uint32_t* __restrict__ sorted_gid, const unsig
     for (int ty = ty0; ty <= ty1; ++ty)
       for (int tx = tx0; tx <= tx1; ++tx) {
         keys[k] = ((unsigned long long)(ty * tiles_x + tx) << rank_bits) | (unsigned long long)i;
-        vals[k] = (uint32_t)k;
-        inst_g_pre[k] = g;
+        vals[k] = g;  // the sort carries the splat itself (keys are unique per instance)
         ++k;
       }
   }
@@ -232,8 +230,7 @@ __global__ void k_tile_count_v(const uint32_t* __restrict__ sv, long long n, lon
 __global__ void k_tile_emit_v(const uint32_t* __restrict__ sv, const unsigned long long* __restrict__ inst_off,
                               long long n, long long G, const SlmSplat* __restrict__ splats,
                               const SlmView* __restrict__ views, const int* __restrict__ view_tile_base,
-                              int rank_bits, unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals,
-                              uint32_t* __restrict__ inst_s_pre) {
+                              int rank_bits, unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const unsigned long long beg = inst_off[i], end = inst_off[i + 1];
     if (beg == end) continue;
@@ -250,20 +247,9 @@ __global__ void k_tile_emit_v(const uint32_t* __restrict__ sv, const unsigned lo
       for (int tx = tx0; tx <= tx1; ++tx) {
         keys[k] = ((unsigned long long)(view_tile_base[v] + ty * tiles_x + tx) << rank_bits) |
                   (unsigned long long)rank;
-        vals[k] = (uint32_t)k;
-        inst_s_pre[k] = (uint32_t)gs;
+        vals[k] = (uint32_t)gs;  // the sort carries the global splat (keys are unique per instance)
         ++k;
       }
-  }
-}
-
-// post-sort list position j: gid and the inverse permutation pre -> post
-__global__ void k_tile_post(const uint32_t* __restrict__ sorted_pre, const uint32_t* __restrict__ inst_g_pre,
-                            long long n, uint32_t* __restrict__ inst_gid, uint32_t* __restrict__ post_of_pre) {
-  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
-    uint32_t k = sorted_pre[j];
-    inst_gid[j] = inst_g_pre[k];
-    post_of_pre[k] = (uint32_t)j;
   }
 }
 
@@ -657,10 +643,10 @@ int slm_tile_count_v(const uint32_t* sv, long long n, long long G, const SlmSpla
 
 int slm_tile_emit_v(const uint32_t* sv, const unsigned long long* inst_off, long long n, long long G,
                     const SlmSplat* splats, const SlmView* views, const int* view_tile_base, int rank_bits,
-                    unsigned long long* keys, uint32_t* vals, uint32_t* inst_s_pre, cudaStream_t stream) {
+                    unsigned long long* keys, uint32_t* vals, cudaStream_t stream) {
   if (n <= 0) return SLM_OK;
   k_tile_emit_v<<<slm_blocks(n, 256), 256, 0, stream>>>(sv, inst_off, n, G, splats, views, view_tile_base, rank_bits,
-                                                         keys, vals, inst_s_pre);
+                                                         keys, vals);
   return slm_cuda_status();
 }
 
@@ -711,18 +697,12 @@ int slm_tile_count(const uint32_t* sorted_gid, const unsigned long long* sorted_
 
 int slm_tile_emit(const uint32_t* sorted_gid, const unsigned long long* inst_off, long long G, const SlmSplat* splats,
                   int tiles_x, int tiles_y, int rank_bits, unsigned long long* keys, uint32_t* vals,
-                  uint32_t* inst_g_pre, cudaStream_t stream) {
+                  cudaStream_t stream) {
   k_tile_emit<<<slm_blocks(G, 256), 256, 0, stream>>>(sorted_gid, inst_off, G, splats, tiles_x, tiles_y, rank_bits,
-                                                       keys, vals, inst_g_pre);
+                                                       keys, vals);
   return slm_cuda_status();
 }
 
-int slm_tile_post(const uint32_t* sorted_pre, const uint32_t* inst_g_pre, long long n, uint32_t* inst_gid,
-                  uint32_t* post_of_pre, cudaStream_t stream) {
-  if (n <= 0) return SLM_OK;
-  k_tile_post<<<slm_blocks(n, 256), 256, 0, stream>>>(sorted_pre, inst_g_pre, n, inst_gid, post_of_pre);
-  return slm_cuda_status();
-}
 
 int slm_inst_count(const uint32_t* mask, const uint32_t* inst_gid, long long n, long long* cnt, int* used,
                    int* pair_cnt, cudaStream_t stream) {

@@ -158,7 +158,6 @@ class ViewFrame:
         self.n_inst = 0
         self.sorted_gid = None   # int32 [G] depth order
         self.inst_off = None     # int64 [G+1] instances per depth rank (pre-sort order)
-        self.post_of_pre = None  # int32 [n_inst]
         self.inst_mask = None    # int32 [n_inst*8] keep mask per instance
         self.inst_start = None   # int64 [n_inst] first entry of the instance's run
 
@@ -196,22 +195,17 @@ def project_and_bin(scene: GaussianScene, frame: ViewFrame, cfg_s: _lib.SlmRastC
     tile_bits = _bits(n_tiles)
     ik = _empty(total, torch.int64, dev)
     iv = _empty(total, torch.int32, dev)
-    ig = _empty(total, torch.int32, dev)
     call("slm_tile_emit", ptr(sgid), ptr(inst_off), G, ptr(splats), frame.tiles_x, frame.tiles_y, rank_bits,
-         ptr(ik), ptr(iv), ptr(ig), stream_ptr())
+         ptr(ik), ptr(iv), stream_ptr())
     sk = torch.empty_like(ik)
-    sv = torch.empty_like(iv)
-    sort_u64(ik, sk, iv, sv, total, 0, rank_bits + tile_bits)
+    inst_gid = _empty(total, torch.int32, dev)   # the sorted values: each tile's splats in depth order
+    sort_u64(ik, sk, iv, inst_gid, total, 0, rank_bits + tile_bits)
     ranges = torch.empty(2 * n_tiles, dtype=torch.int32, device=dev)
     call("slm_tile_ranges", ptr(sk), total, rank_bits, ptr(ranges), n_tiles, stream_ptr())
-    inst_gid = _empty(total, torch.int32, dev)
-    post_of_pre = _empty(total, torch.int32, dev)
-    call("slm_tile_post", ptr(sv), ptr(ig), total, ptr(inst_gid), ptr(post_of_pre), stream_ptr())
     frame.inst_gid = inst_gid
     frame.ranges = ranges
     frame.sorted_gid = sgid
     frame.inst_off = inst_off
-    frame.post_of_pre = post_of_pre
     return skeys, sgid
 
 
@@ -371,20 +365,15 @@ class CacheSet:
         rank_bits = _bits(G)
         ik = _empty(ni, torch.int64, dev)
         iv = _empty(ni, torch.int32, dev)
-        ig = _empty(ni, torch.int32, dev)
         call("slm_tile_emit_v", ptr(sv), ptr(inst_off), VG, G, ptr(splats_all), ptr(self.views_dev),
-             ptr(self.view_tile_base_dev), rank_bits, ptr(ik), ptr(iv), ptr(ig), stream_ptr())
+             ptr(self.view_tile_base_dev), rank_bits, ptr(ik), ptr(iv), stream_ptr())
         sk = torch.empty_like(ik)
-        siv = torch.empty_like(iv)
-        sort_u64(ik, sk, iv, siv, ni, 0, rank_bits + _bits(nt))
+        inst_gid = _empty(ni, torch.int32, dev)      # sorted values: global splat v * G + g per instance
+        sort_u64(ik, sk, iv, inst_gid, ni, 0, rank_bits + _bits(nt))
         del ik, iv
         ranges = torch.empty(2 * nt, dtype=torch.int32, device=dev)
         call("slm_tile_ranges", ptr(sk), ni, rank_bits, ptr(ranges), nt, stream_ptr())
         del sk
-        inst_gid = _empty(ni, torch.int32, dev)      # global splat index v * G + g per instance
-        post_of_pre = _empty(ni, torch.int32, dev)
-        call("slm_tile_post", ptr(siv), ptr(ig), ni, ptr(inst_gid), ptr(post_of_pre), stream_ptr())
-        del siv, ig
         inst_mask = torch.zeros(max(ni, 1) * MASK_WORDS, dtype=torch.int32, device=dev)
         T.tick("project_sort_bin")
 
@@ -514,7 +503,7 @@ class CacheSet:
                  R, 0, _bits(Pn), stream_ptr())
             del ws, qk, rid
             call("slm_invert_perm", ptr(self.pair_runs), R, ptr(self.run_slot), stream_ptr())
-        del sv, inst_off, post_of_pre
+        del sv, inst_off
         del pidx, pair_nruns, tile_nruns, inst_used, run_of, ent_of
         T.tick("runs_pairs")
 

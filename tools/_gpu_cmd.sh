@@ -1,1 +1,2 @@
-bash tools/gpu_ab.sh c3 bw1m3 bw1m4 > gpurun_out/ab8.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -5 > gpurun_out/pytest_gpu.log
+bash tools/gpu_launches_build.sh r02b

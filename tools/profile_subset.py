@@ -48,7 +48,9 @@ def main():
     out = {}
     for rep in range(args.reps):
         T = PhaseTimer()
+        torch.cuda.nvtx.range_push("build")
         cs = CacheSet(scene, cams, gts, timer=T)
+        torch.cuda.nvtx.range_pop()
         T.tick("done")
         phases = T.summary()
         a = ev()
