@@ -1,3 +1,2 @@
-mkdir -p gpurun_out/ncu
-timeout 1200 ncu --nvtx --nvtx-include "build/" --kernel-name-base demangled -k regex:'k_raster' --set full --import-source on --clock-control none -c 2 \
-  -o gpurun_out/ncu/raster_r02 python tools/profile_subset.py --config c3 --reps 1 --product-only > gpurun_out/ncu/raster_r02.log 2>&1
+timeout 900 python bench.py --config c1 --steps 5 --warmup 3 > gpurun_out/bench_c1.log 2>&1
+timeout 900 python bench.py --config c1 --impl reference --steps 2 --warmup 1 > gpurun_out/bench_c1_ref.log 2>&1
