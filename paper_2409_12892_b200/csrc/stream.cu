@@ -407,11 +407,7 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
               hdr[7] = L.rf;
               // generic-proxy header writes before the async-proxy copies land
               asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-              // diag: the chunk's run -> pair indices (their chain tables) into
-              // the pair-m section, which that mode does not use
-              const unsigned bq = (MODE & MODE_DIAG) ? br : 0u;
-              mbar_arrive_tx(&full[s], b4 + bd + bx + bp + br + ST_PERM + bq);
-              if (MODE & MODE_DIAG) bulk_g2s(st + L.pdy, A.run_q + aq, bq, &full[s], pol);
+              mbar_arrive_tx(&full[s], b4 + bd + bx + bp + br + ST_PERM);
               // record streams: device, or the host-mapped offloaded tail
               // (the split is a chunk boundary and e_hbase <= a16 <= a4)
               const bool off = A.rec4_h && m.e0 >= A.e_split;

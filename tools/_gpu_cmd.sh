@@ -1,2 +1,2 @@
-timeout 900 python bench.py --config c1 --steps 5 --warmup 3 > gpurun_out/bench_c1.log 2>&1
-timeout 900 python bench.py --config c1 --impl reference --steps 2 --warmup 1 > gpurun_out/bench_c1_ref.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_large_regime.py tests/test_offload.py -m gpu -x -q 2>&1 | tail -3 > gpurun_out/pytest_quick.log
+bash tools/gpu_ab.sh c3 pmgather > gpurun_out/ab10.log 2>&1
