@@ -230,21 +230,23 @@ __global__ void k_chunk_perm(const int* __restrict__ chunk_run, long long n_chun
   for (long long c = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; c < n_chunks;
        c += ((long long)gridDim.x * blockDim.x) >> 5) {
     const int k0 = chunk_run[c], n = chunk_run[c + 1] - k0;
-    long long len[RL];
-    int rank[RL];
+    const long long e0 = run_start[k0];
+    int len[RL], rank[RL];  // run lengths <= 256: one 32-bit shuffle per comparison
 #pragma unroll
     for (int h = 0; h < RL; ++h) {
       const int r = lane + 32 * h;
-      len[h] = r < n ? run_start[k0 + r + 1] - run_start[k0 + r] : -1;
+      const long long s0 = r < n ? run_start[k0 + r] : 0;
+      len[h] = r < n ? (int)(run_start[k0 + r + 1] - s0) : -1;
       rank[h] = 0;
       // the run's word: chunk-local first entry | length << 16
-      if (r < n) run_fn[k0 + r] = (uint32_t)(run_start[k0 + r] - run_start[k0]) | ((uint32_t)len[h] << 16);
+      if (r < n) run_fn[k0 + r] = (uint32_t)(s0 - e0) | ((uint32_t)len[h] << 16);
     }
 #pragma unroll
     for (int hj = 0; hj < RL; ++hj) {
+      if (32 * hj >= n) break;  // warp-uniform
 #pragma unroll 8
       for (int j = 0; j < 32; ++j) {
-        const long long lj = __shfl_sync(0xffffffffu, len[hj], j);
+        const int lj = __shfl_sync(0xffffffffu, len[hj], j);
         const int rj = j + 32 * hj;
 #pragma unroll
         for (int h = 0; h < RL; ++h) rank[h] += (lj > len[h]) || (lj == len[h] && rj < lane + 32 * h);
