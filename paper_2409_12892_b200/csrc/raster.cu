@@ -374,8 +374,11 @@ __device__ __forceinline__ unsigned transpose32(unsigned x, int lane) {
 #define RW (RB / 32)
 template <bool FILL>
 __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
-  __shared__ double s_mx[RB], s_my[RB], s_ca[RB], s_cb[RB], s_cc[RB], s_o[RB];
-  __shared__ double s_c0[RB], s_c1[RB], s_c2[RB];
+  // per-instance fp64 staging, one array each so that every access is one
+  // base + k * 16 (or 8) with immediate offsets: (mx, my), (ca, 2 cb), (cc, o)
+  // and the colour (c0, c1, c2); 2 cb is exact, so q is bit-identical
+  __shared__ double2 s_geo[3 * RB];
+  __shared__ double s_col[3 * RB];
   __shared__ int4 s_box[RB];
   __shared__ uint32_t s_gid[RB];
   __shared__ uint32_t s_mask[RB * RW];              // keep masks of the batch (COUNT out, FILL in)
@@ -433,10 +436,12 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
     if (j < rng.y) {
       uint32_t g = A.inst_gid[j];
       const SlmSplat s = A.splats[g];
-      s_mx[threadIdx.x] = s.mx; s_my[threadIdx.x] = s.my;
-      s_ca[threadIdx.x] = s.ca; s_cb[threadIdx.x] = s.cb; s_cc[threadIdx.x] = s.cc;
-      s_o[threadIdx.x] = s.o;
-      s_c0[threadIdx.x] = s.c0; s_c1[threadIdx.x] = s.c1; s_c2[threadIdx.x] = s.c2;
+      s_geo[threadIdx.x] = make_double2(s.mx, s.my);
+      s_geo[RB + threadIdx.x] = make_double2(s.ca, 2.0 * s.cb);
+      s_geo[2 * RB + threadIdx.x] = make_double2(s.cc, s.o);
+      s_col[threadIdx.x] = s.c0;
+      s_col[RB + threadIdx.x] = s.c1;
+      s_col[2 * RB + threadIdx.x] = s.c2;
       s_box[threadIdx.x] = make_int4(s.x0, s.x1, s.y0, s.y1);
       s_gid[threadIdx.x] = g;
       if (FILL) {
@@ -505,19 +510,20 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
           const int i = __ffs(wq) - 1;
           const int k = s_list[warp][b0 + i];
           wq &= wq - 1u;
-          const double dx = __dsub_rn(dxp, s_mx[k]);
-          const double dy = __dsub_rn(dyp, s_my[k]);
-          const double q = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(s_ca[k], dx), dx), __dmul_rn(s_cc[k], __dmul_rn(dy, dy))),
-                                     __dmul_rn(__dmul_rn(__dmul_rn(2.0, s_cb[k]), dy), dx));
+          const double2 g0 = s_geo[k], g1 = s_geo[RB + k], g2 = s_geo[2 * RB + k];
+          const double dx = __dsub_rn(dxp, g0.x);
+          const double dy = __dsub_rn(dyp, g0.y);
+          const double q = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(g1.x, dx), dx), __dmul_rn(g2.x, __dmul_rn(dy, dy))),
+                                     __dmul_rn(__dmul_rn(g1.y, dy), dx));
           const double ex = __dmul_rn(-0.5, q);
-          double a = ex >= -40.0 ? __dmul_rn(s_o[k], slm_exp_neg(ex)) : (tail ? __dmul_rn(s_o[k], exp(ex)) : 0.0);
+          double a = ex >= -40.0 ? __dmul_rn(g2.y, slm_exp_neg(ex)) : (tail ? __dmul_rn(g2.y, exp(ex)) : 0.0);
           a = a < aclamp ? a : aclamp;
           if ((a >= amin) && (a > 0.0)) {  // T >= t_stop holds while the lane is not done
             kw |= 1u << i;
             const double wgt = __dmul_rn(a, T);
-            C0 = __dadd_rn(C0, __dmul_rn(wgt, s_c0[k]));
-            C1 = __dadd_rn(C1, __dmul_rn(wgt, s_c1[k]));
-            C2 = __dadd_rn(C2, __dmul_rn(wgt, s_c2[k]));
+            C0 = __dadd_rn(C0, __dmul_rn(wgt, s_col[k]));
+            C1 = __dadd_rn(C1, __dmul_rn(wgt, s_col[RB + k]));
+            C2 = __dadd_rn(C2, __dmul_rn(wgt, s_col[2 * RB + k]));
             T = __dmul_rn(T, 1.0 - a);
             ++cnt;
             if (T < tstop) {
@@ -542,17 +548,19 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
           if (wq == 0u) continue;
           const int k = s_list[warp][b0 + __ffs(wq) - 1];
           wq &= wq - 1u;
-          const double dx = __dsub_rn(dxp, s_mx[k]);
-          const double dy = __dsub_rn(dyp, s_my[k]);
-          const double q = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(s_ca[k], dx), dx), __dmul_rn(s_cc[k], __dmul_rn(dy, dy))),
-                                     __dmul_rn(__dmul_rn(__dmul_rn(2.0, s_cb[k]), dy), dx));
+          const double2 g0 = s_geo[k], g1 = s_geo[RB + k], g2 = s_geo[2 * RB + k];
+          const double dx = __dsub_rn(dxp, g0.x);
+          const double dy = __dsub_rn(dyp, g0.y);
+          const double q = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(g1.x, dx), dx), __dmul_rn(g2.x, __dmul_rn(dy, dy))),
+                                     __dmul_rn(__dmul_rn(g1.y, dy), dx));
           const double ex = __dmul_rn(-0.5, q);
-          double a = ex >= -40.0 ? __dmul_rn(s_o[k], slm_exp_neg(ex)) : (tail ? __dmul_rn(s_o[k], exp(ex)) : 0.0);
+          double a = ex >= -40.0 ? __dmul_rn(g2.y, slm_exp_neg(ex)) : (tail ? __dmul_rn(g2.y, exp(ex)) : 0.0);
           a = a < aclamp ? a : aclamp;
           const double wgt = __dmul_rn(a, T);
-          C0 = __dadd_rn(C0, __dmul_rn(wgt, s_c0[k]));
-          C1 = __dadd_rn(C1, __dmul_rn(wgt, s_c1[k]));
-          C2 = __dadd_rn(C2, __dmul_rn(wgt, s_c2[k]));
+          const double c0 = s_col[k], c1 = s_col[RB + k], c2 = s_col[2 * RB + k];
+          C0 = __dadd_rn(C0, __dmul_rn(wgt, c0));
+          C1 = __dadd_rn(C1, __dmul_rn(wgt, c1));
+          C2 = __dadd_rn(C2, __dmul_rn(wgt, c2));
           if (A.rec4) {
             const unsigned m = s_mask[k * RW + warp];
             const double iom = 1.0 / (1.0 - a);  // stored values are fp32: one fp64 reciprocal suffices
@@ -567,9 +575,9 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
               dest -= A.e_hbase;
             }
             r4[dest] = make_float4(a < aclamp ? (float)a : 0.0f, (float)wgt,
-                                   (float)(s_c0[k] * T - (tot0 - C0) * iom),
-                                   (float)(s_c1[k] * T - (tot1 - C1) * iom));
-            rd2[dest] = (float)(s_c2[k] * T - (tot2 - C2) * iom);
+                                   (float)(c0 * T - (tot0 - C0) * iom),
+                                   (float)(c1 * T - (tot1 - C1) * iom));
+            rd2[dest] = (float)(c2 * T - (tot2 - C2) * iom);
             rpx[dest] = (uint8_t)threadIdx.x;
           }
           if (A.trav_gid) {
