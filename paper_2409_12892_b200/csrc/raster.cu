@@ -372,6 +372,19 @@ __device__ __forceinline__ unsigned transpose32(unsigned x, int lane) {
 
 #define RB 256
 #define RW (RB / 32)
+
+// 16-byte shared load at a 32-bit shared-window address (one IMAD per
+// instance instead of re-forming the generic window address per access)
+__device__ __forceinline__ double2 lds2(unsigned a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double lds1(unsigned a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
 template <bool FILL>
 __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
   // per-instance fp64 staging, one array each so that every access is one
@@ -379,6 +392,8 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
   // and the colour (c0, c1, c2); 2 cb is exact, so q is bit-identical
   __shared__ double2 s_geo[3 * RB];
   __shared__ double s_col[3 * RB];
+  unsigned a_geo = (unsigned)__cvta_generic_to_shared(s_geo), a_col = (unsigned)__cvta_generic_to_shared(s_col);
+  asm volatile("" : "+r"(a_geo), "+r"(a_col));  // opaque: kept in registers, not re-formed per access
   __shared__ int4 s_box[RB];
   __shared__ uint32_t s_gid[RB];
   __shared__ uint32_t s_mask[RB * RW];              // keep masks of the batch (COUNT out, FILL in)
@@ -510,7 +525,8 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
           const int i = __ffs(wq) - 1;
           const int k = s_list[warp][b0 + i];
           wq &= wq - 1u;
-          const double2 g0 = s_geo[k], g1 = s_geo[RB + k], g2 = s_geo[2 * RB + k];
+          const unsigned ag = a_geo + 16u * k;
+          const double2 g0 = lds2(ag), g1 = lds2(ag + 16u * RB), g2 = lds2(ag + 32u * RB);
           const double dx = __dsub_rn(dxp, g0.x);
           const double dy = __dsub_rn(dyp, g0.y);
           const double q = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(g1.x, dx), dx), __dmul_rn(g2.x, __dmul_rn(dy, dy))),
@@ -521,9 +537,10 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
           if ((a >= amin) && (a > 0.0)) {  // T >= t_stop holds while the lane is not done
             kw |= 1u << i;
             const double wgt = __dmul_rn(a, T);
-            C0 = __dadd_rn(C0, __dmul_rn(wgt, s_col[k]));
-            C1 = __dadd_rn(C1, __dmul_rn(wgt, s_col[RB + k]));
-            C2 = __dadd_rn(C2, __dmul_rn(wgt, s_col[2 * RB + k]));
+            const unsigned ac = a_col + 8u * k;
+            C0 = __dadd_rn(C0, __dmul_rn(wgt, lds1(ac)));
+            C1 = __dadd_rn(C1, __dmul_rn(wgt, lds1(ac + 8u * RB)));
+            C2 = __dadd_rn(C2, __dmul_rn(wgt, lds1(ac + 16u * RB)));
             T = __dmul_rn(T, 1.0 - a);
             ++cnt;
             if (T < tstop) {
@@ -548,7 +565,8 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
           if (wq == 0u) continue;
           const int k = s_list[warp][b0 + __ffs(wq) - 1];
           wq &= wq - 1u;
-          const double2 g0 = s_geo[k], g1 = s_geo[RB + k], g2 = s_geo[2 * RB + k];
+          const unsigned ag = a_geo + 16u * k;
+          const double2 g0 = lds2(ag), g1 = lds2(ag + 16u * RB), g2 = lds2(ag + 32u * RB);
           const double dx = __dsub_rn(dxp, g0.x);
           const double dy = __dsub_rn(dyp, g0.y);
           const double q = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(g1.x, dx), dx), __dmul_rn(g2.x, __dmul_rn(dy, dy))),
@@ -557,7 +575,8 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
           double a = ex >= -40.0 ? __dmul_rn(g2.y, slm_exp_neg(ex)) : (tail ? __dmul_rn(g2.y, exp(ex)) : 0.0);
           a = a < aclamp ? a : aclamp;
           const double wgt = __dmul_rn(a, T);
-          const double c0 = s_col[k], c1 = s_col[RB + k], c2 = s_col[2 * RB + k];
+          const unsigned ac = a_col + 8u * k;
+          const double c0 = lds1(ac), c1 = lds1(ac + 8u * RB), c2 = lds1(ac + 16u * RB);
           C0 = __dadd_rn(C0, __dmul_rn(wgt, c0));
           C1 = __dadd_rn(C1, __dmul_rn(wgt, c1));
           C2 = __dadd_rn(C2, __dmul_rn(wgt, c2));
