@@ -8,7 +8,7 @@
 #define SLM_PM_MINB 4
 #endif
 #ifndef SLM_BW_MINB
-#define SLM_BW_MINB 4
+#define SLM_BW_MINB 6
 #endif
 #ifndef SLM_BW1_MINB
 #define SLM_BW1_MINB 3   // the diag backward (moments + chain per pair) keeps more registers
@@ -36,10 +36,12 @@ struct Tab {
 // Precomputed once per cache (k_gauss_tab) together with the position and the
 // SH coefficients, so the per-(gaussian, view) chain reads one contiguous,
 // 16-byte aligned row per gaussian (gtab_floats(K) floats):
-//   [Rg 9 | s2 3 | Mq 36 | dopa | pos 3 | SH coefficients 3K (channel-major), pad]
+//   [Rg 9 | s2 3 | Mq 36 | dopa | pos 3 | Sigma_world 6 (xx xy xz yy yz zz), pad 2 |
+//    SH coefficients 3K (channel-major), pad]
 #define GT_DOPA 48
 #define GT_POS 49
-#define GT_SH 52
+#define GT_SIG 52
+#define GT_SH 60
 __host__ __device__ constexpr int gtab_floats(int K) { return GT_SH + ((3 * K + 3) & ~3); }
 template <typename Rt>
 __device__ __forceinline__ void gauss_static(const float* __restrict__ xs, long long G, long long g, Rt (&Rg)[9],
@@ -92,6 +94,17 @@ static __global__ void __launch_bounds__(256) k_gauss_tab(const float* __restric
     o[GT_DOPA] = dopa;
 #pragma unroll
     for (int i = 0; i < 3; ++i) o[GT_POS + i] = xs[i * G + g];
+    // world covariance Sigma = Rg diag(s2) Rg^T (upper triangle)
+    {
+      int k = 0;
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = i; j < 3; ++j, ++k)
+          o[GT_SIG + k] = Rg[i * 3] * s2[0] * Rg[j * 3] + Rg[i * 3 + 1] * s2[1] * Rg[j * 3 + 1] +
+                          Rg[i * 3 + 2] * s2[2] * Rg[j * 3 + 2];
+      o[GT_SIG + 6] = o[GT_SIG + 7] = 0.f;
+    }
 #pragma unroll
     for (int i = GT_SH; i < GT; ++i) o[i] = i - GT_SH < 3 * K ? xs[(long long)(11 + i - GT_SH) * G + g] : 0.f;
     float4* dst = reinterpret_cast<float4*>(gtab + (size_t)g * GT);
@@ -242,6 +255,116 @@ __device__ __forceinline__ void pair_tab(const float* __restrict__ xs, long long
     T.dcol[ch][2] = T.mask[ch] * (dcdd[ch][2] - d2 * dd) * ivn;
   }
   T.dopa = dopa;
+}
+
+// Backward row of one (gaussian, view) pair for the J^T chain (ref:
+// jacobian.py:314-353) from its 9 run-partial sums a = (a_mu (2), a_cov (3,
+// 1/2-scaled on 0 and 2), a_opa, a_col (3)), in the world-covariance form:
+//   row[0..2]  position: U^T a_mu + dcov_pos^T a_cov + (I - d d^T)/|v| grad_d
+//              (sum_k ct_k Y_k), ct_k = sum_ch mask_ch a_col,ch coef(ch, k)
+//   row[3..8]  B = U^T Abar U (Abar = [[a_c0, a_c1/2], [a_c1/2, a_c2]]): the
+//              gradient w.r.t. the world covariance, upper triangle; summed
+//              over the gaussian's pairs and turned into the quaternion /
+//              log-scale gradients once per gaussian (k_gm_to_am)
+//   row[9]     opacity sigma' a_opa;  row[10 + ch K + k] SH a_col,ch mask_ch Y_k
+// (P - 1 values).  The camera-frame covariance comes from the chain row's
+// Sigma_world, so the per-pair work has no rotation / scale chain.
+template <int K>
+__device__ __forceinline__ void pair_back_row(long long g, const SlmCamera& cam, uint32_t clampbits,
+                                              const float (&a)[9], const float* __restrict__ gtab, float* row) {
+  constexpr int GT = gtab_floats(K);
+  const float* grow = gtab + (size_t)g * GT;
+  float t[16];
+  ldg_row<4>(grow + GT_DOPA, t);       // dopa, position
+  ldg_row<8>(grow + GT_SIG, t + 4);    // Sigma_world
+  const float dopa = t[0], p0 = t[1], p1 = t[2], p2 = t[3];
+  const float Sw[9] = {t[4], t[5], t[6], t[5], t[7], t[8], t[6], t[8], t[9]};
+  float R[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) R[i] = (float)cam.R[i];
+  const float fx = (float)cam.fx, fy = (float)cam.fy;
+  const float X = R[0] * p0 + R[1] * p1 + R[2] * p2 + (float)cam.t[0];
+  const float Yc = R[3] * p0 + R[4] * p1 + R[5] * p2 + (float)cam.t[1];
+  const float Z = R[6] * p0 + R[7] * p1 + R[8] * p2 + (float)cam.t[2];
+  const float iz = 1.f / Z, iz2 = iz * iz;
+  const float A00 = fx * iz, A02 = -fx * X * iz2, A11 = fy * iz, A12 = -fy * Yc * iz2;
+  float U[2][3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    U[0][j] = A00 * R[j] + A02 * R[6 + j];
+    U[1][j] = A11 * R[3 + j] + A12 * R[6 + j];
+  }
+  // camera-frame covariance Sc = R Sigma R^T, P = Sc A^T
+  float RS[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) RS[i * 3 + j] = R[i * 3] * Sw[j] + R[i * 3 + 1] * Sw[3 + j] + R[i * 3 + 2] * Sw[6 + j];
+  float Sc[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) Sc[i * 3 + k] = RS[i * 3] * R[k * 3] + RS[i * 3 + 1] * R[k * 3 + 1] + RS[i * 3 + 2] * R[k * 3 + 2];
+  float P[3][2];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    P[i][0] = Sc[i * 3] * A00 + Sc[i * 3 + 2] * A02;
+    P[i][1] = Sc[i * 3 + 1] * A11 + Sc[i * 3 + 2] * A12;
+  }
+  const float cxx = -fx * iz2, cyy = -fy * iz2;
+  const float kx = 2.f * fx * X * iz2 * iz, ky = 2.f * fy * Yc * iz2 * iz;
+  float dX[3][3];
+  dX[0][0] = 2.f * cxx * P[2][0]; dX[0][1] = cxx * P[2][1]; dX[0][2] = 0.f;
+  dX[1][0] = 0.f; dX[1][1] = cyy * P[2][0]; dX[1][2] = 2.f * cyy * P[2][1];
+  const float r00 = cxx * P[0][0] + kx * P[2][0], r01 = cxx * P[0][1] + kx * P[2][1];
+  const float r10 = cyy * P[1][0] + ky * P[2][0], r11 = cyy * P[1][1] + ky * P[2][1];
+  dX[2][0] = 2.f * r00; dX[2][1] = r01 + r10; dX[2][2] = 2.f * r11;
+  // a_cov through the camera-frame position: g_cam[r] = sum_p dX[r][p] a_cov[p]
+  float gc[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) gc[r] = dX[r][0] * a[2] + dX[r][1] * a[3] + dX[r][2] * a[4];
+  float pos[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j)
+    pos[j] = U[0][j] * a[0] + U[1][j] * a[1] + gc[0] * R[j] + gc[1] * R[3 + j] + gc[2] * R[6 + j];
+  // B = U^T Abar U
+  const float h = 0.5f * a[3];
+  float AU[2][3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    AU[0][j] = a[2] * U[0][j] + h * U[1][j];
+    AU[1][j] = h * U[0][j] + a[4] * U[1][j];
+  }
+  {
+    int k = 3;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = i; j < 3; ++j, ++k) row[k] = U[0][i] * AU[0][j] + U[1][i] * AU[1][j];
+  }
+  row[9] = dopa * a[5];
+  // colour: SH block and the view-direction (position) term
+  float sh[3 * K];
+  ldg_row<GT - GT_SH>(grow + GT_SH, sh);
+  const float v0 = p0 - (float)cam.C[0], v1 = p1 - (float)cam.C[1], v2 = p2 - (float)cam.C[2];
+  const float ivn = 1.f / sqrtf(v0 * v0 + v1 * v1 + v2 * v2);
+  const float d0 = v0 * ivn, d1 = v1 * ivn, d2 = v2 * ivn;
+  float Y[K];
+  sh_basis<float, K>(d0, d1, d2, Y);
+  float w[3];
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    w[ch] = (clampbits >> ch) & 1u ? 0.f : a[6 + ch];
+#pragma unroll
+    for (int k = 0; k < K; ++k) row[10 + ch * K + k] = w[ch] * Y[k];
+  }
+  float gd[1][3];
+  auto ct = [&](int, int k) { return w[0] * sh[k] + w[1] * sh[K + k] + w[2] * sh[2 * K + k]; };
+  sh_grad_dot1<K>(d0, d1, d2, ct, gd[0]);
+  const float dd = gd[0][0] * d0 + gd[0][1] * d1 + gd[0][2] * d2;
+  row[0] = pos[0] + (gd[0][0] - d0 * dd) * ivn;
+  row[1] = pos[1] + (gd[0][1] - d1 * dd) * ivn;
+  row[2] = pos[2] + (gd[0][2] - d2 * dd) * ivn;
 }
 
 // Forward chain of applyJ (ref: jacobian.py:434-443): thread per pair (pairs

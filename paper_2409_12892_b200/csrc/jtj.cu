@@ -32,7 +32,8 @@ template <int K, int MODE>
 __global__ void __launch_bounds__(32 * PK_WARPS, MODE == 0 ? SLM_BW_MINB : SLM_BW1_MINB) k_gauss_backward_packed(SlmBackArgs A, const int* __restrict__ warp_g0,
                                                                        int n_warps) {
   constexpr int P = 11 + 3 * K;
-  constexpr int PP = P > 32 ? 65 : 33;  // odd row stride, every lane's column pair inside the row
+  constexpr int PR = MODE == 0 ? P - 1 : P;  // row / scratch width (J^T: world-covariance form)
+  constexpr int PP = PR | 1;  // odd row stride: conflict-free row writes and column reads
   __shared__ float s_v[PK_WARPS][32 * PP];
   const unsigned F = 0xffffffffu;
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
@@ -42,9 +43,9 @@ __global__ void __launch_bounds__(32 * PK_WARPS, MODE == 0 ? SLM_BW_MINB : SLM_B
   // epilogue here -- per-lane attribute-strided p / M / out accesses -- was
   // measured 1.5x slower)
   auto flush = [&](long long g, float c0, float c1) {
-    float* o = A.gm + (size_t)g * P;
-    if (lane < P) o[lane] = c0;  // P < 32 below SH degree 2
-    if (lane + 32 < P) o[lane + 32] = c1;
+    float* o = A.gm + (size_t)g * PR;
+    if (lane < PR) o[lane] = c0;  // PR < 32 below SH degree 2
+    if (lane + 32 < PR) o[lane + 32] = c1;
   };
   for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n_warps; w += (gridDim.x * blockDim.x) >> 5) {
     const int ga = warp_g0[w], gb = warp_g0[w + 1];
@@ -71,21 +72,7 @@ __global__ void __launch_bounds__(32 * PK_WARPS, MODE == 0 ? SLM_BW_MINB : SLM_B
             a[4] += v.x; a[5] += v.y; a[6] += v.z; a[7] += v.w;
             a[8] += __ldg(A.pacc1 + rr);
           }
-          Tab<K> T;
-          pair_tab<K>(A.xs, G, myg, A.cams[vm & 0xffffu], vm >> 16, T, A.gtab);
-#pragma unroll
-          for (int j = 0; j < 3; ++j)
-            row[j] = T.dmu[0][j] * a[0] + T.dmu[1][j] * a[1] + T.dcol[0][j] * a[6] + T.dcol[1][j] * a[7] +
-                     T.dcol[2][j] * a[8] + T.dcov[0][j] * a[2] + T.dcov[1][j] * a[3] + T.dcov[2][j] * a[4];
-#pragma unroll
-          for (int j = 3; j < 10; ++j) row[j] = T.dcov[0][j] * a[2] + T.dcov[1][j] * a[3] + T.dcov[2][j] * a[4];
-          row[10] = T.dopa * a[5];
-#pragma unroll
-          for (int ch = 0; ch < 3; ++ch) {
-            const float sc = a[6 + ch] * T.mask[ch];
-#pragma unroll
-            for (int k = 0; k < K; ++k) row[11 + ch * K + k] = sc * T.Y[k];
-          }
+          pair_back_row<K>(myg, A.cams[vm & 0xffffu], vm >> 16, a, A.gtab, row);
         } else {
           // diag from the run moments (stream.cu diag pass): S (5x5 upper
           // triangle), V_ch (3 x 5), T3_ch, O / o^2; the pair's chain applied
@@ -174,12 +161,12 @@ __global__ void __launch_bounds__(32 * PK_WARPS, MODE == 0 ? SLM_BW_MINB : SLM_B
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             c0 += r[k * PP];
-            if (P > 32) c1 += r[k * PP + 32];
+            if (PR > 32 && lane + 32 < PR) c1 += r[k * PP + 32];
           }
         }
         for (; i < i1; ++i, r += PP) {
           c0 += r[0];
-          if (P > 32) c1 += r[32];
+          if (PR > 32 && lane + 32 < PR) c1 += r[32];
         }
       }
       __syncwarp();
@@ -195,9 +182,18 @@ __global__ void __launch_bounds__(32 * PK_WARPS, MODE == 0 ? SLM_BW_MINB : SLM_B
 // gaussian-major scratch -> attribute-major out (tiled transpose, 32 gaussians
 // per tile) with out = scale * v (+ lam * max(M, 1e-12) * p) and fp64 partials
 // of p.(v + lam Mf p)
-template <int P>
+// gaussian-major scratch -> attribute-major out (tiled transpose, 32 gaussians
+// per tile) with out = scale * v (+ lam * max(M, 1e-12) * p) and fp64 partials
+// of p.(v + lam Mf p).  MODE 0 (J^T): the scratch rows are in the
+// world-covariance form (pair_back_row); each gaussian's quaternion and
+// log-scale gradients are formed here from its summed B = dL/dSigma:
+//   Sigma = Rg S^2 Rg^T:  dL/dq_l = 2 <B Rg S^2, Mq_l>_F,
+//                          dL/dlog s_i = 2 s_i^2 r_i^T B r_i
+template <int P, int MODE>
 __global__ void __launch_bounds__(256) k_gm_to_am(SlmBackArgs A) {
+  constexpr int PR = MODE == 0 ? P - 1 : P;
   constexpr int TS = P | 1;  // odd tile stride: conflict-free column reads
+  constexpr int K = (P - 11) / 3;
   __shared__ float t[32 * TS];
   __shared__ double sm[32];
   const long long G = A.G;
@@ -205,7 +201,44 @@ __global__ void __launch_bounds__(256) k_gm_to_am(SlmBackArgs A) {
   for (long long g0 = (long long)blockIdx.x * 32; g0 < G; g0 += (long long)gridDim.x * 32) {
     const int ng = (int)min((long long)32, G - g0);
     __syncthreads();
-    if (ng == 32) {
+    if (MODE == 0) {
+      // rows land at attribute positions: pos 0-2, B -> 3-8 (temporarily),
+      // opacity 9 -> 10, SH 10.. -> 11..
+      for (int i = threadIdx.x; i < ng * PR; i += blockDim.x) {
+        const int gl = i / PR, c = i % PR;
+        t[gl * TS + (c < 9 ? c : c + 1)] = A.gm[(size_t)g0 * PR + i];
+      }
+      __syncthreads();
+      if (threadIdx.x < ng) {
+        float* r = t + threadIdx.x * TS;
+        const float* gt = A.gtab + (size_t)(g0 + threadIdx.x) * gtab_floats(K);
+        float Rg[9], s2[3];
+#pragma unroll
+        for (int i = 0; i < 9; ++i) Rg[i] = gt[i];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) s2[i] = gt[9 + i];
+        const float B[9] = {r[3], r[4], r[5], r[4], r[6], r[7], r[5], r[7], r[8]};
+        float T[9];  // B Rg S^2
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+            T[i * 3 + j] = (B[i * 3] * Rg[j] + B[i * 3 + 1] * Rg[3 + j] + B[i * 3 + 2] * Rg[6 + j]) * s2[j];
+        float gs[3];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) gs[j] = 2.f * (Rg[j] * T[j] + Rg[3 + j] * T[3 + j] + Rg[6 + j] * T[6 + j]);
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+          float q = 0.f;
+#pragma unroll
+          for (int i = 0; i < 9; ++i) q = fmaf(T[i], gt[12 + l * 9 + i], q);
+          r[3 + l] = 2.f * q;
+        }
+        r[7] = gs[0];
+        r[8] = gs[1];
+        r[9] = gs[2];
+      }
+    } else if (ng == 32) {
       // full tile: 32 consecutive rows = 8 * P float4 (16-byte aligned: g0 % 32 == 0)
       const float4* src = reinterpret_cast<const float4*>(A.gm + (size_t)g0 * P);
       for (int i = threadIdx.x; i < 8 * P; i += blockDim.x) {
@@ -303,7 +336,10 @@ int slm_pair_backward(const SlmBackArgs* a, int mode, int sh_degree, cudaStream_
     k_gauss_backward_packed<KK, 0><<<b, 32 * PK_WARPS, 0, st>>>(*a, a->warp_g0, nw);       \
   else                                                                                     \
     k_gauss_backward_packed<KK, 1><<<b, 32 * PK_WARPS, 0, st>>>(*a, a->warp_g0, nw);       \
-  k_gm_to_am<11 + 3 * KK><<<b, 256, 0, st>>>(*a);
+  if (mode == 0)                                                                           \
+    k_gm_to_am<11 + 3 * KK, 0><<<b, 256, 0, st>>>(*a);                                     \
+  else                                                                                     \
+    k_gm_to_am<11 + 3 * KK, 1><<<b, 256, 0, st>>>(*a);
   switch (sh_degree) {
     case 0: SLM_PK(1) break;
     case 1: SLM_PK(4) break;
