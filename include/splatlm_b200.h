@@ -198,6 +198,7 @@ typedef struct {
   long long sa, sg;
   void* pm;                 /* [P*12] out: m = dy/dx p per pair (3 float4) */
   const float* gtab;        /* per-gaussian chain rows (slm_gauss_tab) */
+  int dsig;                 /* 1: p is the padded gaussian-major copy with dSigma (slm_pcg_p*) */
 } SlmFwdArgs;
 
 /* per-gaussian backward chain */
@@ -368,11 +369,16 @@ int slm_pair_backward(const SlmBackArgs* a, int mode, int sh_degree, cudaStream_
 /* ---- PCG (Alg. 1; SPEC pcg_solve 391-399) ------------------ */
 int slm_vec_blocks(void);
 /* p (attribute-major, G*P) and, when p_gm != NULL, its padded gaussian-major
- * copy p_gm[g * pg + a] (pg = slm_gm_stride(P), pad 0) for the forward chain */
+ * copy p_gm[g * pg + a] (pg = slm_gm_stride(P), pad 0) for the forward chain;
+ * with gtab (the cache's chain rows, slm_gauss_tab) each row also carries the
+ * world-covariance perturbation of the rotation / scale block at ((P+3) & ~3) */
 int slm_gm_stride(int P);
-int slm_pcg_pinit(float* p, float* p_gm, const float* b, const float* M, long long G, int P, cudaStream_t s);
+int slm_pcg_pinit(float* p, float* p_gm, const float* b, const float* M, long long G, int P, const float* gtab,
+                  int gtab_stride, cudaStream_t s);
 int slm_pcg_pupdate(float* p, float* p_gm, const double* r, const float* M, const double* st, long long G, int P,
-                    cudaStream_t s);
+                    const float* gtab, int gtab_stride, cudaStream_t s);
+/* the same padded gaussian-major copy (+ dSigma) of a given attribute-major p */
+int slm_gm_pack(const float* p, float* p_gm, long long G, int P, const float* gtab, int gtab_stride, cudaStream_t s);
 int slm_pcg_update(int mode, double* x, double* r, const float* p, const float* g, const float* b, const float* M,
                    double lam, double* st, const double* dot_part, int n_dot, double* part, long long n,
                    cudaStream_t s);

@@ -70,7 +70,8 @@ class SlmTileArgs(C.Structure):
 
 class SlmFwdArgs(C.Structure):
     _fields_ = [("xs", c_vp), ("G", c_ll), ("pair_gid", c_vp), ("pair_vm", c_vp), ("cams", c_vp), ("n_pairs", c_i),
-                ("p", c_vp), ("sa", c_ll), ("sg", c_ll), ("pm", c_vp), ("gtab", c_vp)]
+                ("p", c_vp), ("sa", c_ll), ("sg", c_ll), ("pm", c_vp), ("gtab", c_vp),
+                ("dsig", c_i)]
 
 
 class SlmBackArgs(C.Structure):
@@ -138,8 +139,9 @@ _SIGS = {
     "slm_pair_backward": (c_i, [c_vp, c_i, c_i, c_vp]),
     "slm_vec_blocks": (c_i, []),
     "slm_gm_stride": (c_i, [c_i]),
-    "slm_pcg_pinit": (c_i, [c_vp, c_vp, c_vp, c_vp, c_ll, c_i, c_vp]),
-    "slm_pcg_pupdate": (c_i, [c_vp, c_vp, c_vp, c_vp, c_vp, c_ll, c_i, c_vp]),
+    "slm_gm_pack": (c_i, [c_vp, c_vp, c_ll, c_i, c_vp, c_i, c_vp]),
+    "slm_pcg_pinit": (c_i, [c_vp, c_vp, c_vp, c_vp, c_ll, c_i, c_vp, c_i, c_vp]),
+    "slm_pcg_pupdate": (c_i, [c_vp, c_vp, c_vp, c_vp, c_vp, c_ll, c_i, c_vp, c_i, c_vp]),
     "slm_pcg_update": (c_i, [c_i, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_d, c_vp, c_vp, c_i, c_vp, c_ll, c_vp]),
     "slm_pcg_finalize": (c_i, [c_i, c_vp, c_vp, c_vp]),
     "slm_combine_acc": (c_i, [c_vp, c_vp, c_vp, c_vp, c_ll, c_vp]),

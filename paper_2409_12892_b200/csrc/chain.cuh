@@ -367,6 +367,105 @@ __device__ __forceinline__ void pair_back_row(long long g, const SlmCamera& cam,
   row[2] = pos[2] + (gd[0][2] - d2 * dd) * ivn;
 }
 
+// Forward chain m = dy/dx p of one pair from the padded gaussian-major p row
+// that carries dSigma (k_pcg_p with the chain rows): the camera-dependent
+// part only -- m_mu = U p_pos, m_cov = dcov_pos p_pos + U dSigma U^T, m_col =
+// mask (sum_k coef_k dY_k(dd) + p_sh,k Y_k) with dd = (I - d d^T) p_pos / |v|
+// the view-direction perturbation (ref: jacobian.py:434-443).
+template <int K>
+__device__ __forceinline__ void pair_fwd_dsig(long long g, const SlmCamera& cam, uint32_t clampbits,
+                                              const float* __restrict__ gtab, const float* __restrict__ prow,
+                                              float4* __restrict__ out) {
+  constexpr int GT = gtab_floats(K), P = 11 + 3 * K, DS = (P + 3) & ~3;
+  const float* grow = gtab + (size_t)g * GT;
+  float t[12];
+  ldg_row<4>(grow + GT_DOPA, t);       // dopa, position
+  ldg_row<8>(grow + GT_SIG, t + 4);    // Sigma_world
+  float pp[12];
+  ldg_row<12>(prow, pp);               // p_pos 3, p_q 4, p_s 3, p_opa, p_sh[0]
+  float ds[8];
+  ldg_row<8>(prow + DS, ds);           // dSigma
+  const float dopa = t[0], p0 = t[1], p1 = t[2], p2 = t[3];
+  const float Sw[9] = {t[4], t[5], t[6], t[5], t[7], t[8], t[6], t[8], t[9]};
+  float R[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) R[i] = (float)cam.R[i];
+  const float fx = (float)cam.fx, fy = (float)cam.fy;
+  const float X = R[0] * p0 + R[1] * p1 + R[2] * p2 + (float)cam.t[0];
+  const float Yc = R[3] * p0 + R[4] * p1 + R[5] * p2 + (float)cam.t[1];
+  const float Z = R[6] * p0 + R[7] * p1 + R[8] * p2 + (float)cam.t[2];
+  const float iz = 1.f / Z, iz2 = iz * iz;
+  const float A00 = fx * iz, A02 = -fx * X * iz2, A11 = fy * iz, A12 = -fy * Yc * iz2;
+  float U[2][3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    U[0][j] = A00 * R[j] + A02 * R[6 + j];
+    U[1][j] = A11 * R[3 + j] + A12 * R[6 + j];
+  }
+  float RS[9], Sc[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) RS[i * 3 + j] = R[i * 3] * Sw[j] + R[i * 3 + 1] * Sw[3 + j] + R[i * 3 + 2] * Sw[6 + j];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) Sc[i * 3 + k] = RS[i * 3] * R[k * 3] + RS[i * 3 + 1] * R[k * 3 + 1] + RS[i * 3 + 2] * R[k * 3 + 2];
+  float P2[3][2];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    P2[i][0] = Sc[i * 3] * A00 + Sc[i * 3 + 2] * A02;
+    P2[i][1] = Sc[i * 3 + 1] * A11 + Sc[i * 3 + 2] * A12;
+  }
+  const float cxx = -fx * iz2, cyy = -fy * iz2;
+  const float kx = 2.f * fx * X * iz2 * iz, ky = 2.f * fy * Yc * iz2 * iz;
+  float dX[3][3];
+  dX[0][0] = 2.f * cxx * P2[2][0]; dX[0][1] = cxx * P2[2][1]; dX[0][2] = 0.f;
+  dX[1][0] = 0.f; dX[1][1] = cyy * P2[2][0]; dX[1][2] = 2.f * cyy * P2[2][1];
+  const float r00 = cxx * P2[0][0] + kx * P2[2][0], r01 = cxx * P2[0][1] + kx * P2[2][1];
+  const float r10 = cyy * P2[1][0] + ky * P2[2][0], r11 = cyy * P2[1][1] + ky * P2[2][1];
+  dX[2][0] = 2.f * r00; dX[2][1] = r01 + r10; dX[2][2] = 2.f * r11;
+  // camera-frame position perturbation R p_pos, then the position part of m_cov
+  const float cp[3] = {R[0] * pp[0] + R[1] * pp[1] + R[2] * pp[2], R[3] * pp[0] + R[4] * pp[1] + R[5] * pp[2],
+                       R[6] * pp[0] + R[7] * pp[1] + R[8] * pp[2]};
+  float mc[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) mc[k] = dX[0][k] * cp[0] + dX[1][k] * cp[1] + dX[2][k] * cp[2];
+  // + U dSigma U^T
+  const float D[9] = {ds[0], ds[1], ds[2], ds[1], ds[3], ds[4], ds[2], ds[4], ds[5]};
+  float UD[2][3];
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) UD[r][j] = U[r][0] * D[j] + U[r][1] * D[3 + j] + U[r][2] * D[6 + j];
+  mc[0] += UD[0][0] * U[0][0] + UD[0][1] * U[0][1] + UD[0][2] * U[0][2];
+  mc[1] += UD[0][0] * U[1][0] + UD[0][1] * U[1][1] + UD[0][2] * U[1][2];
+  mc[2] += UD[1][0] * U[1][0] + UD[1][1] * U[1][1] + UD[1][2] * U[1][2];
+  const float mmu0 = U[0][0] * pp[0] + U[0][1] * pp[1] + U[0][2] * pp[2];
+  const float mmu1 = U[1][0] * pp[0] + U[1][1] * pp[1] + U[1][2] * pp[2];
+  // colour
+  const float v0 = p0 - (float)cam.C[0], v1 = p1 - (float)cam.C[1], v2 = p2 - (float)cam.C[2];
+  const float ivn = 1.f / sqrtf(v0 * v0 + v1 * v1 + v2 * v2);
+  const float d0 = v0 * ivn, d1 = v1 * ivn, d2 = v2 * ivn;
+  const float dp = d0 * pp[0] + d1 * pp[1] + d2 * pp[2];
+  float Y[K], dY[K];
+  sh_basis_dir<K>(d0, d1, d2, (pp[0] - d0 * dp) * ivn, (pp[1] - d1 * dp) * ivn, (pp[2] - d2 * dp) * ivn, Y, dY);
+  float sh[3 * K + 4], ps[3 * K + 4];
+  ldg_row<GT - GT_SH>(grow + GT_SH, sh);
+  ldg_row<(P - 11 + 3 + 4) / 4 * 4>(prow + 8, ps);  // p from attribute 8 (16-byte aligned): p_sh at ps[3..]
+  float mcol[3];
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    float sacc = 0.f;
+#pragma unroll
+    for (int k = 0; k < K; ++k) sacc = fmaf(sh[ch * K + k], dY[k], fmaf(ps[3 + ch * K + k], Y[k], sacc));
+    mcol[ch] = (clampbits >> ch) & 1u ? 0.f : sacc;
+  }
+  out[0] = make_float4(dopa * pp[10], mmu0, mmu1, 0.5f * mc[0]);
+  out[1] = make_float4(mc[1], 0.5f * mc[2], mcol[0], mcol[1]);
+  out[2] = make_float4(mcol[2], 0.f, 0.f, 0.f);
+}
+
 // Forward chain of applyJ (ref: jacobian.py:434-443): thread per pair (pairs
 // are (gid, view)-numbered, so neighbouring threads share the gaussian's
 // parameters), m = dy/dx p packed as 3 float4 (48 B).  The product kernel's
@@ -384,6 +483,10 @@ __global__ void __launch_bounds__(128, SLM_PM_MINB) k_pair_m(SlmFwdArgs A) {
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < A.n_pairs; q += gridDim.x * blockDim.x) {
     const long long g = A.pair_gid[q];
     const uint32_t vm = A.pair_vm[q];
+    if (A.dsig) {  // padded gaussian-major p with dSigma: camera-dependent chain only
+      pair_fwd_dsig<K>(g, A.cams[vm & 0xffffu], vm >> 16, A.gtab, p + g * sg, pm + (size_t)q * 3);
+      continue;
+    }
     Tab<K> T;
     pair_tab<K>(A.xs, A.G, g, A.cams[vm & 0xffffu], vm >> 16, T, A.gtab);
     float pv[4 * P4];

@@ -27,8 +27,11 @@
 
 __device__ __forceinline__ float mfloor(float m) { return fmaxf(m, 1e-12f); }
 
-// padded gaussian-major stride of the forward chain's copy of p (16-byte rows)
-__host__ __device__ constexpr int gm_stride(int P) { return (P + 3) & ~3; }
+// padded gaussian-major stride of the forward chain's copy of p (16-byte
+// rows): P values, pad, then (with the chain rows) the 6 entries of the
+// world-covariance perturbation dSigma at GM_DSIG
+__host__ __device__ constexpr int gm_stride(int P) { return ((P + 3) & ~3) + 8; }
+#define GM_DSIG(P) (((P) + 3) & ~3)
 
 // p = r / Mf + beta * p  (INIT: p = x0 = b / Mf, Alg. 1 line 4), r fp64; p is
 // stored fp32 and used consistently as the search direction by the product,
@@ -36,14 +39,24 @@ __host__ __device__ constexpr int gm_stride(int P) { return (P + 3) & ~3; }
 // reads / writes coalesced over gaussians, and (p_gm != NULL) the tile is
 // transposed in shared memory to the padded gaussian-major rows the forward
 // chain loads with 16-byte loads.
-template <bool INIT>
+//
+// With the cache's per-gaussian chain rows (gtab, stride gts: Rg 9 | s2 3 |
+// Mq 36 at 0 / 9 / 12) each gaussian's row also gets the world-covariance
+// perturbation of p's rotation / scale block,
+//   dSigma = sum_l p_q,l (Mq_l S^2 Rg^T + (.)^T) + sum_i 2 s_i^2 p_s,i r_i r_i^T
+// (upper triangle), so the per-pair forward chain only maps it to the image
+// plane (U dSigma U^T) instead of chaining every rotation / scale column.
+#define P_INIT 0
+#define P_UPDATE 1
+#define P_COPY 2   // p_gm (+ dSigma) of a given attribute-major p, p untouched
+template <int MODE>
 __global__ void __launch_bounds__(256) k_pcg_p(float* __restrict__ p, float* __restrict__ p_gm,
                                                const double* __restrict__ r, const float* __restrict__ b,
                                                const float* __restrict__ M, const double* __restrict__ st,
-                                               long long G, int P) {
-  if (!INIT && st[ST_STOP] != 0.0) return;
+                                               long long G, int P, const float* __restrict__ gtab, int gts) {
+  if (MODE == P_UPDATE && st[ST_STOP] != 0.0) return;
   extern __shared__ float tile[];  // [32][PG + 1]
-  const double beta = INIT ? 0.0 : st[ST_BETA];
+  const double beta = MODE == P_UPDATE ? st[ST_BETA] : 0.0;
   const int PG = gm_stride(P), TS = PG + 1;
   for (long long g0 = (long long)blockIdx.x * 32; g0 < G; g0 += (long long)gridDim.x * 32) {
     const int ng = (int)min((long long)32, G - g0);
@@ -53,13 +66,45 @@ __global__ void __launch_bounds__(256) k_pcg_p(float* __restrict__ p, float* __r
       float v = 0.f;
       if (a < P && gl < ng) {
         const long long idx = (long long)a * G + g0 + gl;
-        v = INIT ? (float)((double)b[idx] / (double)mfloor(M[idx]))
-                 : (float)(r[idx] / (double)mfloor(M[idx]) + beta * (double)p[idx]);
-        p[idx] = v;
+        if (MODE == P_COPY) {
+          v = p[idx];
+        } else {
+          v = MODE == P_INIT ? (float)((double)b[idx] / (double)mfloor(M[idx]))
+                             : (float)(r[idx] / (double)mfloor(M[idx]) + beta * (double)p[idx]);
+          p[idx] = v;
+        }
       }
       tile[gl * TS + a] = v;
     }
     if (!p_gm) continue;
+    __syncthreads();
+    if (gtab && (int)threadIdx.x < ng) {
+      float* row = tile + threadIdx.x * TS;
+      const float* gt = gtab + (size_t)(g0 + threadIdx.x) * gts;
+      float Rg[9], s2[3], Mp[9];
+#pragma unroll
+      for (int i = 0; i < 9; ++i) Rg[i] = gt[i];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) s2[i] = gt[9 + i];
+#pragma unroll
+      for (int i = 0; i < 9; ++i)
+        Mp[i] = row[3] * gt[12 + i] + row[4] * gt[21 + i] + row[5] * gt[30 + i] + row[6] * gt[39 + i];
+      float W[9];  // Mp S^2 Rg^T
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          W[i * 3 + j] = Mp[i * 3] * s2[0] * Rg[j * 3] + Mp[i * 3 + 1] * s2[1] * Rg[j * 3 + 1] +
+                         Mp[i * 3 + 2] * s2[2] * Rg[j * 3 + 2];
+      const float cs[3] = {2.f * s2[0] * row[7], 2.f * s2[1] * row[8], 2.f * s2[2] * row[9]};
+      int k = 0;
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = i; j < 3; ++j, ++k)
+          row[GM_DSIG(P) + k] = W[i * 3 + j] + W[j * 3 + i] + cs[0] * Rg[i * 3] * Rg[j * 3] +
+                                cs[1] * Rg[i * 3 + 1] * Rg[j * 3 + 1] + cs[2] * Rg[i * 3 + 2] * Rg[j * 3 + 2];
+    }
     __syncthreads();
     for (int i = threadIdx.x; i < ng * PG; i += blockDim.x) p_gm[g0 * PG + i] = tile[(i / PG) * TS + i % PG];
   }
@@ -207,18 +252,27 @@ int slm_gm_stride(int P) { return gm_stride(P); }
 
 static unsigned p_blocks(long long G) { return (unsigned)std::min<long long>((G + 31) / 32, 148LL * 8); }
 
-int slm_pcg_pinit(float* p, float* p_gm, const float* b, const float* M, long long G, int P, cudaStream_t s) {
+int slm_pcg_pinit(float* p, float* p_gm, const float* b, const float* M, long long G, int P, const float* gtab,
+                  int gtab_stride, cudaStream_t s) {
   if (G <= 0) return SLM_OK;
   const size_t sm = (size_t)32 * (gm_stride(P) + 1) * sizeof(float);
-  k_pcg_p<true><<<p_blocks(G), 256, sm, s>>>(p, p_gm, nullptr, b, M, nullptr, G, P);
+  k_pcg_p<P_INIT><<<p_blocks(G), 256, sm, s>>>(p, p_gm, nullptr, b, M, nullptr, G, P, gtab, gtab_stride);
   return slm_cuda_status();
 }
 
 int slm_pcg_pupdate(float* p, float* p_gm, const double* r, const float* M, const double* st, long long G, int P,
-                    cudaStream_t s) {
+                    const float* gtab, int gtab_stride, cudaStream_t s) {
   if (G <= 0) return SLM_OK;
   const size_t sm = (size_t)32 * (gm_stride(P) + 1) * sizeof(float);
-  k_pcg_p<false><<<p_blocks(G), 256, sm, s>>>(p, p_gm, r, nullptr, M, st, G, P);
+  k_pcg_p<P_UPDATE><<<p_blocks(G), 256, sm, s>>>(p, p_gm, r, nullptr, M, st, G, P, gtab, gtab_stride);
+  return slm_cuda_status();
+}
+
+int slm_gm_pack(const float* p, float* p_gm, long long G, int P, const float* gtab, int gtab_stride, cudaStream_t s) {
+  if (G <= 0) return SLM_OK;
+  const size_t sm = (size_t)32 * (gm_stride(P) + 1) * sizeof(float);
+  k_pcg_p<P_COPY><<<p_blocks(G), 256, sm, s>>>(const_cast<float*>(p), p_gm, nullptr, nullptr, nullptr, nullptr, G, P,
+                                               gtab, gtab_stride);
   return slm_cuda_status();
 }
 

@@ -658,13 +658,24 @@ class CacheSet:
         a.xs, a.G = ptr(self.scene.x32()), G
         a.pair_gid, a.pair_vm, a.cams, a.n_pairs = ptr(self.pair_gid), ptr(self.pair_vm), ptr(self.cams_dev), \
             self.n_pairs
-        if p_gm is not None:
-            a.p, a.sa, a.sg = ptr(p_gm), 1, _lib.load().slm_gm_stride(P)
+        if p_gm is not None:   # written by slm_pcg_p* / gm_pack with this cache's chain rows
+            a.p, a.sa, a.sg, a.dsig = ptr(p_gm), 1, _lib.load().slm_gm_stride(P), 1
         else:
             a.p = ptr(p)
             a.sa, a.sg = (1, P) if gaussian_major else (G, 1)
         a.pm, a.gtab = ptr(self.pm), ptr(self.gtab)
         call("slm_pair_forward", _lib.byref(a), self.scene.sh_degree, stream_ptr())
+
+    @property
+    def gtab_stride(self) -> int:
+        return _lib.load().slm_gauss_tab_floats(self.scene.sh_degree)
+
+    def gm_pack(self, p: torch.Tensor) -> torch.Tensor:
+        """The padded gaussian-major copy of an attribute-major p with its
+        world-covariance perturbation, as the PCG p kernels write it."""
+        out = torch.empty(self.G * _lib.load().slm_gm_stride(self.P), dtype=torch.float32, device=self.device)
+        call("slm_gm_pack", ptr(p), ptr(out), self.G, self.P, ptr(self.gtab), self.gtab_stride, stream_ptr())
+        return out
 
     def _tile_args(self, with_m: bool = False) -> _lib.SlmTileArgs:
         a = _lib.SlmTileArgs()

@@ -112,7 +112,8 @@ def pcg_run(cache: CacheSet, b: torch.Tensor, M: torch.Tensor, lam: float, max_i
     s = stream_ptr()
     ws.st.zero_()
     # p := b / Mf  (= x0, Alg. 1 line 4); g0 = A x0
-    call("slm_pcg_pinit", ptr(ws.p), ptr(ws.p_gm), ptr(b), ptr(M), G, P, s)
+    gt, gts = (cache.gtab, cache.gtab_stride) if ws.p_gm is not None and cache.G > 0 else (None, 0)
+    call("slm_pcg_pinit", ptr(ws.p), ptr(ws.p_gm), ptr(b), ptr(M), G, P, ptr(gt), gts, s)
     _product(cache, ws.p, ws.g, lam, M, dot_part, timer, ws.p_gm)
     call("slm_pcg_update", 0, ptr(ws.x), ptr(ws.r), ptr(ws.p), ptr(ws.g), ptr(b), ptr(M), float(lam),
          ptr(ws.st), ptr(dot_part), nb, ptr(ws.part), n, s)
@@ -124,7 +125,7 @@ def pcg_run(cache: CacheSet, b: torch.Tensor, M: torch.Tensor, lam: float, max_i
     # drains between iterations; on an early exit the one product queued
     # ahead runs but its result is discarded by the gated update.
     for it in range(max_iters):
-        call("slm_pcg_pupdate", ptr(ws.p), ptr(ws.p_gm), ptr(ws.r), ptr(M), ptr(ws.st), G, P, s)
+        call("slm_pcg_pupdate", ptr(ws.p), ptr(ws.p_gm), ptr(ws.r), ptr(M), ptr(ws.st), G, P, ptr(gt), gts, s)
         _product(cache, ws.p, ws.g, lam, M, dot_part, timer, ws.p_gm)
         call("slm_pcg_update", 1, ptr(ws.x), ptr(ws.r), ptr(ws.p), ptr(ws.g), ptr(b), ptr(M), float(lam),
              ptr(ws.st), ptr(dot_part), nb, ptr(ws.part), n, s)

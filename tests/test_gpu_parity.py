@@ -344,3 +344,18 @@ def test_determinism_at_scale():
         del cs
     for a, b in zip(outs[0], outs[1]):
         assert torch.equal(a, b)
+
+
+def test_forward_chain_dsigma_path(prob, cacheset, oracle_views):
+    """The PCG path's forward chain (padded gaussian-major p carrying the
+    world-covariance perturbation, slm_gm_pack / slm_pcg_p*) gives the same
+    product as the attribute-major path and the oracle."""
+    s = prob["scene"]
+    p = np.random.default_rng(11).standard_normal(s.param_count)
+    pd = torch.from_numpy(p).float().cuda()
+    ref = O.jtwj(p, prob["osc"], [ov["gview"] for ov in oracle_views])
+    a, b = torch.empty_like(pd), torch.empty_like(pd)
+    cacheset.jtwj(pd, a)
+    cacheset.jtwj(pd, b, p_gm=cacheset.gm_pack(pd))
+    assert rel(b.cpu().numpy(), a.cpu().numpy()) < 1e-5
+    assert rel(b.cpu().numpy(), ref) < FTOL

@@ -64,10 +64,7 @@ def main():
         p = torch.randn(scene.param_count, device=dev)
         g = torch.empty_like(p)
         if args.product_only:
-            PG = _lib.load().slm_gm_stride(cs.P)
-            p_gm = torch.zeros(cs.G, PG, device=dev)
-            p_gm[:, :cs.P] = p.view(cs.P, cs.G).t()
-            p_gm = p_gm.reshape(-1)
+            p_gm = cs.gm_pack(p)
             dp = torch.zeros(_lib.load().slm_backward_blocks(cs.G), dtype=torch.float64, device=dev)
             cs.jtwj(p, g, 1e-4, M, dp, False, p_gm=p_gm)      # warm
             torch.cuda.synchronize()
@@ -79,10 +76,7 @@ def main():
             print(json.dumps(dict(phases, E=cs.E, N=cs.N, R=cs.R, pairs=cs.n_pairs, G=cs.G)))
             return
         # the padded gaussian-major copy the PCG p kernels hand to the product
-        PG = _lib.load().slm_gm_stride(cs.P)
-        p_gm = torch.zeros(cs.G, PG, device=dev)
-        p_gm[:, :cs.P] = p.view(cs.P, cs.G).t()
-        p_gm = p_gm.reshape(-1)
+        p_gm = cs.gm_pack(p)
         k = []
         for _ in range(3):
             e0 = ev()
