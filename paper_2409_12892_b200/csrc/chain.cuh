@@ -7,6 +7,9 @@
 #ifndef SLM_PM_MINB
 #define SLM_PM_MINB 4
 #endif
+#ifndef SLM_PMD_MINB
+#define SLM_PMD_MINB 5   // the dSigma forward chain (PCG path)
+#endif
 #ifndef SLM_BW_MINB
 #define SLM_BW_MINB 6
 #endif
@@ -473,8 +476,8 @@ __device__ __forceinline__ void pair_fwd_dsig(long long g, const SlmCamera& cam,
 // p is read either attribute-major / unpadded gaussian-major (p[a sa + g sg])
 // or, when sa = 1 and sg is a multiple of 4 >= P (the padded gaussian-major
 // copy the PCG kernels write), as 16-byte row loads.
-template <int K>
-__global__ void __launch_bounds__(128, SLM_PM_MINB) k_pair_m(SlmFwdArgs A) {
+template <int K, bool DSIG>
+__global__ void __launch_bounds__(128, DSIG ? SLM_PMD_MINB : SLM_PM_MINB) k_pair_m(SlmFwdArgs A) {
   constexpr int P = 11 + 3 * K, P4 = (P + 3) / 4;
   float4* __restrict__ pm = reinterpret_cast<float4*>(A.pm);
   const long long sa = A.sa, sg = A.sg;
@@ -483,7 +486,7 @@ __global__ void __launch_bounds__(128, SLM_PM_MINB) k_pair_m(SlmFwdArgs A) {
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < A.n_pairs; q += gridDim.x * blockDim.x) {
     const long long g = A.pair_gid[q];
     const uint32_t vm = A.pair_vm[q];
-    if (A.dsig) {  // padded gaussian-major p with dSigma: camera-dependent chain only
+    if (DSIG) {  // padded gaussian-major p with dSigma: camera-dependent chain only
       pair_fwd_dsig<K>(g, A.cams[vm & 0xffffu], vm >> 16, A.gtab, p + g * sg, pm + (size_t)q * 3);
       continue;
     }

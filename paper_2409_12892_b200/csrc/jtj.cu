@@ -309,13 +309,19 @@ int slm_pair_forward(const SlmFwdArgs* a, int sh_degree, cudaStream_t st) {
   if (a->n_pairs <= 0) return SLM_OK;
   if (!a->pm || !a->gtab) return SLM_ERR_ARG;
   unsigned b = slm_blocks(a->n_pairs, 128, 1LL << 30);
+#define SLM_PM(KK)                                  \
+  if (a->dsig)                                      \
+    k_pair_m<KK, true><<<b, 128, 0, st>>>(*a);      \
+  else                                              \
+    k_pair_m<KK, false><<<b, 128, 0, st>>>(*a);
   switch (sh_degree) {
-    case 0: k_pair_m<1><<<b, 128, 0, st>>>(*a); break;
-    case 1: k_pair_m<4><<<b, 128, 0, st>>>(*a); break;
-    case 2: k_pair_m<9><<<b, 128, 0, st>>>(*a); break;
-    case 3: k_pair_m<16><<<b, 128, 0, st>>>(*a); break;
+    case 0: SLM_PM(1) break;
+    case 1: SLM_PM(4) break;
+    case 2: SLM_PM(9) break;
+    case 3: SLM_PM(16) break;
     default: return SLM_ERR_ARG;
   }
+#undef SLM_PM
   return slm_cuda_status();
 }
 
