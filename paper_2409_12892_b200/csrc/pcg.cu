@@ -250,7 +250,7 @@ int slm_vec_blocks() { return VEC_BLOCKS; }
 
 int slm_gm_stride(int P) { return gm_stride(P); }
 
-static unsigned p_blocks(long long G) { return (unsigned)std::min<long long>((G + 31) / 32, 148LL * 8); }
+static unsigned p_blocks(long long G) { return (unsigned)std::min<long long>((G + 31) / 32, 1LL << 30); }  // one 32-gaussian tile per block
 
 int slm_pcg_pinit(float* p, float* p_gm, const float* b, const float* M, long long G, int P, const float* gtab,
                   int gtab_stride, cudaStream_t s) {
