@@ -582,7 +582,8 @@ __global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
           C2 = __dadd_rn(C2, __dmul_rn(wgt, c2));
           if (A.rec4) {
             const unsigned m = s_mask[k * RW + warp];
-            const double iom = 1.0 / (1.0 - a);  // stored values are fp32: one fp64 reciprocal suffices
+            // stored values are fp32: an fp32 reciprocal (1 ulp) suffices (a <= alpha_clamp = 0.99)
+            const double iom = (double)__frcp_rn((float)(1.0 - a));
             long long dest = s_start[k] + s_pre[k * RW + warp] + __popc(m & lanes_below);
             slm_f4* r4 = A.rec4;
             float* rd2 = A.rec_d2;
