@@ -79,6 +79,11 @@ class ClockSampler:
             self._p = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
+            # nvidia-smi's NVML start-up stalls the driver for tens of ms: let
+            # it finish (first row) before the caller opens the timed region
+            t_end = time.time() + 5.0
+            while not self.rows and time.time() < t_end:
+                time.sleep(0.01)
         except Exception:
             self._p = None
         return self
@@ -236,7 +241,7 @@ def run_ours(args, cfg):
         sc = GaussianScene(xs, scene.sh_degree, scene.background)
         # the images stay in pinned host memory: lm_direction copies each
         # subset's images on a side stream while the previous subset is solved
-        r = lm_direction(sc, cams, gts_host, sched, lam, iters, None, loss, rank, world)
+        r = lm_direction(sc, cams, gts_host, sched, lam, iters, None, loss, rank, world, offload=offload)
         out = out_host.copy_(r.delta, non_blocking=True)
         del sc, xs
     e1.record(stream)
