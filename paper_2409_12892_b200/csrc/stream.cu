@@ -23,8 +23,8 @@
 //   pass J  : one run per warp, lanes over its entries, per-warp shared pixel
 //             accumulators (a run never repeats a pixel), summed in fixed warp
 //             order -> deterministic, no atomics.
-//   pass J^T: 8-lane groups on the chunk's length-sorted schedule, 9 partials
-//             per run, 8-lane reduce-scatter, one 32-byte store per run.
+//   pass J^T: GL-lane groups (8) on the chunk's length-sorted schedule, 9
+//             partials per run, GL-lane reduce-scatter, one 32-byte record per run.
 #include "chain.cuh"
 
 #define NW 8
@@ -39,6 +39,52 @@ static_assert(CR % 32 == 0 && CR <= 255, "run slots are bytes, 32 per J^T round"
 #define SLM_JT_UNROLL 2
 #endif
 constexpr int kJtUnroll = SLM_JT_UNROLL;  // J^T entry-loop unroll (tuning)
+#ifndef SLM_JT_GL
+#define SLM_JT_GL 8
+#endif
+#ifndef SLM_DG_GL
+#define SLM_DG_GL 4
+#endif
+// lanes per run in the J^T and diag passes (groups of GL lanes, 32 / GL runs
+// per warp at a time): the per-run reduce-scatter costs log2(GL) shuffle
+// levels per GL values, so narrower groups spend fewer shuffles per run but
+// walk each run longer.  Measured at C3: diag 4 lanes 14.84 -> 14.56 ms
+// (40 values to reduce per run); J^T 8 lanes 9.93 vs 10.21 ms with 4 (9 values)
+constexpr int kJtGL = SLM_JT_GL, kDgGL = SLM_DG_GL;
+static_assert((kJtGL == 4 || kJtGL == 8) && (kDgGL == 4 || kDgGL == 8), "group width");
+static_assert(CR % (NW * 32 / 8) == 0, "J^T rounds");
+
+// GL-lane reduce-scatter of NB blocks of GL values: lane lg ends with the
+// group total of value b * GL + lg in res[b]; a fixed pattern, so the sums
+// are deterministic
+template <int GL, int NB>
+__device__ __forceinline__ void group_rs(const float* a, float* res, int lg) {
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    float v[GL];
+#pragma unroll
+    for (int k = 0; k < GL; ++k) v[k] = a[b * GL + k];
+#pragma unroll
+    for (int h = GL / 2; h >= 1; h >>= 1) {
+      const bool up = lg & h;
+#pragma unroll
+      for (int k = 0; k < h; ++k) v[k] = (up ? v[k + h] : v[k]) + __shfl_xor_sync(0xffffffffu, up ? v[k] : v[k + h], h);
+    }
+    res[b] = v[0];
+  }
+}
+
+template <int GL>
+__device__ __forceinline__ float group_sum(float v) {
+#pragma unroll
+  for (int h = GL / 2; h >= 1; h >>= 1) v += __shfl_xor_sync(0xffffffffu, v, h);
+  return v;
+}
+
+// the 8 J^T partials as stored: a[2] and a[4] carry 1/2, a[5] the 1/o factor
+__device__ __forceinline__ float jt_scale(int vi, float v, float io) {
+  return vi == 5 ? v * io : ((vi == 2 || vi == 4) ? 0.5f * v : v);
+}
 #define PAR 16           // floats per run parameter record
 #define TMETA 64         // producer chunk-metadata window
 #define TQ 4             // tile queue depth (producer -> consumers)
@@ -433,7 +479,6 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
   unsigned g = 0;
   float4* acc = s_acc + warp * 256;
   const int p = threadIdx.x;
-  const int slot = lane >> 3, lg = lane & 7;  // J^T: 4 groups of 8 lanes per warp
   for (unsigned tk = 0;; ++tk) {
     const unsigned qs = tk % TQ;
     mbar_wait(&tq_full[qs], (tk / TQ) & 1u);
@@ -549,9 +594,11 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
       // colour coefficients c_ch, sum gr_ch (dd_ch da + alphaT c_ch)^2 =
       // D^T S D + 2 sum_ch c_ch D.V_ch + sum_ch c_ch^2 T3_ch: the backward
       // applies the pair's chain once per pair instead of once per entry.
-      // Same 8-lane groups / length-sorted schedule as the J^T pass; lanes
+      // Same GL-lane groups / length-sorted schedule as the J^T pass; lanes
       // past their run's end add exact zeros (selects).
       const bool rhs = A.u != nullptr;
+      constexpr int GL = kDgGL, RPW = 32 / GL, RPR = NW * RPW;  // runs per warp / per round
+      const int slot = lane / GL, lg = lane % GL;
       for (int ci = c0; ci < c1; ++ci, ++g) {
         const int s = (int)(g % NSM);
         mbar_wait(&full[s], (g / NSM) & 1u);
@@ -561,8 +608,8 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
         const float4* s4 = reinterpret_cast<const float4*>(st);
         const float* sd2 = reinterpret_cast<const float*>(st + hdr[4]);
         const uint8_t* spx = st + hdr[5];
-        for (int rd = 0; rd < CR / 32 && rd * 32 < hdr[0]; ++rd) {  // 32 runs per round, longest first
-          const int ri = st[OFF_PERM + rd * 32 + (((warp + ci) & (NW - 1)) * 4 + slot)];
+        for (int rd = 0; rd < CR / RPR && rd * RPR < hdr[0]; ++rd) {  // RPR runs per round, longest first
+          const int ri = st[OFF_PERM + rd * RPR + ((warp + ci) & (NW - 1)) * RPW + slot];
           int n = 0, f0 = 0, sl = 0;
           float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = q0;
           float io = 0.f;
@@ -587,7 +634,7 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
           const float4* pr = s4 + f0;
           const float* pd = sd2 + f0;
           const uint8_t* pp = spx + f0;
-          for (int j = lg; j < nmax; j += 8) {
+          for (int j = lg; j < nmax; j += GL) {
             const bool ok = j < n;
             const float4 r = pr[j];
             const int pl = pp[j];
@@ -630,40 +677,25 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
               a8 = fmaf(at, uu.z, a8);
             }
           }
-          // 8-lane reduce-scatter of the 40 moment floats (5 blocks of 8: lane
-          // lg ends with values lg + 8 b); fixed pattern -> deterministic
-          const unsigned F = 0xffffffffu;
-          const bool u4 = lg & 4, u2 = lg & 2, u1 = lg & 1;
-          float res[5];
-#pragma unroll
-          for (int h = 0; h < 5; ++h) {
-            const float* v = m + 8 * h;
-            float w4[4], w2[2];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) w4[k] = (u4 ? v[k + 4] : v[k]) + __shfl_xor_sync(F, u4 ? v[k] : v[k + 4], 4);
-#pragma unroll
-            for (int k = 0; k < 2; ++k) w2[k] = (u2 ? w4[k + 2] : w4[k]) + __shfl_xor_sync(F, u2 ? w4[k] : w4[k + 2], 2);
-            res[h] = (u1 ? w2[1] : w2[0]) + __shfl_xor_sync(F, u1 ? w2[0] : w2[1], 1);
-          }
+          // GL-lane reduce-scatter of the 40 moment floats: lane lg ends with
+          // values lg + GL b; O (value 33) carries 1/o^2 (opacity da =
+          // alpha_eff dopa / o)
+          float res[DIAG_M / GL];
+          group_rs<GL, DIAG_M / GL>(m, res, lg);
           if (ri != 0xff) {
             float* o = A.out + (size_t)sl * DIAG_M;  // pair-run-slot order
-            res[4] = lg == 1 ? res[4] * io * io : res[4];  // O (value 33) carries 1/o^2: opacity da = alpha_eff dopa / o
+            res[33 / GL] = lg == 33 % GL ? res[33 / GL] * io * io : res[33 / GL];
 #pragma unroll
-            for (int h = 0; h < 5; ++h) o[8 * h + lg] = res[h];
+            for (int h = 0; h < DIAG_M / GL; ++h) o[GL * h + lg] = res[h];
           }
           if (rhs) {
             const float a[8] = {a01.x, a01.y, a23.x, a23.y, a4, a5, a67.x, a67.y};
-            float w4[4], w2[2];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) w4[k] = (u4 ? a[k + 4] : a[k]) + __shfl_xor_sync(F, u4 ? a[k] : a[k + 4], 4);
-#pragma unroll
-            for (int k = 0; k < 2; ++k) w2[k] = (u2 ? w4[k + 2] : w4[k]) + __shfl_xor_sync(F, u2 ? w4[k] : w4[k + 2], 2);
-            const float w1 = (u1 ? w2[1] : w2[0]) + __shfl_xor_sync(F, u1 ? w2[0] : w2[1], 1);
-            a8 += __shfl_xor_sync(F, a8, 4);
-            a8 += __shfl_xor_sync(F, a8, 2);
-            a8 += __shfl_xor_sync(F, a8, 1);
+            float ra[8 / GL];
+            group_rs<GL, 8 / GL>(a, ra, lg);
+            a8 = group_sum<GL>(a8);
             if (ri != 0xff) {
-              A.rhs8[(size_t)sl * 8 + lg] = lg == 5 ? w1 * io : ((lg == 2 || lg == 4) ? 0.5f * w1 : w1);
+#pragma unroll
+              for (int h = 0; h < 8 / GL; ++h) A.rhs8[(size_t)sl * 8 + GL * h + lg] = jt_scale(GL * h + lg, ra[h], io);
               if (lg == 0) A.rhs1[sl] = a8;
             }
           }
@@ -675,8 +707,10 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
 
     if (MODE & MODE_JT) {
       consumer_sync();
-      // pass J^T: 4 runs per warp (8 lanes each) from the chunk's
+      // pass J^T: 32 / GL runs per warp (GL lanes each) from the chunk's
       // length-sorted schedule; the warp's slot block rotates with the chunk
+      constexpr int GL = kJtGL, RPW = 32 / GL, RPR = NW * RPW;
+      const int slot = lane / GL, lg = lane % GL;
       for (int ci = c0; ci < c1; ++ci, ++g) {
         const int s = (int)(g % NSM);
         mbar_wait(&full[s], (g / NSM) & 1u);
@@ -686,18 +720,18 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
         const float4* s4 = reinterpret_cast<const float4*>(st);
         const float* sd2 = reinterpret_cast<const float*>(st + hdr[4]);
         const uint8_t* spx = st + hdr[5];
-        for (int rd = 0; rd < CR / 32 && rd * 32 < hdr[0]; ++rd) {  // 32 runs per round, longest first
-          const int ri = st[OFF_PERM + rd * 32 + (((warp + ci) & (NW - 1)) * 4 + slot)];
+        for (int rd = 0; rd < CR / RPR && rd * RPR < hdr[0]; ++rd) {  // RPR runs per round, longest first
+          const int ri = st[OFF_PERM + rd * RPR + ((warp + ci) & (NW - 1)) * RPW + slot];
           int n = 0, f0 = 0;
           float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = q0;
           float io = 0.f;
-          int slot = 0;
+          int sl = 0;
           if (ri != 0xff) {
             const float4* P4 = reinterpret_cast<const float4*>(st + hdr[6]) + ri * 2;
             q0 = P4[0];
             s1 = P4[1];
             io = s1.z;
-            slot = __float_as_int(s1.w);
+            sl = __float_as_int(s1.w);
             const uint32_t fn = rf[ri];
             f0 = (int)(fn & 0xffffu);
             n = (int)(fn >> 16);
@@ -716,7 +750,7 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
           const uint8_t* pp = spx + f0;
           const RunE ke = run_e_of(q0, s1);
 #pragma unroll(kJtUnroll)
-          for (int j = lg; j < nmax; j += 8) {
+          for (int j = lg; j < nmax; j += GL) {
             const bool ok = j < n;
             const float4 r = pr[j];
             const float d2 = pd[j];
@@ -734,25 +768,18 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
             a67 = __ffma2_rn(make_float2(ry, ry), make_float2(uu.x, uu.y), a67);
             a8 = fmaf(ry, uu.z, a8);
           }
-          const float a[9] = {a01.x, a01.y, a23.x, a23.y, a4, a5, a67.x, a67.y, a8};
-          // 8-lane reduce-scatter of a[0..7] (lane lg ends with the group sum of
-          // value lg) plus a butterfly for a[8]; fixed pattern -> deterministic
-          const unsigned F = 0xffffffffu;
-          const bool u4 = lg & 4, u2 = lg & 2, u1 = lg & 1;
-          float w4[4], w2[2];
-  #pragma unroll
-          for (int k = 0; k < 4; ++k) w4[k] = (u4 ? a[k + 4] : a[k]) + __shfl_xor_sync(F, u4 ? a[k] : a[k + 4], 4);
-  #pragma unroll
-          for (int k = 0; k < 2; ++k) w2[k] = (u2 ? w4[k + 2] : w4[k]) + __shfl_xor_sync(F, u2 ? w4[k] : w4[k + 2], 2);
-          const float w1 = (u1 ? w2[1] : w2[0]) + __shfl_xor_sync(F, u1 ? w2[0] : w2[1], 1);
-          a8 += __shfl_xor_sync(F, a8, 4);
-          a8 += __shfl_xor_sync(F, a8, 2);
-          a8 += __shfl_xor_sync(F, a8, 1);
+          // GL-lane reduce-scatter of a[0..7] (lane lg ends with the group
+          // sums of values lg + GL h) plus a butterfly for a8
+          const float a[8] = {a01.x, a01.y, a23.x, a23.y, a4, a5, a67.x, a67.y};
+          float ra[8 / GL];
+          group_rs<GL, 8 / GL>(a, ra, lg);
+          a8 = group_sum<GL>(a8);
           if (ri != 0xff) {
             // pair-run-slot order (read contiguously by the backward): partials
             // 0-7 as one 32-byte record, partial 8 in A.out1
-            A.out[(size_t)slot * 8 + lg] = lg == 5 ? w1 * io : ((lg == 2 || lg == 4) ? 0.5f * w1 : w1);
-            if (lg == 0) A.out1[slot] = a8;
+#pragma unroll
+            for (int h = 0; h < 8 / GL; ++h) A.out[(size_t)sl * 8 + GL * h + lg] = jt_scale(GL * h + lg, ra[h], io);
+            if (lg == 0) A.out1[sl] = a8;
           }
         }
         __syncwarp();
