@@ -181,9 +181,6 @@ __global__ void __launch_bounds__(32 * PK_WARPS, MODE == 0 ? SLM_BW_MINB : SLM_B
 
 // gaussian-major scratch -> attribute-major out (tiled transpose, 32 gaussians
 // per tile) with out = scale * v (+ lam * max(M, 1e-12) * p) and fp64 partials
-// of p.(v + lam Mf p)
-// gaussian-major scratch -> attribute-major out (tiled transpose, 32 gaussians
-// per tile) with out = scale * v (+ lam * max(M, 1e-12) * p) and fp64 partials
 // of p.(v + lam Mf p).  MODE 0 (J^T): the scratch rows are in the
 // world-covariance form (pair_back_row); each gaussian's quaternion and
 // log-scale gradients are formed here from its summed B = dL/dSigma:

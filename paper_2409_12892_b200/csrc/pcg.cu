@@ -80,7 +80,17 @@ __global__ void __launch_bounds__(256) k_pcg_p(float* __restrict__ p, float* __r
     __syncthreads();
     if (gtab && (int)threadIdx.x < ng) {
       float* row = tile + threadIdx.x * TS;
-      const float* gt = gtab + (size_t)(g0 + threadIdx.x) * gts;
+      // the chain row's first 48 floats (Rg | s2 | Mq) as 12 16-byte loads
+      const float4* gt4 = reinterpret_cast<const float4*>(gtab + (size_t)(g0 + threadIdx.x) * gts);
+      float gt[48];
+#pragma unroll
+      for (int k = 0; k < 12; ++k) {
+        const float4 v = __ldg(gt4 + k);
+        gt[4 * k] = v.x;
+        gt[4 * k + 1] = v.y;
+        gt[4 * k + 2] = v.z;
+        gt[4 * k + 3] = v.w;
+      }
       float Rg[9], s2[3], Mp[9];
 #pragma unroll
       for (int i = 0; i < 9; ++i) Rg[i] = gt[i];
@@ -255,6 +265,7 @@ static unsigned p_blocks(long long G) { return (unsigned)std::min<long long>((G 
 int slm_pcg_pinit(float* p, float* p_gm, const float* b, const float* M, long long G, int P, const float* gtab,
                   int gtab_stride, cudaStream_t s) {
   if (G <= 0) return SLM_OK;
+  if (gtab && gtab_stride % 4) return SLM_ERR_ARG;  // 16-byte chain-row loads
   const size_t sm = (size_t)32 * (gm_stride(P) + 1) * sizeof(float);
   k_pcg_p<P_INIT><<<p_blocks(G), 256, sm, s>>>(p, p_gm, nullptr, b, M, nullptr, G, P, gtab, gtab_stride);
   return slm_cuda_status();
@@ -263,6 +274,7 @@ int slm_pcg_pinit(float* p, float* p_gm, const float* b, const float* M, long lo
 int slm_pcg_pupdate(float* p, float* p_gm, const double* r, const float* M, const double* st, long long G, int P,
                     const float* gtab, int gtab_stride, cudaStream_t s) {
   if (G <= 0) return SLM_OK;
+  if (gtab && gtab_stride % 4) return SLM_ERR_ARG;  // 16-byte chain-row loads
   const size_t sm = (size_t)32 * (gm_stride(P) + 1) * sizeof(float);
   k_pcg_p<P_UPDATE><<<p_blocks(G), 256, sm, s>>>(p, p_gm, r, nullptr, M, st, G, P, gtab, gtab_stride);
   return slm_cuda_status();
@@ -270,6 +282,7 @@ int slm_pcg_pupdate(float* p, float* p_gm, const double* r, const float* M, cons
 
 int slm_gm_pack(const float* p, float* p_gm, long long G, int P, const float* gtab, int gtab_stride, cudaStream_t s) {
   if (G <= 0) return SLM_OK;
+  if (gtab && gtab_stride % 4) return SLM_ERR_ARG;  // 16-byte chain-row loads
   const size_t sm = (size_t)32 * (gm_stride(P) + 1) * sizeof(float);
   k_pcg_p<P_COPY><<<p_blocks(G), 256, sm, s>>>(const_cast<float*>(p), p_gm, nullptr, nullptr, nullptr, nullptr, G, P,
                                                gtab, gtab_stride);
