@@ -257,12 +257,12 @@ int slm_sort_pairs_u64(void* ws, long long ws_bytes, const unsigned long long* k
  * rasterizer.py:253-261, 283-287) */
 int slm_tile_count(const uint32_t* sorted_gid, const unsigned long long* sorted_key, long long G,
                    const SlmSplat* splats, int tiles_x, int tiles_y, unsigned long long* n_inst, cudaStream_t s);
-/* (tile, depth rank) keys of every (tile, splat) instance, the splat as the
- * value: after the key sort the values are the tile's instance list */
+/* tile keys of every (tile, splat) instance, emitted in depth-rank order, the
+ * splat as the value: after a STABLE key sort (slm_sort_pairs_u32 on the tile
+ * bits) the values are each tile's instance list in depth order */
 int slm_tile_emit(const uint32_t* sorted_gid, const unsigned long long* inst_off, long long G, const SlmSplat* splats,
-                  int tiles_x, int tiles_y, int rank_bits, unsigned long long* keys, uint32_t* vals, cudaStream_t s);
-int slm_tile_ranges(const unsigned long long* keys, long long n, int rank_bits, slm_u2* ranges, int n_tiles,
-                    cudaStream_t s);
+                  int tiles_x, int tiles_y, uint32_t* keys, uint32_t* vals, cudaStream_t s);
+int slm_tile_ranges(const uint32_t* keys, long long n, slm_u2* ranges, int n_tiles, cudaStream_t s);
 /* render (rasterizer.py:319-358): COUNT pass = image, T_final, per-pixel
  * counts and per-instance keep masks; FILL pass = run-ordered cache records
  * (build_cache, jacobian.py:383-409) and/or the Traversals arrays */
@@ -288,8 +288,8 @@ int slm_preprocess_views(const double* x, long long G, int sh_degree, const SlmC
 int slm_tile_count_v(const uint32_t* sv, long long n, long long G, const SlmSplat* splats, const SlmView* views,
                      unsigned long long* n_inst, cudaStream_t s);
 int slm_tile_emit_v(const uint32_t* sv, const unsigned long long* inst_off, long long n, long long G,
-                    const SlmSplat* splats, const SlmView* views, const int* view_tile_base, int rank_bits,
-                    unsigned long long* keys, uint32_t* vals, cudaStream_t s);
+                    const SlmSplat* splats, const SlmView* views, const int* view_tile_base, uint32_t* keys,
+                    uint32_t* vals, cudaStream_t s);
 long long slm_sort_keys_u32_workspace(long long n);
 int slm_sort_keys_u32(void* ws, long long ws_bytes, const uint32_t* kin, uint32_t* kout, long long n, int begin_bit,
                       int end_bit, cudaStream_t s);

@@ -98,8 +98,8 @@ _SIGS = {
     "slm_sort_pairs_u64_workspace": (c_ll, [c_ll]),
     "slm_sort_pairs_u64": (c_i, [c_vp, c_ll, c_vp, c_vp, c_vp, c_vp, c_ll, c_i, c_i, c_vp]),
     "slm_tile_count": (c_i, [c_vp, c_vp, c_ll, c_vp, c_i, c_i, c_vp, c_vp]),
-    "slm_tile_emit": (c_i, [c_vp, c_vp, c_ll, c_vp, c_i, c_i, c_i, c_vp, c_vp, c_vp]),
-    "slm_tile_ranges": (c_i, [c_vp, c_ll, c_i, c_vp, c_i, c_vp]),
+    "slm_tile_emit": (c_i, [c_vp, c_vp, c_ll, c_vp, c_i, c_i, c_vp, c_vp, c_vp]),
+    "slm_tile_ranges": (c_i, [c_vp, c_ll, c_vp, c_i, c_vp]),
     "slm_raster_count": (c_i, [c_vp, c_vp]),
     "slm_raster_fill": (c_i, [c_vp, c_vp]),
     "slm_inst_count": (c_i, [c_vp, c_vp, c_ll, c_vp, c_vp, c_vp, c_vp]),
@@ -107,7 +107,7 @@ _SIGS = {
     "slm_tile_runs": (c_i, [c_vp, c_i, c_vp, c_vp, c_ll, c_i, c_vp, c_vp, c_vp, c_i, c_vp]),
     "slm_preprocess_views": (c_i, [c_vp, c_ll, c_i, c_vp, c_i, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "slm_tile_count_v": (c_i, [c_vp, c_ll, c_ll, c_vp, c_vp, c_vp, c_vp]),
-    "slm_tile_emit_v": (c_i, [c_vp, c_vp, c_ll, c_ll, c_vp, c_vp, c_vp, c_i, c_vp, c_vp, c_vp]),
+    "slm_tile_emit_v": (c_i, [c_vp, c_vp, c_ll, c_ll, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "slm_sort_keys_u32_workspace": (c_ll, [c_ll]),
     "slm_sort_keys_u32": (c_i, [c_vp, c_ll, c_vp, c_vp, c_ll, c_i, c_i, c_vp]),
     "slm_residuals": (c_i, [c_vp, c_i, c_vp]),

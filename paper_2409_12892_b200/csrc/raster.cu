@@ -185,9 +185,13 @@ __global__ void k_tile_count(const uint32_t* __restrict__ sorted_gid, const unsi
 // instances are emitted per splat in (tile row, tile column) order with the
 // key (tile, depth rank) -- unique per instance -- and the splat as the value,
 // so after the key sort the values are each tile's splats in depth order
+// Instances are emitted in depth-rank order (inst_off is the scan over the
+// depth-sorted splats), so their key is the tile alone: a STABLE radix sort
+// by tile leaves every tile's splats in depth order (17 key bits at C3
+// instead of tile | rank = 37: 3 radix passes instead of 5, and 4-byte keys)
 __global__ void k_tile_emit(const uint32_t* __restrict__ sorted_gid, const unsigned long long* __restrict__ inst_off,
                             long long G, const SlmSplat* __restrict__ splats, int tiles_x, int tiles_y,
-                            int rank_bits, unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals) {
+                            uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   for (; i < G; i += (long long)gridDim.x * blockDim.x) {
     unsigned long long beg = inst_off[i], end = inst_off[i + 1];
@@ -198,8 +202,8 @@ __global__ void k_tile_emit(const uint32_t* __restrict__ sorted_gid, const unsig
     unsigned long long k = beg;
     for (int ty = ty0; ty <= ty1; ++ty)
       for (int tx = tx0; tx <= tx1; ++tx) {
-        keys[k] = ((unsigned long long)(ty * tiles_x + tx) << rank_bits) | (unsigned long long)i;
-        vals[k] = g;  // the sort carries the splat itself (keys are unique per instance)
+        keys[k] = (uint32_t)(ty * tiles_x + tx);
+        vals[k] = g;  // the sort carries the splat itself
         ++k;
       }
   }
@@ -230,14 +234,13 @@ __global__ void k_tile_count_v(const uint32_t* __restrict__ sv, long long n, lon
 __global__ void k_tile_emit_v(const uint32_t* __restrict__ sv, const unsigned long long* __restrict__ inst_off,
                               long long n, long long G, const SlmSplat* __restrict__ splats,
                               const SlmView* __restrict__ views, const int* __restrict__ view_tile_base,
-                              int rank_bits, unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals) {
+                              uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const unsigned long long beg = inst_off[i], end = inst_off[i + 1];
     if (beg == end) continue;
     const uint32_t e = sv[i];
     const int v = (int)(e >> 24);
     const long long gs = (long long)v * G + (e & 0xffffffu);
-    const long long rank = i - (long long)v * G;
     const SlmView vw = views[v];
     const int tiles_x = tiles_x_of(vw);
     int tx0, tx1, ty0, ty1;
@@ -245,9 +248,8 @@ __global__ void k_tile_emit_v(const uint32_t* __restrict__ sv, const unsigned lo
     unsigned long long k = beg;
     for (int ty = ty0; ty <= ty1; ++ty)
       for (int tx = tx0; tx <= tx1; ++tx) {
-        keys[k] = ((unsigned long long)(view_tile_base[v] + ty * tiles_x + tx) << rank_bits) |
-                  (unsigned long long)rank;
-        vals[k] = (uint32_t)gs;  // the sort carries the global splat (keys are unique per instance)
+        keys[k] = (uint32_t)(view_tile_base[v] + ty * tiles_x + tx);  // (view, depth) emission order, see k_tile_emit
+        vals[k] = (uint32_t)gs;  // the sort carries the global splat
         ++k;
       }
   }
@@ -332,13 +334,12 @@ __global__ void k_tile_runs(const slm_u2* __restrict__ ranges, int n_tiles, cons
   }
 }
 
-__global__ void k_tile_ranges(const unsigned long long* __restrict__ keys, long long n, int rank_bits,
-                              uint2* __restrict__ ranges) {
+__global__ void k_tile_ranges(const uint32_t* __restrict__ keys, long long n, uint2* __restrict__ ranges) {
   long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   for (; j < n; j += (long long)gridDim.x * blockDim.x) {
-    unsigned t = (unsigned)(keys[j] >> rank_bits);
-    if (j == 0 || (unsigned)(keys[j - 1] >> rank_bits) != t) ranges[t].x = (unsigned)j;
-    if (j == n - 1 || (unsigned)(keys[j + 1] >> rank_bits) != t) ranges[t].y = (unsigned)(j + 1);
+    const uint32_t t = keys[j];
+    if (j == 0 || keys[j - 1] != t) ranges[t].x = (unsigned)j;
+    if (j == n - 1 || keys[j + 1] != t) ranges[t].y = (unsigned)(j + 1);
   }
 }
 
@@ -670,11 +671,11 @@ int slm_tile_count_v(const uint32_t* sv, long long n, long long G, const SlmSpla
 }
 
 int slm_tile_emit_v(const uint32_t* sv, const unsigned long long* inst_off, long long n, long long G,
-                    const SlmSplat* splats, const SlmView* views, const int* view_tile_base, int rank_bits,
-                    unsigned long long* keys, uint32_t* vals, cudaStream_t stream) {
+                    const SlmSplat* splats, const SlmView* views, const int* view_tile_base, uint32_t* keys,
+                    uint32_t* vals, cudaStream_t stream) {
   if (n <= 0) return SLM_OK;
-  k_tile_emit_v<<<slm_blocks(n, 256), 256, 0, stream>>>(sv, inst_off, n, G, splats, views, view_tile_base, rank_bits,
-                                                         keys, vals);
+  k_tile_emit_v<<<slm_blocks(n, 256), 256, 0, stream>>>(sv, inst_off, n, G, splats, views, view_tile_base, keys,
+                                                         vals);
   return slm_cuda_status();
 }
 
@@ -724,10 +725,8 @@ int slm_tile_count(const uint32_t* sorted_gid, const unsigned long long* sorted_
 }
 
 int slm_tile_emit(const uint32_t* sorted_gid, const unsigned long long* inst_off, long long G, const SlmSplat* splats,
-                  int tiles_x, int tiles_y, int rank_bits, unsigned long long* keys, uint32_t* vals,
-                  cudaStream_t stream) {
-  k_tile_emit<<<slm_blocks(G, 256), 256, 0, stream>>>(sorted_gid, inst_off, G, splats, tiles_x, tiles_y, rank_bits,
-                                                       keys, vals);
+                  int tiles_x, int tiles_y, uint32_t* keys, uint32_t* vals, cudaStream_t stream) {
+  k_tile_emit<<<slm_blocks(G, 256), 256, 0, stream>>>(sorted_gid, inst_off, G, splats, tiles_x, tiles_y, keys, vals);
   return slm_cuda_status();
 }
 
@@ -756,10 +755,9 @@ int slm_tile_runs(const slm_u2* ranges, int n_tiles, const int* used, const int*
   return slm_cuda_status();
 }
 
-int slm_tile_ranges(const unsigned long long* keys, long long n, int rank_bits, uint2* ranges, int n_tiles,
-                    cudaStream_t stream) {
+int slm_tile_ranges(const uint32_t* keys, long long n, uint2* ranges, int n_tiles, cudaStream_t stream) {
   cudaMemsetAsync(ranges, 0, sizeof(uint2) * (size_t)n_tiles, stream);
-  if (n > 0) k_tile_ranges<<<slm_blocks(n, 256), 256, 0, stream>>>(keys, n, rank_bits, ranges);
+  if (n > 0) k_tile_ranges<<<slm_blocks(n, 256), 256, 0, stream>>>(keys, n, ranges);
   return slm_cuda_status();
 }
 

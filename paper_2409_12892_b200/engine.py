@@ -78,6 +78,12 @@ def scan_i32(inp: torch.Tensor, out: torch.Tensor):
     call("slm_scan_i32", ptr(ws), ws.numel(), ptr(inp), ptr(out), n, stream_ptr())
 
 
+def sort_u32(kin, kout, vin, vout, n, begin_bit, end_bit):
+    ws = _empty(_lib.load().slm_sort_pairs_u32_workspace(n), torch.uint8, kin.device)
+    call("slm_sort_pairs_u32", ptr(ws), ws.numel(), ptr(kin), ptr(kout), ptr(vin), ptr(vout), n, begin_bit,
+         end_bit, stream_ptr())
+
+
 def sort_u64(kin, kout, vin, vout, n, begin_bit, end_bit):
     ws = _empty(_lib.load().slm_sort_pairs_u64_workspace(n), torch.uint8, kin.device)
     call("slm_sort_pairs_u64", ptr(ws), ws.numel(), ptr(kin), ptr(kout), ptr(vin), ptr(vout), n, begin_bit,
@@ -191,17 +197,15 @@ def project_and_bin(scene: GaussianScene, frame: ViewFrame, cfg_s: _lib.SlmRastC
     total = int(inst_off[G].item())
     frame.n_inst = total
     n_tiles = frame.n_tiles
-    rank_bits = _bits(G)
-    tile_bits = _bits(n_tiles)
-    ik = _empty(total, torch.int64, dev)
+    ik = _empty(total, torch.int32, dev)
     iv = _empty(total, torch.int32, dev)
-    call("slm_tile_emit", ptr(sgid), ptr(inst_off), G, ptr(splats), frame.tiles_x, frame.tiles_y, rank_bits,
+    call("slm_tile_emit", ptr(sgid), ptr(inst_off), G, ptr(splats), frame.tiles_x, frame.tiles_y,
          ptr(ik), ptr(iv), stream_ptr())
     sk = torch.empty_like(ik)
     inst_gid = _empty(total, torch.int32, dev)   # the sorted values: each tile's splats in depth order
-    sort_u64(ik, sk, iv, inst_gid, total, 0, rank_bits + tile_bits)
+    sort_u32(ik, sk, iv, inst_gid, total, 0, _bits(n_tiles))   # stable: depth order within a tile
     ranges = torch.empty(2 * n_tiles, dtype=torch.int32, device=dev)
-    call("slm_tile_ranges", ptr(sk), total, rank_bits, ptr(ranges), n_tiles, stream_ptr())
+    call("slm_tile_ranges", ptr(sk), total, ptr(ranges), n_tiles, stream_ptr())
     frame.inst_gid = inst_gid
     frame.ranges = ranges
     frame.sorted_gid = sgid
@@ -362,17 +366,16 @@ class CacheSet:
         del n_inst
         ni = int(inst_off[VG].item())
         self.n_inst_total = ni
-        rank_bits = _bits(G)
-        ik = _empty(ni, torch.int64, dev)
+        ik = _empty(ni, torch.int32, dev)
         iv = _empty(ni, torch.int32, dev)
         call("slm_tile_emit_v", ptr(sv), ptr(inst_off), VG, G, ptr(splats_all), ptr(self.views_dev),
-             ptr(self.view_tile_base_dev), rank_bits, ptr(ik), ptr(iv), stream_ptr())
+             ptr(self.view_tile_base_dev), ptr(ik), ptr(iv), stream_ptr())
         sk = torch.empty_like(ik)
         inst_gid = _empty(ni, torch.int32, dev)      # sorted values: global splat v * G + g per instance
-        sort_u64(ik, sk, iv, inst_gid, ni, 0, rank_bits + _bits(nt))
+        sort_u32(ik, sk, iv, inst_gid, ni, 0, _bits(nt))   # stable: (view, depth) emission order within a tile
         del ik, iv
         ranges = torch.empty(2 * nt, dtype=torch.int32, device=dev)
-        call("slm_tile_ranges", ptr(sk), ni, rank_bits, ptr(ranges), nt, stream_ptr())
+        call("slm_tile_ranges", ptr(sk), ni, ptr(ranges), nt, stream_ptr())
         del sk
         inst_mask = torch.zeros(max(ni, 1) * MASK_WORDS, dtype=torch.int32, device=dev)
         T.tick("project_sort_bin")
