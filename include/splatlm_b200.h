@@ -199,6 +199,7 @@ typedef struct {
   void* pm;                 /* [P*12] out: m = dy/dx p per pair (3 float4) */
   const float* gtab;        /* per-gaussian chain rows (slm_gauss_tab) */
   int dsig;                 /* 1: p is the padded gaussian-major copy with dSigma (slm_pcg_p*) */
+  const float* camf;        /* dsig = 1: [V*20] fp32 camera rows (slm_cameras_f32) */
 } SlmFwdArgs;
 
 /* per-gaussian backward chain */
@@ -225,7 +226,11 @@ typedef struct {
   int lam_out;              /* 1: out += lam * max(M,1e-12) * p as well */
   float* out;
   double* dot_part;
+  const float* camf;        /* [V*20] fp32 camera rows (slm_cameras_f32), mode 0 */
 } SlmBackArgs;
+
+/* fp32 camera rows of the per-pair chains: R 9 | t 3 | C 3 | fx | fy | pad 3 per view */
+int slm_cameras_f32(const SlmCamera* cams, int V, float* out, cudaStream_t s);
 
 /* ---- sizes (ctypes layout checks) --------------------------------------- */
 int slm_camera_size(void);

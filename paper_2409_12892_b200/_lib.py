@@ -71,14 +71,15 @@ class SlmTileArgs(C.Structure):
 class SlmFwdArgs(C.Structure):
     _fields_ = [("xs", c_vp), ("G", c_ll), ("pair_gid", c_vp), ("pair_vm", c_vp), ("cams", c_vp), ("n_pairs", c_i),
                 ("p", c_vp), ("sa", c_ll), ("sg", c_ll), ("pm", c_vp), ("gtab", c_vp),
-                ("dsig", c_i)]
+                ("dsig", c_i), ("camf", c_vp)]
 
 
 class SlmBackArgs(C.Structure):
     _fields_ = [("xs", c_vp), ("G", c_ll), ("gpo", c_vp), ("pair_vm", c_vp), ("cams", c_vp), ("pacc", c_vp), ("pacc1", c_vp),
                 ("pair_run_off", c_vp), ("warp_g0", c_vp), ("pair_gid", c_vp), ("n_pairs", c_ll), ("gm", c_vp), ("gtab", c_vp),
                 ("scale", c_f),
-                ("p", c_vp), ("Mdiag", c_vp), ("lam", c_d), ("lam_out", c_i), ("out", c_vp), ("dot_part", c_vp)]
+                ("p", c_vp), ("Mdiag", c_vp), ("lam", c_d), ("lam_out", c_i), ("out", c_vp), ("dot_part", c_vp),
+                ("camf", c_vp)]
 
 
 SPLAT_BYTES = 96
@@ -139,6 +140,7 @@ _SIGS = {
     "slm_pair_backward": (c_i, [c_vp, c_i, c_i, c_vp]),
     "slm_vec_blocks": (c_i, []),
     "slm_gm_stride": (c_i, [c_i]),
+    "slm_cameras_f32": (c_i, [c_vp, c_i, c_vp, c_vp]),
     "slm_gm_pack": (c_i, [c_vp, c_vp, c_ll, c_i, c_vp, c_i, c_vp]),
     "slm_pcg_pinit": (c_i, [c_vp, c_vp, c_vp, c_vp, c_ll, c_i, c_vp, c_i, c_vp]),
     "slm_pcg_pupdate": (c_i, [c_vp, c_vp, c_vp, c_vp, c_vp, c_ll, c_i, c_vp, c_i, c_vp]),

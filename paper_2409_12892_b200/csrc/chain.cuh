@@ -260,6 +260,28 @@ __device__ __forceinline__ void pair_tab(const float* __restrict__ xs, long long
   T.dopa = dopa;
 }
 
+// fp32 camera row of the per-pair chains (slm_cameras_f32): R 9 | t 3 | C 3 |
+// fx | fy | pad 3 = five 16-byte loads instead of 17 fp64 loads + conversions
+#define CAMF_FLOATS 20
+struct CamF {
+  float R[9], t[3], C[3], fx, fy;
+};
+__device__ __forceinline__ CamF load_camf(const float* __restrict__ camf, int v) {
+  float c[CAMF_FLOATS];
+  ldg_row<CAMF_FLOATS>(camf + (size_t)v * CAMF_FLOATS, c);
+  CamF k;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) k.R[i] = c[i];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    k.t[i] = c[9 + i];
+    k.C[i] = c[12 + i];
+  }
+  k.fx = c[15];
+  k.fy = c[16];
+  return k;
+}
+
 // Backward row of one (gaussian, view) pair for the J^T chain (ref:
 // jacobian.py:314-353) from its 9 run-partial sums a = (a_mu (2), a_cov (3,
 // 1/2-scaled on 0 and 2), a_opa, a_col (3)), in the world-covariance form:
@@ -273,7 +295,7 @@ __device__ __forceinline__ void pair_tab(const float* __restrict__ xs, long long
 // (P - 1 values).  The camera-frame covariance comes from the chain row's
 // Sigma_world, so the per-pair work has no rotation / scale chain.
 template <int K>
-__device__ __forceinline__ void pair_back_row(long long g, const SlmCamera& cam, uint32_t clampbits,
+__device__ __forceinline__ void pair_back_row(long long g, const CamF& cam, uint32_t clampbits,
                                               const float (&a)[9], const float* __restrict__ gtab, float* row) {
   constexpr int GT = gtab_floats(K);
   const float* grow = gtab + (size_t)g * GT;
@@ -284,11 +306,11 @@ __device__ __forceinline__ void pair_back_row(long long g, const SlmCamera& cam,
   const float Sw[9] = {t[4], t[5], t[6], t[5], t[7], t[8], t[6], t[8], t[9]};
   float R[9];
 #pragma unroll
-  for (int i = 0; i < 9; ++i) R[i] = (float)cam.R[i];
-  const float fx = (float)cam.fx, fy = (float)cam.fy;
-  const float X = R[0] * p0 + R[1] * p1 + R[2] * p2 + (float)cam.t[0];
-  const float Yc = R[3] * p0 + R[4] * p1 + R[5] * p2 + (float)cam.t[1];
-  const float Z = R[6] * p0 + R[7] * p1 + R[8] * p2 + (float)cam.t[2];
+  for (int i = 0; i < 9; ++i) R[i] = cam.R[i];
+  const float fx = cam.fx, fy = cam.fy;
+  const float X = R[0] * p0 + R[1] * p1 + R[2] * p2 + cam.t[0];
+  const float Yc = R[3] * p0 + R[4] * p1 + R[5] * p2 + cam.t[1];
+  const float Z = R[6] * p0 + R[7] * p1 + R[8] * p2 + cam.t[2];
   const float iz = 1.f / Z, iz2 = iz * iz;
   const float A00 = fx * iz, A02 = -fx * X * iz2, A11 = fy * iz, A12 = -fy * Yc * iz2;
   float U[2][3];
@@ -349,7 +371,7 @@ __device__ __forceinline__ void pair_back_row(long long g, const SlmCamera& cam,
   // colour: SH block and the view-direction (position) term
   float sh[3 * K];
   ldg_row<GT - GT_SH>(grow + GT_SH, sh);
-  const float v0 = p0 - (float)cam.C[0], v1 = p1 - (float)cam.C[1], v2 = p2 - (float)cam.C[2];
+  const float v0 = p0 - cam.C[0], v1 = p1 - cam.C[1], v2 = p2 - cam.C[2];
   const float ivn = 1.f / sqrtf(v0 * v0 + v1 * v1 + v2 * v2);
   const float d0 = v0 * ivn, d1 = v1 * ivn, d2 = v2 * ivn;
   float Y[K];
@@ -376,7 +398,7 @@ __device__ __forceinline__ void pair_back_row(long long g, const SlmCamera& cam,
 // mask (sum_k coef_k dY_k(dd) + p_sh,k Y_k) with dd = (I - d d^T) p_pos / |v|
 // the view-direction perturbation (ref: jacobian.py:434-443).
 template <int K>
-__device__ __forceinline__ void pair_fwd_dsig(long long g, const SlmCamera& cam, uint32_t clampbits,
+__device__ __forceinline__ void pair_fwd_dsig(long long g, const CamF& cam, uint32_t clampbits,
                                               const float* __restrict__ gtab, const float* __restrict__ prow,
                                               float4* __restrict__ out) {
   constexpr int GT = gtab_floats(K), P = 11 + 3 * K, DS = (P + 3) & ~3;
@@ -392,11 +414,11 @@ __device__ __forceinline__ void pair_fwd_dsig(long long g, const SlmCamera& cam,
   const float Sw[9] = {t[4], t[5], t[6], t[5], t[7], t[8], t[6], t[8], t[9]};
   float R[9];
 #pragma unroll
-  for (int i = 0; i < 9; ++i) R[i] = (float)cam.R[i];
-  const float fx = (float)cam.fx, fy = (float)cam.fy;
-  const float X = R[0] * p0 + R[1] * p1 + R[2] * p2 + (float)cam.t[0];
-  const float Yc = R[3] * p0 + R[4] * p1 + R[5] * p2 + (float)cam.t[1];
-  const float Z = R[6] * p0 + R[7] * p1 + R[8] * p2 + (float)cam.t[2];
+  for (int i = 0; i < 9; ++i) R[i] = cam.R[i];
+  const float fx = cam.fx, fy = cam.fy;
+  const float X = R[0] * p0 + R[1] * p1 + R[2] * p2 + cam.t[0];
+  const float Yc = R[3] * p0 + R[4] * p1 + R[5] * p2 + cam.t[1];
+  const float Z = R[6] * p0 + R[7] * p1 + R[8] * p2 + cam.t[2];
   const float iz = 1.f / Z, iz2 = iz * iz;
   const float A00 = fx * iz, A02 = -fx * X * iz2, A11 = fy * iz, A12 = -fy * Yc * iz2;
   float U[2][3];
@@ -447,7 +469,7 @@ __device__ __forceinline__ void pair_fwd_dsig(long long g, const SlmCamera& cam,
   const float mmu0 = U[0][0] * pp[0] + U[0][1] * pp[1] + U[0][2] * pp[2];
   const float mmu1 = U[1][0] * pp[0] + U[1][1] * pp[1] + U[1][2] * pp[2];
   // colour
-  const float v0 = p0 - (float)cam.C[0], v1 = p1 - (float)cam.C[1], v2 = p2 - (float)cam.C[2];
+  const float v0 = p0 - cam.C[0], v1 = p1 - cam.C[1], v2 = p2 - cam.C[2];
   const float ivn = 1.f / sqrtf(v0 * v0 + v1 * v1 + v2 * v2);
   const float d0 = v0 * ivn, d1 = v1 * ivn, d2 = v2 * ivn;
   const float dp = d0 * pp[0] + d1 * pp[1] + d2 * pp[2];
@@ -487,7 +509,7 @@ __global__ void __launch_bounds__(128, DSIG ? SLM_PMD_MINB : SLM_PM_MINB) k_pair
     const long long g = A.pair_gid[q];
     const uint32_t vm = A.pair_vm[q];
     if (DSIG) {  // padded gaussian-major p with dSigma: camera-dependent chain only
-      pair_fwd_dsig<K>(g, A.cams[vm & 0xffffu], vm >> 16, A.gtab, p + g * sg, pm + (size_t)q * 3);
+      pair_fwd_dsig<K>(g, load_camf(A.camf, vm & 0xffffu), vm >> 16, A.gtab, p + g * sg, pm + (size_t)q * 3);
       continue;
     }
     Tab<K> T;

@@ -306,6 +306,8 @@ class CacheSet:
         self.P = scene.params_per_gaussian
         self.K = num_coefficients(scene.sh_degree)
         self.cams_dev, self.pix_bases = cameras_struct_tensor(self.cameras, dev)
+        self.camf = torch.empty(max(len(self.cameras), 1) * 20, dtype=torch.float32, device=dev)
+        call("slm_cameras_f32", ptr(self.cams_dev), len(self.cameras), ptr(self.camf), stream_ptr())
         self.N = sum(c.num_pixels for c in self.cameras)
         views = (_lib.SlmView * V)()
         for i, c in enumerate(self.cameras):
@@ -659,6 +661,7 @@ class CacheSet:
             return
         a = _lib.SlmFwdArgs()
         a.xs, a.G = ptr(self.scene.x32()), G
+        a.camf = ptr(self.camf)
         a.pair_gid, a.pair_vm, a.cams, a.n_pairs = ptr(self.pair_gid), ptr(self.pair_vm), ptr(self.cams_dev), \
             self.n_pairs
         if p_gm is not None:   # written by slm_pcg_p* / gm_pack with this cache's chain rows
@@ -706,7 +709,7 @@ class CacheSet:
         if mode == 0:
             a.pacc1 = off(run_acc, 8 * self.R)
         a.xs, a.G = ptr(self.scene.x32()), self.G
-        a.gpo, a.pair_vm, a.cams = ptr(self.gpo), ptr(self.pair_vm), ptr(self.cams_dev)
+        a.gpo, a.pair_vm, a.cams, a.camf = ptr(self.gpo), ptr(self.pair_vm), ptr(self.cams_dev), ptr(self.camf)
         a.gtab = ptr(self.gtab)
         a.warp_g0, a.pair_gid, a.n_pairs = ptr(self.warp_g0), ptr(self.pair_gid), self.n_pairs
         a.gm = ptr(self.gm)
