@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(32 * PK_WARPS, MODE == 0 ? SLM_BW_MINB : SLM_B
             a[4] += v.x; a[5] += v.y; a[6] += v.z; a[7] += v.w;
             a[8] += __ldg(A.pacc1 + rr);
           }
-          pair_back_row<K>(myg, A.cams[vm & 0xffffu], vm >> 16, a, A.gtab, row);
+          pair_back_row<K>(myg, load_camf(A.camf, vm & 0xffffu), vm >> 16, a, A.gtab, row);
         } else {
           // diag from the run moments (stream.cu diag pass): S (5x5 upper
           // triangle), V_ch (3 x 5), T3_ch, O / o^2; the pair's chain applied
@@ -277,7 +277,28 @@ __global__ void __launch_bounds__(256) k_gm_to_am(SlmBackArgs A) {
 // ---------------------------------------------------------------------------
 extern "C" {
 
+__global__ void k_cameras_f32(const SlmCamera* __restrict__ cams, int V, float* __restrict__ out) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  const SlmCamera c = cams[v];
+  float* o = out + (size_t)v * CAMF_FLOATS;
+  for (int i = 0; i < 9; ++i) o[i] = (float)c.R[i];
+  for (int i = 0; i < 3; ++i) {
+    o[9 + i] = (float)c.t[i];
+    o[12 + i] = (float)c.C[i];
+  }
+  o[15] = (float)c.fx;
+  o[16] = (float)c.fy;
+  o[17] = o[18] = o[19] = 0.f;
+}
+
 int slm_view_size() { return (int)sizeof(SlmView); }
+
+int slm_cameras_f32(const SlmCamera* cams, int V, float* out, cudaStream_t st) {
+  if (V <= 0) return SLM_OK;
+  k_cameras_f32<<<(V + 127) / 128, 128, 0, st>>>(cams, V, out);
+  return slm_cuda_status();
+}
 int slm_tile_args_size() { return (int)sizeof(SlmTileArgs); }
 int slm_back_args_size() { return (int)sizeof(SlmBackArgs); }
 int slm_diag_moment_floats() { return DIAG_M; }
