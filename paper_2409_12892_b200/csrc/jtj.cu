@@ -66,11 +66,26 @@ __global__ void __launch_bounds__(32 * PK_WARPS, MODE == 0 ? SLM_BW_MINB : SLM_B
 #pragma unroll
           for (int j = 0; j < 9; ++j) a[j] = 0.f;
           const float4* p4 = reinterpret_cast<const float4*>(A.pacc);
-          for (int rr = r0; rr < r1; ++rr) {
+          // two runs per step (both loads in flight; the sums keep the run order)
+          for (int rr = r0; rr < r1; rr += 2) {
+            const bool two = rr + 1 < r1;
             const float4 u = __ldg(p4 + 2 * (size_t)rr), v = __ldg(p4 + 2 * (size_t)rr + 1);
+            const float w8 = __ldg(A.pacc1 + rr);
+            float4 u2 = make_float4(0.f, 0.f, 0.f, 0.f), v2 = u2;
+            float x8 = 0.f;
+            if (two) {
+              u2 = __ldg(p4 + 2 * (size_t)rr + 2);
+              v2 = __ldg(p4 + 2 * (size_t)rr + 3);
+              x8 = __ldg(A.pacc1 + rr + 1);
+            }
             a[0] += u.x; a[1] += u.y; a[2] += u.z; a[3] += u.w;
             a[4] += v.x; a[5] += v.y; a[6] += v.z; a[7] += v.w;
-            a[8] += __ldg(A.pacc1 + rr);
+            a[8] += w8;
+            if (two) {
+              a[0] += u2.x; a[1] += u2.y; a[2] += u2.z; a[3] += u2.w;
+              a[4] += v2.x; a[5] += v2.y; a[6] += v2.z; a[7] += v2.w;
+              a[8] += x8;
+            }
           }
           pair_back_row<K>(myg, load_camf(A.camf, vm & 0xffffu), vm >> 16, a, A.gtab, row);
         } else {
@@ -81,14 +96,29 @@ __global__ void __launch_bounds__(32 * PK_WARPS, MODE == 0 ? SLM_BW_MINB : SLM_B
 #pragma unroll
           for (int j = 0; j < 36; ++j) mo[j] = 0.f;
           const float4* p4 = reinterpret_cast<const float4*>(A.pacc);
-          for (int rr = r0; rr < r1; ++rr) {
+          for (int rr = r0; rr < r1; rr += 2) {  // two runs per step, run order kept
+            const bool two = rr + 1 < r1;
+            float4 v[9], w[9];
 #pragma unroll
             for (int k = 0; k < 9; ++k) {
-              const float4 v = __ldg(p4 + (size_t)rr * (DIAG_M / 4) + k);
-              mo[4 * k] += v.x;
-              mo[4 * k + 1] += v.y;
-              mo[4 * k + 2] += v.z;
-              mo[4 * k + 3] += v.w;
+              v[k] = __ldg(p4 + (size_t)rr * (DIAG_M / 4) + k);
+              w[k] = two ? __ldg(p4 + (size_t)(rr + 1) * (DIAG_M / 4) + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+              mo[4 * k] += v[k].x;
+              mo[4 * k + 1] += v[k].y;
+              mo[4 * k + 2] += v[k].z;
+              mo[4 * k + 3] += v[k].w;
+            }
+            if (two) {
+#pragma unroll
+              for (int k = 0; k < 9; ++k) {
+                mo[4 * k] += w[k].x;
+                mo[4 * k + 1] += w[k].y;
+                mo[4 * k + 2] += w[k].z;
+                mo[4 * k + 3] += w[k].w;
+              }
             }
           }
           Tab<K> T;
