@@ -125,6 +125,10 @@ __device__ __forceinline__ float4 ldg4_ordered(const float4* p) {
   asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
   return v;
 }
+// L1 prefetch of a row part that is loaded (ordered) later: the latency
+// overlaps the work before its use without holding registers
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
 template <int N>
 __device__ __forceinline__ void ldg_row(const float* __restrict__ src, float* dst) {
 #pragma unroll
@@ -299,6 +303,8 @@ __device__ __forceinline__ void pair_back_row(long long g, const CamF& cam, uint
                                               const float (&a)[9], const float* __restrict__ gtab, float* row) {
   constexpr int GT = gtab_floats(K);
   const float* grow = gtab + (size_t)g * GT;
+  prefetch_l1(grow + GT_SH);  // SH coefficients (used last)
+  prefetch_l1(grow + GT_SH + 32);
   float t[16];
   ldg_row<4>(grow + GT_DOPA, t);       // dopa, position
   ldg_row<8>(grow + GT_SIG, t + 4);    // Sigma_world
@@ -403,6 +409,9 @@ __device__ __forceinline__ void pair_fwd_dsig(long long g, const CamF& cam, uint
                                               float4* __restrict__ out) {
   constexpr int GT = gtab_floats(K), P = 11 + 3 * K, DS = (P + 3) & ~3;
   const float* grow = gtab + (size_t)g * GT;
+  prefetch_l1(grow + GT_SH);  // SH coefficients (used last)
+  prefetch_l1(grow + GT_SH + 32);
+  prefetch_l1(prow + 8);
   float t[12];
   ldg_row<4>(grow + GT_DOPA, t);       // dopa, position
   ldg_row<8>(grow + GT_SIG, t + 4);    // Sigma_world
