@@ -45,8 +45,10 @@ CONFIGS = {
     "c3": dict(G=1_000_000, views=200, W=1024, H=1024, subsets=8, iters=8, gen="footprint", degree=3),
     # BASELINE.json configs[3] (Mip-NeRF360 scale; quoted for 8 GPUs, one subset per GPU)
     "c4": dict(G=3_000_000, views=200, W=1552, H=1032, subsets=8, iters=8, gen="footprint", degree=3),
-    # BASELINE.json configs[4] (ScanNet++ scale; 16 subsets, 2 per GPU on 8 GPUs), the gradient cache
-    # sized near the 180 GB of one GPU: K ~ 86 entries per pixel
+    # BASELINE.json configs[4] (ScanNet++ scale; 16 subsets, 2 per GPU on 8 GPUs), "gradient cache sized
+    # near 180 GB HBM per GPU": with the reference's opacity law the T >= 1e-4 stop saturates the
+    # generator near K ~ 50 entries per pixel (2.16e9 entries per subset), i.e. 155 GB per subset in
+    # the reference's 72-byte records; here 45 GB at 21 B/entry (150 GB HBM peak with rho's cache)
     "c5": dict(G=2_000_000, views=400, W=1616, H=1080, subsets=16, iters=8, gen="footprint", degree=3,
                k_target=71.0),
 }
