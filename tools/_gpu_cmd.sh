@@ -1,2 +1,1 @@
-NOFULL=1 bash tools/gpu_ncu_product.sh prod_pf
-NOFULL=1 SLM_LIB=paper_2409_12892_b200/_variants/base/libsplatlm_b200.so bash tools/gpu_ncu_product.sh prod_pfbase
+bash tools/gpu_evidence.sh > gpurun_out/evidence.log 2>&1
