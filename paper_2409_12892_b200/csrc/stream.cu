@@ -175,9 +175,16 @@ __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
 }
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory"); }
 
-__device__ __forceinline__ int view_of_tile(const int* __restrict__ vtb, int n_views, int t) {
+// view of global tile t: the number of views after the first whose first
+// tile is <= t, counted 32 views per ballot (vtb ascending)
+__device__ __forceinline__ int view_of_tile_warp(const int* __restrict__ vtb, int n_views, int t, int lane) {
   int v = 0;
-  while (v + 1 < n_views && vtb[v + 1] <= t) ++v;
+  for (int b = 1; b < n_views; b += 32) {
+    const int i = b + lane;
+    const unsigned m = __ballot_sync(0xffffffffu, i < n_views && __ldg(vtb + i) <= t);
+    v += __popc(m);
+    if (m != 0xffffffffu) break;
+  }
   return v;
 }
 
@@ -346,6 +353,12 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
   // on which CTA runs a tile) and hands them to the consumers in order
   __shared__ uint64_t tq_full[TQ], tq_empty[TQ];
   __shared__ int tq[TQ];
+  // per queued tile, resolved once by the producer: (first pixel lo, hi, view
+  // width, valid columns | valid rows << 8) and the tile's chunk range -- the
+  // consumers start a tile with shared-memory reads instead of a chain of
+  // dependent global loads (view search, view record, chunk offsets)
+  __shared__ int4 tqi[TQ];
+  __shared__ int2 tqc[TQ];
   unsigned char* sp = smem;
   float4* s_u = reinterpret_cast<float4*>(sp);
   sp += 256 * 16;
@@ -378,16 +391,31 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
     unsigned g = 0;
     for (unsigned tk = 0;; ++tk) {
       int t = 0;
+      if (lane == 0) t = A.tile_counter ? atomicAdd(A.tile_counter, 1) : (int)(blockIdx.x + tk * gridDim.x);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      int c0 = 0, c1 = 0;
+      int4 ti = make_int4(0, 0, 0, 0);
+      if (t < A.n_tiles) {
+        const int v = view_of_tile_warp(A.view_tile_base, A.n_views, t, lane);
+        const SlmView vw = A.views[v];
+        const int tiles_x = (vw.W + SLM_TILE - 1) / SLM_TILE;
+        const int lt = t - A.view_tile_base[v];
+        const int x0 = (lt % tiles_x) * SLM_TILE, y0 = (lt / tiles_x) * SLM_TILE;
+        const long long gp0 = vw.pix_base + (long long)y0 * vw.W + x0;
+        ti = make_int4((int)(unsigned)(gp0 & 0xffffffffLL), (int)(gp0 >> 32), vw.W,
+                       min(SLM_TILE, vw.W - x0) | (min(SLM_TILE, vw.H - y0) << 8));
+        c0 = A.tile_chunk_off[t];
+        c1 = A.tile_chunk_off[t + 1];
+      }
       if (lane == 0) {
-        t = A.tile_counter ? atomicAdd(A.tile_counter, 1) : (int)(blockIdx.x + tk * gridDim.x);
         const unsigned qs = tk % TQ;
         if (tk >= TQ) mbar_wait(&tq_empty[qs], ((tk / TQ) - 1) & 1u);
         tq[qs] = t < A.n_tiles ? t : -1;
+        tqi[qs] = ti;
+        tqc[qs] = make_int2(c0, c1);
         mbar_arrive(&tq_full[qs]);
       }
-      t = __shfl_sync(0xffffffffu, t, 0);
       if (t >= A.n_tiles) break;
-      const int c0 = A.tile_chunk_off[t], c1 = A.tile_chunk_off[t + 1];
       for (int pass = 0; pass < n_pass; ++pass) {
         // the cache of a tile is read twice in the fused mode: keep it in L2
         // for the J^T pass, then let it go
@@ -483,17 +511,15 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
     const unsigned qs = tk % TQ;
     mbar_wait(&tq_full[qs], (tk / TQ) & 1u);
     const int t = tq[qs];
+    const int4 ti = tqi[qs];
+    const int2 tc = tqc[qs];
     __syncwarp();
     if (lane == 0) mbar_arrive(&tq_empty[qs]);
     if (t < 0) break;
-    const int v = view_of_tile(A.view_tile_base, A.n_views, t);
-    const SlmView vw = A.views[v];
-    const int tiles_x = (vw.W + SLM_TILE - 1) / SLM_TILE;
-    const int lt = t - A.view_tile_base[v];
-    const int px = (lt % tiles_x) * SLM_TILE + (p & 15), py = (lt / tiles_x) * SLM_TILE + (p >> 4);
-    const bool inside = px < vw.W && py < vw.H;
-    const long long gp = vw.pix_base + (long long)py * vw.W + px;
-    const int c0 = A.tile_chunk_off[t], c1 = A.tile_chunk_off[t + 1];
+    const int px = p & 15, py = p >> 4;
+    const bool inside = px < (ti.w & 0xff) && py < (ti.w >> 8);
+    const long long gp = (((long long)ti.y << 32) | (unsigned)ti.x) + (long long)py * ti.z + px;
+    const int c0 = tc.x, c1 = tc.y;
     // per-pixel weight / input loaded up front so its latency hides behind the J pass
     float4 wt = make_float4(1.f, 1.f, 1.f, 0.f);
     if (MODE & MODE_J) {
