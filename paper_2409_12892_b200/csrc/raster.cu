@@ -12,119 +12,136 @@
 // ---------------------------------------------------------------------------
 // projection (ref: rasterizer.py:78-165)
 // ---------------------------------------------------------------------------
+// view-independent part of the projection of one gaussian (finiteness, the
+// world covariance R diag(s^2) R^T and the opacity), computed once per
+// gaussian and reused for every view of a subset (same fp64 operations, so
+// the per-view results are bit-identical to computing it per view)
+struct GaussPre {
+  double p0, p1, p2;
+  double Sw[9];
+  double o;
+  bool finite;
+};
+
 template <int K>
-__device__ __forceinline__ void preprocess_one(const double* __restrict__ x, long long G, long long g,
-                                               const SlmCamera& cam, const SlmRastCfg& cfg, SlmSplat& s_out,
-                                               unsigned long long& key_out, int* __restrict__ err) {
-  {
-    double p0 = x[g], p1 = x[G + g], p2 = x[2 * G + g];
-    double qw = x[3 * G + g], qx = x[4 * G + g], qy = x[5 * G + g], qz = x[6 * G + g];
-    double l0 = x[7 * G + g], l1 = x[8 * G + g], l2 = x[9 * G + g];
-    double logit = x[10 * G + g];
-    bool finite = isfinite(p0) && isfinite(p1) && isfinite(p2) && isfinite(qw) && isfinite(qx) &&
-                  isfinite(qy) && isfinite(qz) && isfinite(l0) && isfinite(l1) && isfinite(l2) &&
-                  isfinite(logit);
-    for (int a = 11; a < 11 + 3 * K; ++a) finite = finite && isfinite(x[(long long)a * G + g]);
-    if (!finite) atomicOr(err, 1);
-
-    const double* R = cam.R;
-    // cam_points = positions @ R^T + t
-    double X0 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(p0, R[0]), __dmul_rn(p1, R[1])), __dmul_rn(p2, R[2])), cam.t[0]);
-    double X1 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(p0, R[3]), __dmul_rn(p1, R[4])), __dmul_rn(p2, R[5])), cam.t[1]);
-    double X2 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(p0, R[6]), __dmul_rn(p1, R[7])), __dmul_rn(p2, R[8])), cam.t[2]);
-    bool valid = X2 > cfg.z_near;
-    double zz = valid ? X2 : 1.0;
-    double mx = __dadd_rn(__ddiv_rn(__dmul_rn(cam.fx, X0), zz), cam.cx);
-    double my = __dadd_rn(__ddiv_rn(__dmul_rn(cam.fy, X1), zz), cam.cy);
-
-    double qn = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
-    if (qn < 1e-12) atomicOr(err, 2);
-    double w = qw / qn, a = qx / qn, b = qy / qn, c = qz / qn;
-    double Rg[9] = {1 - 2 * (b * b + c * c), 2 * (a * b - w * c), 2 * (a * c + w * b),
-                    2 * (a * b + w * c), 1 - 2 * (a * a + c * c), 2 * (b * c - w * a),
-                    2 * (a * c - w * b), 2 * (b * c + w * a), 1 - 2 * (a * a + b * b)};
-    double s2[3] = {exp(2.0 * l0), exp(2.0 * l1), exp(2.0 * l2)};
-    // world covariance R diag(s^2) R^T
-    double Sw[9];
+__device__ __forceinline__ GaussPre gauss_pre(const double* __restrict__ x, long long G, long long g,
+                                              int* __restrict__ err) {
+  GaussPre P;
+  P.p0 = x[g];
+  P.p1 = x[G + g];
+  P.p2 = x[2 * G + g];
+  double qw = x[3 * G + g], qx = x[4 * G + g], qy = x[5 * G + g], qz = x[6 * G + g];
+  double l0 = x[7 * G + g], l1 = x[8 * G + g], l2 = x[9 * G + g];
+  double logit = x[10 * G + g];
+  bool finite = isfinite(P.p0) && isfinite(P.p1) && isfinite(P.p2) && isfinite(qw) && isfinite(qx) &&
+                isfinite(qy) && isfinite(qz) && isfinite(l0) && isfinite(l1) && isfinite(l2) && isfinite(logit);
+  for (int a = 11; a < 11 + 3 * K; ++a) finite = finite && isfinite(x[(long long)a * G + g]);
+  if (!finite) atomicOr(err, 1);
+  P.finite = finite;
+  double qn = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+  if (qn < 1e-12) atomicOr(err, 2);
+  double w = qw / qn, a = qx / qn, b = qy / qn, c = qz / qn;
+  double Rg[9] = {1 - 2 * (b * b + c * c), 2 * (a * b - w * c), 2 * (a * c + w * b),
+                  2 * (a * b + w * c), 1 - 2 * (a * a + c * c), 2 * (b * c - w * a),
+                  2 * (a * c - w * b), 2 * (b * c + w * a), 1 - 2 * (a * a + b * b)};
+  double s2[3] = {exp(2.0 * l0), exp(2.0 * l1), exp(2.0 * l2)};
+  // world covariance R diag(s^2) R^T
 #pragma unroll
-    for (int i = 0; i < 3; ++i)
+  for (int i = 0; i < 3; ++i)
 #pragma unroll
-      for (int k = 0; k < 3; ++k)
-        Sw[i * 3 + k] = Rg[i * 3 + 0] * s2[0] * Rg[k * 3 + 0] + Rg[i * 3 + 1] * s2[1] * Rg[k * 3 + 1] +
+    for (int k = 0; k < 3; ++k)
+      P.Sw[i * 3 + k] = Rg[i * 3 + 0] * s2[0] * Rg[k * 3 + 0] + Rg[i * 3 + 1] * s2[1] * Rg[k * 3 + 1] +
                         Rg[i * 3 + 2] * s2[2] * Rg[k * 3 + 2];
-    // camera covariance R Sw R^T
-    double T1[9], Sc[9];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int k = 0; k < 3; ++k)
-        T1[i * 3 + k] = R[i * 3 + 0] * Sw[0 * 3 + k] + R[i * 3 + 1] * Sw[1 * 3 + k] + R[i * 3 + 2] * Sw[2 * 3 + k];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int k = 0; k < 3; ++k)
-        Sc[i * 3 + k] = T1[i * 3 + 0] * R[k * 3 + 0] + T1[i * 3 + 1] * R[k * 3 + 1] + T1[i * 3 + 2] * R[k * 3 + 2];
-    double Xs0 = valid ? X0 : 0.0, Xs1 = valid ? X1 : 0.0, Xs2 = valid ? X2 : 1.0;
-    double iz = 1.0 / Xs2;
-    double A00 = cam.fx * iz, A02 = -cam.fx * Xs0 * iz * iz;
-    double A11 = cam.fy * iz, A12 = -cam.fy * Xs1 * iz * iz;
-    // cov2 = A Sc A^T (A has zeros at (0,1), (1,0))
-    double r00 = A00 * Sc[0] + A02 * Sc[6], r01 = A00 * Sc[1] + A02 * Sc[7], r02 = A00 * Sc[2] + A02 * Sc[8];
-    double r11 = A11 * Sc[4] + A12 * Sc[7], r12 = A11 * Sc[5] + A12 * Sc[8], r10 = A11 * Sc[3] + A12 * Sc[6];
-    double c00 = r00 * A00 + r02 * A02;
-    double c01 = r01 * A11 + r02 * A12;
-    double c11 = r11 * A11 + r12 * A12;
-    (void)r10;
-    double va = c00 + cfg.cov_eps, vb = c01, vc = c11 + cfg.cov_eps;
-    double det = va * vc - vb * vb;
-    valid = valid && (det > 0.0);
-    double detu = det > 0.0 ? det : 1.0;
-    double ca = vc / detu, cb = -vb / detu, cc = va / detu;
+  P.o = 1.0 / (1.0 + exp(-logit));
+  return P;
+}
 
-    // view-dependent colour
-    double v0 = p0 - cam.C[0], v1 = p1 - cam.C[1], v2 = p2 - cam.C[2];
-    double vn = sqrt(v0 * v0 + v1 * v1 + v2 * v2);
-    double d0 = v0 / vn, d1 = v1 / vn, d2 = v2 / vn;
-    double Y[16];
-    sh_basis<double, K>(d0, d1, d2, Y);
-    double col[3];
-    unsigned clampbits = 0;
+// the per-view part (ref: rasterizer.py:116-165)
+template <int K>
+__device__ __forceinline__ void preprocess_view(const GaussPre& P, const double* __restrict__ x, long long G,
+                                                long long g, const SlmCamera& cam, const SlmRastCfg& cfg,
+                                                SlmSplat& s_out, unsigned long long& key_out) {
+  const double p0 = P.p0, p1 = P.p1, p2 = P.p2;
+  const double* Sw = P.Sw;
+  const double* R = cam.R;
+  // cam_points = positions @ R^T + t
+  double X0 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(p0, R[0]), __dmul_rn(p1, R[1])), __dmul_rn(p2, R[2])), cam.t[0]);
+  double X1 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(p0, R[3]), __dmul_rn(p1, R[4])), __dmul_rn(p2, R[5])), cam.t[1]);
+  double X2 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(p0, R[6]), __dmul_rn(p1, R[7])), __dmul_rn(p2, R[8])), cam.t[2]);
+  bool valid = X2 > cfg.z_near;
+  double zz = valid ? X2 : 1.0;
+  double mx = __dadd_rn(__ddiv_rn(__dmul_rn(cam.fx, X0), zz), cam.cx);
+  double my = __dadd_rn(__ddiv_rn(__dmul_rn(cam.fy, X1), zz), cam.cy);
+  // camera covariance R Sw R^T
+  double T1[9], Sc[9];
 #pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      double raw = 0.0;
+  for (int i = 0; i < 3; ++i)
 #pragma unroll
-      for (int k = 0; k < K; ++k) raw += x[(long long)(11 + ch * K + k) * G + g] * Y[k];
-      raw += 0.5;
-      col[ch] = raw > 0.0 ? raw : 0.0;
-      if (raw <= 0.0) clampbits |= (1u << (1 + ch));
-    }
-    double lam = 0.5 * (va + vc) + sqrt(0.25 * (va - vc) * (va - vc) + vb * vb);
-    if (cfg.cull_sigma > 0.0) {
-      double rad = cfg.cull_sigma * sqrt(lam);
-      valid = valid && (mx + rad > 0.0) && (mx - rad < (double)cam.W) && (my + rad > 0.0) &&
-              (my - rad < (double)cam.H);
-    }
-    double o = 1.0 / (1.0 + exp(-logit));
-    int x0 = 0, x1 = cam.W - 1, y0 = 0, y1 = cam.H - 1;
-    if (cfg.reach_fac > 0.0) {
-      double reach = cfg.reach_fac * sqrt(lam);
-      double fx0 = ceil(mx - reach - 0.5), fx1 = floor(mx + reach - 0.5);
-      double fy0 = ceil(my - reach - 0.5), fy1 = floor(my + reach - 0.5);
-      x0 = fx0 > 0.0 ? (fx0 < 1e9 ? (int)fx0 : 1000000000) : 0;
-      y0 = fy0 > 0.0 ? (fy0 < 1e9 ? (int)fy0 : 1000000000) : 0;
-      x1 = fx1 < (double)(cam.W - 1) ? (fx1 > -1e9 ? (int)fx1 : -1000000000) : cam.W - 1;
-      y1 = fy1 < (double)(cam.H - 1) ? (fy1 > -1e9 ? (int)fy1 : -1000000000) : cam.H - 1;
-    }
-    if (!finite) valid = false;
-    SlmSplat s;
-    s.mx = mx; s.my = my; s.ca = ca; s.cb = cb; s.cc = cc; s.o = o;
-    s.c0 = col[0]; s.c1 = col[1]; s.c2 = col[2];
-    s.x0 = x0; s.x1 = x1; s.y0 = y0; s.y1 = y1;
-    s.flags = (valid ? SLM_FLAG_VALID : 0u) | clampbits;
-    s.pad = 0;
-    s_out = s;
-    key_out = valid ? (unsigned long long)__double_as_longlong(X2) : ~0ull;
+    for (int k = 0; k < 3; ++k)
+      T1[i * 3 + k] = R[i * 3 + 0] * Sw[0 * 3 + k] + R[i * 3 + 1] * Sw[1 * 3 + k] + R[i * 3 + 2] * Sw[2 * 3 + k];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      Sc[i * 3 + k] = T1[i * 3 + 0] * R[k * 3 + 0] + T1[i * 3 + 1] * R[k * 3 + 1] + T1[i * 3 + 2] * R[k * 3 + 2];
+  double Xs0 = valid ? X0 : 0.0, Xs1 = valid ? X1 : 0.0, Xs2 = valid ? X2 : 1.0;
+  double iz = 1.0 / Xs2;
+  double A00 = cam.fx * iz, A02 = -cam.fx * Xs0 * iz * iz;
+  double A11 = cam.fy * iz, A12 = -cam.fy * Xs1 * iz * iz;
+  // cov2 = A Sc A^T (A has zeros at (0,1), (1,0))
+  double r00 = A00 * Sc[0] + A02 * Sc[6], r01 = A00 * Sc[1] + A02 * Sc[7], r02 = A00 * Sc[2] + A02 * Sc[8];
+  double r11 = A11 * Sc[4] + A12 * Sc[7], r12 = A11 * Sc[5] + A12 * Sc[8];
+  double c00 = r00 * A00 + r02 * A02;
+  double c01 = r01 * A11 + r02 * A12;
+  double c11 = r11 * A11 + r12 * A12;
+  double va = c00 + cfg.cov_eps, vb = c01, vc = c11 + cfg.cov_eps;
+  double det = va * vc - vb * vb;
+  valid = valid && (det > 0.0);
+  double detu = det > 0.0 ? det : 1.0;
+  double ca = vc / detu, cb = -vb / detu, cc = va / detu;
+
+  // view-dependent colour
+  double v0 = p0 - cam.C[0], v1 = p1 - cam.C[1], v2 = p2 - cam.C[2];
+  double vn = sqrt(v0 * v0 + v1 * v1 + v2 * v2);
+  double d0 = v0 / vn, d1 = v1 / vn, d2 = v2 / vn;
+  double Y[16];
+  sh_basis<double, K>(d0, d1, d2, Y);
+  double col[3];
+  unsigned clampbits = 0;
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    double raw = 0.0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) raw += x[(long long)(11 + ch * K + k) * G + g] * Y[k];
+    raw += 0.5;
+    col[ch] = raw > 0.0 ? raw : 0.0;
+    if (raw <= 0.0) clampbits |= (1u << (1 + ch));
   }
+  double lam = 0.5 * (va + vc) + sqrt(0.25 * (va - vc) * (va - vc) + vb * vb);
+  if (cfg.cull_sigma > 0.0) {
+    double rad = cfg.cull_sigma * sqrt(lam);
+    valid = valid && (mx + rad > 0.0) && (mx - rad < (double)cam.W) && (my + rad > 0.0) &&
+            (my - rad < (double)cam.H);
+  }
+  int x0 = 0, x1 = cam.W - 1, y0 = 0, y1 = cam.H - 1;
+  if (cfg.reach_fac > 0.0) {
+    double reach = cfg.reach_fac * sqrt(lam);
+    double fx0 = ceil(mx - reach - 0.5), fx1 = floor(mx + reach - 0.5);
+    double fy0 = ceil(my - reach - 0.5), fy1 = floor(my + reach - 0.5);
+    x0 = fx0 > 0.0 ? (fx0 < 1e9 ? (int)fx0 : 1000000000) : 0;
+    y0 = fy0 > 0.0 ? (fy0 < 1e9 ? (int)fy0 : 1000000000) : 0;
+    x1 = fx1 < (double)(cam.W - 1) ? (fx1 > -1e9 ? (int)fx1 : -1000000000) : cam.W - 1;
+    y1 = fy1 < (double)(cam.H - 1) ? (fy1 > -1e9 ? (int)fy1 : -1000000000) : cam.H - 1;
+  }
+  if (!P.finite) valid = false;
+  SlmSplat s;
+  s.mx = mx; s.my = my; s.ca = ca; s.cb = cb; s.cc = cc; s.o = P.o;
+  s.c0 = col[0]; s.c1 = col[1]; s.c2 = col[2];
+  s.x0 = x0; s.x1 = x1; s.y0 = y0; s.y1 = y1;
+  s.flags = (valid ? SLM_FLAG_VALID : 0u) | clampbits;
+  s.pad = 0;
+  s_out = s;
+  key_out = valid ? (unsigned long long)__double_as_longlong(X2) : ~0ull;
 }
 
 template <int K>
@@ -132,23 +149,25 @@ __global__ void k_preprocess(const double* __restrict__ x, long long G, SlmCamer
                              SlmSplat* __restrict__ out, unsigned long long* __restrict__ depth_key,
                              uint32_t* __restrict__ order_val, int* __restrict__ err) {
   for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < G; g += (long long)gridDim.x * blockDim.x) {
-    preprocess_one<K>(x, G, g, cam, cfg, out[g], depth_key[g], err);
+    const GaussPre P = gauss_pre<K>(x, G, g, err);
+    preprocess_view<K>(P, x, G, g, cam, cfg, out[g], depth_key[g]);
     order_val[g] = (uint32_t)g;
   }
 }
 
-// all views of a subset in one launch: thread per gaussian looping over the
-// views (its parameters stay in L1 across views), element i = v * G + g,
-// value (v << 24) | g
+// all views of a subset in one launch: thread per gaussian, the
+// view-independent part once, then a loop over the views (the SH coefficients
+// stay in L1 across views), element i = v * G + g, value (v << 24) | g
 template <int K>
 __global__ void k_preprocess_views(const double* __restrict__ x, long long G, const SlmCamera* __restrict__ cams,
                                    int V, SlmRastCfg cfg, SlmSplat* __restrict__ out,
                                    unsigned long long* __restrict__ depth_key, uint32_t* __restrict__ order_val,
                                    int* __restrict__ err) {
   for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < G; g += (long long)gridDim.x * blockDim.x) {
+    const GaussPre P = gauss_pre<K>(x, G, g, err);  // once per gaussian
     for (int v = 0; v < V; ++v) {
       const long long i = (long long)v * G + g;
-      preprocess_one<K>(x, G, g, cams[v], cfg, out[i], depth_key[i], err);
+      preprocess_view<K>(P, x, G, g, cams[v], cfg, out[i], depth_key[i]);
       order_val[i] = ((uint32_t)v << 24) | (uint32_t)g;
     }
   }
