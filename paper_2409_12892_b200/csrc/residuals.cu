@@ -31,16 +31,20 @@ __device__ __forceinline__ double gt_at(const ResidArgs& A, size_t i) {
 // correlate1d, residuals.py:58-91).
 #define RT 16
 
-__global__ void __launch_bounds__(256) k_residuals(ResidArgs A) {
+// WIN > 0: the window size as a compile-time constant (the tap loops unroll;
+// 11 is the reference's default, residuals.py); WIN = 0: A.win at run time
+template <int WIN>
+__global__ void __launch_bounds__(256, 4) k_residuals(ResidArgs A) {
   extern __shared__ double sm[];
   __shared__ double red[32];
   __shared__ double taps[SSIM_WIN_MAX];
-  const int half = A.win / 2, IW = RT + 2 * half;
+  const int win = WIN > 0 ? WIN : A.win;
+  const int half = win / 2, IW = RT + 2 * half;
   double* s_a = sm;
   double* s_b = s_a + 3 * IW * IW;
   double* s_h = s_b + 3 * IW * IW;
   const bool ssim = A.mode == 0 && A.lambda2 > 0.0;
-  if (threadIdx.x < A.win) taps[threadIdx.x] = A.taps[threadIdx.x];
+  if (threadIdx.x < win) taps[threadIdx.x] = A.taps[threadIdx.x];
   const int tx = threadIdx.x & (RT - 1), ty = threadIdx.x / RT;
   const int ntx = (A.W + RT - 1) / RT, nty = (A.H + RT - 1) / RT;
   double e_acc = 0.0;
@@ -74,7 +78,8 @@ __global__ void __launch_bounds__(256) k_residuals(ResidArgs A) {
           const double* ra = s_a + c * IW * IW + iy * IW + ix;
           const double* rb = s_b + c * IW * IW + iy * IW + ix;
           double h0 = 0.0, h1 = 0.0, h2 = 0.0, h3 = 0.0, h4 = 0.0;
-          for (int j = 0; j < A.win; ++j) {
+#pragma unroll
+          for (int j = 0; j < win; ++j) {
             const double w = taps[j], a = ra[j], b = rb[j];
             h0 += w * a;
             h1 += w * b;
@@ -86,7 +91,8 @@ __global__ void __launch_bounds__(256) k_residuals(ResidArgs A) {
           o[0] = h0; o[1] = h1; o[2] = h2; o[3] = h3; o[4] = h4;
         }
         __syncthreads();
-        for (int j = 0; j < A.win; ++j) {
+#pragma unroll
+        for (int j = 0; j < win; ++j) {
           const double w = taps[j];
           const double* hh = s_h + ((ty + j) * RT + tx) * 5;
 #pragma unroll
@@ -158,12 +164,19 @@ int slm_residuals(const ResidArgs* a, int blocks, cudaStream_t stream) {
   if (a->win > SSIM_WIN_MAX || a->win % 2 != 1 || blocks <= 0) return SLM_ERR_ARG;
   const int IW = RT + 2 * (a->win / 2);
   const size_t smem = (a->mode == 0 && a->lambda2 > 0.0) ? ((size_t)6 * IW * IW + (size_t)IW * RT * 5) * 8 : 0;
-  static size_t smem_set = 0;  // opt-in above the 48 KB default (static + dynamic)
-  if (smem > smem_set) {
-    cudaFuncSetAttribute(k_residuals, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    smem_set = smem;
+  // opt-in above the 48 KB default (static + dynamic), per device and kernel
+  constexpr int kMaxDev = 64;
+  static size_t smem_set[kMaxDev][2] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int w = a->win == 11 ? 1 : 0;
+  if (dev < kMaxDev && smem > smem_set[dev][w]) {
+    if (w) cudaFuncSetAttribute(k_residuals<11>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    else cudaFuncSetAttribute(k_residuals<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    smem_set[dev][w] = smem;
   }
-  k_residuals<<<blocks, 256, smem, stream>>>(*a);
+  if (w) k_residuals<11><<<blocks, 256, smem, stream>>>(*a);
+  else k_residuals<0><<<blocks, 256, smem, stream>>>(*a);
   return slm_cuda_status();
 }
 
