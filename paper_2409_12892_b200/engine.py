@@ -240,7 +240,7 @@ def residual_pass(frame: ViewFrame, gt: torch.Tensor, loss: LossConfig, gradr: t
     dev = gt.device
     gt = gt.contiguous()
     taps_t, cwy_t, cwx_t = _ssim_tables(H, W, loss.window, loss.sigma, dev)
-    blocks = int(min(max((H * W + 255) // 256, 1), 148 * 8))
+    blocks = int(max(((W + 15) // 16) * ((H + 15) // 16), 1))  # one 16x16 tile per block
     part = torch.empty(blocks, dtype=torch.float64, device=dev)
     a = _lib.SlmResidArgs()
     a.img = ptr(frame.rgb)

@@ -1,2 +1,2 @@
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3 > gpurun_out/pytest_quick.log
-bash tools/gpu_launches_build.sh res
+bash tools/gpu_launches_build.sh res2
