@@ -409,16 +409,6 @@ class CacheSet:
                     self.residual_exports.append(ex)
             self.frames.append(fr)
         T.tick("residuals")
-        # one host sync for the error flags and the per-view energies
-        sums = [err.to(torch.float64).reshape(1)] + [p.sum().reshape(1) for p in energy_parts]
-        host = torch.cat(sums).cpu().tolist()
-        e = int(host[0])
-        if e & 1:
-            raise ValueError("scene contains non-finite parameters")
-        if e & 2:
-            raise ValueError("quaternion with (near-)zero norm")
-        self.energies = host[1:] if have_res else None
-
         # ---- instances -> runs ---------------------------------------------
         inst_cnt = torch.zeros(ni + 1, dtype=torch.int64, device=dev)
         inst_used = torch.zeros(ni + 1, dtype=torch.int32, device=dev)
@@ -428,8 +418,6 @@ class CacheSet:
         scan_i64(inst_cnt, ent_of)
         run_of = torch.empty_like(inst_used)
         scan_i32(inst_used, run_of)
-        tot = torch.stack([ent_of[ni], run_of[ni].to(torch.int64)]).cpu().tolist()
-        self.E, self.R = int(tot[0]), int(tot[1])
         del inst_cnt
 
         # ---- pairs (view, gaussian) ------------------------------------------
@@ -443,7 +431,19 @@ class CacheSet:
         scan_i32(flagV, pair_of)
         tscan = torch.empty_like(flagT)
         scan_i32(flagT, tscan)
-        self.n_pairs = int(pair_of[VG].item())
+        # ONE host sync for the error flags, the per-view energies and the
+        # entry / run / pair counts the next allocations need
+        sums = [err.to(torch.float64).reshape(1), ent_of[ni].to(torch.float64).reshape(1),
+                run_of[ni].to(torch.float64).reshape(1), pair_of[VG].to(torch.float64).reshape(1)] + \
+            [p.sum().reshape(1) for p in energy_parts]
+        host = torch.cat(sums).cpu().tolist()
+        e = int(host[0])
+        if e & 1:
+            raise ValueError("scene contains non-finite parameters")
+        if e & 2:
+            raise ValueError("quaternion with (near-)zero norm")
+        self.E, self.R, self.n_pairs = int(host[1]), int(host[2]), int(host[3])
+        self.energies = host[4:] if have_res else None
         Pn = self.n_pairs
         self.pair_off = torch.empty(Pn + 1, dtype=torch.int64, device=dev)   # entries per pair (stats)
         self.pair_gid = _empty(Pn, torch.int32, dev)

@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3 > gpurun_out/pytest_quick.log
-bash tools/gpu_launches_build.sh res2
+timeout 400 python tools/profile_subset.py --config c3 --reps 3 --skip-pcg > gpurun_out/prof_sync2.json 2>&1
+timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu > gpurun_out/bench_c3_sync.log 2>&1
