@@ -1,1 +1,1 @@
-NOFULL=1 bash tools/gpu_ncu_product.sh prod_c4 c4
+bash tools/gpu_evidence.sh > gpurun_out/evidence.log 2>&1
