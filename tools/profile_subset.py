@@ -46,7 +46,12 @@ def main():
     cams = [cams[i] for i in views]
     gts = [gts[i] for i in views]
     out = {}
+    cs = None
     for rep in range(args.reps):
+        # release the previous rep's cache first: with two 37 GB caches alive
+        # the allocator would cudaMalloc inside the timed FILL phase
+        cs = None
+        torch.cuda.synchronize()
         T = PhaseTimer()
         torch.cuda.nvtx.range_push("build")
         cs = CacheSet(scene, cams, gts, timer=T)
