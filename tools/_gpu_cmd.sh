@@ -1,1 +1,1 @@
-timeout 600 python tools/profile_subset.py --config c3 --reps 2 > gpurun_out/profile_c3.json 2>&1
+NOFULL=1 SLM_LIB=paper_2409_12892_b200/_variants/nogather/libsplatlm_b200.so bash tools/gpu_ncu_product.sh prod_nog
