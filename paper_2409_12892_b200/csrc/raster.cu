@@ -408,8 +408,18 @@ __device__ __forceinline__ double lds1(unsigned a) {
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
   return v;
 }
+// register budgets of the two passes (resident blocks per SM), measured at C3:
+// COUNT 4 blocks (64 registers) 13.98 -> 13.72 ms against the compiler's
+// default 5; FILL 1 (79 registers, 3 blocks resident) 15.01 -> 14.87 ms
+// against 4; higher occupancy (5 / 6) is slower for both
+#ifndef SLM_COUNT_MINB
+#define SLM_COUNT_MINB 4
+#endif
+#ifndef SLM_FILL_MINB
+#define SLM_FILL_MINB 1
+#endif
 template <bool FILL>
-__global__ void __launch_bounds__(RB) k_raster(RasterArgs A) {
+__global__ void __launch_bounds__(RB, FILL ? SLM_FILL_MINB : SLM_COUNT_MINB) k_raster(RasterArgs A) {
   // per-instance fp64 staging, one array each so that every access is one
   // base + k * 16 (or 8) with immediate offsets: (mx, my), (ca, 2 cb), (cc, o)
   // and the colour (c0, c1, c2); 2 cb is exact, so q is bit-identical
