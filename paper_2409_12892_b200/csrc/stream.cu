@@ -85,6 +85,7 @@ __device__ __forceinline__ float group_sum(float v) {
 __device__ __forceinline__ float jt_scale(int vi, float v, float io) {
   return vi == 5 ? v * io : ((vi == 2 || vi == 4) ? 0.5f * v : v);
 }
+__device__ __forceinline__ float jt_scl(int vi) { return (vi == 2 || vi == 4) ? 0.5f : 1.f; }
 #define PAR 16           // floats per run parameter record
 #define TMETA 64         // producer chunk-metadata window
 #define TQ 4             // tile queue depth (producer -> consumers)
@@ -523,7 +524,11 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
     // per-pixel weight / input loaded up front so its latency hides behind the J pass
     float4 wt = make_float4(1.f, 1.f, 1.f, 0.f);
     if (MODE & MODE_J) {
-      if (inside && A.gradr) wt = A.gradr[gp];
+      // only inside pixels use the weight (at the end of the J pass): the
+      // load is unpredicated (outside pixels read the tile's first pixel), so
+      // no select right after it waits on the load at the tile start
+      const long long g0p = ((long long)ti.y << 32) | (unsigned)ti.x;
+      if (A.gradr) wt = A.gradr[inside ? gp : g0p];
     } else if (MODE & MODE_DIAG) {
       wt = inside ? A.gradr[gp] : make_float4(0.f, 0.f, 0.f, 0.f);
       s_c[p] = inside && A.u ? A.u[gp] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -804,7 +809,7 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
             // pair-run-slot order (read contiguously by the backward): partials
             // 0-7 as one 32-byte record, partial 8 in A.out1
 #pragma unroll
-            for (int h = 0; h < 8 / GL; ++h) A.out[(size_t)sl * 8 + GL * h + lg] = jt_scale(GL * h + lg, ra[h], io);
+            for (int h = 0; h < 8 / GL; ++h) A.out[(size_t)sl * 8 + GL * h + lg] = ra[h] * (GL * h + lg == 5 ? io : jt_scl(GL * h + lg));
             if (lg == 0) A.out1[sl] = a8;
           }
         }
