@@ -285,11 +285,17 @@ def run_ours(args, cfg):
     t_prod = statistics.median(prod_ms) / 1e3 if prod_ms else float("nan")
     achieved = alg_bytes / t_prod / 1e9
     peak, peak_kind = peaks()
-    traffic = None
+    # DRAM bytes per product from the committed ncu launch list of this config
+    # (tools/gpu_ncu_product.sh -> tools/traffic_from_ncu.py); null without one
+    traffic, traffic_src = None, None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get(args.config)
+            tj = json.load(open(tf))
+            traffic = tj.get(args.config)
+            src = tj.get("_source", {}).get(args.config, {})
+            if traffic is not None:
+                traffic_src = f"ncu launch list {os.path.basename(src.get('launch_list', '?'))} ({src.get('written', '?')})"
         except Exception:
             traffic = None
     cpu = cpu_baseline(cfg, rep, args) if (world == 1 and not args.no_cpu) else None
@@ -309,7 +315,8 @@ def run_ours(args, cfg):
                    "l2": "inputs larger than L2 (cache >> 126 MB)",
                    "parallelism": f"subsets round-robin over {world} rank(s), one NCCL all_reduce"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
+                     "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_kind": peak_kind,
                      "kernel": "J^T W J p product", "product_ms_median": round(t_prod * 1e3, 4),
                      "algorithmic_bytes": alg_bytes},
         "e2e": {"value": round(e2e_ms, 3), "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
