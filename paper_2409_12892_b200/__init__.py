@@ -11,6 +11,7 @@ combine); see DESIGN.md.  Public API mirrors the reference module layout:
                 apply_jt, diag_jtj, dump_cache, load_cache_dump
     solver:     pcg_solve, solve_normal_equations_batched, lm_direction
     lm:         line_search, compute_rho, trust_region_update, lm_step
+    fit:        adam_fit, lm_fit, two_stage_fit (SPEC-only drivers); CLI: python -m paper_2409_12892_b200
 """
 
 from .errors import CacheOrderError, ImageSizeError, LayoutError, NonSPDError, SplatLMError  # noqa: F401
