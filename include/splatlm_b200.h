@@ -184,6 +184,8 @@ typedef struct {
   const float* d2_h;
   const uint8_t* pix_h;
   long long e_split, e_hbase;
+  int jt_lanes;              /* J^T lanes per run: 8 (0 = default) or 4 (short runs) */
+  int pad_;
 } SlmTileArgs;
 
 /* per-pair forward chain (applyJ) */

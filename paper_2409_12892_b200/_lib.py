@@ -65,7 +65,8 @@ class SlmTileArgs(C.Structure):
                 ("geo", c_vp),
                 ("rec4", c_vp), ("d2", c_vp), ("pix", c_vp),
                 ("gradr", c_vp), ("u", c_vp), ("u_out", c_vp), ("out", c_vp), ("out1", c_vp), ("rhs8", c_vp), ("rhs1", c_vp), ("tile_counter", c_vp),
-                ("rec4_h", c_vp), ("d2_h", c_vp), ("pix_h", c_vp), ("e_split", c_ll), ("e_hbase", c_ll)]
+                ("rec4_h", c_vp), ("d2_h", c_vp), ("pix_h", c_vp), ("e_split", c_ll), ("e_hbase", c_ll),
+                ("jt_lanes", c_i), ("pad_", c_i)]
 
 
 class SlmFwdArgs(C.Structure):

@@ -344,7 +344,7 @@ struct ChunkMeta {
 
 // stage header: [0] runs, [1] run-start offset (k0 - a2), [2] k0 (global run),
 // [3] d2 offset (e0 - a4), [4] pix offset (e0 - a16)
-template <int MODE>
+template <int MODE, int JGL = kJtGL>
 __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int NSM = ns_of(MODE);
@@ -740,7 +740,7 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
       consumer_sync();
       // pass J^T: 32 / GL runs per warp (GL lanes each) from the chunk's
       // length-sorted schedule; the warp's slot block rotates with the chunk
-      constexpr int GL = kJtGL, RPW = 32 / GL, RPR = NW * RPW;
+      constexpr int GL = JGL, RPW = 32 / GL, RPR = NW * RPW;
       const int slot = lane / GL, lg = lane % GL;
       for (int ci = c0; ci < c1; ++ci, ++g) {
         const int s = (int)(g % NSM);
@@ -821,8 +821,8 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
   }
 }
 
-template <int MODE>
-static int launch_stream(const SlmTileArgs* a, cudaStream_t st) {
+template <int MODE, int JGL = kJtGL>
+static int launch_stream_gl(const SlmTileArgs* a, cudaStream_t st) {
   if (a->n_tiles <= 0) return SLM_OK;
   const size_t bytes = stream_smem_bytes(MODE);
   // the dynamic shared-memory opt-in and the occupancy are per device: a
@@ -834,18 +834,27 @@ static int launch_stream(const SlmTileArgs* a, cudaStream_t st) {
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= kMaxDev) return SLM_ERR_ARG;
   if (s_per_sm[dev] == 0) {
-    cudaFuncSetAttribute(k_stream<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaFuncSetAttribute(k_stream<MODE, JGL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     int sms = 148, per_sm = 1;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stream<MODE>, NT, bytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stream<MODE, JGL>, NT, bytes);
     s_sms[dev] = sms;
     s_per_sm[dev] = per_sm < 1 ? 1 : per_sm;
   }
   const int sms = s_sms[dev], per_sm = s_per_sm[dev];
   const int grid = (int)std::min<long long>((long long)a->n_tiles, (long long)sms * per_sm);
   if (a->tile_counter) cudaMemsetAsync(a->tile_counter, 0, sizeof(int), st);
-  k_stream<MODE><<<grid, NT, bytes, st>>>(*a);
+  k_stream<MODE, JGL><<<grid, NT, bytes, st>>>(*a);
   return slm_cuda_status();
+}
+
+// J^T lanes per run: 8 by default; 4 when the runs are short (the caller sets
+// jt_lanes = 4 below ~18 entries per run: C4's 13-entry runs -5 % on the
+// fused kernel, C2 / C3's long runs +20 % / +3 %)
+template <int MODE>
+static int launch_stream(const SlmTileArgs* a, cudaStream_t st) {
+  if ((MODE & MODE_JT) && a->jt_lanes == 4) return launch_stream_gl<MODE, 4>(a, st);
+  return launch_stream_gl<MODE, 8>(a, st);
 }
 
 extern "C" {

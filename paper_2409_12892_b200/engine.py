@@ -35,6 +35,10 @@ MASK_WORDS = TILE * TILE // 32
 CHUNK_RUNS = 64   # SLM_CHUNK_RUNS: max runs per streaming chunk (bytes of schedule per chunk)
 
 
+# below this many entries per run the J^T pass uses 4 lanes per run (stream.cu)
+JT4_ENTRIES_PER_RUN = 18
+
+
 @dataclass(frozen=True)
 class LossConfig:
     """Residual settings of compute_residuals (ref: residuals.py:249-252)."""
@@ -697,6 +701,7 @@ class CacheSet:
         a.geo = ptr(self.pair_geo)
         a.rec4, a.d2 = ptr(self.rec4), ptr(self.rec_d2)
         a.pix = ptr(self.rec_pix)
+        a.jt_lanes = 4 if self.R > 0 and self.E < JT4_ENTRIES_PER_RUN * self.R else 8
         self._offload_args(a, "d2_h", "pix_h")
         a.tile_counter = ptr(self.tile_counter)
         return a

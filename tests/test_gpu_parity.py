@@ -359,3 +359,30 @@ def test_forward_chain_dsigma_path(prob, cacheset, oracle_views):
     cacheset.jtwj(pd, b, p_gm=cacheset.gm_pack(pd))
     assert rel(b.cpu().numpy(), a.cpu().numpy()) < 1e-5
     assert rel(b.cpu().numpy(), ref) < FTOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("lanes_threshold", [0, 10 ** 9])   # 0: always 8 J^T lanes per run; 1e9: always 4
+def test_jt_group_widths(prob, cacheset, oracle_views, monkeypatch, lanes_threshold):
+    """Both J^T group widths (stream.cu launch_stream: 8 lanes per run, or 4
+    below engine.JT4_ENTRIES_PER_RUN entries per run) against the oracle."""
+    from paper_2409_12892_b200 import engine
+    monkeypatch.setattr(engine, "JT4_ENTRIES_PER_RUN", lanes_threshold)
+    assert cacheset._tile_args().jt_lanes == (8 if lanes_threshold == 0 else 4)
+    s = prob["scene"]
+    rng = np.random.default_rng(7)
+    p = rng.standard_normal(s.param_count)
+    out = torch.empty(s.param_count, dtype=torch.float32, device="cuda")
+    cacheset.jtwj(torch.from_numpy(p).float().cuda(), out)
+    assert rel(out.cpu().numpy(), O.jtwj(p, prob["osc"], [ov["gview"] for ov in oracle_views])) < FTOL
+    uu = rng.standard_normal(sum(ov["view"].cam.width * ov["view"].cam.height * 3 for ov in oracle_views))
+    g_ref, off = np.zeros(s.param_count), 0
+    for ov in oracle_views:
+        n = ov["view"].cam.width * ov["view"].cam.height * 3
+        g_ref += O.apply_jt(uu[off:off + n], prob["osc"], ov["gview"])
+        off += n
+    u4 = torch.zeros(uu.size // 3, 4, dtype=torch.float32, device="cuda")
+    u4[:, :3] = torch.from_numpy(uu).float().view(-1, 3)
+    g = torch.empty(s.param_count, dtype=torch.float32, device="cuda")
+    cacheset.apply_jt_raw(u4.view(-1), g)
+    assert rel(g.cpu().numpy(), g_ref) < FTOL
