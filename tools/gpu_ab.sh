@@ -5,5 +5,5 @@ mkdir -p gpurun_out
 for v in "" "$@"; do
   if [ -n "$v" ]; then export SLM_LIB=paper_2409_12892_b200/_variants/$v/libsplatlm_b200.so; else unset SLM_LIB; fi
   echo "== ${v:-default}"
-  timeout 400 python tools/profile_subset.py --config $cfg --reps 2 --skip-pcg 2>&1 | grep -v '"E"\|"N"\|"R"\|"G"'
+  timeout 200 python tools/profile_subset.py --config $cfg --reps 2 --skip-pcg 2>&1 | grep -v '"E"\|"N"\|"R"\|"G"'
 done
