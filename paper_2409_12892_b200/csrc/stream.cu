@@ -780,7 +780,7 @@ __global__ void __launch_bounds__(NT, 2) k_stream(SlmTileArgs A) {
           const float* pd = sd2 + f0;
           const uint8_t* pp = spx + f0;
           const RunE ke = run_e_of(q0, s1);
-#pragma unroll(kJtUnroll)
+#pragma unroll(GL == 4 ? 1 : kJtUnroll)  // 4-lane groups (short runs): no unroll, -1 % at C4
           for (int j = lg; j < nmax; j += GL) {
             const bool ok = j < n;
             const float4 r = pr[j];

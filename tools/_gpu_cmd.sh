@@ -1,10 +1,8 @@
 mkdir -p gpurun_out
-timeout 900 python bench.py --config c5 --steps 1 --warmup 3 --no-cpu > gpurun_out/bench_c5.log 2>&1
-timeout 600 python bench.py --config c1 --steps 5 --warmup 3 --no-cpu > gpurun_out/bench_c1.log 2>&1
-timeout 600 python bench.py --config c2 --steps 3 --warmup 3 --no-cpu > gpurun_out/bench_c2.log 2>&1
-for f in bench_c5 bench_c1 bench_c2; do python -c "
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_c2_subset.py tests/test_large_regime.py -m gpu -q -x 2>&1 | tail -2 > gpurun_out/pytest_gpu.log
+timeout 900 python bench.py --config c4 --steps 2 --warmup 3 --no-cpu > gpurun_out/bench_c4.log 2>&1
+cat gpurun_out/pytest_gpu.log; python -c "
 import json
-l=[x for x in open('gpurun_out/$f.log') if x.startswith('{')]
-d=json.loads(l[-1]) if l else None
-print('$f', d and (d['value'], d['e2e']['value'], d['roofline']['product_ms_median'], d['roofline']['frac'], d['config'].get('entries_per_pixel')))
-"; done
+l=[x for x in open('gpurun_out/bench_c4.log') if x.startswith('{')]
+d=json.loads(l[-1]); print(d['value'], d['e2e']['value'], d['roofline']['product_ms_median'], d['roofline']['frac'])
+"
