@@ -854,7 +854,7 @@ static int launch_stream_gl(const SlmTileArgs* a, cudaStream_t st) {
 template <int MODE>
 static int launch_stream(const SlmTileArgs* a, cudaStream_t st) {
   if ((MODE & MODE_JT) && a->jt_lanes == 4) return launch_stream_gl<MODE, 4>(a, st);
-  return launch_stream_gl<MODE, 8>(a, st);
+  return launch_stream_gl<MODE, kJtGL>(a, st);
 }
 
 extern "C" {
